@@ -1,0 +1,231 @@
+/*
+ * mfseg_sm100.h — C ABI of the B200 (sm_100a) segmentation core.
+ *
+ * Drop-in boundary for the data-parallel hot path of the reference `mfseg`
+ * package (arXiv 1903.12294).  Every entry point below replaces one Python
+ * function of the reference; the citation after each declaration names it
+ * (paths relative to /root/reference/pkg/src/mfseg/).
+ *
+ * Conventions
+ *   - Plain C types only: pointers, sizes, POD structs.  No torch types.
+ *   - All array pointers are DEVICE pointers unless a name ends in `_host`.
+ *     The caller owns every buffer, including the workspace sized by the
+ *     matching *_workspace_size() query.  The library never frees caller memory.
+ *   - Every call is stream-ordered on the caller's `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  Calls that return host
+ *     values synchronise that stream.
+ *   - Return value: 0 on success, non-zero on error; the message is available
+ *     from mfseg_last_error() (thread-local).  No C++ exception crosses the ABI.
+ *   - Layouts follow the reference: field values are timestep-major, x-fastest
+ *     (flat = i + nx*(j + ny*k), model.py:112); point xyz is (N,3) row-major
+ *     (model.py:86-89); labels are int32 (engine.py:374-375).
+ *   - Arithmetic is IEEE fp64 with the reference's operation order and no FMA
+ *     contraction, so labels are bit-identical to the reference's.
+ */
+#ifndef MFSEG_SM100_H
+#define MFSEG_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFSEG_ABI_VERSION 1
+
+/* Clustering geometry and weights: ClusterParams (model.py:198-228) plus the
+ * extent minima and interval distances C = extent/k (model.py:275-280). */
+typedef struct mfseg_params {
+    int32_t k[4];          /* clusters per axis (x, y, z, t) */
+    double mins[4];        /* DomainExtent minima (x, y, z, t) */
+    double C[4];           /* interval distances, computed by the host exactly as the reference */
+    double c_f, w_d, w_p, w_f;
+    double eps_c;
+    int32_t max_iterations;
+    int32_t reserved;
+} mfseg_params;
+
+/* FieldSet (model.py:108-157).  values: [nt][nz][ny][nx] fp64 (already
+ * normalized, ingest.py:321-335), times: [nt]. */
+typedef struct mfseg_field {
+    int32_t nx, ny, nz, nt;
+    double origin[3];
+    double spacing[3];
+    const double *times;
+    const double *values;
+} mfseg_field;
+
+/* PointSet (model.py:78-105): xyz [n][3], t [n], value [n] (normalized). */
+typedef struct mfseg_points {
+    int64_t n;
+    const double *xyz;
+    const double *t;
+    const double *value;
+} mfseg_points;
+
+/* CenterState (engine.py:48-70), structure of arrays of length K. */
+typedef struct mfseg_centers {
+    double *loc;           /* [4][K]: x plane, y plane, z plane, t plane */
+    double *pval;          /* [K], NaN when !has_p */
+    double *fval;          /* [K], NaN when !has_f */
+    uint8_t *has_p, *has_f, *dormant;   /* [K] */
+    int64_t *n_points, *n_fields;        /* [K] */
+} mfseg_centers;
+
+/* Exact per-cluster sums (accumulate, engine.py:244-263) in 128-bit fixed
+ * point (2^-64 units): per cluster 16 int64 words
+ *   [0..7]  x, y, z, t   (lo, hi) pairs   — points and fields together
+ *   [8..9]  point-value sum (lo, hi)
+ *   [10..11] field-value sum (lo, hi)
+ *   [12] n_points  [13] n_fields  [14..15] reserved (0)
+ * Integer addition is associative, so the sums are independent of thread
+ * scheduling and of the number of GPUs the samples are sharded over. */
+#define MFSEG_ACC_WORDS 16
+
+/* Per-iteration progress sink: progress(it, max_delta) (engine.py:368-369). */
+typedef void (*mfseg_progress_fn)(void *user, int32_t iteration, double max_delta);
+
+/* Cross-shard reduction hook for multi-GPU runs: called once per pass with a
+ * device buffer of `n_words` int64 limbs (3 limbs of <=42 bits per 128-bit
+ * word) that must be SUM-all-reduced in place across ranks on `stream`
+ * before it returns.  NULL for single-GPU runs. */
+typedef int (*mfseg_reduce_fn)(void *user, int64_t *limbs, int64_t n_words, void *stream);
+
+const char *mfseg_last_error(void);
+int mfseg_abi_version(void);
+
+/* ---------------------------------------------------------------- full run
+ * engine.run (engine.py:323-381): seed -> initial pass -> iterate
+ * (CenterGrid, assign_iteration, accumulate, update_centers, has_converged)
+ * until converged or max_iterations.  Outputs: labels of the last pass,
+ * final centre state, iterations_used and converged flag (host ints). */
+size_t mfseg_run_workspace_size(const mfseg_params *p, const mfseg_field *f,
+                                const mfseg_points *pts);
+int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts,
+              int32_t *point_labels, int32_t *field_labels, mfseg_centers out,
+              int32_t *iterations_used_host, int32_t *converged_host,
+              mfseg_progress_fn progress, void *progress_user,
+              mfseg_reduce_fn reduce, void *reduce_user,
+              void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- one pass
+ * assign_iteration (engine.py:208-241) for the given centres, with the fused
+ * exact accumulation (engine.py:244-263) into `acc` [K][MFSEG_ACC_WORDS]
+ * (zeroed by the call).  Uses the params' weights as given (the caller
+ * passes w_p = w_f = 0, w_d = 1 for the initial pass, engine.py:348-349).
+ * Labels are int32; the reference's int64 is a host-side widening. */
+size_t mfseg_assign_workspace_size(const mfseg_params *p, const mfseg_field *f,
+                                   const mfseg_points *pts);
+int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts,
+                 mfseg_centers centers, int32_t *point_labels, int32_t *field_labels,
+                 int64_t *acc, void *workspace, size_t workspace_bytes, void *stream);
+
+/* accumulate (engine.py:244-263) for caller-given labels (int32, values in
+ * [0, K)) into acc [K][MFSEG_ACC_WORDS] (zeroed by the call). */
+int mfseg_accumulate(int32_t K, const mfseg_field *f, const mfseg_points *pts,
+                     const int32_t *point_labels, const int32_t *field_labels,
+                     int64_t *acc, void *stream);
+
+/* accumulate's fp64 view: sums [K][4], psum [K], fsum [K], n_p [K], n_f [K]
+ * (each 128-bit sum rounded once to the nearest double). */
+int mfseg_acc_to_double(int32_t K, const int64_t *acc, double *sums, double *psum,
+                        double *fsum, int64_t *n_p, int64_t *n_f, void *stream);
+
+/* update_centers (engine.py:266-286) + has_converged / max_center_delta
+ * (engine.py:289-320): old -> new_state.  `conv_host` gets
+ * {converged (0/1)} and `delta_host` the progress delta (synchronises). */
+int mfseg_update_centers(int32_t K, const int64_t *acc, mfseg_centers old_state,
+                         mfseg_centers new_state, double eps_c, int32_t *conv_host,
+                         double *delta_host, void *stream);
+
+/* update_centers from the reference's fp64 sums (engine.py:266-286):
+ * sums [K][4], psum/fsum [K], n_p/n_f [K] -> new_state (old_state supplies
+ * the frozen values of empty clusters). */
+int mfseg_update_centers_f64(int32_t K, const double *sums, const double *psum,
+                             const double *fsum, const int64_t *n_p, const int64_t *n_f,
+                             mfseg_centers old_state, mfseg_centers new_state, void *stream);
+
+/* has_converged + max_center_delta of two states (engine.py:289-320). */
+int mfseg_compare_centers(int32_t K, mfseg_centers old_state, mfseg_centers new_state,
+                          double eps_c, int32_t *conv_host, double *delta_host, void *stream);
+
+/* ---------------------------------------------------------------- ingest
+ * normalize_variables / _minmax (ingest.py:312-335): in-place (v-lo)/(hi-lo)
+ * on n values, or zeros when hi == lo.  lo/hi returned to the host. */
+int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_host,
+                           double *hi_host, void *stream);
+
+/* build_link_index (ingest.py:261-280): bucket points by (cell, interval).
+ * Outputs (device): keys [n] int64 (flat key sorted ascending; flat =
+ * ((k*ny + j)*nx + i)*n_int + m), members [n] int32 (point indices, stable
+ * within a bucket), n_buckets_host.  Returns 2 if a point is outside the grid. */
+size_t mfseg_link_index_workspace_size(int64_t n);
+int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *keys,
+                     int32_t *members, int64_t *n_buckets_host, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- post
+ * merge_clusters (postproc.py:59-92) over the live centre table (n rows in
+ * ascending id order).  Inputs: ids [n] int32, loc [4][n], p_c/f_c [n]
+ * (NaN = absent), n_points/n_fields [n].  Outputs: rep [n] int32 (the merge
+ * map, = smallest id of the eligibility component), merged table rows
+ * (ascending representative id): m_ids, m_loc [4][n], m_p/m_f, m_np, m_nf
+ * and n_merged_host. */
+size_t mfseg_merge_workspace_size(int32_t n);
+int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *p_c,
+                const double *f_c, const int64_t *n_points, const int64_t *n_fields,
+                double eps_m, int32_t *rep, int32_t *m_ids, double *m_loc, double *m_p,
+                double *m_f, int64_t *m_np, int64_t *m_nf, int32_t *n_merged_host,
+                void *workspace, size_t workspace_bytes, void *stream);
+
+/* merge_map[label] gather (postproc.py:155,164): out[i] = lut[labels[i]]. */
+int mfseg_relabel(const int32_t *labels, int64_t n, const int32_t *lut, int32_t lut_len,
+                  int32_t *out, void *stream);
+
+/* Per-timestep voxel bucketing (postproc.py:162-168): for timestep m and
+ * feature f, the ascending flat cell indices with feature label f.
+ * Output CSR keyed by (m, f_slot) with f_slot = dense feature slot from
+ * `slot_of` [lut_len] (feature id -> slot, -1 unused): seg_start [(nt*nf)+1]
+ * int64, cells [nt*ncell] int32. */
+size_t mfseg_voxel_csr_workspace_size(int64_t n_field_samples, int32_t nt, int32_t n_slots);
+int mfseg_voxel_csr(const int32_t *feature_labels, int32_t nt, int64_t ncell,
+                    const int32_t *slot_of, int32_t lut_len, int32_t n_slots,
+                    int64_t *seg_start, int32_t *cells, void *workspace,
+                    size_t workspace_bytes, void *stream);
+
+/* feature_stats (postproc.py:194-227) for n_slots features from per-sample
+ * slots (-1 = none): stats [n_slots][MFSEG_STAT_WORDS] doubles:
+ *   bbox_min[4], bbox_max[4], p_mean, p_std, f_mean, f_std, n_points, n_fields */
+#define MFSEG_STAT_WORDS 14
+size_t mfseg_feature_stats_workspace_size(int32_t n_slots);
+int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
+                        const mfseg_points *pts, const int32_t *point_slot, double *stats,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * acc [n_words] 128-bit (lo,hi) pairs <-> 3 limbs of 42 bits, for SUM
+ * all-reduce across ranks (exact for up to 2^20 ranks). */
+int mfseg_acc_to_limbs(const int64_t *acc, int64_t n_pairs, int64_t *limbs, void *stream);
+int mfseg_limbs_to_acc(const int64_t *limbs, int64_t n_pairs, int64_t *acc, void *stream);
+
+/* ---------------------------------------------------------------- synthetic data
+ * Counter-based synthetic generator (bench inputs; reproducible bit-for-bit
+ * by the numpy mirror in oracle/synth.py): drifting ellipsoid blobs over a
+ * background plus hashed noise.  See DESIGN.md "Synthetic inputs". */
+typedef struct mfseg_synth {
+    int32_t nx, ny, nz, nt;
+    int64_t n_traj;        /* trajectories, one sample per timestep each */
+    uint64_t seed;
+    double noise;          /* noise amplitude */
+    int32_t n_blobs;
+    int32_t dyadic;        /* 1: quantize values to 2^-20 and xyz to 2^-16 */
+} mfseg_synth;
+int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream);
+int mfseg_synth_points(const mfseg_synth *s, int64_t *traj_id, double *t, double *xyz,
+                       double *value, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFSEG_SM100_H */

@@ -1,0 +1,105 @@
+// Kernel argument blocks and launchers shared by the runtime (run.cu) and the
+// assignment kernels (assign.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace mfseg {
+
+struct FieldArgs {
+    int nx, ny, nz, nt;
+    double ox, oy, oz, sx, sy, sz;
+    const double *times;
+    const double *values;
+    const AxisTile *xt, *yt, *zt;
+    int ntx, nty, ntz;
+    const int *tbin;
+    int kx, ky, kz, kt;
+    double cf, wd, wv;
+    CentersView c;
+    const double *cval;
+    const uint8_t *chas;
+    Grid g;
+    int *labels;
+    unsigned long long *acc;
+    long long *stranded;
+    unsigned long long *n_stranded;
+    long long stranded_cap;
+    int *overflow;
+    int accumulate;
+};
+
+struct PointArgs {
+    long long n;
+    const double *x, *y, *z, *t, *v;   // bin-sorted SoA
+    const int4 *tiles;                 // (bin, start, len, -)
+    const int *n_tiles;
+    double Cx, Cy, Cz, Ct;
+    double cf, wd, wv;
+    CentersView c;
+    const double *cval;
+    const uint8_t *chas;
+    Grid g;
+    int *labels;                       // bin-sorted order
+    unsigned long long *acc;
+    long long *stranded;
+    unsigned long long *n_stranded;
+    long long stranded_cap;
+    int *overflow;
+    int accumulate;
+};
+
+// Stranded-sample fallback (engine.py:195-205): field samples (kind 1) are
+// addressed by flat index, points (kind 0) by bin-sorted position.
+struct FallbackArgs {
+    int K;
+    CentersView c;
+    const double *cval;
+    const uint8_t *chas;
+    double C[4];
+    double cf, wd, wv;
+    // sample source: field (kind 1) or bin-sorted points (kind 0)
+    int kind;
+    int nx, ny, nz, nt;
+    double ox, oy, oz, sx, sy, sz;
+    const double *times, *values;
+    const double *px, *py, *pz, *pt, *pv;
+    long long n_samples;
+    int *labels;
+    const long long *stranded;
+    const unsigned long long *n_stranded;
+    long long cap;
+    unsigned long long *acc;
+    int *overflow;
+    int accumulate;
+};
+
+// grid.cu
+size_t grid_workspace_bytes(int K);
+Grid grid_carve(Carver &cv, int K, int **count_tmp, void **scan_tmp);
+int grid_build(Grid &g, const double *x, const double *y, const double *z, const double *t,
+               const mfseg_params *p, const mfseg_field *f, int *count_tmp, void *scan_tmp,
+               cudaStream_t st);
+// assign.cu
+int field_tile_dims(int *tx, int *ty, int *tz);
+int point_tile_size();
+int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st);
+int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st);
+int launch_fallback(const FallbackArgs &a, cudaStream_t st);
+int launch_accumulate_field(long long n, const mfseg_field *f, const int *labels,
+                            unsigned long long *acc, int *overflow, cudaStream_t st);
+int launch_accumulate_points(const mfseg_points *p, const int *labels, unsigned long long *acc,
+                             int *overflow, cudaStream_t st);
+// update.cu
+size_t update_flags_bytes();
+int launch_update(int K, const unsigned long long *acc, mfseg_centers o, mfseg_centers n,
+                  double eps_c, void *flags_dev, cudaStream_t st);
+void decode_flags(const void *flags_host, int *converged, double *delta);
+int launch_acc_to_double(int K, const unsigned long long *acc, double *sums, double *psum,
+                         double *fsum, long long *n_p, long long *n_f, cudaStream_t st);
+int launch_to_limbs(long long npairs, const unsigned long long *acc, long long *limbs,
+                    cudaStream_t st);
+int launch_from_limbs(long long npairs, const long long *limbs, unsigned long long *acc,
+                      cudaStream_t st);
+
+}  // namespace mfseg

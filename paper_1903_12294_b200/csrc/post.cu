@@ -1,0 +1,645 @@
+// Feature materialisation after segmentation (postproc.py:20-227) and the
+// particle->cell link index (ingest.py:261-280).
+//
+//   mfseg_merge          union-find over the live centre table, smallest-id
+//                        root (postproc.py:20-79); merged rows summed in the
+//                        reference's order: numpy `sum` of loc*n (sequential)
+//                        and CPython 3.12 `sum` of floats (Neumaier) for
+//                        p_c / f_c (postproc.py:82-92)
+//   mfseg_relabel        merge_map[label] gather (postproc.py:155,164)
+//   mfseg_voxel_csr      per (timestep, feature) ascending cell lists
+//                        (postproc.py:162-168) via a stable radix sort
+//   mfseg_feature_stats  bbox / mean / population std / counts
+//                        (postproc.py:194-227), exact fixed-point sums
+//   mfseg_link_index     stable (cell, interval) bucketing (ingest.py:261-280)
+#include <climits>
+#include <cstring>
+
+#include "kernels.cuh"
+
+namespace mfseg {
+namespace {
+
+constexpr double DELTA = 1e-12;   // model.py:16
+
+__device__ __forceinline__ bool values_match(double a, double b, double eps) {
+    bool na = isnan(a), nb = isnan(b);
+    if (na && nb) return true;    // both lack the kind
+    if (na || nb) return false;   // one-sided absence never merges
+    double pct = DDIV(DMUL(2.0, fabs(DSUB(a, b))), DADD(DADD(fabs(a), fabs(b)), DELTA));
+    return pct <= eps;
+}
+
+__device__ int uf_find(int *parent, int a) {
+    int p = ((volatile int *)parent)[a];
+    while (p != a) {
+        a = p;
+        p = ((volatile int *)parent)[a];
+    }
+    return a;
+}
+
+// hook the larger root under the smaller one: the final root of every
+// component is its smallest row (= smallest id, rows are id-ascending)
+__device__ void uf_union(int *parent, int a, int b) {
+    while (true) {
+        a = uf_find(parent, a);
+        b = uf_find(parent, b);
+        if (a == b) return;
+        if (a > b) {
+            int t = a;
+            a = b;
+            b = t;
+        }
+        int old = atomicCAS(&parent[b], b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__global__ void k_uf_init(int n, int *parent) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) parent[i] = i;
+}
+
+// one warp per row i, lanes sweep j > i
+__global__ void k_merge_pairs(int n, const double *pc, const double *fc, double eps, int *parent) {
+    long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (w >= n) return;
+    int i = (int)w;
+    double pi = pc[i], fi = fc[i];
+    for (int j = i + 1 + lane; j < n; j += 32)
+        if (values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps)) uf_union(parent, i, j);
+}
+
+__global__ void k_uf_flatten(int n, int *parent, const int *ids, int *rep_row, int *rep_id,
+                             unsigned *keys, unsigned *vals, int *is_root) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int r = uf_find(parent, i);
+    rep_row[i] = r;
+    rep_id[i] = ids[r];
+    keys[i] = (unsigned)r;
+    vals[i] = (unsigned)i;
+    is_root[i] = r == i;
+}
+
+struct MergeOut {
+    int *m_ids;
+    double *m_loc, *m_p, *m_f;
+    long long *m_np, *m_nf;
+};
+
+// one thread per group, members ascending (stable sort by root row)
+__global__ void k_merge_groups(int n, const unsigned *skeys, const unsigned *members,
+                               const int *is_root, const int *group_of_root, const int *ids,
+                               const double *loc, const double *pc, const double *fc,
+                               const long long *np_, const long long *nf_, MergeOut o, int G) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;   // position in the sorted order
+    if (i >= n) return;
+    if (i > 0 && skeys[i - 1] == skeys[i]) return;  // not the first member of its group
+    int root = (int)skeys[i];
+    int g = group_of_root[root];
+    long long n_p = 0, n_f = 0, n_tot = 0;
+    double ls[4] = {0.0, 0.0, 0.0, 0.0};
+    double pf = 0.0, pcmp = 0.0, ff = 0.0, fcmp = 0.0;
+    for (int q = i; q < n && skeys[q] == (unsigned)root; ++q) {
+        int r = (int)members[q];
+        long long a = np_[r], b = nf_[r], t = a + b;
+        n_p += a;
+        n_f += b;
+        n_tot += t;
+        double dt = (double)t;
+        for (int d = 0; d < 4; ++d) ls[d] = DADD(ls[d], DMUL(loc[(size_t)d * n + r], dt));
+        if (!isnan(pc[r])) {   // Neumaier step (CPython >= 3.12 sum of floats)
+            double x = DMUL(pc[r], (double)a);
+            double t2 = DADD(pf, x);
+            pcmp = fabs(pf) >= fabs(x) ? DADD(pcmp, DADD(DSUB(pf, t2), x))
+                                       : DADD(pcmp, DADD(DSUB(x, t2), pf));
+            pf = t2;
+        }
+        if (!isnan(fc[r])) {
+            double x = DMUL(fc[r], (double)b);
+            double t2 = DADD(ff, x);
+            fcmp = fabs(ff) >= fabs(x) ? DADD(fcmp, DADD(DSUB(ff, t2), x))
+                                       : DADD(fcmp, DADD(DSUB(x, t2), ff));
+            ff = t2;
+        }
+    }
+    if (pcmp != 0.0 && isfinite(pcmp)) pf = DADD(pf, pcmp);
+    if (fcmp != 0.0 && isfinite(fcmp)) ff = DADD(ff, fcmp);
+    double nan = __longlong_as_double(0x7ff8000000000000ll);
+    o.m_ids[g] = ids[root];
+    for (int d = 0; d < 4; ++d) o.m_loc[(size_t)d * G + g] = DDIV(ls[d], (double)n_tot);
+    o.m_p[g] = n_p > 0 ? DDIV(pf, (double)n_p) : nan;
+    o.m_f[g] = n_f > 0 ? DDIV(ff, (double)n_f) : nan;
+    o.m_np[g] = n_p;
+    o.m_nf[g] = n_f;
+}
+
+__global__ void k_relabel(const int *labels, long long n, const int *lut, int lut_len, int *out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int l = labels[i];
+        out[i] = (l >= 0 && l < lut_len) ? lut[l] : -1;
+    }
+}
+
+// ------------------------------------------------------------------ voxel CSR
+__global__ void k_voxel_keys(const int *flab, long long n, long long ncell, const int *slot_of,
+                             int lut_len, int n_slots, unsigned *keys, unsigned *vals,
+                             int *bad) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        long long m = q / ncell;
+        int l = flab[q];
+        int s = (l >= 0 && l < lut_len) ? slot_of[l] : -1;
+        if (s < 0) {
+            *bad = 1;
+            s = 0;
+        }
+        keys[q] = (unsigned)(m * n_slots + s);
+        vals[q] = (unsigned)(q - m * ncell);
+    }
+}
+
+__global__ void k_key_hist(const unsigned *skeys, long long n, long long *cnt) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        // run-length: only the last element of a run adds the run length
+        if (q + 1 == n || skeys[q + 1] != skeys[q]) {
+            long long a = 0, b = q;   // find run start by binary search on sorted keys
+            unsigned k = skeys[q];
+            while (a < b) {
+                long long mid = (a + b) >> 1;
+                if (skeys[mid] < k) a = mid + 1; else b = mid;
+            }
+            cnt[k] = q - a + 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ feature stats
+// per slot words: [0..1] sum pv, [2..3] sum fv, [4..5] ssq pv, [6..7] ssq fv,
+// [8] n_p, [9] n_f, [10..13] bbox min (ordered bits), [14..17] bbox max
+constexpr int SW = 18;
+
+__device__ __forceinline__ unsigned long long okey(double d) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unokey(unsigned long long b) {
+    unsigned long long r = (b >> 63) ? (b & 0x7fffffffffffffffull) : ~b;
+    return __longlong_as_double((long long)r);
+}
+
+__device__ __forceinline__ void warp_sum_fix(unsigned long long &lo, long long &hi) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long ol = __shfl_xor_sync(0xffffffffu, lo, o);
+        long long oh = __shfl_xor_sync(0xffffffffu, hi, o);
+        unsigned long long nl = lo + ol;
+        hi = hi + oh + (nl < lo ? 1 : 0);
+        lo = nl;
+    }
+}
+
+// warp-aggregated add of one sample into its slot's accumulators; the value
+// sums are reduced in 128-bit fixed point (exact, order-free)
+__device__ void stat_add(unsigned long long *S, int slot, bool field, double x, double y,
+                         double z, double t, double v, const double *mean, int pass, int *ovf) {
+    unsigned act = __ballot_sync(0xffffffffu, slot >= 0);
+    int lane = threadIdx.x & 31;
+    while (act) {
+        int leader = __ffs(act) - 1;
+        int L = __shfl_sync(0xffffffffu, slot, leader);
+        bool mine = slot == L;
+        unsigned m = __ballot_sync(0xffffffffu, mine);
+        unsigned long long *s = S + (size_t)L * SW;
+        unsigned long long lo = 0;
+        long long hi = 0;
+        if (pass == 0) {
+            if (mine) d2fix(v, lo, hi, ovf);
+            warp_sum_fix(lo, hi);
+            double bl[4] = {x, y, z, t}, bh[4] = {x, y, z, t};
+            for (int d = 0; d < 4; ++d) {
+                double a = mine ? bl[d] : __builtin_huge_val();
+                double b = mine ? bh[d] : -__builtin_huge_val();
+                for (int o = 16; o > 0; o >>= 1) {
+                    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+                    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+                }
+                bl[d] = a;
+                bh[d] = b;
+            }
+            if (lane == leader) {
+                atomic_add_fix(s + (field ? 2 : 0), lo, hi);
+                atomicAdd(s + (field ? 9 : 8), (unsigned long long)__popc(m));
+                for (int d = 0; d < 4; ++d) {
+                    atomicMin(s + 10 + d, okey(bl[d]));
+                    atomicMax(s + 14 + d, okey(bh[d]));
+                }
+            }
+        } else {
+            if (mine) {
+                double dv = DSUB(v, mean[2 * L + (field ? 1 : 0)]);
+                d2fix(DMUL(dv, dv), lo, hi, ovf);
+            }
+            warp_sum_fix(lo, hi);
+            if (lane == leader) atomic_add_fix(s + (field ? 6 : 4), lo, hi);
+        }
+        act &= ~m;
+    }
+}
+
+struct StatArgs {
+    int n_slots;
+    long long nf, ncell;
+    int nx, ny, nz;
+    double ox, oy, oz, sx, sy, sz;
+    const double *times, *values;
+    const int *fslot;
+    long long np;
+    const double *xyz, *pt, *pv;
+    const int *pslot;
+    unsigned long long *S;
+    const double *mean;
+    int *ovf;
+};
+
+__global__ void k_stats(StatArgs a, int pass) {
+    long long total = a.nf + a.np;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = blockIdx.x * (long long)blockDim.x; base < total; base += stride) {
+        long long q = base + threadIdx.x;
+        int slot = -1;
+        bool field = q < a.nf;
+        double x = 0, y = 0, z = 0, t = 0, v = 0;
+        if (q < total) {
+            if (field) {
+                slot = a.fslot[q];
+                if (slot >= 0) {
+                    long long r = q % a.ncell;
+                    long long m = q / a.ncell;
+                    x = cell_coord(a.ox, a.sx, r % a.nx);
+                    y = cell_coord(a.oy, a.sy, (r / a.nx) % a.ny);
+                    z = cell_coord(a.oz, a.sz, r / ((long long)a.nx * a.ny));
+                    t = a.times[m];
+                    v = a.values[q];
+                }
+            } else {
+                long long p = q - a.nf;
+                slot = a.pslot[p];
+                if (slot >= 0) {
+                    x = a.xyz[3 * p];
+                    y = a.xyz[3 * p + 1];
+                    z = a.xyz[3 * p + 2];
+                    t = a.pt[p];
+                    v = a.pv[p];
+                }
+            }
+        }
+        // field and point lanes are aggregated separately
+        stat_add(a.S, field ? slot : -1, true, x, y, z, t, v, a.mean, pass, a.ovf);
+        stat_add(a.S, field ? -1 : slot, false, x, y, z, t, v, a.mean, pass, a.ovf);
+    }
+}
+
+__global__ void k_stats_means(int n_slots, const unsigned long long *S, double *mean) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_slots) return;
+    const unsigned long long *w = S + (size_t)s * SW;
+    long long np = (long long)w[8], nf = (long long)w[9];
+    mean[2 * s] = np ? DDIV(fix2d(w[0], (long long)w[1]), (double)np) : 0.0;
+    mean[2 * s + 1] = nf ? DDIV(fix2d(w[2], (long long)w[3]), (double)nf) : 0.0;
+}
+
+__global__ void k_stats_final(int n_slots, const unsigned long long *S, const double *mean,
+                              double *out) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_slots) return;
+    const unsigned long long *w = S + (size_t)s * SW;
+    double *o = out + (size_t)s * MFSEG_STAT_WORDS;
+    long long np = (long long)w[8], nf = (long long)w[9];
+    double nan = __longlong_as_double(0x7ff8000000000000ll);
+    for (int d = 0; d < 4; ++d) {
+        bool any = np + nf > 0;
+        o[d] = any ? unokey(w[10 + d]) : nan;
+        o[4 + d] = any ? unokey(w[14 + d]) : nan;
+    }
+    o[8] = np ? mean[2 * s] : nan;
+    o[9] = np ? DSQRT(DDIV(fix2d(w[4], (long long)w[5]), (double)np)) : nan;
+    o[10] = nf ? mean[2 * s + 1] : nan;
+    o[11] = nf ? DSQRT(DDIV(fix2d(w[6], (long long)w[7]), (double)nf)) : nan;
+    o[12] = (double)np;
+    o[13] = (double)nf;
+}
+
+__global__ void k_stats_init(int n_slots, unsigned long long *S) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_slots) return;
+    unsigned long long *w = S + (size_t)s * SW;
+    for (int i = 0; i < 10; ++i) w[i] = 0;
+    for (int d = 0; d < 4; ++d) {
+        w[10 + d] = ~0ull;
+        w[14 + d] = 0ull;
+    }
+}
+
+// ------------------------------------------------------------------ link index
+__global__ void k_link_keys(long long n, const double *xyz, const double *t, int nx, int ny,
+                            int nz, double ox, double oy, double oz, double sx, double sy,
+                            double sz, const double *times, int nt, unsigned long long *keys,
+                            unsigned *vals, int *bad) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double cx = floor(DDIV(DSUB(xyz[3 * i], ox), sx));
+    double cy = floor(DDIV(DSUB(xyz[3 * i + 1], oy), sy));
+    double cz = floor(DDIV(DSUB(xyz[3 * i + 2], oz), sz));
+    if (!(cx >= 0 && cx < nx && cy >= 0 && cy < ny && cz >= 0 && cz < nz)) {
+        *bad = 1;
+        cx = cy = cz = 0;
+    }
+    int n_int = nt - 1 > 1 ? nt - 1 : 1;
+    // searchsorted(times, t, 'right') - 1, clipped to [0, n_int-1]
+    int a = 0, b = nt;
+    double tv = t[i];
+    while (a < b) {
+        int mid = (a + b) >> 1;
+        if (times[mid] <= tv) a = mid + 1; else b = mid;
+    }
+    int m = a - 1;
+    if (m < 0) m = 0;
+    if (m > n_int - 1) m = n_int - 1;
+    long long flat = (((long long)cz * ny + (long long)cy) * nx + (long long)cx) * n_int + m;
+    keys[i] = (unsigned long long)flat;
+    vals[i] = (unsigned)i;
+}
+
+__global__ void k_count_runs(const unsigned long long *k, long long n, unsigned long long *cnt) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n && (i == 0 || k[i] != k[i - 1])) atomicAdd(cnt, 1ull);
+}
+
+int bits_of(unsigned long long v) {
+    int b = 1;
+    while (b < 64 && (1ull << b) <= v) ++b;
+    return b;
+}
+
+}  // namespace
+}  // namespace mfseg
+
+using namespace mfseg;
+
+extern "C" {
+
+size_t mfseg_merge_workspace_size(int32_t n) {
+    Carver cv;
+    cv.take<int>(n);          // parent
+    cv.take<int>(n);          // rep_row
+    cv.take<unsigned>(n);     // keys
+    cv.take<unsigned>(n);     // vals
+    cv.take<unsigned>(n);     // skeys
+    cv.take<unsigned>(n);     // members
+    cv.take<int>(n + 1);      // is_root
+    cv.take<int>(n + 1);      // group_of_root
+    cv.take<char>(radix_tmp_bytes(n > 0 ? n : 1));
+    cv.take<char>(scan_tmp_bytes(n + 1));
+    return cv.off + 256;
+}
+
+int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *p_c,
+                const double *f_c, const int64_t *n_points, const int64_t *n_fields, double eps_m,
+                int32_t *rep, int32_t *m_ids, double *m_loc, double *m_p, double *m_f,
+                int64_t *m_np, int64_t *m_nf, int32_t *n_merged_host, void *workspace,
+                size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) {
+        if (n_merged_host) *n_merged_host = 0;
+        return 0;
+    }
+    if (workspace_bytes < mfseg_merge_workspace_size(n)) {
+        set_error("merge: workspace too small");
+        return 3;
+    }
+    Carver cv(workspace, workspace_bytes);
+    int *parent = cv.take<int>(n);
+    int *rep_row = cv.take<int>(n);
+    unsigned *keys = cv.take<unsigned>(n);
+    unsigned *vals = cv.take<unsigned>(n);
+    unsigned *skeys = cv.take<unsigned>(n);
+    unsigned *members = cv.take<unsigned>(n);
+    int *is_root = cv.take<int>(n + 1);
+    int *group_of_root = cv.take<int>(n + 1);
+    size_t rb = radix_tmp_bytes(n);
+    void *rtmp = cv.take<char>(rb);
+    size_t sb = scan_tmp_bytes(n + 1);
+    void *stmp = cv.take<char>(sb);
+    unsigned g = (unsigned)((n + 255) / 256);
+    k_uf_init<<<g, 256, 0, st>>>(n, parent);
+    k_merge_pairs<<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, st>>>(n, p_c, f_c, eps_m,
+                                                                               parent);
+    MFSEG_CUDA(cudaMemsetAsync(is_root, 0, sizeof(int) * (n + 1), st));
+    k_uf_flatten<<<g, 256, 0, st>>>(n, parent, ids, rep_row, rep, keys, vals, is_root);
+    MFSEG_LAUNCH("merge union-find");
+    MFSEG_TRY(radix_sort_pairs(keys, vals, skeys, members, n, bits_of((unsigned)n), rtmp, rb, st));
+    MFSEG_TRY(scan_exclusive_i32(is_root, group_of_root, n + 1, stmp, sb, st));
+    int G = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&G, group_of_root + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    MergeOut o{m_ids, m_loc, m_p, m_f, (long long *)m_np, (long long *)m_nf};
+    k_merge_groups<<<g, 256, 0, st>>>(n, skeys, members, is_root, group_of_root, ids, loc, p_c,
+                                      f_c, (const long long *)n_points,
+                                      (const long long *)n_fields, o, G);
+    MFSEG_LAUNCH("k_merge_groups");
+    if (n_merged_host) *n_merged_host = G;
+    return 0;
+}
+
+int mfseg_relabel(const int32_t *labels, int64_t n, const int32_t *lut, int32_t lut_len,
+                  int32_t *out, void *stream) {
+    if (n <= 0) return 0;
+    k_relabel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(labels, n, lut, lut_len, out);
+    MFSEG_LAUNCH("k_relabel");
+    return 0;
+}
+
+size_t mfseg_voxel_csr_workspace_size(int64_t n, int32_t nt, int32_t n_slots) {
+    Carver cv;
+    cv.take<unsigned>(n);
+    cv.take<unsigned>(n);
+    cv.take<unsigned>(n);
+    cv.take<long long>((long long)nt * n_slots + 1);
+    cv.take<int>(4);
+    cv.take<char>(radix_tmp_bytes(n > 0 ? n : 1));
+    cv.take<char>(scan_tmp_bytes((long long)nt * n_slots + 1));
+    return cv.off + 256;
+}
+
+int mfseg_voxel_csr(const int32_t *flab, int32_t nt, int64_t ncell, const int32_t *slot_of,
+                    int32_t lut_len, int32_t n_slots, int64_t *seg_start, int32_t *cells,
+                    void *workspace, size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    long long n = (long long)nt * ncell;
+    long long nseg = (long long)nt * n_slots;
+    if (n <= 0) return 0;
+    if (n >= (1ll << 31) || nseg >= (1ll << 32)) {
+        set_error("voxel_csr: too many samples for one call; split by timestep");
+        return 2;
+    }
+    if (workspace_bytes < mfseg_voxel_csr_workspace_size(n, nt, n_slots)) {
+        set_error("voxel_csr: workspace too small");
+        return 3;
+    }
+    Carver cv(workspace, workspace_bytes);
+    unsigned *keys = cv.take<unsigned>(n);
+    unsigned *vals = cv.take<unsigned>(n);
+    unsigned *skeys = cv.take<unsigned>(n);
+    long long *cnt = cv.take<long long>(nseg + 1);
+    int *bad = cv.take<int>(4);
+    size_t rb = radix_tmp_bytes(n);
+    void *rtmp = cv.take<char>(rb);
+    size_t sb = scan_tmp_bytes(nseg + 1);
+    void *stmp = cv.take<char>(sb);
+    MFSEG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    MFSEG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(long long) * (nseg + 1), st));
+    k_voxel_keys<<<148 * 8, 256, 0, st>>>(flab, n, ncell, slot_of, lut_len, n_slots, keys, vals,
+                                          bad);
+    MFSEG_LAUNCH("k_voxel_keys");
+    MFSEG_TRY(radix_sort_pairs(keys, vals, skeys, (unsigned *)cells, n, bits_of((unsigned long long)nseg),
+                               rtmp, rb, st));
+    k_key_hist<<<148 * 8, 256, 0, st>>>(skeys, n, cnt);
+    MFSEG_TRY(scan_exclusive_i64(cnt, (long long *)seg_start, nseg + 1, stmp, sb, st));
+    int hb = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (hb) {
+        set_error("voxel_csr: a field label has no feature slot");
+        return 2;
+    }
+    return 0;
+}
+
+size_t mfseg_feature_stats_workspace_size(int32_t n_slots) {
+    Carver cv;
+    cv.take<unsigned long long>((long long)n_slots * SW);
+    cv.take<double>(2ll * n_slots);
+    cv.take<int>(4);
+    return cv.off + 256;
+}
+
+int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
+                        const mfseg_points *pts, const int32_t *point_slot, double *stats,
+                        void *workspace, size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_slots <= 0) return 0;
+    if (workspace_bytes < mfseg_feature_stats_workspace_size(n_slots)) {
+        set_error("feature_stats: workspace too small");
+        return 3;
+    }
+    Carver cv(workspace, workspace_bytes);
+    StatArgs a;
+    memset(&a, 0, sizeof a);
+    a.n_slots = n_slots;
+    a.S = cv.take<unsigned long long>((long long)n_slots * SW);
+    double *mean = cv.take<double>(2ll * n_slots);
+    a.mean = mean;
+    a.ovf = cv.take<int>(4);
+    if (f && f->nt > 0 && field_slot) {
+        a.ncell = (long long)f->nx * f->ny * f->nz;
+        a.nf = a.ncell * f->nt;
+        a.nx = f->nx;
+        a.ny = f->ny;
+        a.nz = f->nz;
+        a.ox = f->origin[0];
+        a.oy = f->origin[1];
+        a.oz = f->origin[2];
+        a.sx = f->spacing[0];
+        a.sy = f->spacing[1];
+        a.sz = f->spacing[2];
+        a.times = f->times;
+        a.values = f->values;
+        a.fslot = field_slot;
+    }
+    if (pts && pts->n > 0 && point_slot) {
+        a.np = pts->n;
+        a.xyz = pts->xyz;
+        a.pt = pts->t;
+        a.pv = pts->value;
+        a.pslot = point_slot;
+    }
+    unsigned gs = (unsigned)((n_slots + 255) / 256);
+    MFSEG_CUDA(cudaMemsetAsync(a.ovf, 0, sizeof(int), st));
+    k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
+    k_stats<<<148 * 8, 256, 0, st>>>(a, 0);
+    k_stats_means<<<gs, 256, 0, st>>>(n_slots, a.S, mean);
+    k_stats<<<148 * 8, 256, 0, st>>>(a, 1);
+    k_stats_final<<<gs, 256, 0, st>>>(n_slots, a.S, mean, stats);
+    MFSEG_LAUNCH("feature_stats");
+    int h = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&h, a.ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (h) {
+        set_error("feature_stats: fixed-point overflow");
+        return 4;
+    }
+    return 0;
+}
+
+size_t mfseg_link_index_workspace_size(int64_t n) {
+    Carver cv;
+    cv.take<unsigned long long>(n);
+    cv.take<unsigned>(n);
+    cv.take<unsigned long long>(2);
+    cv.take<int>(4);
+    cv.take<char>(radix_tmp_bytes(n > 0 ? n : 1));
+    return cv.off + 256;
+}
+
+int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *keys, int32_t *members,
+                     int64_t *n_buckets_host, void *workspace, size_t workspace_bytes,
+                     void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    long long n = pts ? pts->n : 0;
+    if (n_buckets_host) *n_buckets_host = 0;
+    if (n <= 0) return 0;
+    if (workspace_bytes < mfseg_link_index_workspace_size(n)) {
+        set_error("link_index: workspace too small");
+        return 3;
+    }
+    Carver cv(workspace, workspace_bytes);
+    unsigned long long *k0 = cv.take<unsigned long long>(n);
+    unsigned *v0 = cv.take<unsigned>(n);
+    unsigned long long *cnt = cv.take<unsigned long long>(2);
+    int *bad = cv.take<int>(4);
+    size_t rb = radix_tmp_bytes(n);
+    void *rtmp = cv.take<char>(rb);
+    MFSEG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    MFSEG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    unsigned g = (unsigned)((n + 255) / 256);
+    k_link_keys<<<g, 256, 0, st>>>(n, pts->xyz, pts->t, f->nx, f->ny, f->nz, f->origin[0],
+                                   f->origin[1], f->origin[2], f->spacing[0], f->spacing[1],
+                                   f->spacing[2], f->times, f->nt, k0, v0, bad);
+    MFSEG_LAUNCH("k_link_keys");
+    int n_int = f->nt - 1 > 1 ? f->nt - 1 : 1;
+    unsigned long long maxkey = (unsigned long long)f->nx * f->ny * f->nz * n_int;
+    MFSEG_TRY(radix_sort_pairs64(k0, v0, (unsigned long long *)keys, (unsigned *)members, n,
+                                 bits_of(maxkey), rtmp, rb, st));
+    k_count_runs<<<g, 256, 0, st>>>((const unsigned long long *)keys, n, cnt);
+    MFSEG_LAUNCH("k_count_runs");
+    int hb = 0;
+    unsigned long long nb = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaMemcpyAsync(&nb, cnt, sizeof(nb), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (hb) {
+        set_error("point sample outside the field grid; filter_to_grid first");
+        return 2;
+    }
+    if (n_buckets_host) *n_buckets_host = (int64_t)nb;
+    return 0;
+}
+
+}  // extern "C"

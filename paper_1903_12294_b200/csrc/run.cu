@@ -1,0 +1,731 @@
+// Host-side runtime of the segmentation core: workspace plan, point binning,
+// field tiling, the pass loop of engine.run (engine.py:323-381) and the C ABI.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace mfseg {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+int fail(const char *where, cudaError_t e) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return 1;
+}
+
+}  // namespace mfseg
+
+namespace mfseg {
+namespace {
+
+// ------------------------------------------------------------------ small kernels
+__global__ void k_seed(int K, double4 mins, double4 C, int4 k, mfseg_centers s) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= K) return;
+    int ix = c % k.x, r = c / k.x;
+    int iy = r % k.y;
+    r /= k.y;
+    int iz = r % k.z, it = r / k.z;
+    // mins[d] + (j + 0.5) * C[d]   (engine.py:38)
+    s.loc[c] = DADD(mins.x, DMUL((double)ix + 0.5, C.x));
+    s.loc[K + c] = DADD(mins.y, DMUL((double)iy + 0.5, C.y));
+    s.loc[2 * K + c] = DADD(mins.z, DMUL((double)iz + 0.5, C.z));
+    s.loc[3 * K + c] = DADD(mins.w, DMUL((double)it + 0.5, C.w));
+    double nan = __longlong_as_double(0x7ff8000000000000ll);
+    s.pval[c] = nan;
+    s.fval[c] = nan;
+    s.has_p[c] = s.has_f[c] = s.dormant[c] = 0;
+    s.n_points[c] = s.n_fields[c] = 0;
+}
+
+__global__ void k_tbins(int nt, const double *times, double mn, double C, int k, int *tbin) {
+    int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < nt) tbin[m] = bin_coord(times[m], mn, C, k);
+}
+
+__global__ void k_point_keys(long long n, const double *xyz, const double *t, double4 mins,
+                             double4 C, int4 k, unsigned *keys, unsigned *vals) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int bx = bin_coord(xyz[3 * i], mins.x, C.x, k.x);
+    int by = bin_coord(xyz[3 * i + 1], mins.y, C.y, k.y);
+    int bz = bin_coord(xyz[3 * i + 2], mins.z, C.z, k.z);
+    int bt = bin_coord(t[i], mins.w, C.w, k.w);
+    keys[i] = (unsigned)(((bt * k.z + bz) * k.y + by) * k.x + bx);
+    vals[i] = (unsigned)i;
+}
+
+__global__ void k_point_gather(long long n, const unsigned *perm, const double *xyz,
+                               const double *t, const double *value, double *px, double *py,
+                               double *pz, double *pt, double *pv) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long j = perm[i];
+    px[i] = xyz[3 * j];
+    py[i] = xyz[3 * j + 1];
+    pz[i] = xyz[3 * j + 2];
+    pt[i] = t[j];
+    pv[i] = value[j];
+}
+
+__global__ void k_bin_hist(long long n, const unsigned *skeys, int *cnt) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[skeys[i]], 1);
+}
+
+__global__ void k_tiles_per_bin(int nb, const int *cnt, int tp, int *ntiles) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nb) ntiles[b] = (cnt[b] + tp - 1) / tp;
+}
+
+__global__ void k_make_tiles(int nb, const int *cnt, const int *first, const int *tstart, int tp,
+                             int4 *tiles) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int n = cnt[b], f = first[b], o = tstart[b];
+    for (int q = 0; q * tp < n; ++q) tiles[o + q] = make_int4(b, f + q * tp, min(tp, n - q * tp), 0);
+}
+
+__global__ void k_unpermute(long long n, const unsigned *perm, const int *src, int *dst) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) dst[perm[i]] = src[i];
+}
+
+__global__ void k_copy_state(int K, mfseg_centers s, mfseg_centers d) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= K) return;
+    for (int q = 0; q < 4; ++q) d.loc[q * K + c] = s.loc[q * K + c];
+    d.pval[c] = s.pval[c];
+    d.fval[c] = s.fval[c];
+    d.has_p[c] = s.has_p[c];
+    d.has_f[c] = s.has_f[c];
+    d.dormant[c] = s.dormant[c];
+    d.n_points[c] = s.n_points[c];
+    d.n_fields[c] = s.n_fields[c];
+}
+
+__global__ void k_minmax(const double *v, long long n, unsigned long long *mm) {
+    // mm[0] = ordered-bits min, mm[1] = ordered-bits max (total order on doubles)
+    double lo = __builtin_huge_val(), hi = -__builtin_huge_val();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double x = v[i];
+        lo = fmin(lo, x);
+        hi = fmax(hi, x);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        auto key = [](double d) {
+            unsigned long long b = (unsigned long long)__double_as_longlong(d);
+            return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+        };
+        atomicMin(&mm[0], key(lo));
+        atomicMax(&mm[1], key(hi));
+    }
+}
+
+__global__ void k_normalize(double *v, long long n, double lo, double span, int degenerate) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        v[i] = degenerate ? 0.0 : DDIV(DSUB(v[i], lo), span);
+}
+
+double unkey(unsigned long long b) {
+    unsigned long long r = (b >> 63) ? (b & 0x7fffffffffffffffull) : ~b;
+    double d;
+    memcpy(&d, &r, sizeof d);
+    return d;
+}
+
+int bits_for(long long maxval) {
+    int b = 1;
+    while ((1ll << b) <= maxval) ++b;
+    return b;
+}
+
+// ------------------------------------------------------------------ plan
+struct State {                 // device centre state buffers (length K)
+    mfseg_centers v;
+};
+
+struct Plan {
+    mfseg_params p;
+    mfseg_field f;
+    mfseg_points pts;
+    int K;
+    long long nf, np;
+    cudaStream_t st;
+    // centre state ping-pong
+    mfseg_centers s[2];
+    unsigned long long *acc;
+    long long *limbs;
+    void *flags;
+    // grid
+    Grid g;
+    int *count_tmp;
+    void *grid_scan_tmp;
+    // field
+    AxisTile *xt, *yt, *zt;
+    int ntx, nty, ntz;
+    int *tbin;
+    long long *stranded_f;
+    long long cap_f;
+    unsigned long long *counters;   // [0] field stranded, [1] point stranded
+    int *overflow;
+    // points
+    unsigned *keys, *vals, *skeys, *perm;
+    double *px, *py, *pz, *pt, *pv;
+    int *plabels;                   // bin-sorted labels
+    int *bcnt, *bfirst, *btiles, *tstart;
+    int4 *tiles;
+    long long max_tiles;
+    long long *stranded_p;
+    long long cap_p;
+    void *radix_tmp;
+    size_t radix_bytes;
+    void *scan_tmp;
+    size_t scan_bytes;
+};
+
+std::vector<AxisTile> axis_tiles(int n, double o, double s, double mn, double C, int k, int T) {
+    std::vector<AxisTile> v;
+    int i = 0;
+    while (i < n) {
+        int b = bin_coord(cell_coord(o, s, i), mn, C, k);
+        int j = i;
+        while (j < n && j - i < T && bin_coord(cell_coord(o, s, j), mn, C, k) == b) ++j;
+        v.push_back(AxisTile{i, j - i, b, 0});
+        i = j;
+    }
+    return v;
+}
+
+long long axis_tile_count(int n, double o, double s, double mn, double C, int k, int T) {
+    return (long long)axis_tiles(n, o, s, mn, C, k, T).size();
+}
+
+int check_inputs(const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts) {
+    if (!p) {
+        set_error("params is NULL");
+        return 2;
+    }
+    for (int d = 0; d < 4; ++d)
+        if (p->k[d] < 1 || !(p->C[d] > 0)) {
+            set_error("invalid k or C (k must be >= 1, C > 0)");
+            return 2;
+        }
+    long long K = (long long)p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    if (K > (1ll << 26)) {
+        set_error("too many clusters (K > 2^26)");
+        return 2;
+    }
+    if (f && f->nt > 0 && (f->nx < 1 || f->ny < 1 || f->nz < 1)) {
+        set_error("invalid field dims");
+        return 2;
+    }
+    if (pts && pts->n >= (1ll << 31)) {
+        set_error("more than 2^31-1 point samples on one GPU; shard the points");
+        return 2;
+    }
+    return 0;
+}
+
+// Carve every buffer; with base == nullptr only sizes are computed.
+size_t plan_carve(Plan &P, void *ws, size_t bytes) {
+    Carver cv(ws, bytes);
+    int K = P.K;
+    for (int q = 0; q < 2; ++q) {
+        P.s[q].loc = cv.take<double>(4ll * K);
+        P.s[q].pval = cv.take<double>(K);
+        P.s[q].fval = cv.take<double>(K);
+        P.s[q].has_p = cv.take<uint8_t>(K);
+        P.s[q].has_f = cv.take<uint8_t>(K);
+        P.s[q].dormant = cv.take<uint8_t>(K);
+        P.s[q].n_points = cv.take<int64_t>(K);
+        P.s[q].n_fields = cv.take<int64_t>(K);
+    }
+    P.acc = cv.take<unsigned long long>((long long)K * MFSEG_ACC_WORDS);
+    P.limbs = cv.take<long long>((long long)K * MFSEG_ACC_WORDS / 2 * 3);
+    P.flags = cv.take<char>(update_flags_bytes());
+    P.g = grid_carve(cv, K, &P.count_tmp, &P.grid_scan_tmp);
+    P.counters = cv.take<unsigned long long>(4);
+    P.overflow = cv.take<int>(4);
+    // field
+    P.nf = (P.f.nt > 0) ? (long long)P.f.nx * P.f.ny * P.f.nz * P.f.nt : 0;
+    int TX, TY, TZ;
+    field_tile_dims(&TX, &TY, &TZ);
+    P.ntx = P.nty = P.ntz = 0;
+    if (P.nf > 0) {
+        P.ntx = (int)axis_tile_count(P.f.nx, P.f.origin[0], P.f.spacing[0], P.p.mins[0], P.p.C[0],
+                                     P.p.k[0], TX);
+        P.nty = (int)axis_tile_count(P.f.ny, P.f.origin[1], P.f.spacing[1], P.p.mins[1], P.p.C[1],
+                                     P.p.k[1], TY);
+        P.ntz = (int)axis_tile_count(P.f.nz, P.f.origin[2], P.f.spacing[2], P.p.mins[2], P.p.C[2],
+                                     P.p.k[2], TZ);
+    }
+    P.xt = cv.take<AxisTile>(P.ntx);
+    P.yt = cv.take<AxisTile>(P.nty);
+    P.zt = cv.take<AxisTile>(P.ntz);
+    P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
+    P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
+    P.stranded_f = cv.take<long long>(P.cap_f);
+    // points
+    long long n = P.np;
+    int TP = point_tile_size();
+    P.keys = cv.take<unsigned>(n);
+    P.vals = cv.take<unsigned>(n);
+    P.skeys = cv.take<unsigned>(n);
+    P.perm = cv.take<unsigned>(n);
+    P.px = cv.take<double>(n);
+    P.py = cv.take<double>(n);
+    P.pz = cv.take<double>(n);
+    P.pt = cv.take<double>(n);
+    P.pv = cv.take<double>(n);
+    P.plabels = cv.take<int>(n);
+    P.bcnt = cv.take<int>(K + 1);
+    P.bfirst = cv.take<int>(K + 1);
+    P.btiles = cv.take<int>(K + 1);
+    P.tstart = cv.take<int>(K + 1);
+    P.max_tiles = n > 0 ? (n + TP - 1) / TP + K : 0;
+    P.tiles = cv.take<int4>(P.max_tiles);
+    P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
+    P.stranded_p = cv.take<long long>(P.cap_p);
+    P.radix_bytes = n > 0 ? radix_tmp_bytes(n) : 0;
+    P.radix_tmp = cv.take<char>(P.radix_bytes);
+    P.scan_bytes = scan_tmp_bytes((long long)K + 1) + 1024;
+    P.scan_tmp = cv.take<char>(P.scan_bytes);
+    return cv.off + 1024;
+}
+
+int plan_init(Plan &P, const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts,
+              void *ws, size_t bytes, cudaStream_t st) {
+    MFSEG_TRY(check_inputs(p, f, pts));
+    memset(&P, 0, sizeof P);
+    P.p = *p;
+    if (f) P.f = *f;
+    if (pts) P.pts = *pts;
+    P.K = p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    P.np = pts ? pts->n : 0;
+    P.st = st;
+    size_t need = plan_carve(P, nullptr, 0);
+    if (!ws || bytes < need) {
+        set_error("workspace too small: need " + std::to_string(need) + " bytes");
+        return 3;
+    }
+    plan_carve(P, ws, bytes);
+    return 0;
+}
+
+// once per run: field axis tiles, timestep bins, point binning + sort + tiles
+int plan_prepare(Plan &P) {
+    cudaStream_t st = P.st;
+    const mfseg_params &p = P.p;
+    if (P.nf > 0) {
+        int TX, TY, TZ;
+        field_tile_dims(&TX, &TY, &TZ);
+        auto xt = axis_tiles(P.f.nx, P.f.origin[0], P.f.spacing[0], p.mins[0], p.C[0], p.k[0], TX);
+        auto yt = axis_tiles(P.f.ny, P.f.origin[1], P.f.spacing[1], p.mins[1], p.C[1], p.k[1], TY);
+        auto zt = axis_tiles(P.f.nz, P.f.origin[2], P.f.spacing[2], p.mins[2], p.C[2], p.k[2], TZ);
+        MFSEG_CUDA(cudaMemcpyAsync(P.xt, xt.data(), sizeof(AxisTile) * xt.size(),
+                                   cudaMemcpyHostToDevice, st));
+        MFSEG_CUDA(cudaMemcpyAsync(P.yt, yt.data(), sizeof(AxisTile) * yt.size(),
+                                   cudaMemcpyHostToDevice, st));
+        MFSEG_CUDA(cudaMemcpyAsync(P.zt, zt.data(), sizeof(AxisTile) * zt.size(),
+                                   cudaMemcpyHostToDevice, st));
+        MFSEG_CUDA(cudaStreamSynchronize(st));   // host vectors die at scope exit
+        k_tbins<<<(P.f.nt + 255) / 256, 256, 0, st>>>(P.f.nt, P.f.times, p.mins[3], p.C[3],
+                                                        p.k[3], P.tbin);
+        MFSEG_LAUNCH("k_tbins");
+    }
+    long long n = P.np;
+    if (n > 0) {
+        double4 mins = make_double4(p.mins[0], p.mins[1], p.mins[2], p.mins[3]);
+        double4 C = make_double4(p.C[0], p.C[1], p.C[2], p.C[3]);
+        int4 k = make_int4(p.k[0], p.k[1], p.k[2], p.k[3]);
+        unsigned gb = (unsigned)((n + 255) / 256);
+        k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, k, P.keys, P.vals);
+        MFSEG_LAUNCH("k_point_keys");
+        MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, bits_for(P.K - 1),
+                                   P.radix_tmp, P.radix_bytes, st));
+        k_point_gather<<<gb, 256, 0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px,
+                                           P.py, P.pz, P.pt, P.pv);
+        MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (P.K + 1), st));
+        k_bin_hist<<<gb, 256, 0, st>>>(n, P.skeys, P.bcnt);
+        MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, P.K + 1, P.scan_tmp, P.scan_bytes, st));
+        int TP = point_tile_size();
+        unsigned gk = (unsigned)((P.K + 256) / 256);
+        MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (P.K + 1), st));
+        k_tiles_per_bin<<<gk, 256, 0, st>>>(P.K, P.bcnt, TP, P.btiles);
+        MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, P.K + 1, P.scan_tmp, P.scan_bytes, st));
+        k_make_tiles<<<gk, 256, 0, st>>>(P.K, P.bcnt, P.bfirst, P.tstart, TP, P.tiles);
+        MFSEG_LAUNCH("point tiles");
+    }
+    return 0;
+}
+
+CentersView view_of(const mfseg_centers &s, int K) {
+    CentersView v;
+    v.x = s.loc;
+    v.y = s.loc + K;
+    v.z = s.loc + 2ll * K;
+    v.t = s.loc + 3ll * K;
+    v.pval = s.pval;
+    v.fval = s.fval;
+    v.has_p = s.has_p;
+    v.has_f = s.has_f;
+    return v;
+}
+
+// one assignment pass for centre state `c` (grid rebuilt here)
+int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, int32_t *flabels,
+              int accumulate) {
+    cudaStream_t st = P.st;
+    const mfseg_params &p = P.p;
+    int K = P.K;
+    CentersView cv = view_of(c, K);
+    MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
+                         P.count_tmp, P.grid_scan_tmp, st));
+    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 4, st));
+    if (accumulate)
+        MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
+    if (P.nf > 0) {
+        FieldArgs a;
+        memset(&a, 0, sizeof a);
+        a.nx = P.f.nx;
+        a.ny = P.f.ny;
+        a.nz = P.f.nz;
+        a.nt = P.f.nt;
+        a.ox = P.f.origin[0];
+        a.oy = P.f.origin[1];
+        a.oz = P.f.origin[2];
+        a.sx = P.f.spacing[0];
+        a.sy = P.f.spacing[1];
+        a.sz = P.f.spacing[2];
+        a.times = P.f.times;
+        a.values = P.f.values;
+        a.xt = P.xt;
+        a.yt = P.yt;
+        a.zt = P.zt;
+        a.ntx = P.ntx;
+        a.nty = P.nty;
+        a.ntz = P.ntz;
+        a.tbin = P.tbin;
+        a.kx = p.k[0];
+        a.ky = p.k[1];
+        a.kz = p.k[2];
+        a.kt = p.k[3];
+        a.cf = p.c_f;
+        a.wd = wd;
+        a.wv = wf;
+        a.c = cv;
+        a.cval = c.fval;
+        a.chas = c.has_f;
+        a.g = P.g;
+        a.labels = flabels;
+        a.acc = P.acc;
+        a.stranded = P.stranded_f;
+        a.n_stranded = P.counters;
+        a.stranded_cap = P.cap_f;
+        a.overflow = P.overflow;
+        a.accumulate = accumulate;
+        long long ntiles = (long long)P.ntx * P.nty * P.ntz * P.f.nt;
+        MFSEG_TRY(launch_field_assign(a, ntiles, st));
+    }
+    if (P.np > 0) {
+        PointArgs a;
+        memset(&a, 0, sizeof a);
+        a.n = P.np;
+        a.x = P.px;
+        a.y = P.py;
+        a.z = P.pz;
+        a.t = P.pt;
+        a.v = P.pv;
+        a.tiles = P.tiles;
+        a.n_tiles = P.tstart + K;
+        a.Cx = p.C[0];
+        a.Cy = p.C[1];
+        a.Cz = p.C[2];
+        a.Ct = p.C[3];
+        a.cf = p.c_f;
+        a.wd = wd;
+        a.wv = wp;
+        a.c = cv;
+        a.cval = c.pval;
+        a.chas = c.has_p;
+        a.g = P.g;
+        a.labels = P.plabels;
+        a.acc = P.acc;
+        a.stranded = P.stranded_p;
+        a.n_stranded = P.counters + 1;
+        a.stranded_cap = P.cap_p;
+        a.overflow = P.overflow;
+        a.accumulate = accumulate;
+        MFSEG_TRY(launch_point_assign(a, P.max_tiles, st));
+    }
+    // stranded samples
+    for (int kind = 0; kind < 2; ++kind) {
+        if (kind == 1 && P.nf == 0) continue;
+        if (kind == 0 && P.np == 0) continue;
+        FallbackArgs a;
+        memset(&a, 0, sizeof a);
+        a.K = K;
+        a.c = cv;
+        a.cval = kind == 1 ? c.fval : c.pval;
+        a.chas = kind == 1 ? c.has_f : c.has_p;
+        for (int d = 0; d < 4; ++d) a.C[d] = p.C[d];
+        a.cf = p.c_f;
+        a.wd = wd;
+        a.wv = kind == 1 ? wf : wp;
+        a.kind = kind;
+        a.nx = P.f.nx;
+        a.ny = P.f.ny;
+        a.nz = P.f.nz;
+        a.nt = P.f.nt;
+        a.ox = P.f.origin[0];
+        a.oy = P.f.origin[1];
+        a.oz = P.f.origin[2];
+        a.sx = P.f.spacing[0];
+        a.sy = P.f.spacing[1];
+        a.sz = P.f.spacing[2];
+        a.times = P.f.times;
+        a.values = P.f.values;
+        a.px = P.px;
+        a.py = P.py;
+        a.pz = P.pz;
+        a.pt = P.pt;
+        a.pv = P.pv;
+        a.n_samples = kind == 1 ? P.nf : P.np;
+        a.labels = kind == 1 ? flabels : P.plabels;
+        a.stranded = kind == 1 ? P.stranded_f : P.stranded_p;
+        a.n_stranded = P.counters + (kind == 1 ? 0 : 1);
+        a.cap = kind == 1 ? P.cap_f : P.cap_p;
+        a.acc = P.acc;
+        a.overflow = P.overflow;
+        a.accumulate = accumulate;
+        MFSEG_TRY(launch_fallback(a, st));
+    }
+    return 0;
+}
+
+int check_overflow(Plan &P) {
+    int ov = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&ov, P.overflow, sizeof(int), cudaMemcpyDeviceToHost, P.st));
+    MFSEG_CUDA(cudaStreamSynchronize(P.st));
+    if (ov) {
+        set_error(ov == 1 ? "fixed-point accumulator overflow (|coordinate| too large)"
+                          : "internal error in assignment (code " + std::to_string(ov) + ")");
+        return 4;
+    }
+    return 0;
+}
+
+}  // namespace
+}  // namespace mfseg
+
+using namespace mfseg;
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *mfseg_last_error(void) { return mfseg::g_err.c_str(); }
+int mfseg_abi_version(void) { return MFSEG_ABI_VERSION; }
+
+size_t mfseg_run_workspace_size(const mfseg_params *p, const mfseg_field *f,
+                                const mfseg_points *pts) {
+    if (check_inputs(p, f, pts)) return 0;
+    Plan P;
+    memset(&P, 0, sizeof P);
+    P.p = *p;
+    if (f) P.f = *f;
+    if (pts) P.pts = *pts;
+    P.K = p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    P.np = pts ? pts->n : 0;
+    return plan_carve(P, nullptr, 0);
+}
+
+size_t mfseg_assign_workspace_size(const mfseg_params *p, const mfseg_field *f,
+                                   const mfseg_points *pts) {
+    return mfseg_run_workspace_size(p, f, pts);
+}
+
+int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts,
+              int32_t *point_labels, int32_t *field_labels, mfseg_centers out,
+              int32_t *iterations_used_host, int32_t *converged_host, mfseg_progress_fn progress,
+              void *progress_user, mfseg_reduce_fn reduce, void *reduce_user, void *workspace,
+              size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    Plan P;
+    MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
+    if (P.nf == 0 && P.np == 0) {
+        set_error("no samples of either kind");
+        return 2;
+    }
+    int K = P.K;
+    MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
+    MFSEG_TRY(plan_prepare(P));
+    double4 mins = make_double4(p->mins[0], p->mins[1], p->mins[2], p->mins[3]);
+    double4 C = make_double4(p->C[0], p->C[1], p->C[2], p->C[3]);
+    int4 k = make_int4(p->k[0], p->k[1], p->k[2], p->k[3]);
+    unsigned gk = (unsigned)((K + 255) / 256);
+    k_seed<<<gk, 256, 0, st>>>(K, mins, C, k, P.s[0]);
+    MFSEG_LAUNCH("k_seed");
+    int cur = 0;
+    int iterations = 0, converged = 0;
+    alignas(16) char flags_host[64];
+    for (int pass = 0; pass <= p->max_iterations; ++pass) {
+        bool initial = pass == 0;
+        // initial assignment: pure space-time nearest seed (engine.py:346-351)
+        double wd = initial ? 1.0 : p->w_d, wp = initial ? 0.0 : p->w_p, wf = initial ? 0.0 : p->w_f;
+        MFSEG_TRY(plan_pass(P, P.s[cur], wd, wp, wf, field_labels, 1));
+        if (reduce) {
+            long long npairs = (long long)K * MFSEG_ACC_WORDS / 2;
+            MFSEG_TRY(launch_to_limbs(npairs, P.acc, P.limbs, st));
+            int rc = reduce(reduce_user, (int64_t *)P.limbs, npairs * 3, stream);
+            if (rc) {
+                set_error("reduce callback failed");
+                return 5;
+            }
+            MFSEG_TRY(launch_from_limbs(npairs, P.limbs, P.acc, st));
+        }
+        MFSEG_TRY(launch_update(K, P.acc, P.s[cur], P.s[cur ^ 1], p->eps_c, P.flags, st));
+        cur ^= 1;
+        if (initial) continue;
+        MFSEG_CUDA(cudaMemcpyAsync(flags_host, P.flags, update_flags_bytes(),
+                                   cudaMemcpyDeviceToHost, st));
+        MFSEG_CUDA(cudaStreamSynchronize(st));
+        double delta;
+        decode_flags(flags_host, &converged, &delta);
+        iterations = pass;
+        if (progress) progress(progress_user, pass, delta);
+        if (converged) break;
+    }
+    MFSEG_TRY(check_overflow(P));
+    if (P.np > 0) {
+        k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,
+                                                                     point_labels);
+        MFSEG_LAUNCH("k_unpermute");
+    }
+    k_copy_state<<<gk, 256, 0, st>>>(K, P.s[cur], out);
+    MFSEG_LAUNCH("k_copy_state");
+    if (iterations_used_host) *iterations_used_host = iterations;
+    if (converged_host) *converged_host = converged;
+    return 0;
+}
+
+int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts,
+                 mfseg_centers centers, int32_t *point_labels, int32_t *field_labels,
+                 int64_t *acc, void *workspace, size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    Plan P;
+    MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
+    MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
+    MFSEG_TRY(plan_prepare(P));
+    MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1));
+    if (P.np > 0) {
+        k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,
+                                                                     point_labels);
+        MFSEG_LAUNCH("k_unpermute");
+    }
+    if (acc)
+        MFSEG_CUDA(cudaMemcpyAsync(acc, P.acc, sizeof(int64_t) * P.K * MFSEG_ACC_WORDS,
+                                   cudaMemcpyDeviceToDevice, st));
+    return check_overflow(P);
+}
+
+int mfseg_accumulate(int32_t K, const mfseg_field *f, const mfseg_points *pts,
+                     const int32_t *point_labels, const int32_t *field_labels, int64_t *acc,
+                     void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int *ovf = nullptr;
+    MFSEG_CUDA(cudaMallocAsync((void **)&ovf, sizeof(int), st));
+    MFSEG_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    MFSEG_CUDA(cudaMemsetAsync(acc, 0, sizeof(int64_t) * K * MFSEG_ACC_WORDS, st));
+    if (pts && pts->n > 0)
+        MFSEG_TRY(launch_accumulate_points(pts, point_labels, (unsigned long long *)acc, ovf, st));
+    if (f && f->nt > 0) {
+        long long n = (long long)f->nx * f->ny * f->nz * f->nt;
+        MFSEG_TRY(launch_accumulate_field(n, f, field_labels, (unsigned long long *)acc, ovf, st));
+    }
+    int h = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&h, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaFreeAsync(ovf, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (h) {
+        set_error("fixed-point accumulator overflow");
+        return 4;
+    }
+    return 0;
+}
+
+int mfseg_acc_to_double(int32_t K, const int64_t *acc, double *sums, double *psum, double *fsum,
+                        int64_t *n_p, int64_t *n_f, void *stream) {
+    return launch_acc_to_double(K, (const unsigned long long *)acc, sums, psum, fsum,
+                                (long long *)n_p, (long long *)n_f, (cudaStream_t)stream);
+}
+
+int mfseg_update_centers(int32_t K, const int64_t *acc, mfseg_centers old_state,
+                         mfseg_centers new_state, double eps_c, int32_t *conv_host,
+                         double *delta_host, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    void *flags = nullptr;
+    MFSEG_CUDA(cudaMallocAsync(&flags, 64, st));
+    MFSEG_TRY(launch_update(K, (const unsigned long long *)acc, old_state, new_state, eps_c,
+                            flags, st));
+    alignas(16) char h[64];
+    MFSEG_CUDA(cudaMemcpyAsync(h, flags, update_flags_bytes(), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaFreeAsync(flags, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    int conv;
+    double delta;
+    decode_flags(h, &conv, &delta);
+    if (conv_host) *conv_host = conv;
+    if (delta_host) *delta_host = delta;
+    return 0;
+}
+
+int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_host,
+                           double *hi_host, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) {
+        set_error("minmax of an empty array");
+        return 2;
+    }
+    unsigned long long *mm = nullptr;
+    MFSEG_CUDA(cudaMallocAsync((void **)&mm, 16, st));
+    unsigned long long init[2] = {~0ull, 0ull};
+    MFSEG_CUDA(cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
+    k_minmax<<<148 * 4, 256, 0, st>>>(values, n, mm);
+    MFSEG_LAUNCH("k_minmax");
+    unsigned long long h[2];
+    MFSEG_CUDA(cudaMemcpyAsync(h, mm, 16, cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaFreeAsync(mm, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    double lo = unkey(h[0]), hi = unkey(h[1]);
+    if (lo_host) *lo_host = lo;
+    if (hi_host) *hi_host = hi;
+    if (apply) {
+        // (v - lo) / (hi - lo); degenerate range maps to 0 (ingest.py:312-318)
+        volatile double span = hi - lo;
+        k_normalize<<<148 * 8, 256, 0, st>>>(values, n, lo, span, hi == lo);
+        MFSEG_LAUNCH("k_normalize");
+    }
+    return 0;
+}
+
+int mfseg_acc_to_limbs(const int64_t *acc, int64_t n_pairs, int64_t *limbs, void *stream) {
+    return launch_to_limbs(n_pairs, (const unsigned long long *)acc, (long long *)limbs,
+                           (cudaStream_t)stream);
+}
+
+int mfseg_limbs_to_acc(const int64_t *limbs, int64_t n_pairs, int64_t *acc, void *stream) {
+    return launch_from_limbs(n_pairs, (const long long *)limbs, (unsigned long long *)acc,
+                             (cudaStream_t)stream);
+}
+
+}  // extern "C"

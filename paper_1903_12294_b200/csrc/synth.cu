@@ -1,0 +1,164 @@
+// Counter-based synthetic inputs for the benchmark configurations.
+//
+// Same spirit as the reference's generator (drifting blobs over a background
+// plus noise, ingest.py:341-544) but every value is a pure function of
+// (seed, index), so a GPU can generate 5e8 voxels in milliseconds and the
+// numpy mirror (oracle/synth.py) reproduces any sub-block bit for bit.  Only
+// exactly-rounded IEEE ops are used (+ - * / floor, no transcendental).
+#include "kernels.cuh"
+
+namespace mfseg {
+namespace {
+
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ unsigned long long h3(unsigned long long seed,
+                                                          unsigned long long a,
+                                                          unsigned long long b) {
+    return mix64(mix64(seed ^ mix64(a)) + b);
+}
+__host__ __device__ __forceinline__ double u01(unsigned long long h) {
+    return (double)(h >> 11) * 0x1.0p-53;
+}
+
+constexpr int MAXB = 16;
+struct Blob {
+    double cx, cy, cz, rx, ry, rz, vx, vy, vz, fv, pv;
+};
+struct Blobs {
+    int n;
+    Blob b[MAXB];
+};
+
+// blob b of a dataset (dims in cell units, spacing 1, origin 0)
+Blobs make_blobs(const mfseg_synth *s) {
+    Blobs B;
+    B.n = s->n_blobs < MAXB ? s->n_blobs : MAXB;
+    double nx = s->nx, ny = s->ny, nz = s->nz, nt = s->nt > 1 ? s->nt - 1 : 1;
+    for (int b = 0; b < B.n; ++b) {
+        volatile double u[9];
+        for (int q = 0; q < 9; ++q) u[q] = u01(h3(s->seed, 1000 + b, q));
+        Blob &o = B.b[b];
+        volatile double t;
+        t = 0.6 * u[0]; o.cx = nx * (0.2 + t);
+        t = 0.6 * u[1]; o.cy = ny * (0.2 + t);
+        t = 0.6 * u[2]; o.cz = nz * (0.2 + t);
+        t = 0.08 * u[3]; o.rx = nx * (0.06 + t);
+        t = 0.08 * u[4]; o.ry = ny * (0.06 + t);
+        t = 0.08 * u[5]; o.rz = nz * (0.06 + t);
+        t = nx * (u[6] - 0.5); o.vx = (t * 0.3) / nt;
+        t = ny * (u[7] - 0.5); o.vy = (t * 0.3) / nt;
+        t = nz * (u[8] - 0.5); o.vz = (t * 0.3) / nt;
+        o.fv = (double)(b + 1) / (double)(B.n + 1);
+        o.pv = 1.0 - o.fv;
+    }
+    return B;
+}
+
+__device__ int blob_at(const Blobs &B, double x, double y, double z, double m) {
+    for (int b = 0; b < B.n; ++b) {
+        const Blob &o = B.b[b];
+        double dx = DDIV(DSUB(x, DADD(o.cx, DMUL(o.vx, m))), o.rx);
+        double dy = DDIV(DSUB(y, DADD(o.cy, DMUL(o.vy, m))), o.ry);
+        double dz = DDIV(DSUB(z, DADD(o.cz, DMUL(o.vz, m))), o.rz);
+        if (DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz)) <= 1.0) return b;
+    }
+    return -1;
+}
+
+__device__ double noisy(double base, unsigned long long seed, unsigned long long idx,
+                        double noise, int dyadic) {
+    double u = DADD(DADD(DADD(u01(h3(seed, idx, 1)), u01(h3(seed, idx, 2))), u01(h3(seed, idx, 3))),
+                    u01(h3(seed, idx, 4)));
+    double v = DADD(base, DMUL(noise, DSUB(u, 2.0)));
+    if (dyadic) {
+        v = DDIV(floor(DMUL(v, 1048576.0)), 1048576.0);
+        v = fmin(fmax(v, 0.0), 1.0);
+    }
+    return v;
+}
+
+__global__ void k_synth_field(mfseg_synth s, Blobs B, double *values) {
+    long long ncell = (long long)s.nx * s.ny * s.nz;
+    long long n = ncell * s.nt;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        long long r = q;
+        int i = (int)(r % s.nx);
+        r /= s.nx;
+        int j = (int)(r % s.ny);
+        r /= s.ny;
+        int k = (int)(r % s.nz);
+        int m = (int)(r / s.nz);
+        int b = blob_at(B, (double)i + 0.5, (double)j + 0.5, (double)k + 0.5, (double)m);
+        double v = noisy(b >= 0 ? B.b[b].fv : 0.0, s.seed, (unsigned long long)q, s.noise, s.dyadic);
+        if (s.dyadic && q < 2) v = (double)q;   // pin min 0 / max 1: normalization is the identity
+        values[q] = v;
+    }
+}
+
+__global__ void k_synth_points(mfseg_synth s, Blobs B, long long *traj_id, double *t, double *xyz,
+                               double *value) {
+    long long n = s.n_traj * s.nt;
+    double ex = s.nx, ey = s.ny, ez = s.nz;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        long long p = q / s.nt;
+        int m = (int)(q % s.nt);
+        unsigned long long sp = s.seed ^ 0x5bd1e995ull;
+        double x0 = DMUL(ex, u01(h3(sp, p, 11))), y0 = DMUL(ey, u01(h3(sp, p, 12))),
+               z0 = DMUL(ez, u01(h3(sp, p, 13)));
+        double vx = DSUB(DMUL(2.0, u01(h3(sp, p, 14))), 1.0);
+        double vy = DSUB(DMUL(2.0, u01(h3(sp, p, 15))), 1.0);
+        double vz = DSUB(DMUL(2.0, u01(h3(sp, p, 16))), 1.0);
+        double mm = (double)m;
+        double x = DADD(x0, DMUL(vx, mm)), y = DADD(y0, DMUL(vy, mm)), z = DADD(z0, DMUL(vz, mm));
+        // keep inside [0, n) (clip; exact)
+        x = fmin(fmax(x, 0.0), DSUB(ex, 0x1.0p-16));
+        y = fmin(fmax(y, 0.0), DSUB(ey, 0x1.0p-16));
+        z = fmin(fmax(z, 0.0), DSUB(ez, 0x1.0p-16));
+        if (s.dyadic) {
+            x = DDIV(floor(DMUL(x, 65536.0)), 65536.0);
+            y = DDIV(floor(DMUL(y, 65536.0)), 65536.0);
+            z = DDIV(floor(DMUL(z, 65536.0)), 65536.0);
+        }
+        int b = blob_at(B, x, y, z, mm);
+        double v = noisy(b >= 0 ? B.b[b].pv : 0.0, sp, (unsigned long long)q, s.noise, s.dyadic);
+        if (s.dyadic && q < 2) v = (double)q;
+        traj_id[q] = p;
+        t[q] = mm;
+        xyz[3 * q] = x;
+        xyz[3 * q + 1] = y;
+        xyz[3 * q + 2] = z;
+        value[q] = v;
+    }
+}
+
+}  // namespace
+}  // namespace mfseg
+
+using namespace mfseg;
+
+extern "C" {
+
+int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream) {
+    Blobs B = make_blobs(s);
+    k_synth_field<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, values);
+    MFSEG_LAUNCH("k_synth_field");
+    return 0;
+}
+
+int mfseg_synth_points(const mfseg_synth *s, int64_t *traj_id, double *t, double *xyz,
+                       double *value, void *stream) {
+    Blobs B = make_blobs(s);
+    k_synth_points<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, (long long *)traj_id, t,
+                                                               xyz, value);
+    MFSEG_LAUNCH("k_synth_points");
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+"""`pipeline.segment` equivalent (pipeline.py:24-45): normalize -> extent -> run,
+with the data uploaded once and every step on the device."""
+
+from __future__ import annotations
+
+import time
+from typing import Optional
+
+import numpy as np
+
+from .engine import (CenterState, DeviceField, DevicePoints, DeviceRun, device, field_to_device,
+                     points_to_device, run_device)
+from .ingest import NormalizationRecord, domain_extent_device, normalize_device
+from .model import ClusterParams, FieldSet, PointSet, Segmentation
+
+
+def segment_device(pts: DevicePoints, fld: DeviceField, params: ClusterParams, progress=None,
+                   reduce=None, workspace=None, out=None):
+    """Normalize (in place), derive the extent and run, all on device tensors.
+
+    Returns (DeviceRun, NormalizationRecord, extent, per-iteration wall times).
+    """
+    norm = normalize_device(pts, fld, params.normalize)
+    extent = domain_extent_device(pts, fld)
+    iter_times = []
+    last = [time.perf_counter()]
+
+    def sink(it, delta):
+        now = time.perf_counter()
+        iter_times.append(now - last[0])
+        last[0] = now
+        if progress is not None:
+            progress(it, delta)
+
+    r = run_device(pts, fld, extent, params, progress=sink, reduce=reduce, workspace=workspace,
+                   out=out)
+    return r, norm, extent, iter_times
+
+
+def segment(points: Optional[PointSet], fields: Optional[FieldSet], params: ClusterParams,
+            workers: int = 1, chunk_size: Optional[int] = None, progress=None):
+    """Host arrays in, (Segmentation, NormalizationRecord, iteration wall times) out."""
+    dev = device()
+    pts = points_to_device(points, dev)
+    fld = field_to_device(fields, dev)
+    r, norm, extent, iter_times = segment_device(pts, fld, params, progress=progress)
+    seg = to_segmentation(r, params, extent)
+    return seg, norm, iter_times
+
+
+def to_segmentation(r: DeviceRun, params, extent) -> Segmentation:
+    state = CenterState.from_device(r.state)
+    return Segmentation(point_labels=r.point_labels.cpu().numpy(),
+                        field_labels=r.field_labels.cpu().numpy(), centers=state.to_table(),
+                        params=params, extent=extent, iterations_used=r.iterations_used,
+                        converged=r.converged)

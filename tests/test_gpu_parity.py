@@ -1,0 +1,347 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.
+
+Bars (written in the asserts):
+  * labels, counts, ids, merge maps, voxel lists, bboxes: bit-exact;
+  * centre locations/values: within 1e-12 relative of the reference (exact
+    128-bit sums vs numpy's sequential fp64 sums; north_star allows 1e-5);
+  * feature mean/std: within 1e-9 relative to the value scale (north_star 1e-5).
+"""
+import numpy as np
+import pytest
+import torch
+
+from golden_io import Case, names
+
+pytestmark = pytest.mark.gpu
+
+RUNS = names("run_")
+ASSIGNS = names("assign_")
+CENTER_RTOL = 1e-12
+
+
+def pkg():
+    import paper_1903_12294_b200 as P
+    return P
+
+
+def _points(case):
+    P = pkg()
+    return P.PointSet(case["in_p_traj_id"], case["in_p_t"], case["in_p_xyz"].reshape(-1, 3),
+                      case["in_p_value"])
+
+
+def _field(case):
+    P = pkg()
+    dims, origin, spacing, times, values = case.field
+    return P.FieldSet(dims, origin, spacing, times, values.reshape(len(times), -1))
+
+
+def _extent(case):
+    P = pkg()
+    e = case.meta["extent"]
+    return P.DomainExtent.from_dict(e)
+
+
+def _params(case):
+    P = pkg()
+    return P.ClusterParams.from_dict(case.meta["params"])
+
+
+def _state(case, prefix):
+    P = pkg()
+    return P.CenterState(case[prefix + "loc"].copy(), case[prefix + "pval"].copy(),
+                         case[prefix + "fval"].copy(), case[prefix + "has_p"].copy(),
+                         case[prefix + "has_f"].copy(), case[prefix + "n_points"].copy(),
+                         case[prefix + "n_fields"].copy(), case[prefix + "dormant"].copy())
+
+
+def _close(got, want, rtol):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    assert got.shape == want.shape
+    both_nan = np.isnan(got) & np.isnan(want)
+    ok = both_nan | (np.abs(got - want) <= rtol * np.maximum(np.abs(want), 1e-300))
+    assert ok.all(), (got[~ok][:5], want[~ok][:5])
+
+
+@pytest.mark.parametrize("name", ASSIGNS)
+def test_assign_iteration_bit_exact(name):
+    P = pkg()
+    case = Case(name)
+    params = _params(case)
+    ext = _extent(case)
+    C = P.interval_distances(ext, params.k)
+    cs = _state(case, "in_c_")
+    grid = P.CenterGrid(cs.loc, ext, C, params.k)
+    pl, fl = P.assign_iteration(_points(case), _field(case), None, cs, grid, params, C)
+    np.testing.assert_array_equal(pl, case["out_point_labels"])
+    np.testing.assert_array_equal(fl, case["out_field_labels"])
+    assert pl.dtype == np.int64 and fl.dtype == np.int64
+
+
+@pytest.mark.parametrize("name", ASSIGNS)
+def test_accumulate_update_converge(name):
+    P = pkg()
+    case = Case(name)
+    K = len(case["in_c_loc"])
+    sums = P.accumulate(case["out_point_labels"], _points(case), case["out_field_labels"],
+                        _field(case), None, K)
+    for nm, got in zip(("sums", "psum", "fsum"), sums[:3]):
+        _close(got, case[f"out_acc_{nm}"], 1e-13)
+    np.testing.assert_array_equal(sums[3], case["out_acc_n_p"])
+    np.testing.assert_array_equal(sums[4], case["out_acc_n_f"])
+    # update from the reference's own sums: identical arithmetic -> bit-exact
+    old = _state(case, "in_c_")
+    new = P.update_centers(old, *(case[f"out_acc_{n}"] for n in ("sums", "psum", "fsum", "n_p", "n_f")))
+    for f in ("loc", "pval", "fval", "has_p", "has_f", "n_points", "n_fields", "dormant"):
+        np.testing.assert_array_equal(getattr(new, f), case[f"out_new_{f}"], err_msg=f)
+    assert P.has_converged(old, new, case.meta["params"]["eps_c"]) == case.meta["converged"]
+    assert P.max_center_delta(old, new) == case.meta["max_delta"]
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_run_matches_reference(name):
+    P = pkg()
+    case = Case(name)
+    params = _params(case)
+    pts = _points(case) if case["in_p_t"].size else None
+    fld = _field(case) if case["in_f_values"].size else None
+    prog = []
+    seg = P.run(pts, fld, _extent(case), params, progress=lambda i, d: prog.append((i, d)))
+    np.testing.assert_array_equal(seg.point_labels, case["out_point_labels"])
+    np.testing.assert_array_equal(seg.field_labels, case["out_field_labels"])
+    assert seg.point_labels.dtype == np.int32
+    assert seg.iterations_used == case.meta["iterations_used"]
+    assert seg.converged == case.meta["converged"]
+    ids = np.array([c.id for c in seg.centers])
+    np.testing.assert_array_equal(ids, case["out_c_id"])
+    _close([[c.x_c, c.y_c, c.z_c, c.t_c] for c in seg.centers], case["out_c_loc"], CENTER_RTOL)
+    _close([np.nan if c.p_c is None else c.p_c for c in seg.centers], case["out_c_p_c"], CENTER_RTOL)
+    _close([np.nan if c.f_c is None else c.f_c for c in seg.centers], case["out_c_f_c"], CENTER_RTOL)
+    np.testing.assert_array_equal([c.n_points for c in seg.centers], case["out_c_n_points"])
+    np.testing.assert_array_equal([c.n_fields for c in seg.centers], case["out_c_n_fields"])
+    assert [i for i, _ in prog] == [i for i, _ in case.meta["progress"]]
+    got_d = np.array([d for _, d in prog])
+    want_d = np.array([d for _, d in case.meta["progress"]])
+    assert np.all(np.abs(got_d - want_d) <= 1e-6 * np.abs(want_d) + 1e-12)
+
+
+def test_pipeline_segment_frontend_fixture():
+    """Raw inputs -> device normalize -> extent -> run: the reference's recorded
+    service responses (frontend fixtures) within 1e-12."""
+    P = pkg()
+    case = Case("run_slab2_frontend")
+    params = _params(case)
+    raw_p = P.PointSet(case["in_p_traj_id"], case["in_p_t"], case["in_p_xyz"].reshape(-1, 3),
+                       case["in_raw_p_value"])
+    dims, origin, spacing, times, _ = case.field
+    raw_f = P.FieldSet(dims, origin, spacing, times, case["in_raw_f_values"])
+    seg, norm, _ = P.segment(raw_p, raw_f, params)
+    want = case.meta["normalization"]
+    assert norm.to_dict() == want
+    assert seg.extent.to_dict() == case.meta["extent"]
+    np.testing.assert_array_equal(seg.point_labels, case["out_point_labels"])
+    np.testing.assert_array_equal(seg.field_labels, case["out_field_labels"])
+    fx = case.meta["frontend_fixture"]
+    for c, w in zip(seg.centers, fx["centers_all"]):
+        _close([c.x_c, c.y_c, c.z_c, c.t_c, c.p_c, c.f_c],
+               [w["x_c"], w["y_c"], w["z_c"], w["t_c"], w["p_c"], w["f_c"]], CENTER_RTOL)
+        assert (c.n_points, c.n_fields) == (w["n_points"], w["n_fields"])
+    mm, merged = P.merge_clusters(seg.centers, 2.0)
+    assert {str(k): v for k, v in mm.items()} == fx["merge_all"]["merge_map"]
+    w = fx["merge_all"]["centers"][0]
+    _close([merged[0].x_c, merged[0].y_c, merged[0].z_c, merged[0].t_c, merged[0].p_c,
+            merged[0].f_c], [w["x_c"], w["y_c"], w["z_c"], w["t_c"], w["p_c"], w["f_c"]],
+           CENTER_RTOL)
+
+
+def _rows(case, prefix):
+    P = pkg()
+    out = []
+    for i, loc, pc, fc, n_p, n_f in zip(case[prefix + "id"], case[prefix + "loc"],
+                                        case[prefix + "p_c"], case[prefix + "f_c"],
+                                        case[prefix + "n_points"], case[prefix + "n_fields"]):
+        out.append(P.ClusterCenter(int(i), *map(float, loc), None if np.isnan(pc) else float(pc),
+                                   None if np.isnan(fc) else float(fc), int(n_p), int(n_f)))
+    return out
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_merge_bit_exact(name):
+    P = pkg()
+    case = Case(name)
+    rows = _rows(case, "out_c_")
+    for key in case.meta["merges"]:
+        mm, merged = P.merge_clusters(rows, float(key))
+        assert [mm[int(i)] for i in case[f"merge_{key}_ids"]] == list(case[f"merge_{key}_rep"])
+        want = _rows(case, f"merge_{key}_c_")
+        assert merged == want      # dataclass equality: every field bit-identical
+
+
+@pytest.mark.parametrize("name", [n for n in RUNS if n not in ("run_blob_k256", "run_stripes_lo",
+                                                               "run_stripes_hi")])
+def test_features_match_reference(name):
+    P = pkg()
+    case = Case(name)
+    rows = _rows(case, "out_c_")
+    seg = P.Segmentation(case["out_point_labels"], case["out_field_labels"], rows,
+                         _params(case), _extent(case), case.meta["iterations_used"],
+                         case.meta["converged"])
+    pts, fld = _points(case), _field(case)
+    for key, want in case.meta["features"].items():
+        mm = None if key == "identity" else P.merge_clusters(rows, float(key))[0]
+        got = P.build_features(seg, mm, pts, fld)
+        assert [f.id for f in got] == [w["id"] for w in want]
+        for g, w in zip(got, want):
+            assert g.member_clusters == w["member_clusters"]
+            assert [list(map(int, x)) for x in g.polylines] == w["polylines"]
+            assert g.isolated_points == w["isolated_points"]
+            assert {str(m): list(map(int, c)) for m, c in sorted(g.voxels.items())} == w["voxels"]
+            s = g.stats.to_dict()
+            for k in ("bbox_min", "bbox_max", "n_points", "n_fields"):
+                assert s[k] == w["stats"][k], (k, s[k], w["stats"][k])
+            for k in ("p_mean", "p_std", "f_mean", "f_std"):
+                if w["stats"][k] is None:
+                    assert s[k] is None
+                else:
+                    scale = max(abs(w["stats"][k.replace("std", "mean")] or 0.0), 1.0)
+                    assert abs(s[k] - w["stats"][k]) <= 1e-9 * scale, (k, s[k], w["stats"][k])
+
+
+def test_link_index_matches_reference():
+    P = pkg()
+    case = Case("link_blob")
+    li = P.build_link_index(_field(case), _points(case))
+    keys = list(li.buckets)
+    np.testing.assert_array_equal(np.array(keys).reshape(-1, 4), case["out_keys"])
+    np.testing.assert_array_equal([len(li.buckets[k]) for k in keys], case["out_sizes"])
+    np.testing.assert_array_equal(np.concatenate([li.buckets[k] for k in keys]),
+                                  case["out_members"])
+
+
+def test_link_index_rejects_outside_points():
+    P = pkg()
+    fs = P.FieldSet((4, 4, 4), np.zeros(3), np.ones(3), np.array([0.0, 1.0, 2.0]), np.zeros((3, 64)))
+    ps = P.PointSet(np.array([0]), np.array([0.0]), np.array([[9.0, 0.5, 0.5]]), np.array([1.0]))
+    with pytest.raises(P.IngestError):
+        P.build_link_index(fs, ps)
+
+
+# ------------------------------------------------------------------ synthetic, vs the C oracle
+
+def _synthetic(dims, nt, ntraj, seed, dyadic, noise=0.05, n_blobs=5):
+    from paper_1903_12294_b200.ingest import synthetic_device
+    return synthetic_device(dims, nt, ntraj, seed=seed, noise=noise, n_blobs=n_blobs, dyadic=dyadic)
+
+
+@pytest.mark.parametrize("dyadic", [False, True])
+def test_synthetic_generator_matches_numpy_mirror(dyadic):
+    from oracle import synth
+    dims, nt, ntraj = (20, 12, 9), 5, 50
+    fld, pts, tid = _synthetic(dims, nt, ntraj, seed=7, dyadic=dyadic)
+    np.testing.assert_array_equal(fld.values.cpu().numpy().reshape(nt, -1),
+                                  synth.field(dims, nt, seed=7, n_blobs=5, dyadic=dyadic))
+    t_id, t, xyz, v = synth.points(dims, nt, ntraj, seed=7, n_blobs=5, dyadic=dyadic)
+    np.testing.assert_array_equal(tid.cpu().numpy(), t_id)
+    np.testing.assert_array_equal(pts.t.cpu().numpy(), t)
+    np.testing.assert_array_equal(pts.xyz.cpu().numpy(), xyz)
+    np.testing.assert_array_equal(pts.value.cpu().numpy(), v)
+
+
+@pytest.mark.parametrize("dyadic,k,seed", [(True, (6, 5, 4, 3), 1), (False, (6, 5, 4, 3), 2),
+                                           (False, (8, 8, 4, 4), 3), (True, (3, 3, 3, 2), 4)])
+def test_run_vs_c_oracle(dyadic, k, seed):
+    """Full runs on the counter-based generator vs the C restatement."""
+    from oracle import c_oracle
+    from oracle import mfseg_oracle as O
+    from paper_1903_12294_b200 import ClusterParams
+    from paper_1903_12294_b200.engine import CenterState, run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device
+    dims, nt, ntraj = (40, 32, 20), 8, 1500
+    fld, pts, _ = _synthetic(dims, nt, ntraj, seed, dyadic)
+    ext = domain_extent_device(pts, fld)
+    params = ClusterParams(k=k, w_d=0.7, eps_c=1e-12, max_iterations=6, normalize=False)
+    r = run_device(pts, fld, ext, params)
+    floc = O.field_locations(dims, np.zeros(3), np.ones(3), np.arange(nt, dtype=float))
+    ref = c_oracle.run(np.column_stack([pts.xyz.cpu().numpy(), pts.t.cpu().numpy()]),
+                       pts.value.cpu().numpy(), floc, fld.values.cpu().numpy(), ext.mins,
+                       ext.maxs, k, c_f=1.0, w_d=0.7, w_p=1.0, w_f=1.0, eps_c=1e-12,
+                       max_iterations=6)
+    np.testing.assert_array_equal(r.field_labels.cpu().numpy(), ref["field_labels"])
+    np.testing.assert_array_equal(r.point_labels.cpu().numpy(), ref["point_labels"])
+    assert r.iterations_used == ref["iterations_used"]
+    st = CenterState.from_device(r.state)
+    np.testing.assert_array_equal(st.n_points, ref["n_points"])
+    np.testing.assert_array_equal(st.n_fields, ref["n_fields"])
+    if dyadic:   # every sum exact in both -> bit-identical centres
+        np.testing.assert_array_equal(st.loc, ref["loc"])
+        np.testing.assert_array_equal(st.pval, ref["pval"])
+        np.testing.assert_array_equal(st.fval, ref["fval"])
+    else:
+        _close(st.loc, ref["loc"], CENTER_RTOL)
+        _close(st.pval, ref["pval"], CENTER_RTOL)
+
+
+def test_stranded_and_crowded_bins_vs_oracle():
+    """Heavily drifted, crowded centres: many stranded samples and long
+    candidate lists (> one 256-candidate chunk) through the fallback path."""
+    from oracle import c_oracle
+    from oracle import mfseg_oracle as O
+    P = pkg()
+    rng = np.random.default_rng(5)
+    dims, nt = (30, 20, 10), 6
+    fs = P.FieldSet(dims, np.zeros(3), np.ones(3), np.arange(nt, dtype=float),
+                    rng.random((nt, int(np.prod(dims)))))
+    n = 4000
+    loc = rng.random((n, 4)) * [30, 20, 10, 5]
+    ps = P.PointSet(np.arange(n), loc[:, 3].copy(), loc[:, :3].copy(), rng.random(n))
+    ext = P.DomainExtent(0, 30, 0, 20, 0, 10, 0, 5)
+    params = P.ClusterParams(k=(10, 8, 4, 3), w_d=1.0, w_p=0.8, w_f=0.5)
+    K = params.k_total
+    C = P.interval_distances(ext, params.k)
+    seeds = P.seed_centers(ext, params.k)
+    cs = P.CenterState.from_seeds(seeds + rng.uniform(-2.5, 2.5, (K, 4)) * C)
+    cs.loc[:300] = cs.loc[0] + rng.uniform(-0.2, 0.2, (300, 4)) * C     # 300 centres in one bin
+    cs.pval = np.where(rng.random(K) < 0.7, rng.random(K), np.nan)
+    cs.fval = np.where(rng.random(K) < 0.7, rng.random(K), np.nan)
+    cs.has_p, cs.has_f = ~np.isnan(cs.pval), ~np.isnan(cs.fval)
+    grid = P.CenterGrid(cs.loc, ext, C, params.k)
+    pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
+    floc = O.field_locations(dims, np.zeros(3), np.ones(3), fs.times)
+    epl = c_oracle.assign(ps.loc4, ps.value, cs.loc, cs.pval, cs.has_p, ext.mins, C, params.k,
+                          params.w_p, params.w_d, params.c_f)
+    efl = c_oracle.assign(floc, fs.flat_values(), cs.loc, cs.fval, cs.has_f, ext.mins, C,
+                          params.k, params.w_f, params.w_d, params.c_f)
+    np.testing.assert_array_equal(pl, epl)
+    np.testing.assert_array_equal(fl, efl)
+
+
+def test_empty_kinds_and_errors():
+    P = pkg()
+    ext = P.DomainExtent(0, 10, 0, 10, 0, 10, 0, 4)
+    with pytest.raises(ValueError):
+        P.run(None, None, ext, P.ClusterParams())
+    rng = np.random.default_rng(2)
+    loc = rng.random((50, 4)) * [10, 10, 10, 4]
+    pts = P.PointSet(np.arange(50), loc[:, 3].copy(), loc[:, :3].copy(), rng.random(50))
+    seg = P.run(pts, None, ext, P.ClusterParams(k=(1, 1, 1, 1), normalize=False))
+    assert seg.converged and seg.iterations_used <= 2
+    c = seg.centers[0]
+    np.testing.assert_allclose(c.loc4, pts.loc4.mean(axis=0), rtol=1e-14)
+    assert c.f_c is None and len(seg.field_labels) == 0
+
+
+def test_labels_deterministic_across_reruns():
+    from paper_1903_12294_b200 import ClusterParams
+    from paper_1903_12294_b200.engine import CenterState, run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device
+    fld, pts, _ = _synthetic((48, 40, 24), 6, 4000, 11, False)
+    ext = domain_extent_device(pts, fld)
+    params = ClusterParams(k=(6, 5, 3, 2), w_d=0.5, eps_c=1e-12, max_iterations=5)
+    a = run_device(pts, fld, ext, params)
+    sa = CenterState.from_device(a.state)
+    la, lb = a.field_labels.clone(), a.point_labels.clone()
+    b = run_device(pts, fld, ext, params)
+    sb = CenterState.from_device(b.state)
+    assert torch.equal(la, b.field_labels) and torch.equal(lb, b.point_labels)
+    np.testing.assert_array_equal(sa.loc, sb.loc)
