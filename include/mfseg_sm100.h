@@ -43,7 +43,7 @@ typedef struct mfseg_params {
     double c_f, w_d, w_p, w_f;
     double eps_c;
     int32_t max_iterations;
-    int32_t reserved;
+    int32_t n_centers;     /* centres in the state; 0 = k1*k2*k3*k4 (always so in mfseg_run) */
 } mfseg_params;
 
 /* FieldSet (model.py:108-157).  values: [nt][nz][ny][nx] fp64 (already

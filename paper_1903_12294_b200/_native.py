@@ -29,7 +29,7 @@ szt = C.c_size_t
 class Params(C.Structure):
     _fields_ = [("k", i32 * 4), ("mins", f64 * 4), ("C", f64 * 4), ("c_f", f64), ("w_d", f64),
                 ("w_p", f64), ("w_f", f64), ("eps_c", f64), ("max_iterations", i32),
-                ("reserved", i32)]
+                ("n_centers", i32)]
 
 
 class Field(C.Structure):

@@ -182,7 +182,8 @@ struct CentersView {      // read-only centre state for the assign kernels
 };
 
 struct Grid {             // CenterGrid (engine.py:89-134), rebuilt every pass
-    int K;
+    int K;                // centres
+    int NB;               // bins = k1*k2*k3*k4
     int *cbin;            // [K] flat bin of every centre
     int *bin_start;       // [K+1] CSR of centres by bin
     int *bin_ids;         // [K]

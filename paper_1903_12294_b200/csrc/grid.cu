@@ -172,30 +172,28 @@ __global__ void k_cand_fill(int nbins, int4 k, const int *bin_start, const int *
 
 }  // namespace
 
-size_t grid_workspace_bytes(int K) {
+size_t grid_workspace_bytes(int K, int NB) {
     Carver cv;
-    cv.take<int>(K);             // cbin
-    cv.take<int>(K + 1);         // bin_start
-    cv.take<int>(K);             // bin_ids
-    cv.take<int>(K + 1);         // cand_start
-    cv.take<int>(81ll * K);      // cand_ids (each centre is in <= 81 neighbour lists)
-    cv.take<int4>(2ll * K);      // vbox
-    cv.take<int>(K + 1);         // counts / cursor
-    cv.take<char>(scan_tmp_bytes(K + 1));
+    int *ct;
+    void *sc;
+    grid_carve(cv, K, NB, &ct, &sc);
     return cv.off + 256;
 }
 
-Grid grid_carve(Carver &cv, int K, int **count_tmp, void **scan_tmp) {
+// K centres, NB = k1*k2*k3*k4 bins (the reference allows K != NB for a
+// caller-built CenterState, e.g. test_engine.py:250-262).
+Grid grid_carve(Carver &cv, int K, int NB, int **count_tmp, void **scan_tmp) {
     Grid g;
     g.K = K;
+    g.NB = NB;
     g.cbin = cv.take<int>(K);
-    g.bin_start = cv.take<int>(K + 1);
+    g.bin_start = cv.take<int>(NB + 1);
     g.bin_ids = cv.take<int>(K);
-    g.cand_start = cv.take<int>(K + 1);
-    g.cand_ids = cv.take<int>(81ll * K);
+    g.cand_start = cv.take<int>(NB + 1);
+    g.cand_ids = cv.take<int>(81ll * K);     // each centre is in <= 81 neighbour lists
     g.vbox = cv.take<int4>(2ll * K);
-    *count_tmp = cv.take<int>(K + 1);
-    *scan_tmp = cv.take<char>(scan_tmp_bytes(K + 1));
+    *count_tmp = cv.take<int>(NB + 1);
+    *scan_tmp = cv.take<char>(scan_tmp_bytes(NB + 1));
     return g;
 }
 
@@ -203,23 +201,23 @@ Grid grid_carve(Carver &cv, int K, int **count_tmp, void **scan_tmp) {
 int grid_build(Grid &g, const double *x, const double *y, const double *z, const double *t,
                const mfseg_params *p, const mfseg_field *f, int *count_tmp, void *scan_tmp,
                cudaStream_t st) {
-    int K = g.K;
-    int nbins = K;   // bins = k-grid cells = number of seeds
+    int K = g.K, NB = g.NB;
     double4 mins = make_double4(p->mins[0], p->mins[1], p->mins[2], p->mins[3]);
     double4 C = make_double4(p->C[0], p->C[1], p->C[2], p->C[3]);
     int4 k = make_int4(p->k[0], p->k[1], p->k[2], p->k[3]);
     const int B = 256;
-    unsigned gk = (unsigned)((K + B - 1) / B);
-    MFSEG_CUDA(cudaMemsetAsync(count_tmp, 0, sizeof(int) * (K + 1), st));
-    k_center_bins<<<gk, B, 0, st>>>(K, x, y, z, t, mins, C, k, g.cbin, count_tmp);
-    MFSEG_TRY(scan_exclusive_i32(count_tmp, g.bin_start, K + 1, scan_tmp, scan_tmp_bytes(K + 1), st));
-    MFSEG_CUDA(cudaMemsetAsync(count_tmp, 0, sizeof(int) * (K + 1), st));
-    k_center_place<<<gk, B, 0, st>>>(K, g.cbin, g.bin_start, count_tmp, g.bin_ids);
-    k_bin_sort<<<gk, B, 0, st>>>(nbins, g.bin_start, g.bin_ids);
-    k_cand_count<<<gk, B, 0, st>>>(nbins, k, g.bin_start, count_tmp);
-    MFSEG_TRY(scan_exclusive_i32(count_tmp, g.cand_start, K + 1, scan_tmp, scan_tmp_bytes(K + 1), st));
-    k_cand_fill<<<gk, B, 0, st>>>(nbins, k, g.bin_start, g.bin_ids, g.cand_start, g.cand_ids);
-    if (f && f->nt > 0) {
+    unsigned gk = (unsigned)((K + B - 1) / B), gb = (unsigned)((NB + B - 1) / B);
+    size_t sb = scan_tmp_bytes(NB + 1);
+    MFSEG_CUDA(cudaMemsetAsync(count_tmp, 0, sizeof(int) * (NB + 1), st));
+    if (K > 0) k_center_bins<<<gk, B, 0, st>>>(K, x, y, z, t, mins, C, k, g.cbin, count_tmp);
+    MFSEG_TRY(scan_exclusive_i32(count_tmp, g.bin_start, NB + 1, scan_tmp, sb, st));
+    MFSEG_CUDA(cudaMemsetAsync(count_tmp, 0, sizeof(int) * (NB + 1), st));
+    if (K > 0) k_center_place<<<gk, B, 0, st>>>(K, g.cbin, g.bin_start, count_tmp, g.bin_ids);
+    k_bin_sort<<<gb, B, 0, st>>>(NB, g.bin_start, g.bin_ids);
+    k_cand_count<<<gb, B, 0, st>>>(NB, k, g.bin_start, count_tmp);
+    MFSEG_TRY(scan_exclusive_i32(count_tmp, g.cand_start, NB + 1, scan_tmp, sb, st));
+    k_cand_fill<<<gb, B, 0, st>>>(NB, k, g.bin_start, g.bin_ids, g.cand_start, g.cand_ids);
+    if (f && f->nt > 0 && K > 0) {
         FieldGeom fg{f->nx, f->ny, f->nz, f->nt, f->origin[0], f->origin[1], f->origin[2],
                      f->spacing[0], f->spacing[1], f->spacing[2], f->times};
         k_center_vbox<<<gk, B, 0, st>>>(K, x, y, z, t, C, fg, g.vbox);

@@ -75,8 +75,8 @@ struct FallbackArgs {
 };
 
 // grid.cu
-size_t grid_workspace_bytes(int K);
-Grid grid_carve(Carver &cv, int K, int **count_tmp, void **scan_tmp);
+size_t grid_workspace_bytes(int K, int NB);
+Grid grid_carve(Carver &cv, int K, int NB, int **count_tmp, void **scan_tmp);
 int grid_build(Grid &g, const double *x, const double *y, const double *z, const double *t,
                const mfseg_params *p, const mfseg_field *f, int *count_tmp, void *scan_tmp,
                cudaStream_t st);

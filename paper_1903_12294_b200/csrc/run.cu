@@ -158,7 +158,8 @@ struct Plan {
     mfseg_params p;
     mfseg_field f;
     mfseg_points pts;
-    int K;
+    int K;                          // centres
+    int NB;                         // bins = k1*k2*k3*k4
     long long nf, np;
     cudaStream_t st;
     // centre state ping-pong
@@ -220,8 +221,8 @@ int check_inputs(const mfseg_params *p, const mfseg_field *f, const mfseg_points
             set_error("invalid k or C (k must be >= 1, C > 0)");
             return 2;
         }
-    long long K = (long long)p->k[0] * p->k[1] * p->k[2] * p->k[3];
-    if (K > (1ll << 26)) {
+    long long NB = (long long)p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    if (NB > (1ll << 26) || p->n_centers > (1 << 26) || p->n_centers < 0) {
         set_error("too many clusters (K > 2^26)");
         return 2;
     }
@@ -253,7 +254,8 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.acc = cv.take<unsigned long long>((long long)K * MFSEG_ACC_WORDS);
     P.limbs = cv.take<long long>((long long)K * MFSEG_ACC_WORDS / 2 * 3);
     P.flags = cv.take<char>(update_flags_bytes());
-    P.g = grid_carve(cv, K, &P.count_tmp, &P.grid_scan_tmp);
+    int NB = P.NB;
+    P.g = grid_carve(cv, K, NB, &P.count_tmp, &P.grid_scan_tmp);
     P.counters = cv.take<unsigned long long>(4);
     P.overflow = cv.take<int>(4);
     // field
@@ -288,17 +290,17 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.pt = cv.take<double>(n);
     P.pv = cv.take<double>(n);
     P.plabels = cv.take<int>(n);
-    P.bcnt = cv.take<int>(K + 1);
-    P.bfirst = cv.take<int>(K + 1);
-    P.btiles = cv.take<int>(K + 1);
-    P.tstart = cv.take<int>(K + 1);
-    P.max_tiles = n > 0 ? (n + TP - 1) / TP + K : 0;
+    P.bcnt = cv.take<int>(NB + 1);
+    P.bfirst = cv.take<int>(NB + 1);
+    P.btiles = cv.take<int>(NB + 1);
+    P.tstart = cv.take<int>(NB + 1);
+    P.max_tiles = n > 0 ? (n + TP - 1) / TP + NB : 0;
     P.tiles = cv.take<int4>(P.max_tiles);
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
     P.radix_bytes = n > 0 ? radix_tmp_bytes(n) : 0;
     P.radix_tmp = cv.take<char>(P.radix_bytes);
-    P.scan_bytes = scan_tmp_bytes((long long)K + 1) + 1024;
+    P.scan_bytes = scan_tmp_bytes((long long)NB + 1) + 1024;
     P.scan_tmp = cv.take<char>(P.scan_bytes);
     return cv.off + 1024;
 }
@@ -310,7 +312,8 @@ int plan_init(Plan &P, const mfseg_params *p, const mfseg_field *f, const mfseg_
     P.p = *p;
     if (f) P.f = *f;
     if (pts) P.pts = *pts;
-    P.K = p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    P.NB = p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    P.K = p->n_centers > 0 ? p->n_centers : P.NB;
     P.np = pts ? pts->n : 0;
     P.st = st;
     size_t need = plan_carve(P, nullptr, 0);
@@ -351,19 +354,19 @@ int plan_prepare(Plan &P) {
         unsigned gb = (unsigned)((n + 255) / 256);
         k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, k, P.keys, P.vals);
         MFSEG_LAUNCH("k_point_keys");
-        MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, bits_for(P.K - 1),
+        MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, bits_for(P.NB - 1),
                                    P.radix_tmp, P.radix_bytes, st));
         k_point_gather<<<gb, 256, 0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px,
                                            P.py, P.pz, P.pt, P.pv);
-        MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (P.K + 1), st));
+        MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (P.NB + 1), st));
         k_bin_hist<<<gb, 256, 0, st>>>(n, P.skeys, P.bcnt);
-        MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, P.K + 1, P.scan_tmp, P.scan_bytes, st));
+        MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, P.NB + 1, P.scan_tmp, P.scan_bytes, st));
         int TP = point_tile_size();
-        unsigned gk = (unsigned)((P.K + 256) / 256);
-        MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (P.K + 1), st));
-        k_tiles_per_bin<<<gk, 256, 0, st>>>(P.K, P.bcnt, TP, P.btiles);
-        MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, P.K + 1, P.scan_tmp, P.scan_bytes, st));
-        k_make_tiles<<<gk, 256, 0, st>>>(P.K, P.bcnt, P.bfirst, P.tstart, TP, P.tiles);
+        unsigned gk = (unsigned)((P.NB + 256) / 256);
+        MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (P.NB + 1), st));
+        k_tiles_per_bin<<<gk, 256, 0, st>>>(P.NB, P.bcnt, TP, P.btiles);
+        MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, P.NB + 1, P.scan_tmp, P.scan_bytes, st));
+        k_make_tiles<<<gk, 256, 0, st>>>(P.NB, P.bcnt, P.bfirst, P.tstart, TP, P.tiles);
         MFSEG_LAUNCH("point tiles");
     }
     return 0;
@@ -447,7 +450,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.t = P.pt;
         a.v = P.pv;
         a.tiles = P.tiles;
-        a.n_tiles = P.tstart + K;
+        a.n_tiles = P.tstart + P.NB;
         a.Cx = p.C[0];
         a.Cy = p.C[1];
         a.Cz = p.C[2];
@@ -544,7 +547,8 @@ size_t mfseg_run_workspace_size(const mfseg_params *p, const mfseg_field *f,
     P.p = *p;
     if (f) P.f = *f;
     if (pts) P.pts = *pts;
-    P.K = p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    P.NB = p->k[0] * p->k[1] * p->k[2] * p->k[3];
+    P.K = p->n_centers > 0 ? p->n_centers : P.NB;
     P.np = pts ? pts->n : 0;
     return plan_carve(P, nullptr, 0);
 }
@@ -562,6 +566,10 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
     cudaStream_t st = (cudaStream_t)stream;
     Plan P;
     MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
+    if (P.K != P.NB) {
+        set_error("mfseg_run seeds one centre per k-grid cell: n_centers must be 0 or k1*k2*k3*k4");
+        return 2;
+    }
     if (P.nf == 0 && P.np == 0) {
         set_error("no samples of either kind");
         return 2;

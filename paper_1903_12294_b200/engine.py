@@ -268,6 +268,7 @@ def field_distance(loc4, value: float, center: ClusterCenter, params: ClusterPar
 def _run_assign(pts: DevicePoints, fld: DeviceField, state: dict, prm: N.Params, K: int):
     lib = N.load()
     dev = state["loc"].device
+    prm.n_centers = K
     fs, ps = fld.struct(), pts.struct()
     ws_bytes = lib.mfseg_assign_workspace_size(C.byref(prm), C.byref(fs), C.byref(ps))
     if ws_bytes == 0:
@@ -337,12 +338,13 @@ def update_centers(centers: CenterState, sums, psum, fsum, n_p, n_f) -> CenterSt
     K = len(centers.loc)
     old = centers.to_device(dev)
     new = empty_state(K, dev)
-    N.check(lib.mfseg_update_centers_f64(
-        K, N.ptr(to_dev(np.asarray(sums, float).reshape(K, 4), dev=dev)),
-        N.ptr(to_dev(psum, dev=dev)), N.ptr(to_dev(fsum, dev=dev)),
-        N.ptr(to_dev(np.asarray(n_p, np.int64), torch.int64, dev)),
-        N.ptr(to_dev(np.asarray(n_f, np.int64), torch.int64, dev)),
-        state_struct(old), state_struct(new), stream_ptr()), "mfseg_update_centers_f64")
+    # keep every uploaded tensor referenced until the kernel has consumed it
+    args = (to_dev(np.asarray(sums, float).reshape(K, 4), dev=dev), to_dev(psum, dev=dev),
+            to_dev(fsum, dev=dev), to_dev(np.asarray(n_p, np.int64), torch.int64, dev),
+            to_dev(np.asarray(n_f, np.int64), torch.int64, dev))
+    N.check(lib.mfseg_update_centers_f64(K, *(N.ptr(a) for a in args), state_struct(old),
+                                         state_struct(new), stream_ptr()),
+            "mfseg_update_centers_f64")
     return CenterState.from_device(new)
 
 

@@ -27,6 +27,8 @@ def pkg():
 
 def _points(case):
     P = pkg()
+    if case["in_p_t"].size == 0:
+        return P.PointSet.empty()
     return P.PointSet(case["in_p_traj_id"], case["in_p_t"], case["in_p_xyz"].reshape(-1, 3),
                       case["in_p_value"])
 
@@ -34,6 +36,8 @@ def _points(case):
 def _field(case):
     P = pkg()
     dims, origin, spacing, times, values = case.field
+    if values.size == 0:
+        return P.FieldSet.empty()
     return P.FieldSet(dims, origin, spacing, times, values.reshape(len(times), -1))
 
 
