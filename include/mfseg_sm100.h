@@ -95,6 +95,15 @@ typedef int (*mfseg_reduce_fn)(void *user, int64_t *limbs, int64_t n_words, void
 const char *mfseg_last_error(void);
 int mfseg_abi_version(void);
 
+/* Instrumentation (bench.py): total kernel launches issued by this library so
+ * far; optional per-phase device timing of mfseg_run with CUDA events on the
+ * caller's stream (phases: 0 CenterGrid rebuild, 1 field assign, 2 point
+ * assign, 3 stranded fallback, 4 exchange + update).  mfseg_timing_read fills
+ * ms_out[0..n) with accumulated milliseconds and returns the pass count. */
+long long mfseg_launch_count(void);
+void mfseg_timing_enable(int32_t on);
+int32_t mfseg_timing_read(double *ms_out, int32_t n);
+
 /* ---------------------------------------------------------------- full run
  * engine.run (engine.py:323-381): seed -> initial pass -> iterate
  * (CenterGrid, assign_iteration, accumulate, update_centers, has_converged)
@@ -155,6 +164,10 @@ int mfseg_compare_centers(int32_t K, mfseg_centers old_state, mfseg_centers new_
  * on n values, or zeros when hi == lo.  lo/hi returned to the host. */
 int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_host,
                            double *hi_host, void *stream);
+
+/* The same map with a caller-given (global) range, for sharded inputs whose
+ * min/max were all-reduced across ranks. */
+int mfseg_normalize_range(double *values, int64_t n, double lo, double hi, void *stream);
 
 /* build_link_index (ingest.py:261-280): bucket points by (cell, interval).
  * Outputs (device): keys [n] int64 (flat key sorted ascending; flat =

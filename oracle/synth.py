@@ -77,17 +77,18 @@ def _noisy(base, seed, idx, noise, dyadic):
     return v
 
 
-def field(dims, nt, seed=0, noise=0.05, n_blobs=6, dyadic=False, steps=None):
-    """(len(steps), ncell) values of the requested timesteps (default: all)."""
+def field(dims, nt, seed=0, noise=0.05, n_blobs=6, dyadic=False, steps=None, cells=None):
+    """(len(steps), len(cells)) values of the requested timesteps and flat cell
+    indices (default: all)."""
     nx, ny, nz = (int(d) for d in dims)
     ncell = nx * ny * nz
     B = blobs(dims, nt, seed, n_blobs)
     steps = range(nt) if steps is None else steps
-    flat = np.arange(ncell)
+    flat = np.arange(ncell) if cells is None else np.asarray(cells, np.int64)
     x = (flat % nx).astype(float) + 0.5
     y = ((flat // nx) % ny).astype(float) + 0.5
     z = (flat // (nx * ny)).astype(float) + 0.5
-    out = np.empty((len(steps), ncell))
+    out = np.empty((len(steps), len(flat)))
     fv = np.array([o["fv"] for o in B] + [0.0])
     for r, m in enumerate(steps):
         lab = _blob_at(B, x, y, z, float(m))
@@ -95,7 +96,7 @@ def field(dims, nt, seed=0, noise=0.05, n_blobs=6, dyadic=False, steps=None):
         q = np.uint64(m) * np.uint64(ncell) + flat.astype(np.uint64)
         v = _noisy(base, seed, q, noise, dyadic)
         if dyadic and m == 0:
-            v[:2] = [0.0, 1.0]
+            v = np.where(flat < 2, flat.astype(float), v)
         out[r] = v
     return out
 

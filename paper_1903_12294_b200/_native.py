@@ -59,6 +59,9 @@ P = C.POINTER
 _SIGNATURES = {
     "mfseg_last_error": (C.c_char_p, []),
     "mfseg_abi_version": (C.c_int, []),
+    "mfseg_launch_count": (C.c_longlong, []),
+    "mfseg_timing_enable": (None, [i32]),
+    "mfseg_timing_read": (i32, [P(f64), i32]),
     "mfseg_run_workspace_size": (szt, [P(Params), P(Field), P(Points)]),
     "mfseg_run": (C.c_int, [P(Params), P(Field), P(Points), vp, vp, Centers, P(i32), P(i32),
                             PROGRESS_FN, vp, REDUCE_FN, vp, vp, szt, vp]),
@@ -70,6 +73,7 @@ _SIGNATURES = {
     "mfseg_update_centers_f64": (C.c_int, [i32, vp, vp, vp, vp, vp, Centers, Centers, vp]),
     "mfseg_compare_centers": (C.c_int, [i32, Centers, Centers, f64, P(i32), P(f64), vp]),
     "mfseg_minmax_normalize": (C.c_int, [vp, i64, i32, P(f64), P(f64), vp]),
+    "mfseg_normalize_range": (C.c_int, [vp, i64, f64, f64, vp]),
     "mfseg_link_index_workspace_size": (szt, [i64]),
     "mfseg_link_index": (C.c_int, [P(Field), P(Points), vp, vp, P(i64), vp, szt, vp]),
     "mfseg_merge_workspace_size": (szt, [i32]),

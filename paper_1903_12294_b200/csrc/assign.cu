@@ -699,6 +699,7 @@ int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st) {
         set_error("field tile grid too large");
         return 3;
     }
+    ::mfseg::count_launch();
     k_field_assign<FTX, FTY, FTZ, FNT><<<(unsigned)ntiles, FNT, 0, st>>>(a);
     MFSEG_LAUNCH("k_field_assign");
     return 0;
@@ -706,12 +707,14 @@ int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st) {
 
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st) {
     if (max_tiles <= 0) return 0;
+    ::mfseg::count_launch();
     k_point_assign<PNT, PSPT><<<(unsigned)max_tiles, PNT, 0, st>>>(a);
     MFSEG_LAUNCH("k_point_assign");
     return 0;
 }
 
 int launch_fallback(const FallbackArgs &a, cudaStream_t st) {
+    ::mfseg::count_launch();
     k_fallback<<<148 * 4, 256, 0, st>>>(a);
     MFSEG_LAUNCH("k_fallback");
     return 0;
@@ -720,6 +723,7 @@ int launch_fallback(const FallbackArgs &a, cudaStream_t st) {
 int launch_accumulate_field(long long n, const mfseg_field *f, const int *labels,
                             unsigned long long *acc, int *overflow, cudaStream_t st) {
     if (n <= 0) return 0;
+    ::mfseg::count_launch();
     k_accumulate_field<<<148 * 8, 256, 0, st>>>(n, f->nx, f->ny, f->nz, f->origin[0],
                                                 f->origin[1], f->origin[2], f->spacing[0],
                                                 f->spacing[1], f->spacing[2], f->times,
@@ -731,6 +735,7 @@ int launch_accumulate_field(long long n, const mfseg_field *f, const int *labels
 int launch_accumulate_points(const mfseg_points *p, const int *labels, unsigned long long *acc,
                              int *overflow, cudaStream_t st) {
     if (p->n <= 0) return 0;
+    ::mfseg::count_launch();
     k_accumulate_points<<<148 * 8, 256, 0, st>>>(p->n, p->xyz, p->t, p->value, labels, acc,
                                                  overflow);
     MFSEG_LAUNCH("k_accumulate_points");

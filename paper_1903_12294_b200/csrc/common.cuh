@@ -40,6 +40,11 @@ int fail(const char *where, cudaError_t e);
         if (r__ != 0) return r__;        \
     } while (0)
 
+// ------------------------------------------------------------------ instrumentation
+// every kernel launch site calls count_launch(); bench.py reads the counter
+// around its timed region (mfseg_launch_count) to report gpu_launches.
+void count_launch();
+
 // ------------------------------------------------------------------ workspace carving
 struct Carver {
     char *base;

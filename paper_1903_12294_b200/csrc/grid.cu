@@ -209,17 +209,27 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
     unsigned gk = (unsigned)((K + B - 1) / B), gb = (unsigned)((NB + B - 1) / B);
     size_t sb = scan_tmp_bytes(NB + 1);
     MFSEG_CUDA(cudaMemsetAsync(count_tmp, 0, sizeof(int) * (NB + 1), st));
-    if (K > 0) k_center_bins<<<gk, B, 0, st>>>(K, x, y, z, t, mins, C, k, g.cbin, count_tmp);
+    if (K > 0) {
+        ::mfseg::count_launch();
+        k_center_bins<<<gk, B, 0, st>>>(K, x, y, z, t, mins, C, k, g.cbin, count_tmp);
+    }
     MFSEG_TRY(scan_exclusive_i32(count_tmp, g.bin_start, NB + 1, scan_tmp, sb, st));
     MFSEG_CUDA(cudaMemsetAsync(count_tmp, 0, sizeof(int) * (NB + 1), st));
-    if (K > 0) k_center_place<<<gk, B, 0, st>>>(K, g.cbin, g.bin_start, count_tmp, g.bin_ids);
+    if (K > 0) {
+        ::mfseg::count_launch();
+        k_center_place<<<gk, B, 0, st>>>(K, g.cbin, g.bin_start, count_tmp, g.bin_ids);
+    }
+    ::mfseg::count_launch();
     k_bin_sort<<<gb, B, 0, st>>>(NB, g.bin_start, g.bin_ids);
+    ::mfseg::count_launch();
     k_cand_count<<<gb, B, 0, st>>>(NB, k, g.bin_start, count_tmp);
     MFSEG_TRY(scan_exclusive_i32(count_tmp, g.cand_start, NB + 1, scan_tmp, sb, st));
+    ::mfseg::count_launch();
     k_cand_fill<<<gb, B, 0, st>>>(NB, k, g.bin_start, g.bin_ids, g.cand_start, g.cand_ids);
     if (f && f->nt > 0 && K > 0) {
         FieldGeom fg{f->nx, f->ny, f->nz, f->nt, f->origin[0], f->origin[1], f->origin[2],
                      f->spacing[0], f->spacing[1], f->spacing[2], f->times};
+        ::mfseg::count_launch();
         k_center_vbox<<<gk, B, 0, st>>>(K, x, y, z, t, C, fg, g.vbox);
     }
     MFSEG_LAUNCH("grid_build");

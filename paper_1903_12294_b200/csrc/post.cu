@@ -438,10 +438,13 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
     size_t sb = scan_tmp_bytes(n + 1);
     void *stmp = cv.take<char>(sb);
     unsigned g = (unsigned)((n + 255) / 256);
+    ::mfseg::count_launch();
     k_uf_init<<<g, 256, 0, st>>>(n, parent);
+    ::mfseg::count_launch();
     k_merge_pairs<<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, st>>>(n, p_c, f_c, eps_m,
                                                                                parent);
     MFSEG_CUDA(cudaMemsetAsync(is_root, 0, sizeof(int) * (n + 1), st));
+    ::mfseg::count_launch();
     k_uf_flatten<<<g, 256, 0, st>>>(n, parent, ids, rep_row, rep, keys, vals, is_root);
     MFSEG_LAUNCH("merge union-find");
     MFSEG_TRY(radix_sort_pairs(keys, vals, skeys, members, n, bits_of((unsigned)n), rtmp, rb, st));
@@ -450,6 +453,7 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
     MFSEG_CUDA(cudaMemcpyAsync(&G, group_of_root + n, sizeof(int), cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
     MergeOut o{m_ids, m_loc, m_p, m_f, (long long *)m_np, (long long *)m_nf};
+    ::mfseg::count_launch();
     k_merge_groups<<<g, 256, 0, st>>>(n, skeys, members, is_root, group_of_root, ids, loc, p_c,
                                       f_c, (const long long *)n_points,
                                       (const long long *)n_fields, o, G);
@@ -461,6 +465,7 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
 int mfseg_relabel(const int32_t *labels, int64_t n, const int32_t *lut, int32_t lut_len,
                   int32_t *out, void *stream) {
     if (n <= 0) return 0;
+    ::mfseg::count_launch();
     k_relabel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(labels, n, lut, lut_len, out);
     MFSEG_LAUNCH("k_relabel");
     return 0;
@@ -505,11 +510,13 @@ int mfseg_voxel_csr(const int32_t *flab, int32_t nt, int64_t ncell, const int32_
     void *stmp = cv.take<char>(sb);
     MFSEG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
     MFSEG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(long long) * (nseg + 1), st));
+    ::mfseg::count_launch();
     k_voxel_keys<<<148 * 8, 256, 0, st>>>(flab, n, ncell, slot_of, lut_len, n_slots, keys, vals,
                                           bad);
     MFSEG_LAUNCH("k_voxel_keys");
     MFSEG_TRY(radix_sort_pairs(keys, vals, skeys, (unsigned *)cells, n, bits_of((unsigned long long)nseg),
                                rtmp, rb, st));
+    ::mfseg::count_launch();
     k_key_hist<<<148 * 8, 256, 0, st>>>(skeys, n, cnt);
     MFSEG_TRY(scan_exclusive_i64(cnt, (long long *)seg_start, nseg + 1, stmp, sb, st));
     int hb = 0;
@@ -572,10 +579,15 @@ int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *fi
     }
     unsigned gs = (unsigned)((n_slots + 255) / 256);
     MFSEG_CUDA(cudaMemsetAsync(a.ovf, 0, sizeof(int), st));
+    ::mfseg::count_launch();
     k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
+    ::mfseg::count_launch();
     k_stats<<<148 * 8, 256, 0, st>>>(a, 0);
+    ::mfseg::count_launch();
     k_stats_means<<<gs, 256, 0, st>>>(n_slots, a.S, mean);
+    ::mfseg::count_launch();
     k_stats<<<148 * 8, 256, 0, st>>>(a, 1);
+    ::mfseg::count_launch();
     k_stats_final<<<gs, 256, 0, st>>>(n_slots, a.S, mean, stats);
     MFSEG_LAUNCH("feature_stats");
     int h = 0;
@@ -619,6 +631,7 @@ int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *key
     MFSEG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
     MFSEG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
     unsigned g = (unsigned)((n + 255) / 256);
+    ::mfseg::count_launch();
     k_link_keys<<<g, 256, 0, st>>>(n, pts->xyz, pts->t, f->nx, f->ny, f->nz, f->origin[0],
                                    f->origin[1], f->origin[2], f->spacing[0], f->spacing[1],
                                    f->spacing[2], f->times, f->nt, k0, v0, bad);
@@ -627,6 +640,7 @@ int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *key
     unsigned long long maxkey = (unsigned long long)f->nx * f->ny * f->nz * n_int;
     MFSEG_TRY(radix_sort_pairs64(k0, v0, (unsigned long long *)keys, (unsigned *)members, n,
                                  bits_of(maxkey), rtmp, rb, st));
+    ::mfseg::count_launch();
     k_count_runs<<<g, 256, 0, st>>>((const unsigned long long *)keys, n, cnt);
     MFSEG_LAUNCH("k_count_runs");
     int hb = 0;

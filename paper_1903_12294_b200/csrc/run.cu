@@ -1,5 +1,6 @@
 // Host-side runtime of the segmentation core: workspace plan, point binning,
 // field tiling, the pass loop of engine.run (engine.py:323-381) and the C ABI.
+#include <atomic>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -7,6 +8,40 @@
 #include "kernels.cuh"
 
 namespace mfseg {
+
+// ------------------------------------------------------------------ instrumentation
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// per-phase device times of mfseg_run (CUDA events on the caller's stream),
+// read by bench.py for the roofline of the dominant kernel
+struct PhaseTimer {
+    bool on = false;
+    double ms[8] = {0};      // 0 grid, 1 field assign, 2 point assign, 3 fallback, 4 update
+    long long launches[8] = {0};
+    int passes = 0;
+};
+static PhaseTimer g_timer;
+static cudaEvent_t g_ev[6];
+static bool g_ev_made = false;
+
+static void mark(int i, cudaStream_t st) {
+    if (!g_timer.on) return;
+    if (!g_ev_made) {
+        for (auto &e : g_ev) cudaEventCreate(&e);
+        g_ev_made = true;
+    }
+    cudaEventRecord(g_ev[i], st);
+}
+
+// after the stream has been synchronised: fold the pass's event intervals in
+static void harvest() {
+    if (!g_timer.on || !g_ev_made) return;
+    float t;
+    for (int i = 0; i < 5; ++i)
+        if (cudaEventElapsedTime(&t, g_ev[i], g_ev[i + 1]) == cudaSuccess) g_timer.ms[i] += t;
+    g_timer.passes++;
+}
 
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_err;
@@ -342,6 +377,7 @@ int plan_prepare(Plan &P) {
         MFSEG_CUDA(cudaMemcpyAsync(P.zt, zt.data(), sizeof(AxisTile) * zt.size(),
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaStreamSynchronize(st));   // host vectors die at scope exit
+        ::mfseg::count_launch();
         k_tbins<<<(P.f.nt + 255) / 256, 256, 0, st>>>(P.f.nt, P.f.times, p.mins[3], p.C[3],
                                                         p.k[3], P.tbin);
         MFSEG_LAUNCH("k_tbins");
@@ -352,20 +388,25 @@ int plan_prepare(Plan &P) {
         double4 C = make_double4(p.C[0], p.C[1], p.C[2], p.C[3]);
         int4 k = make_int4(p.k[0], p.k[1], p.k[2], p.k[3]);
         unsigned gb = (unsigned)((n + 255) / 256);
+        ::mfseg::count_launch();
         k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, k, P.keys, P.vals);
         MFSEG_LAUNCH("k_point_keys");
         MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, bits_for(P.NB - 1),
                                    P.radix_tmp, P.radix_bytes, st));
+        ::mfseg::count_launch();
         k_point_gather<<<gb, 256, 0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px,
                                            P.py, P.pz, P.pt, P.pv);
         MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (P.NB + 1), st));
+        ::mfseg::count_launch();
         k_bin_hist<<<gb, 256, 0, st>>>(n, P.skeys, P.bcnt);
         MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, P.NB + 1, P.scan_tmp, P.scan_bytes, st));
         int TP = point_tile_size();
         unsigned gk = (unsigned)((P.NB + 256) / 256);
         MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (P.NB + 1), st));
+        ::mfseg::count_launch();
         k_tiles_per_bin<<<gk, 256, 0, st>>>(P.NB, P.bcnt, TP, P.btiles);
         MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, P.NB + 1, P.scan_tmp, P.scan_bytes, st));
+        ::mfseg::count_launch();
         k_make_tiles<<<gk, 256, 0, st>>>(P.NB, P.bcnt, P.bfirst, P.tstart, TP, P.tiles);
         MFSEG_LAUNCH("point tiles");
     }
@@ -392,8 +433,10 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     const mfseg_params &p = P.p;
     int K = P.K;
     CentersView cv = view_of(c, K);
+    mark(0, st);
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
                          P.count_tmp, P.grid_scan_tmp, st));
+    mark(1, st);
     MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 4, st));
     if (accumulate)
         MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
@@ -440,6 +483,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         long long ntiles = (long long)P.ntx * P.nty * P.ntz * P.f.nt;
         MFSEG_TRY(launch_field_assign(a, ntiles, st));
     }
+    mark(2, st);
     if (P.np > 0) {
         PointArgs a;
         memset(&a, 0, sizeof a);
@@ -471,6 +515,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.accumulate = accumulate;
         MFSEG_TRY(launch_point_assign(a, P.max_tiles, st));
     }
+    mark(3, st);
     // stranded samples
     for (int kind = 0; kind < 2; ++kind) {
         if (kind == 1 && P.nf == 0) continue;
@@ -513,6 +558,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.accumulate = accumulate;
         MFSEG_TRY(launch_fallback(a, st));
     }
+    mark(4, st);
     return 0;
 }
 
@@ -537,6 +583,18 @@ using namespace mfseg;
 extern "C" {
 
 const char *mfseg_last_error(void) { return mfseg::g_err.c_str(); }
+
+long long mfseg_launch_count(void) { return mfseg::g_launches.load(); }
+
+void mfseg_timing_enable(int32_t on) {
+    mfseg::g_timer = mfseg::PhaseTimer();
+    mfseg::g_timer.on = on != 0;
+}
+
+int32_t mfseg_timing_read(double *ms_out, int32_t n) {
+    for (int i = 0; i < n && i < 8; ++i) ms_out[i] = mfseg::g_timer.ms[i];
+    return mfseg::g_timer.passes;
+}
 int mfseg_abi_version(void) { return MFSEG_ABI_VERSION; }
 
 size_t mfseg_run_workspace_size(const mfseg_params *p, const mfseg_field *f,
@@ -581,6 +639,7 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
     double4 C = make_double4(p->C[0], p->C[1], p->C[2], p->C[3]);
     int4 k = make_int4(p->k[0], p->k[1], p->k[2], p->k[3]);
     unsigned gk = (unsigned)((K + 255) / 256);
+    ::mfseg::count_launch();
     k_seed<<<gk, 256, 0, st>>>(K, mins, C, k, P.s[0]);
     MFSEG_LAUNCH("k_seed");
     int cur = 0;
@@ -602,7 +661,12 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
             MFSEG_TRY(launch_from_limbs(npairs, P.limbs, P.acc, st));
         }
         MFSEG_TRY(launch_update(K, P.acc, P.s[cur], P.s[cur ^ 1], p->eps_c, P.flags, st));
+        mark(5, st);
         cur ^= 1;
+        if (g_timer.on) {
+            MFSEG_CUDA(cudaStreamSynchronize(st));
+            harvest();
+        }
         if (initial) continue;
         MFSEG_CUDA(cudaMemcpyAsync(flags_host, P.flags, update_flags_bytes(),
                                    cudaMemcpyDeviceToHost, st));
@@ -615,10 +679,12 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
     }
     MFSEG_TRY(check_overflow(P));
     if (P.np > 0) {
+        ::mfseg::count_launch();
         k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,
                                                                      point_labels);
         MFSEG_LAUNCH("k_unpermute");
     }
+    ::mfseg::count_launch();
     k_copy_state<<<gk, 256, 0, st>>>(K, P.s[cur], out);
     MFSEG_LAUNCH("k_copy_state");
     if (iterations_used_host) *iterations_used_host = iterations;
@@ -636,6 +702,7 @@ int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     MFSEG_TRY(plan_prepare(P));
     MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1));
     if (P.np > 0) {
+        ::mfseg::count_launch();
         k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,
                                                                      point_labels);
         MFSEG_LAUNCH("k_unpermute");
@@ -708,6 +775,7 @@ int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_
     MFSEG_CUDA(cudaMallocAsync((void **)&mm, 16, st));
     unsigned long long init[2] = {~0ull, 0ull};
     MFSEG_CUDA(cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
+    ::mfseg::count_launch();
     k_minmax<<<148 * 4, 256, 0, st>>>(values, n, mm);
     MFSEG_LAUNCH("k_minmax");
     unsigned long long h[2];
@@ -720,9 +788,20 @@ int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_
     if (apply) {
         // (v - lo) / (hi - lo); degenerate range maps to 0 (ingest.py:312-318)
         volatile double span = hi - lo;
+        ::mfseg::count_launch();
         k_normalize<<<148 * 8, 256, 0, st>>>(values, n, lo, span, hi == lo);
         MFSEG_LAUNCH("k_normalize");
     }
+    return 0;
+}
+
+int mfseg_normalize_range(double *values, int64_t n, double lo, double hi, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) return 0;
+    volatile double span = hi - lo;
+    ::mfseg::count_launch();
+    k_normalize<<<148 * 8, 256, 0, st>>>(values, n, lo, span, hi == lo);
+    MFSEG_LAUNCH("k_normalize");
     return 0;
 }
 

@@ -107,8 +107,11 @@ int scan_impl(const T *in, T *out, long long n, void *tmp, size_t tmp_bytes, cud
     T *sums = (T *)tmp;
     // k_tile_sums sums in a strided order; k_tile_scan uses a blocked order, but both
     // cover the same tile so the per-tile totals agree.
+    ::mfseg::count_launch();
     k_tile_sums<T><<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, n, sums);
+    ::mfseg::count_launch();
     k_scan_small<T><<<1, SCAN_BLOCK, 0, st>>>(sums, tiles);
+    ::mfseg::count_launch();
     k_tile_scan<T><<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, out, n, sums);
     MFSEG_LAUNCH("scan");
     return 0;
@@ -216,9 +219,11 @@ int radix_impl(const K *keys_in, const unsigned *vals_in, K *keys_out, unsigned 
         K *ko = to_out ? keys_out : kb;
         unsigned *vo = to_out ? vals_out : vb;
         (void)last;
+        ::mfseg::count_launch();
         k_digit_hist<K><<<(unsigned)tiles, RS_BLOCK, 0, st>>>(ki, n, 8 * p, counts, tiles);
         MFSEG_TRY(scan_exclusive_i32((const int *)counts, (int *)offs, 256 * tiles,
                                      scratch, tmp_bytes - used, st));
+        ::mfseg::count_launch();
         k_digit_scatter<K><<<(unsigned)tiles, RS_BLOCK, 0, st>>>(ki, vi, ko, vo, n, 8 * p, offs,
                                                                  tiles);
         MFSEG_LAUNCH("radix scatter");

@@ -147,6 +147,7 @@ extern "C" {
 
 int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream) {
     Blobs B = make_blobs(s);
+    ::mfseg::count_launch();
     k_synth_field<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, values);
     MFSEG_LAUNCH("k_synth_field");
     return 0;
@@ -155,6 +156,7 @@ int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream) {
 int mfseg_synth_points(const mfseg_synth *s, int64_t *traj_id, double *t, double *xyz,
                        double *value, void *stream) {
     Blobs B = make_blobs(s);
+    ::mfseg::count_launch();
     k_synth_points<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, (long long *)traj_id, t,
                                                                xyz, value);
     MFSEG_LAUNCH("k_synth_points");

@@ -217,6 +217,7 @@ size_t update_flags_bytes() { return sizeof(Flags); }
 int launch_update(int K, const unsigned long long *acc, mfseg_centers o, mfseg_centers n,
                   double eps_c, void *flags_dev, cudaStream_t st) {
     MFSEG_CUDA(cudaMemsetAsync(flags_dev, 0, sizeof(Flags), st));
+    ::mfseg::count_launch();
     k_update<<<(K + 255) / 256, 256, 0, st>>>(K, acc, o, n, eps_c, (Flags *)flags_dev);
     MFSEG_LAUNCH("k_update");
     return 0;
@@ -240,6 +241,7 @@ void decode_flags(const void *flags_host, int *converged, double *delta) {
 int launch_acc_to_double(int K, const unsigned long long *acc, double *sums, double *psum,
                          double *fsum, long long *n_p, long long *n_f, cudaStream_t st) {
     if (K <= 0) return 0;
+    ::mfseg::count_launch();
     k_acc_to_double<<<(K + 255) / 256, 256, 0, st>>>(K, acc, sums, psum, fsum, n_p, n_f);
     MFSEG_LAUNCH("k_acc_to_double");
     return 0;
@@ -248,6 +250,7 @@ int launch_acc_to_double(int K, const unsigned long long *acc, double *sums, dou
 int launch_to_limbs(long long npairs, const unsigned long long *acc, long long *limbs,
                     cudaStream_t st) {
     if (npairs <= 0) return 0;
+    ::mfseg::count_launch();
     k_to_limbs<<<(unsigned)((npairs + 255) / 256), 256, 0, st>>>(npairs, acc, limbs);
     MFSEG_LAUNCH("k_to_limbs");
     return 0;
@@ -256,6 +259,7 @@ int launch_to_limbs(long long npairs, const unsigned long long *acc, long long *
 int launch_from_limbs(long long npairs, const long long *limbs, unsigned long long *acc,
                       cudaStream_t st) {
     if (npairs <= 0) return 0;
+    ::mfseg::count_launch();
     k_from_limbs<<<(unsigned)((npairs + 255) / 256), 256, 0, st>>>(npairs, limbs, acc);
     MFSEG_LAUNCH("k_from_limbs");
     return 0;
@@ -271,6 +275,7 @@ int mfseg_update_centers_f64(int32_t K, const double *sums, const double *psum, 
                              const int64_t *n_p, const int64_t *n_f, mfseg_centers old_state,
                              mfseg_centers new_state, void *stream) {
     if (K <= 0) return 0;
+    ::mfseg::count_launch();
     k_update_f64<<<(K + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
         K, sums, psum, fsum, (const long long *)n_p, (const long long *)n_f, old_state, new_state);
     MFSEG_LAUNCH("k_update_f64");
@@ -283,7 +288,10 @@ int mfseg_compare_centers(int32_t K, mfseg_centers old_state, mfseg_centers new_
     Flags *fl = nullptr;
     MFSEG_CUDA(cudaMallocAsync((void **)&fl, sizeof(Flags), st));
     MFSEG_CUDA(cudaMemsetAsync(fl, 0, sizeof(Flags), st));
-    if (K > 0) k_compare<<<(K + 255) / 256, 256, 0, st>>>(K, old_state, new_state, eps_c, fl);
+    if (K > 0) {
+        ::mfseg::count_launch();
+        k_compare<<<(K + 255) / 256, 256, 0, st>>>(K, old_state, new_state, eps_c, fl);
+    }
     MFSEG_LAUNCH("k_compare");
     Flags h;
     MFSEG_CUDA(cudaMemcpyAsync(&h, fl, sizeof(Flags), cudaMemcpyDeviceToHost, st));
