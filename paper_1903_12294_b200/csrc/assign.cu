@@ -23,6 +23,7 @@
 // (independent of the GPU count) and integer addition is associative, so the
 // sums are deterministic and shard-count independent.
 #include <climits>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -693,7 +694,10 @@ int field_tile_dims(int *tx, int *ty, int *tz) {
 }
 int point_tile_size() { return PNT * PSPT; }
 
+int launch_field_assign_v2(const FieldArgs &a, long long ntiles, cudaStream_t st);
+
 int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st) {
+    if (getenv("MFSEG_FIELD_V1") == nullptr) return launch_field_assign_v2(a, ntiles, st);
     if (ntiles <= 0) return 0;
     if (ntiles > 0x7fffffffll) {
         set_error("field tile grid too large");

@@ -27,6 +27,7 @@ struct FieldArgs {
     long long stranded_cap;
     int *overflow;
     int accumulate;
+    int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor
 };
 
 struct PointArgs {

@@ -1,6 +1,7 @@
 // Host-side runtime of the segmentation core: workspace plan, point binning,
 // field tiling, the pass loop of engine.run (engine.py:323-381) and the C ABI.
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -480,6 +481,10 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded_cap = P.cap_f;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
+        {
+            const char *dbg = getenv("MFSEG_DEBUG");
+            a.debug = dbg ? atoi(dbg) : 0;
+        }
         long long ntiles = (long long)P.ntx * P.nty * P.ntz * P.f.nt;
         MFSEG_TRY(launch_field_assign(a, ntiles, st));
     }
