@@ -349,3 +349,97 @@ def test_labels_deterministic_across_reruns():
     sb = CenterState.from_device(b.state)
     assert torch.equal(la, b.field_labels) and torch.equal(lb, b.point_labels)
     np.testing.assert_array_equal(sa.loc, sb.loc)
+
+
+def test_time_slab_sharding_bit_identical():
+    """Two 'ranks' emulated on one GPU: per pass each time slab is assigned
+    separately, the exact 128-bit partial sums are summed through the limb
+    encoding (as the NCCL exchange does), and the centres updated.  Labels and
+    centres must equal the single-GPU run bit for bit."""
+    import ctypes as C
+    from paper_1903_12294_b200 import ClusterParams, _native as N
+    from paper_1903_12294_b200.engine import (DeviceField, DevicePoints, CenterState, _run_assign,
+                                              empty_state, make_params, run_device, state_struct,
+                                              stream_ptr)
+    from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
+    from paper_1903_12294_b200.model import interval_distances
+    from paper_1903_12294_b200.parallel import time_slab
+    lib = N.load()
+    dims, nt = (32, 24, 16), 8
+    fld, pts, _ = _synthetic(dims, nt, 2000, 21, False)
+    normalize_device(pts, fld, True)
+    ext = domain_extent_device(pts, fld)
+    params = ClusterParams(k=(4, 4, 4, 4), w_d=0.8, eps_c=1e-12, max_iterations=4)
+    ref = run_device(pts, fld, ext, params)
+    ref_state = CenterState.from_device(ref.state)
+    K = params.k_total
+    C_ = interval_distances(ext, params.k)
+    ncell = int(np.prod(dims))
+    slabs = []
+    for r in range(2):
+        m0, m1 = time_slab(r, 2, nt)
+        sel = (pts.t >= m0) & (pts.t < m1)
+        slabs.append((DevicePoints(pts.xyz[sel].contiguous(), pts.t[sel].contiguous(),
+                                   pts.value[sel].contiguous()),
+                      DeviceField(fld.dims, fld.origin, fld.spacing, fld.times[m0:m1].clone(),
+                                  fld.values[m0 * ncell:m1 * ncell].clone()),
+                      sel))
+    seeds = CenterState.from_seeds(P_seed(ext, params.k))
+    state = seeds.to_device()
+    for it in range(params.max_iterations + 1):
+        w = (1.0, 0.0, 0.0) if it == 0 else None
+        prm = make_params(ext.mins, C_, params, w)
+        limbs = None
+        labs = []
+        for sp, sf, _ in slabs:
+            pl, fl, acc = _run_assign(sp, sf, state, prm, K)
+            lb = torch.empty(K * 8 * 3, dtype=torch.int64, device=acc.device)
+            N.check(lib.mfseg_acc_to_limbs(N.ptr(acc), K * 8, N.ptr(lb), stream_ptr()), "limbs")
+            limbs = lb if limbs is None else limbs + lb
+            labs.append((pl, fl))
+        acc = torch.empty((K, N.ACC_WORDS), dtype=torch.int64, device=limbs.device)
+        N.check(lib.mfseg_limbs_to_acc(N.ptr(limbs), K * 8, N.ptr(acc), stream_ptr()), "from limbs")
+        new = empty_state(K)
+        conv, delta = C.c_int32(0), C.c_double(0.0)
+        N.check(lib.mfseg_update_centers(K, N.ptr(acc), state_struct(state), state_struct(new),
+                                         params.eps_c, C.byref(conv), C.byref(delta), stream_ptr()),
+                "update")
+        state = new
+        if it > 0 and conv.value:
+            break
+    field_labels = torch.cat([labs[0][1], labs[1][1]])
+    assert torch.equal(field_labels, ref.field_labels)
+    point_labels = torch.empty_like(ref.point_labels)
+    point_labels[slabs[0][2]] = labs[0][0]
+    point_labels[slabs[1][2]] = labs[1][0]
+    assert torch.equal(point_labels, ref.point_labels)
+    st = CenterState.from_device(state)
+    np.testing.assert_array_equal(st.loc, ref_state.loc)
+    np.testing.assert_array_equal(st.pval, ref_state.pval)
+    np.testing.assert_array_equal(st.fval, ref_state.fval)
+
+
+def P_seed(ext, k):
+    from paper_1903_12294_b200 import seed_centers
+    return seed_centers(ext, k)
+
+
+def test_limb_kernels_match_python_encoding():
+    from paper_1903_12294_b200 import _native as N
+    from paper_1903_12294_b200.engine import stream_ptr
+    lib = N.load()
+    rng = np.random.default_rng(3)
+    vals = [int(x) * (1 << 50) + int(y) for x, y in zip(rng.integers(-2**60, 2**60, 64),
+                                                         rng.integers(0, 2**50, 64))]
+    lo = [(v & ((1 << 64) - 1)) for v in vals]
+    hi = [((v >> 64) & ((1 << 64) - 1)) for v in vals]
+    acc = torch.tensor(np.array([x for pair in zip(lo, hi) for x in pair], dtype=np.uint64).view(np.int64),
+                       device="cuda")
+    limbs = torch.empty(64 * 3, dtype=torch.int64, device="cuda")
+    N.check(lib.mfseg_acc_to_limbs(N.ptr(acc), 64, N.ptr(limbs), stream_ptr()), "limbs")
+    L = limbs.cpu().numpy().tolist()
+    for i, v in enumerate(vals):
+        assert L[3 * i] + (L[3 * i + 1] << 42) + (L[3 * i + 2] << 84) == v
+    back = torch.empty_like(acc)
+    N.check(lib.mfseg_limbs_to_acc(N.ptr(limbs), 64, N.ptr(back), stream_ptr()), "acc")
+    assert torch.equal(back, acc)
