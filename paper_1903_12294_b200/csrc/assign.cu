@@ -709,7 +709,10 @@ int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st) {
     return 0;
 }
 
+int launch_point_assign_v3(const PointArgs &a, long long max_tiles, cudaStream_t st);
+
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st) {
+    if (getenv("MFSEG_POINT_V1") == nullptr) return launch_point_assign_v3(a, max_tiles, st);
     if (max_tiles <= 0) return 0;
     ::mfseg::count_launch();
     k_point_assign<PNT, PSPT><<<(unsigned)max_tiles, PNT, 0, st>>>(a);

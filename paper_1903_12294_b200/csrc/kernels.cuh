@@ -48,6 +48,7 @@ struct PointArgs {
     long long stranded_cap;
     int *overflow;
     int accumulate;
+    int debug;
 };
 
 // Stranded-sample fallback (engine.py:195-205): field samples (kind 1) are

@@ -82,15 +82,41 @@ __global__ void k_tbins(int nt, const double *times, double mn, double C, int k,
     if (m < nt) tbin[m] = bin_coord(times[m], mn, C, k);
 }
 
+// Sort key of a point: (sample bin, field-timestep interval, sub-cell), the
+// sub-cell being the Morton interleave of 8 subdivisions per axis inside the
+// bin (t, z, y, x bits from high to low), so consecutive points - a warp's
+// 64 - form compact 4D blocks.  Tiles are cut per (bin, interval) group.
 __global__ void k_point_keys(long long n, const double *xyz, const double *t, double4 mins,
-                             double4 C, int4 k, unsigned *keys, unsigned *vals) {
+                             double4 C, int4 k, const double *times, int nt, int sub_bits,
+                             unsigned *keys, unsigned *vals) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int bx = bin_coord(xyz[3 * i], mins.x, C.x, k.x);
-    int by = bin_coord(xyz[3 * i + 1], mins.y, C.y, k.y);
-    int bz = bin_coord(xyz[3 * i + 2], mins.z, C.z, k.z);
-    int bt = bin_coord(t[i], mins.w, C.w, k.w);
-    keys[i] = (unsigned)(((bt * k.z + bz) * k.y + by) * k.x + bx);
+    const double c[4] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], t[i]};
+    const double mn[4] = {mins.x, mins.y, mins.z, mins.w}, CC[4] = {C.x, C.y, C.z, C.w};
+    const int kk[4] = {k.x, k.y, k.z, k.w};
+    int b[4];
+    unsigned sd[4];
+    for (int d = 0; d < 4; ++d) {
+        const double u = DDIV(DSUB(c[d], mn[d]), CC[d]);
+        b[d] = bin_coord(c[d], mn[d], CC[d], kk[d]);
+        const double f = floor(DMUL(u, 8.0)) - 8.0 * b[d];
+        sd[d] = f < 0.0 ? 0u : (f > 7.0 ? 7u : (unsigned)f);
+    }
+    unsigned sub = 0;
+    for (int bit = 2; bit >= 0; --bit)          // Morton: high bits first, x lowest
+        for (int d = 3; d >= 0; --d) sub = (sub << 1) | ((sd[d] >> bit) & 1u);
+    sub >>= (12 - sub_bits);
+    int m = 0;
+    if (nt > 1) {   // searchsorted(times, t, 'right') - 1, clipped to [0, nt-1]
+        int a = 0, e = nt;
+        while (a < e) {
+            const int mid = (a + e) >> 1;
+            if (times[mid] <= c[3]) a = mid + 1; else e = mid;
+        }
+        m = a - 1 < 0 ? 0 : a - 1;
+    }
+    const unsigned bin = (unsigned)(((b[3] * k.z + b[2]) * k.y + b[1]) * k.x + b[0]);
+    keys[i] = (((unsigned)((unsigned long long)bin * nt + m)) << sub_bits) | sub;
     vals[i] = (unsigned)i;
 }
 
@@ -107,9 +133,9 @@ __global__ void k_point_gather(long long n, const unsigned *perm, const double *
     pv[i] = value[j];
 }
 
-__global__ void k_bin_hist(long long n, const unsigned *skeys, int *cnt) {
+__global__ void k_bin_hist(long long n, const unsigned *skeys, int shift, int *cnt) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[skeys[i]], 1);
+    if (i < n) atomicAdd(&cnt[skeys[i] >> shift], 1);
 }
 
 __global__ void k_tiles_per_bin(int nb, const int *cnt, int tp, int *ntiles) {
@@ -117,12 +143,13 @@ __global__ void k_tiles_per_bin(int nb, const int *cnt, int tp, int *ntiles) {
     if (b < nb) ntiles[b] = (cnt[b] + tp - 1) / tp;
 }
 
-__global__ void k_make_tiles(int nb, const int *cnt, const int *first, const int *tstart, int tp,
-                             int4 *tiles) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nb) return;
-    int n = cnt[b], f = first[b], o = tstart[b];
-    for (int q = 0; q * tp < n; ++q) tiles[o + q] = make_int4(b, f + q * tp, min(tp, n - q * tp), 0);
+__global__ void k_make_tiles(int ng, const int *cnt, const int *first, const int *tstart, int tp,
+                             int per_bin, int4 *tiles) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    int n = cnt[g], f = first[g], o = tstart[g];
+    for (int q = 0; q * tp < n; ++q)
+        tiles[o + q] = make_int4(g / per_bin, f + q * tp, min(tp, n - q * tp), g);
 }
 
 __global__ void k_unpermute(long long n, const unsigned *perm, const int *src, int *dst) {
@@ -219,7 +246,8 @@ struct Plan {
     unsigned *keys, *vals, *skeys, *perm;
     double *px, *py, *pz, *pt, *pv;
     int *plabels;                   // bin-sorted labels
-    int *bcnt, *bfirst, *btiles, *tstart;
+    int *bcnt, *bfirst, *btiles, *tstart;   // per (bin, interval) group
+    int ngroups, nint, sub_bits, key_bits;
     int4 *tiles;
     long long max_tiles;
     long long *stranded_p;
@@ -326,17 +354,28 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.pt = cv.take<double>(n);
     P.pv = cv.take<double>(n);
     P.plabels = cv.take<int>(n);
-    P.bcnt = cv.take<int>(NB + 1);
-    P.bfirst = cv.take<int>(NB + 1);
-    P.btiles = cv.take<int>(NB + 1);
-    P.tstart = cv.take<int>(NB + 1);
-    P.max_tiles = n > 0 ? (n + TP - 1) / TP + NB : 0;
+    // point tile groups: one per sample bin.  (A bin never straddles a time
+    // slab because multi-GPU slabs are whole t-bins, parallel.time_slab.)
+    P.nint = 1;
+    {
+        long long G = (long long)NB * P.nint;
+        int gb = bits_for(G - 1);
+        P.ngroups = (int)G;
+        P.sub_bits = gb + 12 <= 32 ? 12 : (32 - gb > 0 ? 32 - gb : 0);
+        P.key_bits = gb + P.sub_bits;
+    }
+    const int NG = P.ngroups;
+    P.bcnt = cv.take<int>(NG + 1);
+    P.bfirst = cv.take<int>(NG + 1);
+    P.btiles = cv.take<int>(NG + 1);
+    P.tstart = cv.take<int>(NG + 1);
+    P.max_tiles = n > 0 ? (n + TP - 1) / TP + NG : 0;
     P.tiles = cv.take<int4>(P.max_tiles);
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
     P.radix_bytes = n > 0 ? radix_tmp_bytes(n) : 0;
     P.radix_tmp = cv.take<char>(P.radix_bytes);
-    P.scan_bytes = scan_tmp_bytes((long long)NB + 1) + 1024;
+    P.scan_bytes = scan_tmp_bytes((long long)(NG > NB ? NG : NB) + 1) + 1024;
     P.scan_tmp = cv.take<char>(P.scan_bytes);
     return cv.off + 1024;
 }
@@ -390,25 +429,31 @@ int plan_prepare(Plan &P) {
         int4 k = make_int4(p.k[0], p.k[1], p.k[2], p.k[3]);
         unsigned gb = (unsigned)((n + 255) / 256);
         ::mfseg::count_launch();
-        k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, k, P.keys, P.vals);
+        k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, k, P.f.times, P.nint,
+                                         P.sub_bits, P.keys, P.vals);
         MFSEG_LAUNCH("k_point_keys");
-        MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, bits_for(P.NB - 1),
-                                   P.radix_tmp, P.radix_bytes, st));
+        if (P.key_bits > 32) {
+            set_error("too many (bin, timestep) groups for 32-bit point keys");
+            return 2;
+        }
+        MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, P.key_bits, P.radix_tmp,
+                                   P.radix_bytes, st));
         ::mfseg::count_launch();
         k_point_gather<<<gb, 256, 0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px,
                                            P.py, P.pz, P.pt, P.pv);
-        MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (P.NB + 1), st));
+        const int NG = P.ngroups;
+        MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (NG + 1), st));
         ::mfseg::count_launch();
-        k_bin_hist<<<gb, 256, 0, st>>>(n, P.skeys, P.bcnt);
-        MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, P.NB + 1, P.scan_tmp, P.scan_bytes, st));
+        k_bin_hist<<<gb, 256, 0, st>>>(n, P.skeys, P.sub_bits, P.bcnt);
+        MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, NG + 1, P.scan_tmp, P.scan_bytes, st));
         int TP = point_tile_size();
-        unsigned gk = (unsigned)((P.NB + 256) / 256);
-        MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (P.NB + 1), st));
+        unsigned gk = (unsigned)((NG + 256) / 256);
+        MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (NG + 1), st));
         ::mfseg::count_launch();
-        k_tiles_per_bin<<<gk, 256, 0, st>>>(P.NB, P.bcnt, TP, P.btiles);
-        MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, P.NB + 1, P.scan_tmp, P.scan_bytes, st));
+        k_tiles_per_bin<<<gk, 256, 0, st>>>(NG, P.bcnt, TP, P.btiles);
+        MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, NG + 1, P.scan_tmp, P.scan_bytes, st));
         ::mfseg::count_launch();
-        k_make_tiles<<<gk, 256, 0, st>>>(P.NB, P.bcnt, P.bfirst, P.tstart, TP, P.tiles);
+        k_make_tiles<<<gk, 256, 0, st>>>(NG, P.bcnt, P.bfirst, P.tstart, TP, P.nint, P.tiles);
         MFSEG_LAUNCH("point tiles");
     }
     return 0;
@@ -499,7 +544,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.t = P.pt;
         a.v = P.pv;
         a.tiles = P.tiles;
-        a.n_tiles = P.tstart + P.NB;
+        a.n_tiles = P.tstart + P.ngroups;
         a.Cx = p.C[0];
         a.Cy = p.C[1];
         a.Cz = p.C[2];
@@ -518,6 +563,10 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded_cap = P.cap_p;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
+        {
+            const char *dbg = getenv("MFSEG_DEBUG");
+            a.debug = dbg ? atoi(dbg) : 0;
+        }
         MFSEG_TRY(launch_point_assign(a, P.max_tiles, st));
     }
     mark(3, st);

@@ -60,11 +60,13 @@ def _state(case, prefix):
                          case[prefix + "n_fields"].copy(), case[prefix + "dormant"].copy())
 
 
-def _close(got, want, rtol):
+def _close(got, want, rtol, scale=1.0):
+    """|got - want| <= rtol * max(|want|, scale): relative, except near zero where
+    sums of O(scale) terms cancel (e.g. a mean of noise around 0)."""
     got, want = np.asarray(got, float), np.asarray(want, float)
     assert got.shape == want.shape
     both_nan = np.isnan(got) & np.isnan(want)
-    ok = both_nan | (np.abs(got - want) <= rtol * np.maximum(np.abs(want), 1e-300))
+    ok = both_nan | (np.abs(got - want) <= rtol * np.maximum(np.abs(want), scale))
     assert ok.all(), (got[~ok][:5], want[~ok][:5])
 
 

@@ -14,8 +14,10 @@ ext = domain_extent_device(pts, fld)
 params = ClusterParams(k=cfg["k"], eps_c=1e-12, max_iterations=iters)
 res = {}
 for tag in ("v1", "v2"):
-    if tag == "v1": os.environ["MFSEG_FIELD_V1"] = "1"
-    else: os.environ.pop("MFSEG_FIELD_V1", None)
+    if tag == "v1":
+        os.environ["MFSEG_FIELD_V1"] = "1"; os.environ["MFSEG_POINT_V1"] = "1"
+    else:
+        os.environ.pop("MFSEG_FIELD_V1", None); os.environ.pop("MFSEG_POINT_V1", None)
     r = run_device(pts, fld, ext, params)
     torch.cuda.synchronize()
     t0 = time.perf_counter(); r = run_device(pts, fld, ext, params); torch.cuda.synchronize()
