@@ -14,6 +14,8 @@ struct FieldArgs {
     const AxisTile *xt, *yt, *zt;
     int ntx, nty, ntz;
     const int *tbin;
+    const AxisTile *tt;   // time tiles: runs of <= 4 timesteps inside one t-bin
+    int ntt;
     int kx, ky, kz, kt;
     double cf, wd, wv;
     CentersView c;

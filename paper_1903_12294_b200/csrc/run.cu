@@ -236,8 +236,9 @@ struct Plan {
     void *grid_scan_tmp;
     // field
     AxisTile *xt, *yt, *zt;
-    int ntx, nty, ntz;
+    int ntx, nty, ntz, ntt;
     int *tbin;
+    AxisTile *tt;
     long long *stranded_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
@@ -339,6 +340,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.yt = cv.take<AxisTile>(P.nty);
     P.zt = cv.take<AxisTile>(P.ntz);
     P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
+    P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     // points
@@ -415,6 +417,23 @@ int plan_prepare(Plan &P) {
         MFSEG_CUDA(cudaMemcpyAsync(P.yt, yt.data(), sizeof(AxisTile) * yt.size(),
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaMemcpyAsync(P.zt, zt.data(), sizeof(AxisTile) * zt.size(),
+                                   cudaMemcpyHostToDevice, st));
+        // time tiles: runs of <= 4 timesteps with the same t-bin (host copy of the
+        // times; bin_coord on the host rounds exactly like the device)
+        std::vector<double> th(P.f.nt);
+        MFSEG_CUDA(cudaMemcpyAsync(th.data(), P.f.times, sizeof(double) * P.f.nt,
+                                   cudaMemcpyDeviceToHost, st));
+        MFSEG_CUDA(cudaStreamSynchronize(st));
+        std::vector<AxisTile> tts;
+        for (int m0 = 0; m0 < P.f.nt;) {
+            const int b = bin_coord(th[m0], p.mins[3], p.C[3], p.k[3]);
+            int m1 = m0;
+            while (m1 < P.f.nt && m1 - m0 < 4 && bin_coord(th[m1], p.mins[3], p.C[3], p.k[3]) == b) ++m1;
+            tts.push_back(AxisTile{m0, m1 - m0, b, 0});
+            m0 = m1;
+        }
+        P.ntt = (int)tts.size();
+        MFSEG_CUDA(cudaMemcpyAsync(P.tt, tts.data(), sizeof(AxisTile) * tts.size(),
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaStreamSynchronize(st));   // host vectors die at scope exit
         ::mfseg::count_launch();
@@ -508,6 +527,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.nty = P.nty;
         a.ntz = P.ntz;
         a.tbin = P.tbin;
+        a.tt = P.tt;
+        a.ntt = P.ntt;
         a.kx = p.k[0];
         a.ky = p.k[1];
         a.kz = p.k[2];

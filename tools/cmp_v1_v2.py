@@ -13,18 +13,20 @@ normalize_device(pts, fld, True)
 ext = domain_extent_device(pts, fld)
 params = ClusterParams(k=cfg["k"], eps_c=1e-12, max_iterations=iters)
 res = {}
-for tag in ("v1", "v2"):
+for tag in ("v1", "v2", "v3"):
+    for e in ("MFSEG_FIELD_V1", "MFSEG_POINT_V1", "MFSEG_FIELD_V3"):
+        os.environ.pop(e, None)
     if tag == "v1":
         os.environ["MFSEG_FIELD_V1"] = "1"; os.environ["MFSEG_POINT_V1"] = "1"
-    else:
-        os.environ.pop("MFSEG_FIELD_V1", None); os.environ.pop("MFSEG_POINT_V1", None)
+    elif tag == "v2":
+        os.environ["MFSEG_FIELD_V3"] = "1"
     r = run_device(pts, fld, ext, params)
     torch.cuda.synchronize()
     t0 = time.perf_counter(); r = run_device(pts, fld, ext, params); torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     res[tag] = (r.field_labels.clone(), r.point_labels.clone(), CenterState.from_device(r.state), dt, r.iterations_used)
     print(tag, "run %.3f s" % dt, "iters", r.iterations_used, flush=True)
-a, b = res["v1"], res["v2"]
+a, b = res["v1"], res["v3"]
 print("field labels identical:", torch.equal(a[0], b[0]), "mismatches:", int((a[0] != b[0]).sum()))
 print("point labels identical:", torch.equal(a[1], b[1]))
 print("centres identical:", np.array_equal(a[2].loc, b[2].loc), "max rel diff:",
