@@ -641,6 +641,109 @@ __global__ void k_fallback(FallbackArgs a) {
     }
 }
 
+// ====================================================================== deferred samples
+// Samples of tiles whose candidate set is too crowded for the fast path
+// (labels -2).  One warp per sample: the reference's windowed predicate
+// (candidates of the sample's bin, exact box test, fp64 D, lowest id on ties),
+// then per-sample fixed-point accumulation; samples without a valid candidate
+// go to the stranded list for k_fallback.
+struct DeferredGeo {
+    Grid g;
+    const int *tbin;
+    int4 k;
+    double mins[4];
+    const long long *list;
+    const unsigned long long *count;
+    long long cap;
+};
+
+__device__ void deferred_one(const FallbackArgs &a, const DeferredGeo &G, long long idx) {
+    const int lane = threadIdx.x & 31;
+    double s0, s1, s2, s3, v;
+    int bt;
+    if (a.kind == 1) {
+        long long r = idx;
+        const int i = (int)(r % a.nx);
+        r /= a.nx;
+        const int j = (int)(r % a.ny);
+        r /= a.ny;
+        const int k = (int)(r % a.nz);
+        const int m = (int)(r / a.nz);
+        s0 = cell_coord(a.ox, a.sx, i);
+        s1 = cell_coord(a.oy, a.sy, j);
+        s2 = cell_coord(a.oz, a.sz, k);
+        s3 = a.times[m];
+        v = a.values[idx];
+        bt = G.tbin[m];
+    } else {
+        s0 = a.px[idx];
+        s1 = a.py[idx];
+        s2 = a.pz[idx];
+        s3 = a.pt[idx];
+        v = a.pv[idx];
+        bt = bin_coord(s3, G.mins[3], a.C[3], G.k.w);
+    }
+    const int bx = bin_coord(s0, G.mins[0], a.C[0], G.k.x);
+    const int by = bin_coord(s1, G.mins[1], a.C[1], G.k.y);
+    const int bz = bin_coord(s2, G.mins[2], a.C[2], G.k.z);
+    const int sbin = ((bt * G.k.z + bz) * G.k.y + by) * G.k.x + bx;
+    double bD = INF;
+    int bI = INT_MAX;
+    for (int p = G.g.cand_start[sbin] + lane; p < G.g.cand_start[sbin + 1]; p += 32) {
+        const int c = G.g.cand_ids[p];
+        const double dx = DSUB(a.c.x[c], s0), dy = DSUB(a.c.y[c], s1), dz = DSUB(a.c.z[c], s2),
+                     dt = DSUB(a.c.t[c], s3);
+        if (!(fabs(dx) <= a.C[0] && fabs(dy) <= a.C[1] && fabs(dz) <= a.C[2] && fabs(dt) <= a.C[3]))
+            continue;
+        const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
+        const double ct = DMUL(a.cf, dt);
+        const bool h = a.chas[c] != 0;
+        const double D = metric_tail(qq, DMUL(ct, ct), v, h ? a.cval[c] : 0.0, h, a.wv, a.wd);
+        if (better(D, c, bD, bI)) {
+            bD = D;
+            bI = c;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oD = __shfl_xor_sync(0xffffffffu, bD, o);
+        const int oI = __shfl_xor_sync(0xffffffffu, bI, o);
+        if (better(oD, oI, bD, bI)) {
+            bD = oD;
+            bI = oI;
+        }
+    }
+    if (lane != 0) return;
+    if (bI == INT_MAX) {   // stranded: the fallback kernel runs next
+        a.labels[idx] = -1;
+        const unsigned long long q = atomicAdd((unsigned long long *)a.n_stranded, 1ull);
+        if ((long long)q < a.cap) ((long long *)a.stranded)[q] = idx;
+        return;
+    }
+    a.labels[idx] = bI;
+    if (a.accumulate) {
+        unsigned long long *p = a.acc + (size_t)bI * MFSEG_ACC_WORDS;
+        atomic_add_double_fix(p + ACC_X + 0, s0, a.overflow);
+        atomic_add_double_fix(p + ACC_X + 2, s1, a.overflow);
+        atomic_add_double_fix(p + ACC_X + 4, s2, a.overflow);
+        atomic_add_double_fix(p + ACC_X + 6, s3, a.overflow);
+        atomic_add_double_fix(p + (a.kind == 1 ? ACC_FV : ACC_PV), v, a.overflow);
+        atomicAdd(p + (a.kind == 1 ? ACC_NF : ACC_NP), 1ull);
+    }
+}
+
+__global__ void k_deferred(FallbackArgs a, DeferredGeo G) {
+    const long long n = (long long)*G.count;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (n <= G.cap) {
+        for (long long q = wid; q < n; q += warps) deferred_one(a, G, G.list[q]);
+    } else {
+        for (long long q = wid; q < a.n_samples; q += warps)
+            if (a.labels[q] == -2) deferred_one(a, G, q);
+    }
+}
+
 // ====================================================================== accumulate (given labels)
 // accumulate (engine.py:244-263) for caller-supplied labels: per-sample fixed
 // point + integer atomics, exact and order-free.
@@ -717,6 +820,23 @@ int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st
     ::mfseg::count_launch();
     k_point_assign<PNT, PSPT><<<(unsigned)max_tiles, PNT, 0, st>>>(a);
     MFSEG_LAUNCH("k_point_assign");
+    return 0;
+}
+
+int launch_deferred(const FallbackArgs &a, const Grid &g, const int *tbin, const int4 &k,
+                    const double *mins, const long long *list, const unsigned long long *count,
+                    long long cap, cudaStream_t st) {
+    DeferredGeo G;
+    G.g = g;
+    G.tbin = tbin;
+    G.k = k;
+    for (int d = 0; d < 4; ++d) G.mins[d] = mins[d];
+    G.list = list;
+    G.count = count;
+    G.cap = cap;
+    ::mfseg::count_launch();
+    k_deferred<<<148 * 4, 256, 0, st>>>(a, G);
+    MFSEG_LAUNCH("k_deferred");
     return 0;
 }
 

@@ -626,7 +626,7 @@ __device__ __forceinline__ __int128 get128(const unsigned long long *p) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
+__global__ void __launch_bounds__(NT, 3) k_field_assign4(FieldArgs a) {
     __shared__ Smem4 S;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     long long tile = blockIdx.x;
@@ -714,23 +714,18 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
         }
     }
 
-    int sl[NS];                        // fast path: survivor slot per sample
-    double bD[NS];                     // exact mode: running best
-    int bI[NS];
+    int sl[NS];                        // survivor slot per sample (-1: stranded)
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        sl[k] = -1;
-        bD[k] = INF_D;
-        bI[k] = INT_MAX;
-    }
+    for (int k = 0; k < NS; ++k) sl[k] = -1;
     int nfast = 0;
     const int L0 = a.g.cand_start[sbin], L1 = a.g.cand_start[sbin + 1];
-    const bool single_chunk = (L1 - L0) <= NT;
+    // crowded candidate lists are deferred whole to k_deferred (exact, per sample)
+    bool deferred = (L1 - L0) > NT;
     const double px = S.x[lx], py = S.y[ly];
 
-    for (int cb = L0; cb < L1; cb += NT) {
+    if (!deferred && L1 > L0) {
         // ---- phase A: exact fp64 bounds over the 4D tile, one candidate per thread
-        const int ci = cb + tid;
+        const int ci = L0 + tid;
         bool have = ci < L1;
         int id = 0;
         double cx = 0, cy = 0, cz = 0, ctr = 0, cv = 0, Dlo = INF_D, Dhi = INF_D;
@@ -790,12 +785,12 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
             off += q < w ? S.wc[q] : 0;
             nsurv += S.wc[q];
         }
-        const bool fast = single_chunk && nsurv <= SCAP;
+        deferred = nsurv > SCAP;
         const int pos = off + __popc(bal & ((1u << lane) - 1u));
-        for (int sb = 0; sb < nsurv; sb += SCAP) {
-            const int cnt = min(SCAP, nsurv - sb);
-            if (surv && pos >= sb && pos < sb + SCAP) {
-                const int p = pos - sb;
+        if (!deferred && nsurv > 0) {
+            const int cnt = nsurv;
+            if (surv) {
+                const int p = pos;
                 S.id[p] = id;
                 S.c[p][0] = cx;
                 S.c[p][1] = cy;
@@ -836,7 +831,7 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
             }
             __syncthreads();
 
-            if (fast) {
+            {
                 nfast = cnt;
                 const float fwd = (float)a.wd;
                 const float vwl = (float)wvlo, vwh = (float)wvhi;
@@ -888,7 +883,7 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
                 cvmax = warp_max_f(cvmax);
                 const float Wb = (useval ? (float)a.wv * (fmaxf(fabsf(vwl), fabsf(vwh)) + cvmax) : 0.f) +
                                  slack;
-                const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) / (1.f - KCULL);
+                const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);   // >= /(1-KCULL)
                 const unsigned keep0 = __ballot_sync(0xffffffffu, lane < cnt && (dl_r[0] <= thr || (a.debug & 1)));
                 const unsigned keep1 =
                     __ballot_sync(0xffffffffu, lane + 32 < cnt && (dl_r[1] <= thr || (a.debug & 1)));
@@ -928,15 +923,14 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
                 }
                 // ---- certify or resolve exactly
                 unsigned need = 0;
-                float thrk[NS];
+                const float wvf = useval ? (float)a.wv : 0.f;
 #pragma unroll
                 for (int k = 0; k < NS; ++k) {
-                    const float W = (useval ? (float)a.wv * (fabsf(fv[k]) + cvmax) : 0.f) + slack;
+                    const float W = fmaf(wvf, fabsf(fv[k]) + cvmax, slack);
                     const bool ok = !(a.debug & 2) && b1[k] < INF_F &&
                                     b2[k] * (1.f - KSCR) > b1[k] * (1.f + KSCR) + 2.f * KSCR * W;
                     sl[k] = ok ? i1[k] : -1;
                     if (!ok && (livem >> k & 1)) need |= 1u << k;
-                    thrk[k] = b1[k] < INF_F ? (b1[k] * (1.f + KSCR) + 2.f * KSCR * W) / (1.f - KSCR) : INF_F;
                 }
                 if (__any_sync(0xffffffffu, need != 0)) {
                     if (need) {
@@ -944,6 +938,11 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
                         for (int k = 0; k < NS; ++k) {
                             if (!(need >> k & 1)) continue;
                             const int zi = lz0 + 2 * (k / TT), ti = k % TT;
+                            const float W = fmaf(wvf, fabsf(fv[k]) + cvmax, slack);
+                            // (b1 (1+k) + 2 k W) / (1-k) <= that * (1 + 2^-17)
+                            const float thrk = b1[k] < INF_F
+                                                   ? (b1[k] * (1.f + KSCR) + 2.f * KSCR * W) * (1.f + 0x1.0p-17f)
+                                                   : INF_F;
                             double eD = INF_D;
                             int eI = INT_MAX, eS = -1;
                             for (int s = 0; s < cnt; ++s) {
@@ -952,7 +951,7 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
                                 if (T[lx] == INF_F || T[TX + ly] == INF_F || az == INF_F) continue;
                                 const float d = fmaf(fwd, sqrt_approx(T[lx] + T[TX + ly] + az),
                                                      S.wvf[s] * fabsf(fv[k] - S.cvf[s]));
-                                if (d > thrk[k]) continue;
+                                if (d > thrk) continue;
                                 const double dx = DSUB(S.c[s][0], px), dy = DSUB(S.c[s][1], py),
                                              dz = DSUB(S.c[s][2], S.z[zi]);
                                 const double ct = DMUL(a.cf, DSUB(S.c[s][3], S.t[ti]));
@@ -972,48 +971,29 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
 #pragma unroll
                 for (int k = 0; k < NS; ++k)
                     if (!(livem >> k & 1)) sl[k] = -1;
-                break;
             }
-            // ---- exact mode (crowded bins): every valid survivor of the window
-            for (int s = 0; s < cnt; ++s) {
-                const float *T = S.tab[s];
-                if (T[lx] == INF_F || T[TX + ly] == INF_F) continue;
-#pragma unroll
-                for (int k = 0; k < NS; ++k) {
-                    const int zi = lz0 + 2 * (k / TT), ti = k % TT;
-                    if (!(livem >> k & 1) || T[TX + TY + zi * TT + ti] == INF_F) continue;
-                    const double dx = DSUB(S.c[s][0], px), dy = DSUB(S.c[s][1], py),
-                                 dz = DSUB(S.c[s][2], S.z[zi]);
-                    const double ct = DMUL(a.cf, DSUB(S.c[s][3], S.t[ti]));
-                    const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
-                    const double D = metric_tail(qq, DMUL(ct, ct), v[k], S.c[s][4], S.has[s], a.wv, a.wd);
-                    if (better(D, S.id[s], bD[k], bI[k])) {
-                        bD[k] = D;
-                        bI[k] = S.id[s];
-                    }
-                }
-            }
-            __syncthreads();
         }
-        if (fast) break;
     }
 
     // ---- labels + stranded list
-    int lab[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-        const bool lv = livem >> k & 1;
-        lab[k] = !lv ? -1 : nfast ? (sl[k] >= 0 ? S.id[sl[k]] : -1) : (bI[k] != INT_MAX ? bI[k] : -1);
-        if (lv) {
-            const long long f = fbase + 2 * (k / TT) * plane + (k % TT) * vol;
-            a.labels[f] = lab[k];
-            if (lab[k] < 0) {
+        if (!(livem >> k & 1)) continue;
+        const long long f = fbase + 2 * (k / TT) * plane + (k % TT) * vol;
+        if (deferred) {
+            a.labels[f] = -2;
+            const unsigned long long p = atomicAdd(a.n_deferred, 1ull);
+            if ((long long)p < a.deferred_cap) a.deferred[p] = f;
+        } else {
+            const int lab = sl[k] >= 0 ? S.id[sl[k]] : -1;
+            a.labels[f] = lab;
+            if (lab < 0) {
                 const unsigned long long p = atomicAdd(a.n_stranded, 1ull);
                 if ((long long)p < a.stranded_cap) a.stranded[p] = f;
             }
         }
     }
-    if (a.accumulate && nfast) {
+    if (a.accumulate && nfast && !deferred) {
         // ---- per-warp records from __reduce_add_sync count marginals
         const unsigned MX = 0x11111111u << (lane & 3);
         const unsigned MY = 0x000F000Fu << (4 * ((lane >> 2) & 3));
@@ -1137,18 +1117,6 @@ __global__ void __launch_bounds__(NT, 2) k_field_assign4(FieldArgs a) {
             if (wd < 4) atomic_add_fix(dst + 2 * wd, (unsigned long long)acc, (long long)(acc >> 64));
             else if (wd == 4) atomic_add_double_fix(dst + 10, vs, &ovf_local);
             else atomicAdd(dst + 13, (unsigned long long)n);
-        }
-    } else if (a.accumulate) {
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            if (lab[k] < 0) continue;
-            unsigned long long *dst = a.acc + (size_t)lab[k] * MFSEG_ACC_WORDS;
-            atomic_add_double_fix(dst + 0, px, &ovf_local);
-            atomic_add_double_fix(dst + 2, py, &ovf_local);
-            atomic_add_double_fix(dst + 4, S.z[lz0 + 2 * (k / TT)], &ovf_local);
-            atomic_add_double_fix(dst + 6, S.t[k % TT], &ovf_local);
-            atomic_add_double_fix(dst + 10, v[k], &ovf_local);
-            atomicAdd(dst + 13, 1ull);
         }
     }
     if (ovf_local) *a.overflow = 1;

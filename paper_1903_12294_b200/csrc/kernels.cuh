@@ -27,6 +27,9 @@ struct FieldArgs {
     long long *stranded;
     unsigned long long *n_stranded;
     long long stranded_cap;
+    long long *deferred;              // samples of crowded tiles, resolved by k_deferred
+    unsigned long long *n_deferred;
+    long long deferred_cap;
     int *overflow;
     int accumulate;
     int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor
@@ -48,6 +51,9 @@ struct PointArgs {
     long long *stranded;
     unsigned long long *n_stranded;
     long long stranded_cap;
+    long long *deferred;
+    unsigned long long *n_deferred;
+    long long deferred_cap;
     int *overflow;
     int accumulate;
     int debug;
@@ -90,6 +96,9 @@ int point_tile_size();
 int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st);
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st);
 int launch_fallback(const FallbackArgs &a, cudaStream_t st);
+int launch_deferred(const FallbackArgs &a, const Grid &g, const int *tbin, const int4 &k,
+                    const double *mins, const long long *list, const unsigned long long *count,
+                    long long cap, cudaStream_t st);
 int launch_accumulate_field(long long n, const mfseg_field *f, const int *labels,
                             unsigned long long *acc, int *overflow, cudaStream_t st);
 int launch_accumulate_points(const mfseg_points *p, const int *labels, unsigned long long *acc,

@@ -239,7 +239,7 @@ struct Plan {
     int ntx, nty, ntz, ntt;
     int *tbin;
     AxisTile *tt;
-    long long *stranded_f;
+    long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
     int *overflow;
@@ -251,7 +251,7 @@ struct Plan {
     int ngroups, nint, sub_bits, key_bits;
     int4 *tiles;
     long long max_tiles;
-    long long *stranded_p;
+    long long *stranded_p, *deferred_p;
     long long cap_p;
     void *radix_tmp;
     size_t radix_bytes;
@@ -343,6 +343,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
+    P.deferred_f = cv.take<long long>(P.cap_f);
     // points
     long long n = P.np;
     int TP = point_tile_size();
@@ -375,6 +376,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tiles = cv.take<int4>(P.max_tiles);
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
+    P.deferred_p = cv.take<long long>(P.cap_p);
     P.radix_bytes = n > 0 ? radix_tmp_bytes(n) : 0;
     P.radix_tmp = cv.take<char>(P.radix_bytes);
     P.scan_bytes = scan_tmp_bytes((long long)(NG > NB ? NG : NB) + 1) + 1024;
@@ -545,6 +547,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded = P.stranded_f;
         a.n_stranded = P.counters;
         a.stranded_cap = P.cap_f;
+        a.deferred = P.deferred_f;
+        a.n_deferred = P.counters + 2;
+        a.deferred_cap = P.cap_f;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
         {
@@ -582,6 +587,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded = P.stranded_p;
         a.n_stranded = P.counters + 1;
         a.stranded_cap = P.cap_p;
+        a.deferred = P.deferred_p;
+        a.n_deferred = P.counters + 3;
+        a.deferred_cap = P.cap_p;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
         {
@@ -631,6 +639,10 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.acc = P.acc;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
+        // crowded tiles first (may add stranded samples), then the fallback
+        const int4 kk = make_int4(p.k[0], p.k[1], p.k[2], p.k[3]);
+        MFSEG_TRY(launch_deferred(a, P.g, P.tbin, kk, p.mins, kind == 1 ? P.deferred_f : P.deferred_p,
+                                  P.counters + (kind == 1 ? 2 : 3), a.cap, st));
         MFSEG_TRY(launch_fallback(a, st));
     }
     mark(4, st);
