@@ -787,7 +787,7 @@ __global__ void k_accumulate_points(long long n, const double *xyz, const double
 
 // ---------------------------------------------------------------------- launchers
 constexpr int FTX = 16, FTY = 8, FTZ = 4, FNT = 256;
-constexpr int PNT = 128, PSPT = 2;
+constexpr int PNT = 128, PSPT = 2;   // tile = 256 points for v1 and v3 (k_point_assign3: 128 thr x 2)
 
 int field_tile_dims(int *tx, int *ty, int *tz) {
     *tx = FTX;
@@ -795,7 +795,8 @@ int field_tile_dims(int *tx, int *ty, int *tz) {
     *tz = FTZ;
     return 0;
 }
-int point_tile_size() { return PNT * PSPT; }
+static_assert(PNT * PSPT == POINT_TILE, "v1 point tile size");
+int point_tile_size() { return POINT_TILE; }
 
 int launch_field_assign_v2(const FieldArgs &a, long long ntiles, cudaStream_t st);
 

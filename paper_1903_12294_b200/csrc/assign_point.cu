@@ -32,7 +32,8 @@ constexpr double INF_D = __builtin_huge_val();
 constexpr float INF_F = __builtin_huge_valf();
 
 constexpr int NT = 128, NW = 4;
-constexpr int SCAP = 64;
+static_assert(2 * NT == POINT_TILE, "k_point_assign3 covers POINT_TILE points per tile");
+constexpr int SCAP = 128;
 constexpr int RMAX = 16;
 constexpr float KSCR = 0x1.0p-18f;
 constexpr float KCULL = 0x1.0p-16f;
@@ -83,6 +84,9 @@ struct PSmem {
     int nrec[NW];
     double red[8 * NW];
     int wc[NW];
+    double o[4];                // tile origin
+    float delta[4], Cf[4];      // guard bands, fp32 box half-widths (t scaled by c_f)
+    float Aabs;                 // absolute error allowance of the fp32 distance
 };
 
 // exact reference box test + metric of one pair (engine.py:137-149, 179-181)
@@ -147,35 +151,39 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
             thi[d] = fmax(thi[d], s_hi[d * NW + q]);
         }
     }
-    // warp box (fp64, for the fp32 relative coordinates) = lo/hi from the warp reduction
     const bool useval = a.wv > 0.0;
-    // tile origin and guard bands
-    const double o[4] = {tlo[0], tlo[1], tlo[2], tlo[3]};
-    float delta[4], rp0[4], rp1[4];
+    if (tid < 4) {   // per-tile constants, shared
+        const int d = tid;
+        const double sc = d == 3 ? a.cf : 1.0;
+        S.o[d] = tlo[d];
+        S.delta[d] = (float)(DMUL(DMUL(DADD(DSUB(thi[d], tlo[d]), Cd[d]), sc), 0x1.0p-21));   // 2x the 2^-22 bound
+        S.Cf[d] = (float)DMUL(Cd[d], sc);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const float D0 = S.delta[0], D1 = S.delta[1], D2 = S.delta[2], D3 = S.delta[3];
+        S.Aabs = 1.1f * (float)a.wd * sqrtf(D0 * D0 + D1 * D1 + D2 * D2 + D3 * D3) +
+                 3e-13f * (float)(a.wd + a.wv);
+    }
+    float rp0[4], rp1[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-        const double E = DSUB(thi[d], tlo[d]);
         const double sc = d == 3 ? a.cf : 1.0;
-        delta[d] = (float)(DMUL(DMUL(DADD(E, Cd[d]), sc), 0x1.0p-21));   // 2x the 2^-22 bound
-        rp0[d] = (float)DMUL(DSUB(P0[d], o[d]), sc);
-        rp1[d] = (float)DMUL(DSUB(P1[d], o[d]), sc);
+        rp0[d] = (float)DMUL(DSUB(P0[d], S.o[d]), sc);
+        rp1[d] = (float)DMUL(DSUB(P1[d], S.o[d]), sc);
     }
     const float fwd = (float)a.wd;
-    const float Delta = sqrtf(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2] +
-                              delta[3] * delta[3]);
-    const float Aabs = 1.1f * fwd * Delta + 3e-13f * (float)(a.wd + a.wv);
-    const float Cf[4] = {(float)Cd[0], (float)Cd[1], (float)Cd[2], (float)(Cd[3] * a.cf)};
 
     int sl0 = -1, sl1 = -1;
-    double bD0 = INF_D, bD1 = INF_D;
-    int bI0 = INT_MAX, bI1 = INT_MAX;
     int nfast = 0;
     const int L0 = a.g.cand_start[sbin], L1 = a.g.cand_start[sbin + 1];
-    const bool single_chunk = (L1 - L0) <= NT;
+    bool deferred = (L1 - L0) > NT;     // crowded candidate lists -> k_deferred
+    __syncthreads();                    // S.Aabs
+    const float Aabs = S.Aabs;
 
-    for (int cb = L0; cb < L1; cb += NT) {
+    if (!deferred && L1 > L0) {
         // ---- phase A: exact fp64 classification + bounds over the tile box
-        const int ci = cb + tid;
+        const int ci = L0 + tid;
         bool have = ci < L1;
         int id = 0;
         double c4[4] = {0, 0, 0, 0}, cv = 0, Dlo = INF_D, Dhi = INF_D;
@@ -231,12 +239,12 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
             off += q < w ? S.wc[q] : 0;
             nsurv += S.wc[q];
         }
-        const bool fast = single_chunk && nsurv <= SCAP;
+        deferred = nsurv > SCAP;
         const int pos = off + __popc(bal & ((1u << lane) - 1u));
-        for (int sb = 0; sb < nsurv; sb += SCAP) {
-            const int cnt = min(SCAP, nsurv - sb);
-            if (surv && pos >= sb && pos < sb + SCAP) {
-                const int p = pos - sb;
+        if (!deferred && nsurv > 0) {
+            const int cnt = nsurv;
+            if (surv) {
+                const int p = pos;
                 S.id[p] = id;
                 S.c[p][0] = c4[0];
                 S.c[p][1] = c4[1];
@@ -245,15 +253,17 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
                 S.c[p][4] = cv;
 #pragma unroll
                 for (int d = 0; d < 4; ++d)
-                    S.rc[p][d] = (float)DMUL(DSUB(c4[d], o[d]), d == 3 ? a.cf : 1.0);
+                    S.rc[p][d] = (float)DMUL(DSUB(c4[d], S.o[d]), d == 3 ? a.cf : 1.0);
                 S.cvf[p] = (float)cv;
                 S.wvf[p] = (useval && chas) ? (float)a.wv : 0.f;
                 S.has[p] = chas;
                 S.full[p] = full;
             }
             __syncthreads();
-            if (fast) {
+            {
                 nfast = cnt;
+                const float delta[4] = {S.delta[0], S.delta[1], S.delta[2], S.delta[3]};
+                const float Cf[4] = {S.Cf[0], S.Cf[1], S.Cf[2], S.Cf[3]};
                 // ---- warp culling over the warp's point box (fp32, relative)
                 float wl[4], wh[4];
 #pragma unroll
@@ -270,9 +280,11 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
                     vh = (float)hi[4];
                 }
                 float ubw = INF_F, cvmax = 0.f;
-                float dl_r[2] = {INF_F, INF_F};
+                float dl_r[SCAP / 32];
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
+                for (int r = 0; r < SCAP / 32; ++r) dl_r[r] = INF_F;
+#pragma unroll
+                for (int r = 0; r < SCAP / 32; ++r) {
                     const int s = lane + 32 * r;
                     if (s < cnt) {
                         float ql = 0.f, qh = 0.f;
@@ -304,18 +316,19 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
                 ubw = wmin_f(ubw);
                 cvmax = wmax_f(cvmax);
                 const float Wb = useval ? (float)a.wv * (fmaxf(fabsf(vl), fabsf(vh)) + cvmax) : 0.f;
-                const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * Aabs) / (1.f - KCULL);
-                const unsigned keep0 = __ballot_sync(0xffffffffu, lane < cnt && (dl_r[0] <= thr || (a.debug & 1)));
-                const unsigned keep1 =
-                    __ballot_sync(0xffffffffu, lane + 32 < cnt && (dl_r[1] <= thr || (a.debug & 1)));
+                const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * Aabs) * (1.f + 0x1.0p-15f);
+                unsigned keep[SCAP / 32];
+#pragma unroll
+                for (int r = 0; r < SCAP / 32; ++r)
+                    keep[r] = __ballot_sync(0xffffffffu, lane + 32 * r < cnt && (dl_r[r] <= thr || (a.debug & 1)));
                 // ---- per-point fp32 screen
                 const float fv0 = (float)P0[4], fv1 = (float)P1[4];
                 float b1a = INF_F, b2a = INF_F, b1b = INF_F, b2b = INF_F;
                 int i1a = -1, i1b = -1;
                 bool unsure_a = false, unsure_b = false;   // box test inside the guard band
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    unsigned it = half ? keep1 : keep0;
+                for (int half = 0; half < SCAP / 32; ++half) {
+                    unsigned it = keep[half];
                     while (it) {
                         const int s = __ffs(it) - 1 + 32 * half;
                         it &= it - 1;
@@ -371,10 +384,10 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
                     // exact fp64 over every survivor inside the margin (all of them
                     // when the screen was unsure about a box test or overflowed)
                     const float ta = (b1a < INF_F && !unsure_a)
-                                         ? (b1a * (1.f + KSCR) + 2.f * KSCR * Wa + 2.f * Aabs) / (1.f - KSCR)
+                                         ? (b1a * (1.f + KSCR) + 2.f * KSCR * Wa + 2.f * Aabs) * (1.f + 0x1.0p-17f)
                                          : INF_F;
                     const float tb = (b1b < INF_F && !unsure_b)
-                                         ? (b1b * (1.f + KSCR) + 2.f * KSCR * Wq + 2.f * Aabs) / (1.f - KSCR)
+                                         ? (b1b * (1.f + KSCR) + 2.f * KSCR * Wq + 2.f * Aabs) * (1.f + 0x1.0p-17f)
                                          : INF_F;
                     double eDa = INF_D, eDb = INF_D;
                     int eIa = INT_MAX, eIb = INT_MAX, eSa = -1, eSb = -1;
@@ -413,44 +426,40 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
                 }
                 if (!live0) sl0 = -1;
                 if (!live1) sl1 = -1;
-                break;
             }
-            // ---- exact mode (crowded bins)
-            for (int s = 0; s < cnt; ++s) {
-                const int cid = S.id[s];
-                double D;
-                if (live0 && exact_pair(S.c[s], P0[0], P0[1], P0[2], P0[3], P0[4], S.has[s], a.cf, a.wv,
-                                        a.wd, Cd, D) && better(D, cid, bD0, bI0)) {
-                    bD0 = D; bI0 = cid;
-                }
-                if (live1 && exact_pair(S.c[s], P1[0], P1[1], P1[2], P1[3], P1[4], S.has[s], a.cf, a.wv,
-                                        a.wd, Cd, D) && better(D, cid, bD1, bI1)) {
-                    bD1 = D; bI1 = cid;
-                }
-            }
-            __syncthreads();
         }
-        if (fast) break;
     }
 
-    const int lab0 = !live0 ? -1 : nfast ? (sl0 >= 0 ? S.id[sl0] : -1) : (bI0 != INT_MAX ? bI0 : -1);
-    const int lab1 = !live1 ? -1 : nfast ? (sl1 >= 0 ? S.id[sl1] : -1) : (bI1 != INT_MAX ? bI1 : -1);
+    const int lab0 = (live0 && sl0 >= 0) ? S.id[sl0] : -1;
+    const int lab1 = (live1 && sl1 >= 0) ? S.id[sl1] : -1;
     if (live0) {
-        a.labels[p0] = lab0;
-        if (lab0 < 0) {
-            const unsigned long long q = atomicAdd(a.n_stranded, 1ull);
-            if ((long long)q < a.stranded_cap) a.stranded[q] = p0;
+        if (deferred) {
+            a.labels[p0] = -2;
+            const unsigned long long q = atomicAdd(a.n_deferred, 1ull);
+            if ((long long)q < a.deferred_cap) a.deferred[q] = p0;
+        } else {
+            a.labels[p0] = lab0;
+            if (lab0 < 0) {
+                const unsigned long long q = atomicAdd(a.n_stranded, 1ull);
+                if ((long long)q < a.stranded_cap) a.stranded[q] = p0;
+            }
         }
     }
     if (live1) {
-        a.labels[p1] = lab1;
-        if (lab1 < 0) {
-            const unsigned long long q = atomicAdd(a.n_stranded, 1ull);
-            if ((long long)q < a.stranded_cap) a.stranded[q] = p1;
+        if (deferred) {
+            a.labels[p1] = -2;
+            const unsigned long long q = atomicAdd(a.n_deferred, 1ull);
+            if ((long long)q < a.deferred_cap) a.deferred[q] = p1;
+        } else {
+            a.labels[p1] = lab1;
+            if (lab1 < 0) {
+                const unsigned long long q = atomicAdd(a.n_stranded, 1ull);
+                if ((long long)q < a.stranded_cap) a.stranded[q] = p1;
+            }
         }
     }
     int ovf_local = 0;
-    if (a.accumulate && nfast) {
+    if (a.accumulate && nfast && !deferred) {
         int nrec = 0;
         unsigned m0 = __ballot_sync(0xffffffffu, sl0 >= 0), m1 = __ballot_sync(0xffffffffu, sl1 >= 0);
         while (m0 | m1) {
@@ -504,16 +513,6 @@ __global__ void __launch_bounds__(NT, 4) k_point_assign3(PointArgs a) {
             if (wd < 4) atomic_add_double_fix(dst + 2 * wd, acc, &ovf_local);
             else if (wd == 4) atomic_add_double_fix(dst + 8, acc, &ovf_local);   // point-value sum
             else atomicAdd(dst + 12, (unsigned long long)n);                     // n_points
-        }
-    } else if (a.accumulate) {
-        const int labs[2] = {lab0, lab1};
-        const double *Ps[2] = {P0, P1};
-        for (int r = 0; r < 2; ++r) {
-            if (labs[r] < 0) continue;
-            unsigned long long *dst = a.acc + (size_t)labs[r] * MFSEG_ACC_WORDS;
-            for (int d = 0; d < 4; ++d) atomic_add_double_fix(dst + 2 * d, Ps[r][d], &ovf_local);
-            atomic_add_double_fix(dst + 8, Ps[r][4], &ovf_local);
-            atomicAdd(dst + 12, 1ull);
         }
     }
     if (ovf_local) *a.overflow = 1;

@@ -84,6 +84,10 @@ struct FallbackArgs {
     int accumulate;
 };
 
+// points per point tile: k_point_assign3 = 128 threads x 2 points (and the
+// v1 kernel's 128 x 2); the runtime cuts tiles with this size.
+constexpr int POINT_TILE = 256;
+
 // grid.cu
 size_t grid_workspace_bytes(int K, int NB);
 Grid grid_carve(Carver &cv, int K, int NB, int **count_tmp, void **scan_tmp);
