@@ -51,12 +51,26 @@ def stream_ptr() -> int:
 
 
 def to_dev(a, dtype=torch.float64, dev=None):
-    """Host array (numpy / tensor) -> contiguous device tensor."""
+    """Host array (numpy / tensor) -> contiguous device tensor.  Arrays backed by
+    pinned memory (e.g. numpy views of pinned torch tensors) are copied by DMA
+    asynchronously on the current stream."""
     dev = dev or device()
     if isinstance(a, torch.Tensor):
         return a.to(device=dev, dtype=dtype).contiguous()
     t = torch.from_numpy(np.ascontiguousarray(a))
-    return t.to(device=dev, dtype=dtype, non_blocking=True).contiguous()
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(device=dev, non_blocking=True).contiguous()
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy through a pinned staging buffer (fast D2H DMA)."""
+    if t.numel() == 0:
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
 
 
 @dataclass
@@ -172,12 +186,15 @@ class CenterState:
                    np.zeros(K, np.int64), np.zeros(K, bool))
 
     def to_table(self) -> list:
+        """Live clusters only, as the public centre table (engine.py:72-86)."""
         live = np.flatnonzero(self.n_points + self.n_fields > 0)
-        return [ClusterCenter(int(c), float(self.loc[c, 0]), float(self.loc[c, 1]),
-                              float(self.loc[c, 2]), float(self.loc[c, 3]),
-                              float(self.pval[c]) if self.has_p[c] else None,
-                              float(self.fval[c]) if self.has_f[c] else None,
-                              int(self.n_points[c]), int(self.n_fields[c])) for c in live]
+        loc = self.loc[live].tolist()
+        pv = np.where(self.has_p[live], self.pval[live], np.nan).tolist()
+        fv = np.where(self.has_f[live], self.fval[live], np.nan).tolist()
+        hp, hf = self.has_p[live].tolist(), self.has_f[live].tolist()
+        npt, nfl = self.n_points[live].tolist(), self.n_fields[live].tolist()
+        return [ClusterCenter(c, l[0], l[1], l[2], l[3], p if a else None, f if b else None, n1, n2)
+                for c, l, p, f, a, b, n1, n2 in zip(live.tolist(), loc, pv, fv, hp, hf, npt, nfl)]
 
     # --- device round trip -------------------------------------------------
     def to_device(self, dev=None) -> dict:
@@ -194,10 +211,16 @@ class CenterState:
 
     @classmethod
     def from_device(cls, d: dict) -> "CenterState":
-        return cls(d["loc"].cpu().numpy().T.copy(), d["pval"].cpu().numpy(),
-                   d["fval"].cpu().numpy(), d["has_p"].cpu().numpy().astype(bool),
-                   d["has_f"].cpu().numpy().astype(bool), d["n_points"].cpu().numpy(),
-                   d["n_fields"].cpu().numpy(), d["dormant"].cpu().numpy().astype(bool))
+        # one packed D2H copy instead of eight
+        K = d["pval"].numel()
+        f = torch.cat([d["loc"].reshape(-1), d["pval"], d["fval"],
+                       d["n_points"].view(torch.float64), d["n_fields"].view(torch.float64)])
+        b = torch.cat([d["has_p"], d["has_f"], d["dormant"]])
+        fh, bh = to_host(f), to_host(b).astype(bool)
+        ints = fh[6 * K:].view(np.int64)
+        return cls(fh[:4 * K].reshape(4, K).T.copy(), fh[4 * K:5 * K].copy(),
+                   fh[5 * K:6 * K].copy(), bh[:K], bh[K:2 * K], ints[:K].copy(),
+                   ints[K:].copy(), bh[2 * K:])
 
 
 def empty_state(K: int, dev=None) -> dict:
@@ -451,8 +474,8 @@ def run(points: Optional[PointSet], fields: Optional[FieldSet], extent: DomainEx
     r = run_device(points_to_device(points, dev), field_to_device(fields, dev), extent, params,
                    progress=progress)
     state = CenterState.from_device(r.state)
-    return Segmentation(point_labels=r.point_labels.cpu().numpy(),
-                        field_labels=r.field_labels.cpu().numpy(),
+    return Segmentation(point_labels=to_host(r.point_labels),
+                        field_labels=to_host(r.field_labels),
                         centers=state.to_table(), params=params, extent=extent,
                         iterations_used=r.iterations_used, converged=r.converged)
 

@@ -9,7 +9,7 @@ from typing import Optional
 import numpy as np
 
 from .engine import (CenterState, DeviceField, DevicePoints, DeviceRun, device, field_to_device,
-                     points_to_device, run_device)
+                     points_to_device, run_device, to_host)
 from .ingest import NormalizationRecord, domain_extent_device, normalize_device
 from .model import ClusterParams, FieldSet, PointSet, Segmentation
 
@@ -50,7 +50,7 @@ def segment(points: Optional[PointSet], fields: Optional[FieldSet], params: Clus
 
 def to_segmentation(r: DeviceRun, params, extent) -> Segmentation:
     state = CenterState.from_device(r.state)
-    return Segmentation(point_labels=r.point_labels.cpu().numpy(),
-                        field_labels=r.field_labels.cpu().numpy(), centers=state.to_table(),
+    return Segmentation(point_labels=to_host(r.point_labels),
+                        field_labels=to_host(r.field_labels), centers=state.to_table(),
                         params=params, extent=extent, iterations_used=r.iterations_used,
                         converged=r.converged)
