@@ -789,19 +789,31 @@ __global__ void k_accumulate_points(long long n, const double *xyz, const double
 constexpr int FTX = 16, FTY = 8, FTZ = 4, FNT = 256;
 constexpr int PNT = 128, PSPT = 2;   // tile = 256 points for v1 and v3 (k_point_assign3: 128 thr x 2)
 
+// field kernel generation: 5 (default), or 4 / 3 / 1 for comparisons
+int field_version() {
+    if (getenv("MFSEG_FIELD_V1")) return 1;
+    if (getenv("MFSEG_FIELD_V3")) return 3;
+    if (getenv("MFSEG_FIELD_V4")) return 4;
+    return 5;
+}
+
 int field_tile_dims(int *tx, int *ty, int *tz) {
+    const bool v5 = field_version() == 5;
     *tx = FTX;
-    *ty = FTY;
-    *tz = FTZ;
+    *ty = v5 ? 16 : FTY;
+    *tz = v5 ? 16 : FTZ;
     return 0;
 }
 static_assert(PNT * PSPT == POINT_TILE, "v1 point tile size");
 int point_tile_size() { return POINT_TILE; }
 
 int launch_field_assign_v2(const FieldArgs &a, long long ntiles, cudaStream_t st);
+int launch_field_assign_v5(const FieldArgs &a, cudaStream_t st);
 
 int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st) {
-    if (getenv("MFSEG_FIELD_V1") == nullptr) return launch_field_assign_v2(a, ntiles, st);
+    const int ver = field_version();
+    if (ver == 5) return launch_field_assign_v5(a, st);
+    if (ver != 1) return launch_field_assign_v2(a, ntiles, st);
     if (ntiles <= 0) return 0;
     if (ntiles > 0x7fffffffll) {
         set_error("field tile grid too large");

@@ -133,14 +133,23 @@ __global__ void k_point_gather(long long n, const unsigned *perm, const double *
     pv[i] = value[j];
 }
 
-__global__ void k_bin_hist(long long n, const unsigned *skeys, int shift, int *cnt) {
+// Group starts of the sorted keys by boundary detection (no atomics: sorted keys
+// would serialise a histogram on the same counters).  Thread i in [0, n] writes
+// first[q] = i for every group q in (group(i-1), group(i)]; group(n) = ng.
+__global__ void k_bin_first(long long n, const unsigned *skeys, int shift, int ng, int *first) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[skeys[i] >> shift], 1);
+    if (i > n) return;
+    int g = i < n ? (int)(skeys[i] >> shift) : ng;
+    int gp = i > 0 ? (int)(skeys[i - 1] >> shift) : -1;
+    for (int q = gp + 1; q <= g; ++q) first[q] = (int)i;
 }
 
-__global__ void k_tiles_per_bin(int nb, const int *cnt, int tp, int *ntiles) {
+__global__ void k_tiles_per_bin(int nb, const int *first, int tp, int *cnt, int *ntiles) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < nb) ntiles[b] = (cnt[b] + tp - 1) / tp;
+    if (b >= nb) return;
+    int c = first[b + 1] - first[b];
+    cnt[b] = c;
+    ntiles[b] = (c + tp - 1) / tp;
 }
 
 __global__ void k_make_tiles(int ng, const int *cnt, const int *first, const int *tstart, int tp,
@@ -463,15 +472,14 @@ int plan_prepare(Plan &P) {
         k_point_gather<<<gb, 256, 0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px,
                                            P.py, P.pz, P.pt, P.pv);
         const int NG = P.ngroups;
-        MFSEG_CUDA(cudaMemsetAsync(P.bcnt, 0, sizeof(int) * (NG + 1), st));
         ::mfseg::count_launch();
-        k_bin_hist<<<gb, 256, 0, st>>>(n, P.skeys, P.sub_bits, P.bcnt);
-        MFSEG_TRY(scan_exclusive_i32(P.bcnt, P.bfirst, NG + 1, P.scan_tmp, P.scan_bytes, st));
+        k_bin_first<<<(unsigned)((n + 256) / 256), 256, 0, st>>>(n, P.skeys, P.sub_bits, NG,
+                                                                 P.bfirst);
         int TP = point_tile_size();
         unsigned gk = (unsigned)((NG + 256) / 256);
         MFSEG_CUDA(cudaMemsetAsync(P.btiles, 0, sizeof(int) * (NG + 1), st));
         ::mfseg::count_launch();
-        k_tiles_per_bin<<<gk, 256, 0, st>>>(NG, P.bcnt, TP, P.btiles);
+        k_tiles_per_bin<<<gk, 256, 0, st>>>(NG, P.bfirst, TP, P.bcnt, P.btiles);
         MFSEG_TRY(scan_exclusive_i32(P.btiles, P.tstart, NG + 1, P.scan_tmp, P.scan_bytes, st));
         ::mfseg::count_launch();
         k_make_tiles<<<gk, 256, 0, st>>>(NG, P.bcnt, P.bfirst, P.tstart, TP, P.nint, P.tiles);
