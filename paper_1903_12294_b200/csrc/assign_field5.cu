@@ -56,10 +56,20 @@ constexpr int CAP = 128;                           // candidates per block (more
 constexpr unsigned SLOT_MASK = 127u;               // 7 slot bits in the packed keys
 constexpr int TE = BX + BY + BZ + BT;              // 52 table entries per candidate
 constexpr int OZ = BX + BY, OT = BX + BY + BZ;     // table offsets of z and t
-constexpr int NQ = 13;                             // quads: x 4, y 4, z 4, t 1
+constexpr int GX = 8, GY = 4, GZ = 4, GT = 2;      // brick: 8x4x4 voxels x 2 timesteps
+constexpr int QY = BX / GX, QZ = QY + BY / GY, QT = QZ + BZ / GZ;
+constexpr int NQ = QT + BT / GT;                   // brick-row groups: x 2, y 4, z 4, t 2
 constexpr int HW = 27;                             // histogram words: x 8, y 8, z 8, t 2, n 1
 constexpr float KSCR = 0x1.0p-18f;
 constexpr float KCULL = 0x1.0p-16f;
+
+struct Ctx {
+    AxisTile X, Y, Z, T;
+    int cnt, nrounds;
+    bool deferred;
+    float cvmax, fwd, wvf, slack;
+    long long plane, vol;
+};
 
 struct __align__(16) Smem5 {
     float tab[CAP][TE];             // 16-byte aligned rows (52 floats)
@@ -75,6 +85,7 @@ struct __align__(16) Smem5 {
     unsigned char has[CAP];
     int wc[NW];
     float red[NW];
+    Ctx ctx;
 };
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -117,6 +128,284 @@ __device__ __forceinline__ long long warp_reserve(unsigned long long *counter, i
 }
 
 }  // namespace
+
+
+// One table row: entries e[i] = fl32((s (c - coord[i]))^2) (fp64 as the reference,
+// s = c_f for time) inside the validity box [lo, hi], +inf outside, and the
+// (min, max) of each group of G entries over the indices that exist (< len).
+template <int N, int G>
+__device__ __forceinline__ void table_row(float *e, float2 *mm, const double *coord, double cc,
+                                          double scale, bool scaled, unsigned lo, unsigned hi,
+                                          int len) {
+    float mn = INF_F, mx = 0.0f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        float val = INF_F;
+        if ((unsigned)i >= lo && (unsigned)i <= hi) {
+            double d = DSUB(cc, coord[i]);
+            if (scaled) d = DMUL(scale, d);
+            val = to_f(DMUL(d, d));
+        }
+        e[i] = val;
+        if (i < len) {
+            mn = fminf(mn, val);
+            mx = fmaxf(mx, val);
+        }
+        if (i % G == G - 1) {
+            mm[i / G] = make_float2(mn, mx);
+            mn = INF_F;
+            mx = 0.0f;
+        }
+    }
+}
+
+// One warp brick: lane (lx, ly) = (8 bx + lane % 8, 4 by + lane / 8), samples
+// k = 4 r + q at z = 4 bz + q, timestep 2 bt + r.  FULL: all 256 samples exist.
+template <bool USEVAL, bool FULL>
+__device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bx, int by,
+                                      int bz, int bt, int &ovf_local) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
+    const int z0 = GZ * bz, t0 = GT * bt;
+    const long long fbase = (((long long)(C.T.start + t0) * a.nz + C.Z.start + z0) * a.ny +
+                             (C.Y.start + ly)) * (long long)a.nx + (C.X.start + lx);
+    unsigned livem = 0xFFu;
+    if (!FULL) {
+        livem = 0;
+        if (lx < C.X.len && ly < C.Y.len) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (z0 + (k & 3) < C.Z.len && t0 + (k >> 2) < C.T.len) livem |= 1u << k;
+        }
+    }
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * C.plane + (k >> 2) * C.vol) : 0.0;
+
+    int sl[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sl[k] = -1;
+    const float fwd = C.fwd, wvf = C.wvf, slack = C.slack, cvmax = C.cvmax;
+    if (!C.deferred && C.cnt > 0) {
+        float fv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            fv[k] = (FULL || (livem >> k & 1)) ? (float)v[k] : __int_as_float(0x7fffffff);
+        // brick value range: min/max of fl(v) = fl(min/max of v) (rounding is monotone)
+        float vwl = 0.0f, vwh = 0.0f;
+        if (USEVAL) {
+            float lo = INF_F, hi = -INF_F;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                lo = fminf(lo, fv[k]);   // NaN (missing sample) ignored
+                hi = fmaxf(hi, fv[k]);
+            }
+            vwl = warp_min_f(lo);
+            vwh = warp_max_f(hi);
+        }
+        // ---- warp culling from the group (min, max) tables
+        float dl[4];
+        float ubw = INF_F;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            dl[r] = INF_F;
+            const int s = lane + 32 * r;
+            if (r < C.nrounds && s < C.cnt) {
+                const float2 qx = S.qmm[s][bx], qy = S.qmm[s][QY + by], qz = S.qmm[s][QZ + bz],
+                             qt = S.qmm[s][QT + bt];
+                float vtl = 0.0f, vth = 0.0f;
+                if (USEVAL) {
+                    const float wvs = S.wvf[s];
+                    if (wvs > 0.0f) {
+                        const float cvs = S.cvf[s];
+                        const float pl = vwl - cvs, ph = vwh - cvs;
+                        vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
+                        vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
+                    }
+                }
+                dl[r] = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
+                ubw = fminf(ubw, fmaf(fwd, sqrt_approx((qx.y + qy.y) + (qz.y + qt.y)), vth));
+            }
+        }
+        ubw = warp_min_f(ubw);
+        const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vwl), fabsf(vwh)) + cvmax) : 0.f) + slack;
+        const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
+        unsigned keep[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
+
+        // ---- per-sample fp32 screen with packed (d, slot) keys
+        unsigned b1[8], b2[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            b1[k] = 0xFFFFFFFFu;
+            b2[k] = 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            unsigned it = keep[r];
+            while (it) {
+                const int s = __ffs(it) - 1 + 32 * r;
+                it &= it - 1;
+                const float *T = S.tab[s];
+                const float axy = T[lx] + T[BX + ly];
+                const float4 tz = *reinterpret_cast<const float4 *>(T + OZ + z0);
+                const float2 tt = *reinterpret_cast<const float2 *>(T + OT + t0);
+                const float az[4] = {axy + tz.x, axy + tz.y, axy + tz.z, axy + tz.w};
+                float cvs = 0.0f, wvs = 0.0f;
+                if (USEVAL) {
+                    cvs = S.cvf[s];
+                    wvs = S.wvf[s];
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float sq = az[k & 3] + ((k >> 2) ? tt.y : tt.x);
+                    const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf(fv[k] - cvs))
+                                           : fwd * sqrt_approx(sq);
+                    const unsigned key = (__float_as_uint(d) & ~SLOT_MASK) | (unsigned)s;
+                    b2[k] = min(b2[k], max(b1[k], key));
+                    b1[k] = min(b1[k], key);
+                }
+            }
+        }
+        // ---- certify, or resolve exactly
+        unsigned need = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float t1 = __uint_as_float(min(b1[k] & ~SLOT_MASK, INF_BITS));
+            const float t2 = __uint_as_float(min(b2[k] & ~SLOT_MASK, INF_BITS));
+            const float u1 = t1 * (1.f + 0x1.0p-15f);
+            const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
+            const bool ok = !(a.debug & 2) && b1[k] < INF_BITS &&
+                            t2 * (1.f - KSCR) > u1 * (1.f + KSCR) + 2.f * KSCR * W;
+            sl[k] = ok ? (int)(b1[k] & SLOT_MASK) : -1;
+            if (!ok && (livem >> k & 1)) need |= 1u << k;
+        }
+        if (__any_sync(0xffffffffu, need != 0) && need) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (!(need >> k & 1)) continue;
+                const int zi = z0 + (k & 3), ti = t0 + (k >> 2);
+                const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
+                const float u1 = __uint_as_float(b1[k] & ~SLOT_MASK) * (1.f + 0x1.0p-15f);
+                const float thrk = b1[k] < INF_BITS
+                                       ? (u1 * (1.f + KSCR) + 2.f * KSCR * W) * (1.f + 0x1.0p-17f)
+                                       : INF_F;
+                const double px = S.x[lx], py = S.y[ly], pz = S.z[zi];
+                double eD = INF_D;
+                int eI = INT_MAX, eS = -1;
+#pragma unroll 1
+                for (int r = 0; r < 4; ++r) {
+                    unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
+                    while (it) {
+                        const int s = __ffs(it) - 1 + 32 * r;
+                        it &= it - 1;
+                        const float *T = S.tab[s];
+                        const float ex = T[lx], ey = T[BX + ly], ez = T[OZ + zi], et = T[OT + ti];
+                        if (ex == INF_F || ey == INF_F || ez == INF_F || et == INF_F) continue;
+                        const float sq = ((ex + ey) + ez) + et;
+                        const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), S.wvf[s] * fabsf(fv[k] - S.cvf[s]))
+                                               : fwd * sqrt_approx(sq);
+                        if (d > thrk) continue;
+                        const double dx = DSUB(S.c[s][0], px), dy = DSUB(S.c[s][1], py),
+                                     dz = DSUB(S.c[s][2], pz);
+                        const double ct = DMUL(a.cf, DSUB(S.c[s][3], S.t[ti]));
+                        const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
+                        const double D = metric_tail(qq, DMUL(ct, ct), v[k], S.c[s][4], S.has[s],
+                                                     a.wv, a.wd);
+                        if (better(D, S.id[s], eD, eI)) {
+                            eD = D;
+                            eI = S.id[s];
+                            eS = s;
+                        }
+                    }
+                }
+                sl[k] = eS;
+            }
+        }
+    }
+
+    // ---- labels; deferred / stranded samples to their lists (warp-aggregated)
+    int nlist = 0;
+    int *lab_base = a.labels + fbase;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (!FULL && !(livem >> k & 1)) continue;
+        const int lab = C.deferred ? -2 : (sl[k] >= 0 ? S.id[sl[k]] : -1);
+        lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
+        if (lab < 0) ++nlist;
+    }
+    if (__any_sync(0xffffffffu, nlist > 0)) {
+        unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
+        long long *lst = C.deferred ? a.deferred : a.stranded;
+        const long long cap = C.deferred ? a.deferred_cap : a.stranded_cap;
+        long long p = warp_reserve(ctr, nlist);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (!(livem >> k & 1)) continue;
+            if (!C.deferred && sl[k] >= 0) continue;
+            if (p < cap) lst[p] = fbase + (k & 3) * C.plane + (k >> 2) * C.vol;
+            ++p;
+        }
+    }
+
+    // ---- partial sums: count marginals (shared atomics) + per-warp value sums
+    if (a.accumulate && !C.deferred && C.cnt > 0) {
+        unsigned todo = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (sl[k] >= 0 && (FULL || (livem >> k & 1))) todo |= 1u << k;
+        const unsigned MX = 0x01010101u << (lane & 7);
+        const unsigned MY = 0xFFu << (8 * (lane >> 3));
+        while (true) {
+            int mine = -1;
+#pragma unroll
+            for (int k = 7; k >= 0; --k)
+                if (todo >> k & 1) mine = sl[k];
+            const unsigned act = __ballot_sync(0xffffffffu, mine >= 0);
+            if (!act) break;
+            const int L = __shfl_sync(0xffffffffu, mine, __ffs(act) - 1);
+            // count; z counts (8 bits per z); t counts (16 bits per timestep)
+            unsigned c = 0, zp = 0, tp = 0;
+            double vs = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if ((todo >> k & 1) && sl[k] == L) {
+                    todo &= ~(1u << k);
+                    ++c;
+                    zp += 1u << (8 * (k & 3));
+                    tp += 1u << (16 * (k >> 2));
+                    vs = DADD(vs, v[k]);
+                }
+            }
+            const unsigned sx = __reduce_add_sync(MX, c);
+            const unsigned sy = __reduce_add_sync(MY, c);
+            const unsigned sz = __reduce_add_sync(0xffffffffu, zp);
+            const unsigned st = __reduce_add_sync(0xffffffffu, tp);
+            vs = warp_sum_d(vs);
+            unsigned *h = S.hist[L];
+            if (lane < 8) {
+                const int i = lx;
+                if (sx) atomicAdd(&h[i >> 1], sx << (16 * (i & 1)));
+            }
+            if ((lane & 7) == 0) {
+                const int i = ly;
+                if (sy) atomicAdd(&h[8 + (i >> 1)], sy << (16 * (i & 1)));
+            }
+            if (lane == 0) {   // z pairs (z0, z0+1), (z0+2, z0+3); t pair (t0, t0+1); n
+                const unsigned c0 = sz & 0xFFu, c1 = (sz >> 8) & 0xFFu, c2 = (sz >> 16) & 0xFFu,
+                               c3 = sz >> 24;
+                if (c0 | c1) atomicAdd(&h[16 + (z0 >> 1)], c0 | (c1 << 16));
+                if (c2 | c3) atomicAdd(&h[17 + (z0 >> 1)], c2 | (c3 << 16));
+                atomicAdd(&h[24 + (t0 >> 1)], st);
+                atomicAdd(&h[26], (st & 0xFFFFu) + (st >> 16));
+                S.wsum[w][L] = DADD(S.wsum[w][L], vs);
+            }
+        }
+    }
+}
 
 template <bool USEVAL>
 __global__ void __launch_bounds__(NT, 3) k_field_assign5(FieldArgs a) {
@@ -223,326 +512,59 @@ __global__ void __launch_bounds__(NT, 3) k_field_assign5(FieldArgs a) {
     }
 
     if (!deferred && cnt > 0) {
-        // ---- fp32 tables (fp64 differences and squares as the reference, rounded once)
-        for (int e = tid; e < cnt * TE; e += NT) {
-            const int p = e / TE, j = e - p * TE;
+        // ---- fp32 tables + group (min, max): one (axis, candidate) row per thread
+        for (int j = tid; j < 4 * cnt; j += NT) {
+            const int ax = j / cnt, p = j - ax * cnt;   // axis-major: warps stay on one axis
             const unsigned b = S.box[p];
-            float val = INF_F;
-            if (j < BX) {
-                if (j >= (int)(b & 15u) && j <= (int)((b >> 4) & 15u)) {
-                    const double d = DSUB(S.c[p][0], S.x[j]);
-                    val = to_f(DMUL(d, d));
-                }
-            } else if (j < OZ) {
-                const int i = j - BX;
-                if (i >= (int)((b >> 8) & 15u) && i <= (int)((b >> 12) & 15u)) {
-                    const double d = DSUB(S.c[p][1], S.y[i]);
-                    val = to_f(DMUL(d, d));
-                }
-            } else if (j < OT) {
-                const int i = j - OZ;
-                if (i >= (int)((b >> 16) & 15u) && i <= (int)((b >> 20) & 15u)) {
-                    const double d = DSUB(S.c[p][2], S.z[i]);
-                    val = to_f(DMUL(d, d));
-                }
-            } else {
-                const int i = j - OT;
-                if (i >= (int)((b >> 24) & 3u) && i <= (int)((b >> 26) & 3u)) {
-                    const double ct = DMUL(a.cf, DSUB(S.c[p][3], S.t[i]));
-                    val = to_f(DMUL(ct, ct));
-                }
-            }
-            S.tab[p][j] = val;
+            const double cc = S.c[p][ax];
+            if (ax == 0)
+                table_row<BX, GX>(S.tab[p], S.qmm[p], S.x, cc, 1.0, false, b & 15u, (b >> 4) & 15u, X.len);
+            else if (ax == 1)
+                table_row<BY, GY>(S.tab[p] + BX, S.qmm[p] + QY, S.y, cc, 1.0, false, (b >> 8) & 15u,
+                                  (b >> 12) & 15u, Y.len);
+            else if (ax == 2)
+                table_row<BZ, GZ>(S.tab[p] + OZ, S.qmm[p] + QZ, S.z, cc, 1.0, false, (b >> 16) & 15u,
+                                  (b >> 20) & 15u, Z.len);
+            else
+                table_row<BT, GT>(S.tab[p] + OT, S.qmm[p] + QT, S.t, cc, a.cf, true, (b >> 24) & 3u,
+                                  (b >> 26) & 3u, Tm.len);
         }
         if (a.accumulate) {
             for (int e = tid; e < cnt * HW; e += NT) (&S.hist[0][0])[e] = 0u;
             for (int e = tid; e < NW * CAP; e += NT) (&S.wsum[0][0])[e] = 0.0;
         }
         __syncthreads();
-        // quad (min, max) over the entries that exist in this block
-        for (int e = tid; e < cnt * NQ; e += NT) {
-            const int p = e / NQ, q = e - p * NQ;
-            int base, lo, n;
-            if (q < 4) {
-                base = 4 * q;
-                lo = base;
-                n = X.len;
-            } else if (q < 8) {
-                base = BX + 4 * (q - 4);
-                lo = 4 * (q - 4);
-                n = Y.len;
-            } else if (q < 12) {
-                base = OZ + 4 * (q - 8);
-                lo = 4 * (q - 8);
-                n = Z.len;
-            } else {
-                base = OT;
-                lo = 0;
-                n = Tm.len;
-            }
-            float mn = INF_F, mx = 0.0f;
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (lo + r < n) {
-                    const float v = S.tab[p][base + r];
-                    mn = fminf(mn, v);
-                    mx = fmaxf(mx, v);
-                }
-            S.qmm[p][q] = make_float2(mn, mx);
-        }
-        __syncthreads();
     }
 
-    // ---- bricks: warp w takes bricks w, w + 8, ..., 4x4x4 voxels x 4 timesteps each
-    const long long plane = (long long)a.ny * a.nx, vol = plane * a.nz;
-    const float fwd = (float)a.wd;
-    const float wvf = USEVAL ? (float)a.wv : 0.0f;
-    const float slack = 3e-13f * (float)(a.wd + a.wv);
-    const int nrounds = (cnt + 31) >> 5;
+    // ---- bricks: warp w takes bricks w, w + 8, ... (8x4x4 voxels x 2 timesteps each)
+    if (tid == 0) {
+        Ctx &C = S.ctx;
+        C.X = X;
+        C.Y = Y;
+        C.Z = Z;
+        C.T = Tm;
+        C.cnt = cnt;
+        C.nrounds = (cnt + 31) >> 5;
+        C.deferred = deferred;
+        C.cvmax = cvmax;
+        C.plane = (long long)a.ny * a.nx;
+        C.vol = C.plane * a.nz;
+        C.fwd = (float)a.wd;
+        C.wvf = USEVAL ? (float)a.wv : 0.0f;
+        C.slack = 3e-13f * (float)(a.wd + a.wv);
+    }
+    __syncthreads();
+    const Ctx &C = S.ctx;
     for (int bi = w; bi < 64; bi += NW) {
-        const int bx = bi & 3, by = (bi >> 2) & 3, bz = bi >> 4;
-        if (4 * bx >= X.len || 4 * by >= Y.len || 4 * bz >= Z.len) continue;   // warp-uniform
-        const int lx = 4 * bx + (lane & 3), ly = 4 * by + ((lane >> 2) & 3);
-        const int lz0 = 4 * bz + (lane >> 4);
-        const bool rowok = lx < X.len && ly < Y.len;
-        const long long fbase = (((long long)Tm.start * a.nz + Z.start + lz0) * a.ny + (Y.start + ly)) *
-                                    (long long)a.nx + (X.start + lx);
-        unsigned livem = 0;   // bit k: sample k = q*4 + t at (lx, ly, lz0 + 2q, t) exists
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int t = 0; t < BT; ++t) {
-                const int k = q * BT + t;
-                const bool lv = rowok && lz0 + 2 * q < Z.len && t < Tm.len;
-                if (lv) livem |= 1u << k;
-                v[k] = lv ? __ldg(a.values + fbase + 2 * q * plane + t * vol) : 0.0;
-            }
-
-        int sl[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) sl[k] = -1;
-        if (!deferred && cnt > 0) {
-            float fv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) fv[k] = (livem >> k & 1) ? (float)v[k] : __int_as_float(0x7fffffff);
-            // brick value range: min/max of fl(v) = fl(min/max of v) (rounding is monotone)
-            float vwl = 0.0f, vwh = 0.0f;
-            if (USEVAL) {
-                float lo = INF_F, hi = -INF_F;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    lo = fminf(lo, fv[k]);   // NaN (dead sample) ignored
-                    hi = fmaxf(hi, fv[k]);
-                }
-                vwl = warp_min_f(lo);
-                vwh = warp_max_f(hi);
-            }
-            // ---- warp culling from the quad tables
-            float dl[4];
-            float ubw = INF_F;
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                dl[r] = INF_F;
-                const int s = lane + 32 * r;
-                if (r < nrounds && s < cnt) {
-                    const float2 qx = S.qmm[s][bx], qy = S.qmm[s][4 + by], qz = S.qmm[s][8 + bz],
-                                 qt = S.qmm[s][12];
-                    float vtl = 0.0f, vth = 0.0f;
-                    if (USEVAL) {
-                        const float wvs = S.wvf[s];
-                        if (wvs > 0.0f) {
-                            const float cvs = S.cvf[s];
-                            const float pl = vwl - cvs, ph = vwh - cvs;
-                            vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
-                            vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
-                        }
-                    }
-                    dl[r] = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
-                    ubw = fminf(ubw, fmaf(fwd, sqrt_approx((qx.y + qy.y) + (qz.y + qt.y)), vth));
-                }
-            }
-            ubw = warp_min_f(ubw);
-            const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vwl), fabsf(vwh)) + cvmax) : 0.f) + slack;
-            const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
-            unsigned keep[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                keep[r] = __ballot_sync(0xffffffffu,
-                                        dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
-
-            // ---- per-sample fp32 screen with packed (d, slot) keys
-            unsigned b1[8], b2[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                b1[k] = 0xFFFFFFFFu;
-                b2[k] = 0xFFFFFFFFu;
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                unsigned it = keep[r];
-                while (it) {
-                    const int s = __ffs(it) - 1 + 32 * r;
-                    it &= it - 1;
-                    const float *T = S.tab[s];
-                    const float axy = T[lx] + T[BX + ly];
-                    const float a0 = axy + T[OZ + lz0], a1 = axy + T[OZ + lz0 + 2];
-                    const float4 tt = *reinterpret_cast<const float4 *>(T + OT);
-                    const float ta[4] = {tt.x, tt.y, tt.z, tt.w};
-                    float cvs = 0.0f, wvs = 0.0f;
-                    if (USEVAL) {
-                        cvs = S.cvf[s];
-                        wvs = S.wvf[s];
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const float sq = (k < 4 ? a0 : a1) + ta[k & 3];
-                        const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf(fv[k] - cvs))
-                                               : fwd * sqrt_approx(sq);
-                        const unsigned key = (__float_as_uint(d) & ~SLOT_MASK) | (unsigned)s;
-                        b2[k] = min(b2[k], max(b1[k], key));
-                        b1[k] = min(b1[k], key);
-                    }
-                }
-            }
-            // ---- certify, or resolve exactly
-            unsigned need = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const float t1 = __uint_as_float(min(b1[k] & ~SLOT_MASK, INF_BITS));
-                const float t2 = __uint_as_float(min(b2[k] & ~SLOT_MASK, INF_BITS));
-                const float u1 = t1 * (1.f + 0x1.0p-15f);
-                const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
-                const bool ok = !(a.debug & 2) && b1[k] < INF_BITS &&
-                                t2 * (1.f - KSCR) > u1 * (1.f + KSCR) + 2.f * KSCR * W;
-                sl[k] = ok ? (int)(b1[k] & SLOT_MASK) : -1;
-                if (!ok && (livem >> k & 1)) need |= 1u << k;
-            }
-            if (__any_sync(0xffffffffu, need != 0) && need) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (!(need >> k & 1)) continue;
-                    const int zi = lz0 + 2 * (k >> 2), ti = k & 3;
-                    const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
-                    const float u1 = __uint_as_float(b1[k] & ~SLOT_MASK) * (1.f + 0x1.0p-15f);
-                    const float thrk = b1[k] < INF_BITS
-                                           ? (u1 * (1.f + KSCR) + 2.f * KSCR * W) * (1.f + 0x1.0p-17f)
-                                           : INF_F;
-                    const double px = S.x[lx], py = S.y[ly], pz = S.z[zi];
-                    double eD = INF_D;
-                    int eI = INT_MAX, eS = -1;
-#pragma unroll 1
-                    for (int r = 0; r < 4; ++r) {
-                        unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
-                        while (it) {
-                            const int s = __ffs(it) - 1 + 32 * r;
-                            it &= it - 1;
-                            const float *T = S.tab[s];
-                            const float ex = T[lx], ey = T[BX + ly], ez = T[OZ + zi], et = T[OT + ti];
-                            if (ex == INF_F || ey == INF_F || ez == INF_F || et == INF_F) continue;
-                            const float sq = ((ex + ey) + ez) + et;
-                            const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), S.wvf[s] * fabsf(fv[k] - S.cvf[s]))
-                                                   : fwd * sqrt_approx(sq);
-                            if (d > thrk) continue;
-                            const double dx = DSUB(S.c[s][0], px), dy = DSUB(S.c[s][1], py),
-                                         dz = DSUB(S.c[s][2], pz);
-                            const double ct = DMUL(a.cf, DSUB(S.c[s][3], S.t[ti]));
-                            const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
-                            const double D = metric_tail(qq, DMUL(ct, ct), v[k], S.c[s][4], S.has[s],
-                                                         a.wv, a.wd);
-                            if (better(D, S.id[s], eD, eI)) {
-                                eD = D;
-                                eI = S.id[s];
-                                eS = s;
-                            }
-                        }
-                    }
-                    sl[k] = eS;
-                }
-            }
-        }
-
-        // ---- labels; deferred / stranded samples to their lists (warp-aggregated)
-        int nlist = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (!(livem >> k & 1)) continue;
-            const long long f = fbase + 2 * (k >> 2) * plane + (k & 3) * vol;
-            const int lab = deferred ? -2 : (sl[k] >= 0 ? S.id[sl[k]] : -1);
-            a.labels[f] = lab;
-            if (lab < 0) ++nlist;
-        }
-        if (__any_sync(0xffffffffu, nlist > 0)) {
-            unsigned long long *ctr = deferred ? a.n_deferred : a.n_stranded;
-            long long *lst = deferred ? a.deferred : a.stranded;
-            const long long cap = deferred ? a.deferred_cap : a.stranded_cap;
-            long long p = warp_reserve(ctr, nlist);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (!(livem >> k & 1)) continue;
-                if (!deferred && sl[k] >= 0) continue;
-                if (p < cap) lst[p] = fbase + 2 * (k >> 2) * plane + (k & 3) * vol;
-                ++p;
-            }
-        }
-
-        // ---- partial sums: count marginals (shared atomics) + per-warp value sums
-        if (a.accumulate && !deferred && cnt > 0) {
-            unsigned todo = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (sl[k] >= 0 && (livem >> k & 1)) todo |= 1u << k;
-            const unsigned MX = 0x11111111u << (lane & 3);
-            const unsigned MY = 0x000F000Fu << (4 * ((lane >> 2) & 3));
-            while (true) {
-                int mine = -1;
-#pragma unroll
-                for (int k = 7; k >= 0; --k)
-                    if (todo >> k & 1) mine = sl[k];
-                const unsigned act = __ballot_sync(0xffffffffu, mine >= 0);
-                if (!act) break;
-                const int L = __shfl_sync(0xffffffffu, mine, __ffs(act) - 1);
-                unsigned c = 0, czp = 0, ctp = 0;   // count; z pair (16|16); t counts (8 bits each)
-                double vs = 0.0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if ((todo >> k & 1) && sl[k] == L) {
-                        todo &= ~(1u << k);
-                        ++c;
-                        czp += (k < 4) ? 1u : 0x10000u;
-                        ctp += 1u << (8 * (k & 3));
-                        vs = DADD(vs, v[k]);
-                    }
-                }
-                const unsigned sx = __reduce_add_sync(MX, c);
-                const unsigned sy = __reduce_add_sync(MY, c);
-                const unsigned sz = __reduce_add_sync(lane < 16 ? 0x0000FFFFu : 0xFFFF0000u, czp);
-                const unsigned st = __reduce_add_sync(0xffffffffu, ctp);
-                vs = warp_sum_d(vs);
-                unsigned *h = S.hist[L];
-                if (lane < 4) {
-                    const int i = 4 * bx + lane;
-                    if (sx) atomicAdd(&h[i >> 1], sx << (16 * (i & 1)));
-                }
-                if (lane < 16 && (lane & 3) == 0) {
-                    const int i = 4 * by + (lane >> 2);
-                    if (sy) atomicAdd(&h[8 + (i >> 1)], sy << (16 * (i & 1)));
-                }
-                if (lane == 0 || lane == 16) {   // z = lz0 (low half) and lz0 + 2 (high half)
-                    const int i0 = lz0, i1 = lz0 + 2;
-                    if (sz & 0xFFFFu) atomicAdd(&h[16 + (i0 >> 1)], (sz & 0xFFFFu) << (16 * (i0 & 1)));
-                    if (sz >> 16) atomicAdd(&h[16 + (i1 >> 1)], (sz >> 16) << (16 * (i1 & 1)));
-                }
-                if (lane == 0) {
-                    const unsigned t0 = st & 0xFFu, t1 = (st >> 8) & 0xFFu, t2 = (st >> 16) & 0xFFu,
-                                   t3 = st >> 24;
-                    atomicAdd(&h[24], t0 | (t1 << 16));
-                    atomicAdd(&h[25], t2 | (t3 << 16));
-                    atomicAdd(&h[26], t0 + t1 + t2 + t3);
-                    S.wsum[w][L] = DADD(S.wsum[w][L], vs);
-                }
-            }
-        }
+        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+        if (GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= Tm.len)
+            continue;   // warp-uniform
+        const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len && GZ * bz + GZ <= Z.len &&
+                          GT * bt + GT <= Tm.len;
+        if (full)
+            brick<USEVAL, true>(a, S, C, bx, by, bz, bt, ovf_local);
+        else
+            brick<USEVAL, false>(a, S, C, bx, by, bz, bt, ovf_local);
     }
 
     // ---- once per block: marginals x fixed-point coordinates -> global 128-bit sums
