@@ -407,8 +407,8 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
     }
 }
 
-template <bool USEVAL>
-__global__ void __launch_bounds__(NT, 3) k_field_assign5(FieldArgs a) {
+template <bool USEVAL, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem5 &S = *reinterpret_cast<Smem5 *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -617,17 +617,25 @@ int launch_field_assign_v5(const FieldArgs &a, cudaStream_t st) {
     const size_t smem = sizeof(Smem5);
     static bool configured = false;
     if (!configured) {
-        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<true>,
+        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<true, 3>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<false>,
+        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<false, 3>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<true, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<false, 2>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
+    const bool two = getenv("MFSEG_F5_MINB2") != nullptr;
     ::mfseg::count_launch();
-    if (a.wv > 0.0)
-        k_field_assign5<true><<<(unsigned)n, NT, smem, st>>>(a);
-    else
-        k_field_assign5<false><<<(unsigned)n, NT, smem, st>>>(a);
+    if (a.wv > 0.0) {
+        if (two) k_field_assign5<true, 2><<<(unsigned)n, NT, smem, st>>>(a);
+        else k_field_assign5<true, 3><<<(unsigned)n, NT, smem, st>>>(a);
+    } else {
+        if (two) k_field_assign5<false, 2><<<(unsigned)n, NT, smem, st>>>(a);
+        else k_field_assign5<false, 3><<<(unsigned)n, NT, smem, st>>>(a);
+    }
     MFSEG_LAUNCH("k_field_assign5");
     return 0;
 }
