@@ -805,7 +805,13 @@ int field_tile_dims(int *tx, int *ty, int *tz) {
     return 0;
 }
 static_assert(PNT * PSPT == POINT_TILE, "v1 point tile size");
-int point_tile_size() { return POINT_TILE; }
+// point kernel generation: 4 (default), or 3 / 1 for comparisons
+int point_version() {
+    if (getenv("MFSEG_POINT_V1")) return 1;
+    if (getenv("MFSEG_POINT_V3")) return 3;
+    return 4;
+}
+int point_tile_size() { return point_version() == 4 ? POINT_CHUNK : POINT_TILE; }
 
 int launch_field_assign_v2(const FieldArgs &a, long long ntiles, cudaStream_t st);
 int launch_field_assign_v5(const FieldArgs &a, cudaStream_t st);
@@ -826,9 +832,12 @@ int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st) {
 }
 
 int launch_point_assign_v3(const PointArgs &a, long long max_tiles, cudaStream_t st);
+int launch_point_assign_v4(const PointArgs &a, long long max_tiles, cudaStream_t st);
 
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st) {
-    if (getenv("MFSEG_POINT_V1") == nullptr) return launch_point_assign_v3(a, max_tiles, st);
+    const int ver = point_version();
+    if (ver == 4) return launch_point_assign_v4(a, max_tiles, st);
+    if (ver == 3) return launch_point_assign_v3(a, max_tiles, st);
     if (max_tiles <= 0) return 0;
     ::mfseg::count_launch();
     k_point_assign<PNT, PSPT><<<(unsigned)max_tiles, PNT, 0, st>>>(a);

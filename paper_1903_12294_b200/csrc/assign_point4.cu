@@ -1,0 +1,562 @@
+// k_point_assign4 — windowed exact assignment of point samples, one CTA per
+// chunk of <= 2048 bin-sorted points of one sample bin (v4, the default).
+//
+// Same contract as the field kernels (exact reference labels, lowest id on
+// ties; engine.py:137-192).  Points are sorted once per run by (sample bin,
+// 4^4 Morton sub-cell) and cut into chunks of one bin; per chunk the exact
+// fp64 bounding box is computed once per run (k_tile_box).  Per CTA:
+//
+//  1. the bin's candidates are classified against the chunk box in exact fp64
+//     (no sample can pass the box test / every sample passes / partial) and
+//     get chunk-relative fp32 coordinates rc = fl32(fl64(c - o) s) (o = box
+//     minimum corner, s = c_f for time, 1 otherwise); points get rp likewise,
+//     so |(rc - rp)_d - s (c - x)_d| <= 2^-22 (E_d + C_d) s =: delta_d / 2 and
+//     |d32 - D| <= 2^-19 (D + W) + w_d ||delta|| (v3 analysis, assign_point.cu).
+//  2. each warp walks 64-point warp tiles (2 points per lane): fp32 bounds over
+//     the warp tile's box cull the candidates (margin 2^-16 relative), then the
+//     per-point screen keeps best/second best as packed (d, slot) keys (three
+//     integer min/max per pair; truncation 2^-16 relative, covered by the
+//     certification exactly as in k_field_assign5) and certifies with margin
+//     2^-18 relative + 2 w_d ||delta|| absolute.  Box tests inside the
+//     +-delta guard band, near ties and overflow go to exact fp64.
+//  3. partial sums: per warp and slot fp64 running sums (the warp's tiles in a
+//     fixed order), per slot point counts with shared atomics; once per CTA
+//     the warp sums are converted exactly to 128-bit fixed point and added to
+//     the global sums.  Chunks are canonical (never split across GPUs when the
+//     time slabs are whole t-bins), so the sums are deterministic.
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace mfseg {
+namespace {
+
+constexpr double INF_D = __builtin_huge_val();
+constexpr float INF_F = __builtin_huge_valf();
+constexpr unsigned INF_BITS = 0x7F800000u;
+
+constexpr int NT = 256, NW = 8;
+constexpr int CAP = 128;
+constexpr unsigned SLOT_MASK = 127u;
+constexpr float KSCR = 0x1.0p-18f;
+constexpr float KCULL = 0x1.0p-16f;
+static_assert(POINT_CHUNK % 64 == 0, "warp tiles of 64 points");
+
+struct PCtx {
+    double o[4];
+    float delta[4], Cf[4];
+    float Aabs, cvmax, fwd, wvf;
+    int cnt, nrounds, len;
+    long long start;
+    bool deferred;
+};
+
+struct __align__(16) PSmem4 {
+    float4 rc[CAP];                 // chunk-relative fp32 centre coordinates
+    double c[CAP][5];               // cx, cy, cz, ct (raw), cv
+    double wsum[NW][5][CAP];        // per-warp fp64 sums of x, y, z, t, v
+    unsigned n[CAP];
+    int id[CAP];
+    float cvf[CAP], wvf[CAP];
+    unsigned char has[CAP], full[CAP];
+    int wc[NW];
+    float red[NW];
+    PCtx ctx;
+};
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float wmin_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float wmax_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double wmin_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double wmax_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ long long warp_reserve(unsigned long long *counter, int n) {
+    const int lane = threadIdx.x & 31;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total > 0) base = atomicAdd(counter, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return (long long)base + incl - n;
+}
+
+// exact reference box test + metric of one pair (engine.py:137-149, 179-181)
+__device__ __forceinline__ bool exact_pair(const double *c, const double *P, bool has, double cf,
+                                           double wv, double wd, const double *C, double &D) {
+    const double dx = DSUB(c[0], P[0]), dy = DSUB(c[1], P[1]), dz = DSUB(c[2], P[2]),
+                 dt = DSUB(c[3], P[3]);
+    if (!(fabs(dx) <= C[0] && fabs(dy) <= C[1] && fabs(dz) <= C[2] && fabs(dt) <= C[3])) return false;
+    const double q = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
+    const double ct = DMUL(cf, dt);
+    D = metric_tail(q, DMUL(ct, ct), P[4], c[4], has, wv, wd);
+    return true;
+}
+
+// fp32 screen distance of one (point, slot) pair; box test with the guard band
+__device__ __forceinline__ float pair_d32(const float4 &r, const float *rp, const PCtx &C, bool full,
+                                          float fv, float cvs, float wvs, bool useval, bool &unsure) {
+    const float dx = r.x - rp[0], dy = r.y - rp[1], dz = r.z - rp[2], dt = r.w - rp[3];
+    if (!full) {
+        const float m0 = fabsf(dx) - C.Cf[0], m1 = fabsf(dy) - C.Cf[1], m2 = fabsf(dz) - C.Cf[2],
+                    m3 = fabsf(dt) - C.Cf[3];
+        const bool out = m0 > C.delta[0] || m1 > C.delta[1] || m2 > C.delta[2] || m3 > C.delta[3];
+        const bool in = m0 < -C.delta[0] && m1 < -C.delta[1] && m2 < -C.delta[2] && m3 < -C.delta[3];
+        if (out) return INF_F;
+        if (!in) unsure = true;
+    }
+    const float q = fmaf(dt, dt, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+    return useval ? fmaf(C.fwd, sqrt_approx(q), wvs * fabsf(fv - cvs)) : C.fwd * sqrt_approx(q);
+}
+
+template <bool USEVAL>
+__device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const PCtx &C, int wt,
+                                           int &ovf_local) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double Cd[4] = {a.Cx, a.Cy, a.Cz, a.Ct};
+    const int off0 = 64 * wt + lane, off1 = off0 + 32;
+    const bool live0 = off0 < C.len, live1 = off1 < C.len;
+    const long long p0 = C.start + off0, p1 = C.start + off1;
+    double P0[5] = {0, 0, 0, 0, 0}, P1[5] = {0, 0, 0, 0, 0};
+    if (live0) {
+        P0[0] = a.x[p0]; P0[1] = a.y[p0]; P0[2] = a.z[p0]; P0[3] = a.t[p0]; P0[4] = a.v[p0];
+    }
+    if (live1) {
+        P1[0] = a.x[p1]; P1[1] = a.y[p1]; P1[2] = a.z[p1]; P1[3] = a.t[p1]; P1[4] = a.v[p1];
+    }
+    int sl0 = -1, sl1 = -1;
+    if (!C.deferred && C.cnt > 0) {
+        float rp0[4], rp1[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const double sc = d == 3 ? a.cf : 1.0;
+            rp0[d] = (float)DMUL(DSUB(P0[d], C.o[d]), sc);
+            rp1[d] = (float)DMUL(DSUB(P1[d], C.o[d]), sc);
+        }
+        // warp-tile box (fp32, chunk-relative) and value range
+        float wl[4], wh[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            float l = INF_F, h = -INF_F;
+            if (live0) { l = rp0[d]; h = rp0[d]; }
+            if (live1) { l = fminf(l, rp1[d]); h = fmaxf(h, rp1[d]); }
+            wl[d] = wmin_f(l);
+            wh[d] = wmax_f(h);
+        }
+        const float fv0 = (float)P0[4], fv1 = (float)P1[4];
+        float vl = 0.f, vh = 0.f;
+        if (USEVAL) {
+            float l = INF_F, h = -INF_F;
+            if (live0) { l = fv0; h = fv0; }
+            if (live1) { l = fminf(l, fv1); h = fmaxf(h, fv1); }
+            vl = wmin_f(l);
+            vh = wmax_f(h);
+        }
+        // ---- warp culling (fp32 bounds over the warp-tile box, guard bands widen the box test)
+        float dl[4];
+        float ubw = INF_F;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            dl[r] = INF_F;
+            const int s = lane + 32 * r;
+            if (r < C.nrounds && s < C.cnt) {
+                const float4 rc = S.rc[s];
+                const float rcv[4] = {rc.x, rc.y, rc.z, rc.w};
+                float ql = 0.f, qh = 0.f;
+                bool wfull = true, none = false;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const float cw = C.Cf[d] + C.delta[d], cn = C.Cf[d] - C.delta[d];
+                    const float a1 = rcv[d] - wl[d], b1 = rcv[d] - wh[d];   // a1 >= b1
+                    if (a1 < -cw || b1 > cw) none = true;
+                    if (!(a1 <= cn && b1 >= -cn)) wfull = false;
+                    const float e1 = fminf(a1, cw), e2 = fmaxf(b1, -cw);
+                    const float mx = fmaxf(fabsf(e1), fabsf(e2));
+                    const float mn = (e2 <= 0.f && e1 >= 0.f) ? 0.f : fminf(fabsf(e1), fabsf(e2));
+                    ql = fmaf(mn, mn, ql);
+                    qh = fmaf(mx, mx, qh);
+                }
+                float vtl = 0.f, vth = 0.f;
+                if (USEVAL) {
+                    const float wvs = S.wvf[s];
+                    if (wvs > 0.f) {
+                        const float cvs = S.cvf[s];
+                        const float pl = vl - cvs, ph = vh - cvs;
+                        vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
+                        vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
+                    }
+                }
+                if (!none) dl[r] = fmaf(C.fwd, sqrt_approx(ql), vtl);
+                if (wfull && !none) ubw = fminf(ubw, fmaf(C.fwd, sqrt_approx(qh), vth));
+            }
+        }
+        ubw = wmin_f(ubw);
+        const float Wb = USEVAL ? C.wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f;
+        const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * C.Aabs) * (1.f + 0x1.0p-15f);
+        unsigned keep[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
+
+        // ---- per-point screen, packed (d, slot) keys
+        unsigned a1k = 0xFFFFFFFFu, a2k = 0xFFFFFFFFu, b1k = 0xFFFFFFFFu, b2k = 0xFFFFFFFFu;
+        bool unsure0 = false, unsure1 = false;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            unsigned it = keep[r];
+            while (it) {
+                const int s = __ffs(it) - 1 + 32 * r;
+                it &= it - 1;
+                const float4 rc = S.rc[s];
+                const bool fl = S.full[s];
+                float cvs = 0.f, wvs = 0.f;
+                if (USEVAL) {
+                    cvs = S.cvf[s];
+                    wvs = S.wvf[s];
+                }
+                const float d0 = pair_d32(rc, rp0, C, fl, fv0, cvs, wvs, USEVAL, unsure0);
+                const float d1 = pair_d32(rc, rp1, C, fl, fv1, cvs, wvs, USEVAL, unsure1);
+                const unsigned k0 = (__float_as_uint(d0) & ~SLOT_MASK) | (unsigned)s;
+                const unsigned k1 = (__float_as_uint(d1) & ~SLOT_MASK) | (unsigned)s;
+                a2k = min(a2k, max(a1k, k0));
+                a1k = min(a1k, k0);
+                b2k = min(b2k, max(b1k, k1));
+                b1k = min(b1k, k1);
+            }
+        }
+        // ---- certify, or resolve exactly
+        const float W0 = USEVAL ? C.wvf * (fabsf(fv0) + C.cvmax) : 0.f;
+        const float W1 = USEVAL ? C.wvf * (fabsf(fv1) + C.cvmax) : 0.f;
+        const float u0 = __uint_as_float(min(a1k & ~SLOT_MASK, INF_BITS)) * (1.f + 0x1.0p-15f);
+        const float u1 = __uint_as_float(min(b1k & ~SLOT_MASK, INF_BITS)) * (1.f + 0x1.0p-15f);
+        const float s0 = __uint_as_float(min(a2k & ~SLOT_MASK, INF_BITS));
+        const float s1 = __uint_as_float(min(b2k & ~SLOT_MASK, INF_BITS));
+        const bool ok0 = !(a.debug & 2) && !unsure0 && a1k < INF_BITS &&
+                         s0 * (1.f - KSCR) > u0 * (1.f + KSCR) + 2.f * KSCR * W0 + 2.f * C.Aabs;
+        const bool ok1 = !(a.debug & 2) && !unsure1 && b1k < INF_BITS &&
+                         s1 * (1.f - KSCR) > u1 * (1.f + KSCR) + 2.f * KSCR * W1 + 2.f * C.Aabs;
+        sl0 = ok0 ? (int)(a1k & SLOT_MASK) : -1;
+        sl1 = ok1 ? (int)(b1k & SLOT_MASK) : -1;
+        const bool need0 = live0 && !ok0, need1 = live1 && !ok1;
+        if (__any_sync(0xffffffffu, need0 || need1) && (need0 || need1)) {
+            // exact fp64 over every kept candidate inside the margin (all of them
+            // when a box test was inside the guard band or the screen overflowed)
+            const float t0 = (a1k < INF_BITS && !unsure0)
+                                 ? (u0 * (1.f + KSCR) + 2.f * KSCR * W0 + 2.f * C.Aabs) * (1.f + 0x1.0p-17f)
+                                 : INF_F;
+            const float t1 = (b1k < INF_BITS && !unsure1)
+                                 ? (u1 * (1.f + KSCR) + 2.f * KSCR * W1 + 2.f * C.Aabs) * (1.f + 0x1.0p-17f)
+                                 : INF_F;
+            double eD0 = INF_D, eD1 = INF_D;
+            int eI0 = INT_MAX, eI1 = INT_MAX, eS0 = -1, eS1 = -1;
+#pragma unroll 1
+            for (int r = 0; r < 4; ++r) {
+                unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
+                while (it) {
+                    const int s = __ffs(it) - 1 + 32 * r;
+                    it &= it - 1;
+                    const float4 rc = S.rc[s];
+                    const int cid = S.id[s];
+                    const float cvs = S.cvf[s], wvs = S.wvf[s];
+                    bool dummy = false;
+                    double D;
+                    if (need0) {
+                        const float d = pair_d32(rc, rp0, C, false, fv0, cvs, wvs, USEVAL, dummy);
+                        if (!(d > t0) && exact_pair(S.c[s], P0, S.has[s], a.cf, a.wv, a.wd, Cd, D) &&
+                            better(D, cid, eD0, eI0)) {
+                            eD0 = D; eI0 = cid; eS0 = s;
+                        }
+                    }
+                    if (need1) {
+                        const float d = pair_d32(rc, rp1, C, false, fv1, cvs, wvs, USEVAL, dummy);
+                        if (!(d > t1) && exact_pair(S.c[s], P1, S.has[s], a.cf, a.wv, a.wd, Cd, D) &&
+                            better(D, cid, eD1, eI1)) {
+                            eD1 = D; eI1 = cid; eS1 = s;
+                        }
+                    }
+                }
+            }
+            if (need0) sl0 = eS0;
+            if (need1) sl1 = eS1;
+        }
+        if (!live0) sl0 = -1;
+        if (!live1) sl1 = -1;
+    }
+
+    // ---- labels (bin-sorted order); deferred / stranded lists (warp-aggregated)
+    int nlist = 0;
+    if (live0) {
+        const int lab = C.deferred ? -2 : (sl0 >= 0 ? S.id[sl0] : -1);
+        a.labels[p0] = lab;
+        if (lab < 0) ++nlist;
+    }
+    if (live1) {
+        const int lab = C.deferred ? -2 : (sl1 >= 0 ? S.id[sl1] : -1);
+        a.labels[p1] = lab;
+        if (lab < 0) ++nlist;
+    }
+    if (__any_sync(0xffffffffu, nlist > 0)) {
+        unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
+        long long *lst = C.deferred ? a.deferred : a.stranded;
+        const long long cap = C.deferred ? a.deferred_cap : a.stranded_cap;
+        long long p = warp_reserve(ctr, nlist);
+        if (live0 && (C.deferred || sl0 < 0)) {
+            if (p < cap) lst[p] = p0;
+            ++p;
+        }
+        if (live1 && (C.deferred || sl1 < 0)) {
+            if (p < cap) lst[p] = p1;
+        }
+    }
+
+    // ---- partial sums: per-warp fp64 running sums + shared counts
+    if (a.accumulate && !C.deferred && C.cnt > 0) {
+        unsigned m0 = __ballot_sync(0xffffffffu, sl0 >= 0), m1 = __ballot_sync(0xffffffffu, sl1 >= 0);
+        while (m0 | m1) {
+            const int L = m0 ? __shfl_sync(0xffffffffu, sl0, __ffs(m0) - 1)
+                             : __shfl_sync(0xffffffffu, sl1, __ffs(m1) - 1);
+            const unsigned g0 = __ballot_sync(0xffffffffu, sl0 == L);
+            const unsigned g1 = __ballot_sync(0xffffffffu, sl1 == L);
+            m0 &= ~g0;
+            m1 &= ~g1;
+            double s5[5];
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+                double v = 0.0;
+                if (sl0 == L) v = P0[d];
+                if (sl1 == L) v = DADD(v, P1[d]);
+                s5[d] = warp_sum_d(v);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int d = 0; d < 5; ++d) S.wsum[w][d][L] = DADD(S.wsum[w][d][L], s5[d]);
+                atomicAdd(&S.n[L], (unsigned)(__popc(g0) + __popc(g1)));
+            }
+        }
+    }
+    (void)ovf_local;
+}
+
+}  // namespace
+
+template <bool USEVAL>
+__global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
+    if ((int)blockIdx.x >= *a.n_tiles) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PSmem4 &S = *reinterpret_cast<PSmem4 *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int4 T = a.tiles[blockIdx.x];
+    const double *box = a.tile_box + 8 * (size_t)blockIdx.x;   // lo[4], hi[4]
+    const double Cd[4] = {a.Cx, a.Cy, a.Cz, a.Ct};
+    int ovf_local = 0;
+    if (tid < 4) {   // chunk frame: origin, guard bands, fp32 box half-widths
+        const int d = tid;
+        const double sc = d == 3 ? a.cf : 1.0;
+        S.ctx.o[d] = box[d];
+        S.ctx.delta[d] = (float)(DMUL(DMUL(DADD(DSUB(box[4 + d], box[d]), Cd[d]), sc), 0x1.0p-21));
+        S.ctx.Cf[d] = (float)DMUL(Cd[d], sc);
+    }
+    __syncthreads();
+    const int L0 = a.g.cand_start[T.x], L1 = a.g.cand_start[T.x + 1];
+    bool deferred = (L1 - L0) > NT;
+    int cnt = 0;
+    float cvmax = 0.f;
+    if (!deferred) {
+        // ---- candidates classified against the chunk box (exact fp64), compacted
+        const int ci = L0 + tid;
+        bool have = ci < L1, full = false;
+        int id = 0;
+        double c4[4] = {0, 0, 0, 0};
+        if (have) {
+            id = a.g.cand_ids[ci];
+            c4[0] = a.c.x[id];
+            c4[1] = a.c.y[id];
+            c4[2] = a.c.z[id];
+            c4[3] = a.c.t[id];
+            full = true;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const double da = DSUB(c4[d], box[d]), db = DSUB(c4[d], box[4 + d]);   // da >= db
+                if (da < -Cd[d] || db > Cd[d]) have = false;    // no sample passes
+                if (!(da <= Cd[d] && db >= -Cd[d])) full = false;   // not every sample
+            }
+            if (!have) full = false;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, have);
+        if (lane == 0) S.wc[w] = __popc(bal);
+        __syncthreads();
+        int off = 0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            off += q < w ? S.wc[q] : 0;
+            cnt += S.wc[q];
+        }
+        deferred = cnt > CAP;
+        float mycv = 0.f;
+        if (!deferred && have) {
+            const int p = off + __popc(bal & ((1u << lane) - 1u));
+            const bool chas = a.chas[id] != 0;
+            const double cv = chas ? a.cval[id] : 0.0;
+            S.id[p] = id;
+            S.c[p][0] = c4[0];
+            S.c[p][1] = c4[1];
+            S.c[p][2] = c4[2];
+            S.c[p][3] = c4[3];
+            S.c[p][4] = cv;
+            S.rc[p] = make_float4((float)DSUB(c4[0], S.ctx.o[0]), (float)DSUB(c4[1], S.ctx.o[1]),
+                                  (float)DSUB(c4[2], S.ctx.o[2]),
+                                  (float)DMUL(DSUB(c4[3], S.ctx.o[3]), a.cf));
+            S.cvf[p] = (float)cv;
+            S.wvf[p] = (USEVAL && chas) ? (float)a.wv : 0.f;
+            S.has[p] = chas;
+            S.full[p] = full;
+            if (USEVAL && chas) mycv = fabsf((float)cv);
+        }
+        if (USEVAL) {
+            mycv = wmax_f(mycv);
+            if (lane == 0) S.red[w] = mycv;
+        }
+        __syncthreads();
+        if (USEVAL) {
+#pragma unroll
+            for (int q = 0; q < NW; ++q) cvmax = fmaxf(cvmax, S.red[q]);
+        }
+        if (!deferred && a.accumulate) {
+            for (int e = tid; e < cnt; e += NT) S.n[e] = 0u;
+            for (int e = tid; e < NW * 5 * CAP; e += NT) (&S.wsum[0][0][0])[e] = 0.0;
+        }
+    }
+    if (tid == 0) {
+        PCtx &C = S.ctx;
+        const float D0 = C.delta[0], D1 = C.delta[1], D2 = C.delta[2], D3 = C.delta[3];
+        C.Aabs = 1.1f * (float)a.wd * sqrtf(D0 * D0 + D1 * D1 + D2 * D2 + D3 * D3) +
+                 3e-13f * (float)(a.wd + a.wv);
+        C.cvmax = cvmax;
+        C.fwd = (float)a.wd;
+        C.wvf = USEVAL ? (float)a.wv : 0.f;
+        C.cnt = cnt;
+        C.nrounds = (cnt + 31) >> 5;
+        C.len = T.z;
+        C.start = T.y;
+        C.deferred = deferred;
+    }
+    __syncthreads();
+    const PCtx &C = S.ctx;
+    for (int wt = w; 64 * wt < C.len; wt += NW) point_warp<USEVAL>(a, S, C, wt, ovf_local);
+
+    // ---- once per CTA: exact per-slot totals -> global 128-bit sums
+    if (a.accumulate && !deferred && cnt > 0) {
+        __syncthreads();
+        for (int e = tid; e < cnt * 6; e += NT) {
+            const int s = e / 6, wd = e - s * 6;
+            const unsigned n = S.n[s];
+            if (n == 0) continue;
+            unsigned long long *dst = a.acc + (size_t)S.id[s] * MFSEG_ACC_WORDS;
+            if (wd == 5) {
+                atomicAdd(dst + 12, (unsigned long long)n);   // n_points
+                continue;
+            }
+            __int128 acc = 0;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+                unsigned long long lo;
+                long long hi;
+                d2fix(S.wsum[q][wd][s], lo, hi, &ovf_local);
+                acc += (__int128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+            }
+            atomic_add_fix(dst + (wd < 4 ? 2 * wd : 8), (unsigned long long)acc, (long long)(acc >> 64));
+        }
+    }
+    if (ovf_local) *a.overflow = 1;
+}
+
+// exact fp64 bounding box of every point chunk (once per run): one warp per chunk
+__global__ void k_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles,
+                           const double *x, const double *y, const double *z, const double *t,
+                           double *box) {
+    const long long tile = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (tile >= max_tiles || tile >= *n_tiles) return;
+    const int4 T = tiles[tile];
+    double lo[4] = {INF_D, INF_D, INF_D, INF_D}, hi[4] = {-INF_D, -INF_D, -INF_D, -INF_D};
+    for (int i = lane; i < T.z; i += 32) {
+        const long long p = (long long)T.y + i;
+        const double v[4] = {x[p], y[p], z[p], t[p]};
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            lo[d] = fmin(lo[d], v[d]);
+            hi[d] = fmax(hi[d], v[d]);
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        lo[d] = wmin_d(lo[d]);
+        hi[d] = wmax_d(hi[d]);
+    }
+    if (lane < 4) {
+        box[8 * tile + lane] = lo[lane];
+        box[8 * tile + 4 + lane] = hi[lane];
+    }
+}
+
+int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,
+                    const double *y, const double *z, const double *t, double *box,
+                    cudaStream_t st) {
+    if (max_tiles <= 0) return 0;
+    ::mfseg::count_launch();
+    const long long threads = max_tiles * 32;
+    k_tile_box<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(tiles, n_tiles, max_tiles, x, y, z,
+                                                                   t, box);
+    MFSEG_LAUNCH("k_tile_box");
+    return 0;
+}
+
+int launch_point_assign_v4(const PointArgs &a, long long max_tiles, cudaStream_t st) {
+    if (max_tiles <= 0) return 0;
+    if (max_tiles > 0x7fffffffll) {
+        set_error("point chunk grid too large");
+        return 3;
+    }
+    const size_t smem = sizeof(PSmem4);
+    static bool configured = false;
+    if (!configured) {
+        MFSEG_CUDA(cudaFuncSetAttribute(k_point_assign4<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MFSEG_CUDA(cudaFuncSetAttribute(k_point_assign4<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    ::mfseg::count_launch();
+    if (a.wv > 0.0)
+        k_point_assign4<true><<<(unsigned)max_tiles, NT, smem, st>>>(a);
+    else
+        k_point_assign4<false><<<(unsigned)max_tiles, NT, smem, st>>>(a);
+    MFSEG_LAUNCH("k_point_assign4");
+    return 0;
+}
+
+}  // namespace mfseg

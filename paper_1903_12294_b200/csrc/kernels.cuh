@@ -40,6 +40,7 @@ struct PointArgs {
     const double *x, *y, *z, *t, *v;   // bin-sorted SoA
     const int4 *tiles;                 // (bin, start, len, -)
     const int *n_tiles;
+    const double *tile_box;            // [tile][8]: exact lo[4], hi[4] (k_point_assign4)
     double Cx, Cy, Cz, Ct;
     double cf, wd, wv;
     CentersView c;
@@ -87,6 +88,8 @@ struct FallbackArgs {
 // points per point tile: k_point_assign3 = 128 threads x 2 points (and the
 // v1 kernel's 128 x 2); the runtime cuts tiles with this size.
 constexpr int POINT_TILE = 256;
+// points per chunk of k_point_assign4 (8 warps x 4 warp tiles of 64 points)
+constexpr int POINT_CHUNK = 2048;
 
 // grid.cu
 size_t grid_workspace_bytes(int K, int NB);
@@ -97,6 +100,10 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
 // assign.cu
 int field_tile_dims(int *tx, int *ty, int *tz);
 int point_tile_size();
+int point_version();
+int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,
+                    const double *y, const double *z, const double *t, double *box,
+                    cudaStream_t st);
 int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st);
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st);
 int launch_fallback(const FallbackArgs &a, cudaStream_t st);

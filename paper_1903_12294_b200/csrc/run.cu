@@ -259,6 +259,7 @@ struct Plan {
     int *bcnt, *bfirst, *btiles, *tstart;   // per (bin, interval) group
     int ngroups, nint, sub_bits, key_bits;
     int4 *tiles;
+    double *tbox;                   // exact box per point chunk (v4)
     long long max_tiles;
     long long *stranded_p, *deferred_p;
     long long cap_p;
@@ -383,6 +384,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tstart = cv.take<int>(NG + 1);
     P.max_tiles = n > 0 ? (n + TP - 1) / TP + NG : 0;
     P.tiles = cv.take<int4>(P.max_tiles);
+    P.tbox = cv.take<double>(8 * P.max_tiles);
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
     P.deferred_p = cv.take<long long>(P.cap_p);
@@ -484,6 +486,9 @@ int plan_prepare(Plan &P) {
         ::mfseg::count_launch();
         k_make_tiles<<<gk, 256, 0, st>>>(NG, P.bcnt, P.bfirst, P.tstart, TP, P.nint, P.tiles);
         MFSEG_LAUNCH("point tiles");
+        if (point_version() == 4)
+            MFSEG_TRY(launch_tile_box(P.tiles, P.tstart + NG, P.max_tiles, P.px, P.py, P.pz, P.pt,
+                                      P.tbox, st));
     }
     return 0;
 }
@@ -579,6 +584,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.v = P.pv;
         a.tiles = P.tiles;
         a.n_tiles = P.tstart + P.ngroups;
+        a.tile_box = P.tbox;
         a.Cx = p.C[0];
         a.Cy = p.C[1];
         a.Cz = p.C[2];

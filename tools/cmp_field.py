@@ -10,7 +10,7 @@ from paper_1903_12294_b200.engine import run_device, CenterState
 from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device, synthetic_device
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-vers = sys.argv[3:] or ["v4", "v5"]
+vers = sys.argv[3:] or ["v4", "v5"]   # v1/v3/v4/v5 (field) or any MFSEG_* env name, "default"
 fld, pts, _ = synthetic_device(cfg["dims"], cfg["nt"], cfg["n_traj"], seed=0)
 normalize_device(pts, fld, True)
 ext = domain_extent_device(pts, fld)
@@ -18,9 +18,11 @@ params = ClusterParams(k=cfg["k"], eps_c=1e-12, max_iterations=iters)
 lib = N.load()
 res = {}
 for tag in vers:
-    for e in ("MFSEG_FIELD_V1", "MFSEG_FIELD_V3", "MFSEG_FIELD_V4"):
+    for e in [x for x in os.environ if x.startswith("MFSEG_")]:
         os.environ.pop(e, None)
-    if tag != "v5":
+    if tag.startswith("MFSEG_"):
+        os.environ[tag] = "1"
+    elif tag not in ("v5", "default"):
         os.environ["MFSEG_FIELD_" + tag.upper()] = "1"
     r = run_device(pts, fld, ext, params)
     torch.cuda.synchronize()
