@@ -178,10 +178,12 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         }
         // ---- warp culling (fp32 bounds over the warp-tile box, guard bands widen the box test)
         float dl[4];
+        bool wf[4];
         float ubw = INF_F;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             dl[r] = INF_F;
+            wf[r] = false;
             const int s = lane + 32 * r;
             if (r < C.nrounds && s < C.cnt) {
                 const float4 rc = S.rc[s];
@@ -211,16 +213,19 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                     }
                 }
                 if (!none) dl[r] = fmaf(C.fwd, sqrt_approx(ql), vtl);
+                wf[r] = wfull && !none;   // every point of the warp tile passes the box test
                 if (wfull && !none) ubw = fminf(ubw, fmaf(C.fwd, sqrt_approx(qh), vth));
             }
         }
         ubw = wmin_f(ubw);
         const float Wb = USEVAL ? C.wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * C.Aabs) * (1.f + 0x1.0p-15f);
-        unsigned keep[4];
+        unsigned keep[4], kfull[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r) {
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
+            kfull[r] = __ballot_sync(0xffffffffu, wf[r]);
+        }
 
         // ---- per-point screen, packed (d, slot) keys
         unsigned a1k = 0xFFFFFFFFu, a2k = 0xFFFFFFFFu, b1k = 0xFFFFFFFFu, b2k = 0xFFFFFFFFu;
@@ -229,10 +234,10 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         for (int r = 0; r < 4; ++r) {
             unsigned it = keep[r];
             while (it) {
-                const int s = __ffs(it) - 1 + 32 * r;
+                const int b = __ffs(it) - 1, s = b + 32 * r;
                 it &= it - 1;
                 const float4 rc = S.rc[s];
-                const bool fl = S.full[s];
+                const bool fl = (kfull[r] >> b) & 1u;
                 float cvs = 0.f, wvs = 0.f;
                 if (USEVAL) {
                     cvs = S.cvf[s];
