@@ -235,6 +235,11 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
         for (int r = 0; r < 4; ++r)
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
+        if ((a.debug & 8) && lane == 0) {
+            atomicAdd(a.stats, 1ull);
+            atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
+                                                         __popc(keep[2]) + __popc(keep[3])));
+        }
 
         // ---- per-sample fp32 screen with packed (d, slot) keys
         unsigned b1[8], b2[8];
@@ -283,6 +288,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             sl[k] = ok ? (int)(b1[k] & SLOT_MASK) : -1;
             if (!ok && (livem >> k & 1)) need |= 1u << k;
         }
+        if ((a.debug & 8) && need) atomicAdd(a.stats + 2, (unsigned long long)__popc(need));
         if (__any_sync(0xffffffffu, need != 0) && need) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {

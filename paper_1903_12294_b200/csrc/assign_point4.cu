@@ -218,6 +218,43 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             }
         }
         ubw = wmin_f(ubw);
+        // Upper bound from the points themselves: screen every point against the
+        // candidate with the smallest lower bound; if it is valid for all of them,
+        // max over points of d32 bounds every point's best (box UBs need a
+        // candidate whose window covers the whole warp tile).
+        unsigned a1k = 0xFFFFFFFFu, a2k = 0xFFFFFFFFu, b1k = 0xFFFFFFFFu, b2k = 0xFFFFFFFFu;
+        bool unsure0 = false, unsure1 = false;
+        int sstar = -1;
+        {
+            unsigned mk = 0xFFFFFFFFu;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (dl[r] < INF_F) mk = min(mk, (__float_as_uint(dl[r]) & ~SLOT_MASK) | (unsigned)(lane + 32 * r));
+            mk = __reduce_min_sync(0xffffffffu, mk);
+            if (mk != 0xFFFFFFFFu) {
+                sstar = (int)(mk & SLOT_MASK);
+                const float4 rc = S.rc[sstar];
+                float cvs = 0.f, wvs = 0.f;
+                if (USEVAL) {
+                    cvs = S.cvf[sstar];
+                    wvs = S.wvf[sstar];
+                }
+                bool un0 = false, un1 = false;
+                const float d0 = pair_d32(rc, rp0, C, false, fv0, cvs, wvs, USEVAL, un0);
+                const float d1 = pair_d32(rc, rp1, C, false, fv1, cvs, wvs, USEVAL, un1);
+                const unsigned k0 = (__float_as_uint(d0) & ~SLOT_MASK) | (unsigned)sstar;
+                const unsigned k1 = (__float_as_uint(d1) & ~SLOT_MASK) | (unsigned)sstar;
+                a1k = k0;
+                b1k = k1;
+                unsure0 = un0;
+                unsure1 = un1;
+                // per-point upper bound of d32 (INF when the box test is not certain)
+                const float u0 = (!live0) ? 0.f : (un0 ? INF_F : __uint_as_float(min(k0 & ~SLOT_MASK, INF_BITS)) * (1.f + 0x1.0p-15f));
+                const float u1 = (!live1) ? 0.f : (un1 ? INF_F : __uint_as_float(min(k1 & ~SLOT_MASK, INF_BITS)) * (1.f + 0x1.0p-15f));
+                const float um = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(u0, u1))));
+                ubw = fminf(ubw, um);
+            }
+        }
         const float Wb = USEVAL ? C.wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * C.Aabs) * (1.f + 0x1.0p-15f);
         unsigned keep[4], kfull[4];
@@ -226,13 +263,19 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
             kfull[r] = __ballot_sync(0xffffffffu, wf[r]);
         }
+        if ((a.debug & 8) && lane == 0) {
+            atomicAdd(a.stats, 1ull);
+            atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
+                                                         __popc(keep[2]) + __popc(keep[3])));
+        }
+        unsigned scan[4];   // kept candidates still to screen (s* already is)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) scan[r] = keep[r] & ~((sstar >> 5) == r ? (1u << (sstar & 31)) : 0u);
 
         // ---- per-point screen, packed (d, slot) keys
-        unsigned a1k = 0xFFFFFFFFu, a2k = 0xFFFFFFFFu, b1k = 0xFFFFFFFFu, b2k = 0xFFFFFFFFu;
-        bool unsure0 = false, unsure1 = false;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            unsigned it = keep[r];
+            unsigned it = scan[r];
             while (it) {
                 const int b = __ffs(it) - 1, s = b + 32 * r;
                 it &= it - 1;
@@ -267,6 +310,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         sl0 = ok0 ? (int)(a1k & SLOT_MASK) : -1;
         sl1 = ok1 ? (int)(b1k & SLOT_MASK) : -1;
         const bool need0 = live0 && !ok0, need1 = live1 && !ok1;
+        if ((a.debug & 8) && (need0 || need1)) atomicAdd(a.stats + 2, (unsigned long long)(need0 + need1));
         if (__any_sync(0xffffffffu, need0 || need1) && (need0 || need1)) {
             // exact fp64 over every kept candidate inside the margin (all of them
             // when a box test was inside the guard band or the screen overflowed)

@@ -32,7 +32,8 @@ struct FieldArgs {
     long long deferred_cap;
     int *overflow;
     int accumulate;
-    int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor
+    int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor, bit3: stats
+    unsigned long long *stats;   // debug bit3: [0] bricks, [1] kept candidates, [2] exact samples
 };
 
 struct PointArgs {
@@ -58,6 +59,7 @@ struct PointArgs {
     int *overflow;
     int accumulate;
     int debug;
+    unsigned long long *stats;   // debug bit3: [0] warp tiles, [1] kept candidates, [2] exact points
 };
 
 // Stranded-sample fallback (engine.py:195-205): field samples (kind 1) are

@@ -331,7 +331,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.flags = cv.take<char>(update_flags_bytes());
     int NB = P.NB;
     P.g = grid_carve(cv, K, NB, &P.count_tmp, &P.grid_scan_tmp);
-    P.counters = cv.take<unsigned long long>(4);
+    P.counters = cv.take<unsigned long long>(16);   // [8..16): debug stats
     P.overflow = cv.take<int>(4);
     // field
     P.nf = (P.f.nt > 0) ? (long long)P.f.nx * P.f.ny * P.f.nz * P.f.nt : 0;
@@ -517,7 +517,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
                          P.count_tmp, P.grid_scan_tmp, st));
     mark(1, st);
-    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 4, st));
+    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 16, st));
     if (accumulate)
         MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
     if (P.nf > 0) {
@@ -562,6 +562,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded_cap = P.cap_f;
         a.deferred = P.deferred_f;
         a.n_deferred = P.counters + 2;
+        a.stats = P.counters + 8;
         a.deferred_cap = P.cap_f;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
@@ -603,6 +604,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded_cap = P.cap_p;
         a.deferred = P.deferred_p;
         a.n_deferred = P.counters + 3;
+        a.stats = P.counters + 12;
         a.deferred_cap = P.cap_p;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
@@ -660,6 +662,18 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         MFSEG_TRY(launch_fallback(a, st));
     }
     mark(4, st);
+    if (const char *dbg = getenv("MFSEG_DEBUG")) {
+        if (atoi(dbg) & 8) {
+            unsigned long long h[16];
+            MFSEG_CUDA(cudaMemcpyAsync(h, P.counters, sizeof h, cudaMemcpyDeviceToHost, st));
+            MFSEG_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr,
+                    "[mfseg stats] field: bricks %llu kept/brick %.2f exact %llu | points: warp tiles %llu "
+                    "kept/tile %.2f exact %llu | stranded f %llu p %llu deferred f %llu p %llu\n",
+                    h[8], h[8] ? (double)h[9] / h[8] : 0.0, h[10], h[12], h[12] ? (double)h[13] / h[12] : 0.0,
+                    h[14], h[0], h[1], h[2], h[3]);
+        }
+    }
     return 0;
 }
 
