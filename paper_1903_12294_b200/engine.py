@@ -63,14 +63,28 @@ def to_dev(a, dtype=torch.float64, dev=None):
     return t.to(device=dev, non_blocking=True).contiguous()
 
 
+def to_host_async(t: torch.Tensor):
+    """Start a device -> pinned host copy; returns (host tensor, event).  The
+    numpy view is valid once the event has completed (see `host_ready`)."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    if t.numel():
+        h.copy_(t, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return h, ev
+
+
+def host_ready(pending) -> np.ndarray:
+    h, ev = pending
+    ev.synchronize()
+    return h.numpy()
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     """Device tensor -> numpy through a pinned staging buffer (fast D2H DMA)."""
     if t.numel() == 0:
         return t.cpu().numpy()
-    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    h.copy_(t, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    return h.numpy()
+    return host_ready(to_host_async(t))
 
 
 @dataclass

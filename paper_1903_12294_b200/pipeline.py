@@ -9,7 +9,7 @@ from typing import Optional
 import numpy as np
 
 from .engine import (CenterState, DeviceField, DevicePoints, DeviceRun, device, field_to_device,
-                     points_to_device, run_device, to_host)
+                     points_to_device, run_device, host_ready, to_host_async)
 from .ingest import NormalizationRecord, domain_extent_device, normalize_device
 from .model import ClusterParams, FieldSet, PointSet, Segmentation
 
@@ -49,8 +49,10 @@ def segment(points: Optional[PointSet], fields: Optional[FieldSet], params: Clus
 
 
 def to_segmentation(r: DeviceRun, params, extent) -> Segmentation:
+    # label copies run on the copy engine while the host builds the centre table
     state = CenterState.from_device(r.state)
-    return Segmentation(point_labels=to_host(r.point_labels),
-                        field_labels=to_host(r.field_labels), centers=state.to_table(),
+    pl, fl = to_host_async(r.point_labels), to_host_async(r.field_labels)
+    table = state.to_table()
+    return Segmentation(point_labels=host_ready(pl), field_labels=host_ready(fl), centers=table,
                         params=params, extent=extent, iterations_used=r.iterations_used,
                         converged=r.converged)
