@@ -277,7 +277,10 @@ def run_ours(args):
     fld_all, pts_all, tid = synthetic_device(cfg["dims"], nt_total, cfg["n_traj"], seed=args.seed,
                                              dev=dev)
     ncell = int(np.prod(cfg["dims"]))
-    m0, m1 = rank * cfg["nt"], (rank + 1) * cfg["nt"]
+    # whole t-bins per rank (the extent's t range is [0, nt_total - 1])
+    from paper_1903_12294_b200.parallel import tbin_slabs
+    m0, m1 = tbin_slabs(np.arange(nt_total, dtype=float), 0.0, (nt_total - 1.0) / k[3], k[3],
+                        world)[rank]
     fld_raw = DeviceField(fld_all.dims, fld_all.origin, fld_all.spacing,
                           fld_all.times[m0:m1].clone(),
                           fld_all.values[m0 * ncell:m1 * ncell].clone())

@@ -35,6 +35,25 @@ def time_slab(rank: int, world: int, nt: int):
     return m0, m0 + base + (1 if rank < extra else 0)
 
 
+def tbin_slabs(times, t_min: float, C_t: float, k_t: int, world: int):
+    """Contiguous timestep slabs [m0, m1) per rank whose boundaries fall on t-bin
+    changes (bin = clip(floor((t - t_min) / C_t), 0, k_t - 1), engine.py:111-113),
+    as balanced as the bin boundaries allow.  Whole t-bins per rank keep every
+    field and point tile on one GPU, so the fixed-order partial sums (and the
+    centres) are bit-identical for any rank count."""
+    t = np.asarray(times, dtype=np.float64)
+    nt = len(t)
+    b = np.clip(np.floor((t - t_min) / C_t), 0, k_t - 1).astype(np.int64)
+    cuts = np.flatnonzero(b[1:] != b[:-1]) + 1          # allowed slab starts
+    bounds = [0]
+    for r in range(1, world):
+        target = r * nt / world
+        ok = cuts[cuts >= bounds[-1]]
+        bounds.append(int(ok[np.argmin(np.abs(ok - target))]) if len(ok) else nt)
+    bounds.append(nt)
+    return [(bounds[r], max(bounds[r], bounds[r + 1])) for r in range(world)]
+
+
 def global_minmax(lo: float, hi: float, group=None, device=None):
     """Exact global (min, max) of per-rank values (inf/-inf for empty ranks)."""
     t = torch.tensor([lo, -hi], dtype=torch.float64, device=device)

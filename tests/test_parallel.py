@@ -17,7 +17,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1903_12294_b200.parallel import allreduce_limbs, global_minmax, time_slab
+from paper_1903_12294_b200.parallel import allreduce_limbs, global_minmax, tbin_slabs, time_slab
 
 M42 = (1 << 42) - 1
 
@@ -81,6 +81,30 @@ def test_time_slab_partition():
                 assert 0 <= a <= b <= nt
                 covered.extend(range(a, b))
             assert covered == list(range(nt))
+
+
+def test_tbin_slabs_whole_bins():
+    """Slab boundaries fall on t-bin changes and the slabs partition the steps."""
+    for nt, k_t, world in ((32, 8, 2), (64, 16, 4), (256, 64, 8), (33, 8, 3), (7, 2, 4), (10, 1, 2)):
+        times = np.arange(nt, dtype=float)
+        C_t = (nt - 1.0) / k_t
+        slabs = tbin_slabs(times, 0.0, C_t, k_t, world)
+        b = np.clip(np.floor(times / C_t), 0, k_t - 1)
+        covered = []
+        for m0, m1 in slabs:
+            covered.extend(range(m0, m1))
+            if 0 < m0 < nt and m1 > m0:
+                assert b[m0] != b[m0 - 1]           # starts a new t-bin
+        assert covered == list(range(nt))
+        owners = {}
+        for r, (m0, m1) in enumerate(slabs):
+            for m in range(m0, m1):
+                assert owners.setdefault(b[m], r) == r   # a t-bin lives on one rank
+    # the bench's weak-scaling layout: 32 steps per rank, k_t = 8 per rank
+    for world in (1, 2, 4, 8):
+        nt = 32 * world
+        assert tbin_slabs(np.arange(nt, dtype=float), 0.0, (nt - 1.0) / (8 * world), 8 * world,
+                          world) == [(32 * r, 32 * r + 32) for r in range(world)]
 
 
 def _minmax_fn(rank, world):
