@@ -45,6 +45,7 @@ static_assert(POINT_CHUNK % 64 == 0, "warp tiles of 64 points");
 struct PCtx {
     double o[4];
     float delta[4], Cf[4];
+    float iC[4], uhi, ulo;          // 1 / Cf; 1 +- eps (box test band)
     float Aabs, cvmax, fwd, wvf;
     int cnt, nrounds, len;
     long long start;
@@ -118,19 +119,22 @@ __device__ __forceinline__ bool exact_pair(const double *c, const double *P, boo
 }
 
 // fp32 screen distance of one (point, slot) pair; box test with the guard band
+// as u = max_d |d_d| / Cf_d against 1 +- eps (eps = max_d delta_d / Cf_d + 2^-22
+// covers the two fp32 roundings of u): u > 1 + eps -> outside for sure (+inf);
+// u >= 1 - eps -> within the band, `unsure` (exact fp64 decides).
 __device__ __forceinline__ float pair_d32(const float4 &r, const float *rp, const PCtx &C, bool full,
                                           float fv, float cvs, float wvs, bool useval, bool &unsure) {
     const float dx = r.x - rp[0], dy = r.y - rp[1], dz = r.z - rp[2], dt = r.w - rp[3];
-    if (!full) {
-        const float m0 = fabsf(dx) - C.Cf[0], m1 = fabsf(dy) - C.Cf[1], m2 = fabsf(dz) - C.Cf[2],
-                    m3 = fabsf(dt) - C.Cf[3];
-        const bool out = m0 > C.delta[0] || m1 > C.delta[1] || m2 > C.delta[2] || m3 > C.delta[3];
-        const bool in = m0 < -C.delta[0] && m1 < -C.delta[1] && m2 < -C.delta[2] && m3 < -C.delta[3];
-        if (out) return INF_F;
-        if (!in) unsure = true;
-    }
     const float q = fmaf(dt, dt, fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-    return useval ? fmaf(C.fwd, sqrt_approx(q), wvs * fabsf(fv - cvs)) : C.fwd * sqrt_approx(q);
+    float d = useval ? fmaf(C.fwd, sqrt_approx(q), wvs * fabsf(fv - cvs)) : C.fwd * sqrt_approx(q);
+    if (!full) {
+        const float u = fmaxf(fmaxf(fabsf(dx) * C.iC[0], fabsf(dy) * C.iC[1]),
+                              fmaxf(fabsf(dz) * C.iC[2], fabsf(dt) * C.iC[3]));
+        const bool out = u > C.uhi;
+        unsure |= !out && u >= C.ulo;
+        d = out ? INF_F : d;
+    }
+    return d;
 }
 
 template <bool USEVAL>
@@ -501,6 +505,14 @@ __global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
     }
     if (tid == 0) {
         PCtx &C = S.ctx;
+        float eps = 0.f;
+        for (int d = 0; d < 4; ++d) {
+            C.iC[d] = 1.0f / C.Cf[d];
+            eps = fmaxf(eps, C.delta[d] / C.Cf[d]);
+        }
+        eps = eps * 1.0001f + 0x1.0p-22f;
+        C.uhi = 1.0f + eps;
+        C.ulo = 1.0f - eps;
         const float D0 = C.delta[0], D1 = C.delta[1], D2 = C.delta[2], D3 = C.delta[3];
         C.Aabs = 1.1f * (float)a.wd * sqrtf(D0 * D0 + D1 * D1 + D2 * D2 + D3 * D3) +
                  3e-13f * (float)(a.wd + a.wv);

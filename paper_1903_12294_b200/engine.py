@@ -23,6 +23,8 @@ both and the whole run is bit-identical.
 
 from __future__ import annotations
 
+import gc
+
 import ctypes as C
 import itertools
 from dataclasses import dataclass
@@ -207,8 +209,17 @@ class CenterState:
         fv = np.where(self.has_f[live], self.fval[live], np.nan).tolist()
         hp, hf = self.has_p[live].tolist(), self.has_f[live].tolist()
         npt, nfl = self.n_points[live].tolist(), self.n_fields[live].tolist()
-        return [ClusterCenter(c, l[0], l[1], l[2], l[3], p if a else None, f if b else None, n1, n2)
-                for c, l, p, f, a, b, n1, n2 in zip(live.tolist(), loc, pv, fv, hp, hf, npt, nfl)]
+        # tens of thousands of small objects: keep the cyclic GC from rescanning
+        # the heap several times while they are created (none of them is cyclic)
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            return [ClusterCenter(c, l[0], l[1], l[2], l[3], p if a else None, f if b else None,
+                                  n1, n2)
+                    for c, l, p, f, a, b, n1, n2 in zip(live.tolist(), loc, pv, fv, hp, hf, npt, nfl)]
+        finally:
+            if gc_on:
+                gc.enable()
 
     # --- device round trip -------------------------------------------------
     def to_device(self, dev=None) -> dict:
