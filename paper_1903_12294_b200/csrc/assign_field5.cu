@@ -205,11 +205,13 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             vwh = warp_max_f(hi);
         }
         // ---- warp culling from the group (min, max) tables
-        float dl[4];
+        float dl[4], shi[4];
         float ubw = INF_F;
+        unsigned ubkey = 0xFFFFFFFFu;   // (ub | slot) of the best fully valid candidate
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             dl[r] = INF_F;
+            shi[r] = INF_F;
             const int s = lane + 32 * r;
             if (r < C.nrounds && s < C.cnt) {
                 const float2 qx = S.qmm[s][bx], qy = S.qmm[s][QY + by], qz = S.qmm[s][QZ + bz],
@@ -225,7 +227,10 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                     }
                 }
                 dl[r] = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
-                ubw = fminf(ubw, fmaf(fwd, sqrt_approx((qx.y + qy.y) + (qz.y + qt.y)), vth));
+                shi[r] = (qx.y + qy.y) + (qz.y + qt.y);
+                const float ub = fmaf(fwd, sqrt_approx(shi[r]), vth);
+                ubw = fminf(ubw, ub);
+                if (ub < INF_F) ubkey = min(ubkey, (__float_as_uint(ub) & ~SLOT_MASK) | (unsigned)s);
             }
         }
         ubw = warp_min_f(ubw);
@@ -235,12 +240,82 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
         for (int r = 0; r < 4; ++r)
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
+
+        // ---- dominance: drop kept candidates s with D(s) > D(s*) on the whole brick,
+        // s* = the fully valid candidate with the smallest upper bound.  The squared
+        // distance difference is linear in each coordinate, so its minimum over the
+        // brick is the sum over axes of the smaller endpoint difference (fp32 table
+        // values, margin 2^-20 (S_s + S_s*) >> their rounding); the sqrt gap is at
+        // least dS / (sqrt S_s,max + sqrt S_s*,max); the value terms differ by at
+        // most w_v |cv_s - cv_s*| (both have values) or w_v max|v - cv_s*| (only s*).
+        ubkey = __reduce_min_sync(0xffffffffu, ubkey);
+        int sstar = -1;
+        if (ubkey != 0xFFFFFFFFu && !(a.debug & 1)) {
+            sstar = (int)(ubkey & SLOT_MASK);
+            const int xa = GX * bx, ya = GY * by, za = GZ * bz, ta = GT * bt;
+            const int xb = FULL ? xa + GX - 1 : min(xa + GX - 1, C.X.len - 1);
+            const int yb = FULL ? ya + GY - 1 : min(ya + GY - 1, C.Y.len - 1);
+            const int zb = FULL ? za + GZ - 1 : min(za + GZ - 1, C.Z.len - 1);
+            const int tb = FULL ? ta + GT - 1 : min(ta + GT - 1, C.T.len - 1);
+            const float *Q = S.tab[sstar];
+            const float qx0 = Q[xa], qx1 = Q[xb], qy0 = Q[BX + ya], qy1 = Q[BX + yb];
+            const float qz0 = Q[OZ + za], qz1 = Q[OZ + zb], qt0 = Q[OT + ta], qt1 = Q[OT + tb];
+            const float2 mqx = S.qmm[sstar][bx], mqy = S.qmm[sstar][QY + by], mqz = S.qmm[sstar][QZ + bz],
+                         mqt = S.qmm[sstar][QT + bt];
+            const float shq = (mqx.y + mqy.y) + (mqz.y + mqt.y);
+            const float rq = sqrt_approx(shq);
+            float cvq = 0.f, wvq = 0.f;
+            if (USEVAL) {
+                cvq = S.cvf[sstar];
+                wvq = S.wvf[sstar];
+            }
+            const float vabs = fmaxf(fabsf(vwl), fabsf(vwh));
+            const float vq = fmaxf(fabsf(vwl - cvq), fabsf(vwh - cvq));
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int s = lane + 32 * r;
+                bool dom = false;
+                if ((keep[r] >> lane & 1u) && s != sstar) {
+                    const float *T = S.tab[s];
+                    const float ex0 = T[xa], ex1 = T[xb], ey0 = T[BX + ya], ey1 = T[BX + yb];
+                    const float ez0 = T[OZ + za], ez1 = T[OZ + zb], et0 = T[OT + ta], et1 = T[OT + tb];
+                    const float emax = fmaxf(fmaxf(fmaxf(ex0, ex1), fmaxf(ey0, ey1)),
+                                             fmaxf(fmaxf(ez0, ez1), fmaxf(et0, et1)));
+                    if (emax < INF_F) {   // valid on the whole brick (windows are intervals)
+                        const float dS = (fminf(ex0 - qx0, ex1 - qx1) + fminf(ey0 - qy0, ey1 - qy1)) +
+                                         (fminf(ez0 - qz0, ez1 - qz1) + fminf(et0 - qt0, et1 - qt1));
+                        const float dSlb = dS - 0x1.0p-20f * (shi[r] + shq);
+                        if (dSlb > 0.f) {
+                            const float den = (sqrt_approx(shi[r]) + rq) * (1.f + 0x1.0p-20f);
+                            const float gap = __fdividef(dSlb, den) * (1.f - 0x1.0p-19f);
+                            float Vb = 0.f;
+                            if (USEVAL && wvq > 0.f) {
+                                const float cvs = S.cvf[s];
+                                const float V = S.wvf[s] > 0.f ? wvf * fabsf(cvs - cvq) : wvf * vq;
+                                Vb = V * (1.f + 0x1.0p-18f) +
+                                     0x1.0p-18f * wvf * (fabsf(cvs) + fabsf(cvq) + vabs);
+                            }
+                            const float rel = 0x1.0p-30f * (fwd * den + Wb) + slack;
+                            dom = fwd * gap * (1.f - 0x1.0p-20f) > Vb + rel;
+                        }
+                    }
+                }
+                keep[r] &= ~__ballot_sync(0xffffffffu, dom);
+            }
+        }
         if ((a.debug & 8) && lane == 0) {
             atomicAdd(a.stats, 1ull);
             atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
                                                          __popc(keep[2]) + __popc(keep[3])));
         }
 
+        const int nkeep = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
+        if (nkeep == 1 && sstar >= 0) {
+            // s* is valid on the whole brick and every other candidate is culled or
+            // dominated: it is the exact argmin of every sample
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sl[k] = (livem >> k & 1) ? sstar : -1;
+        } else {
         // ---- per-sample fp32 screen with packed (d, slot) keys
         unsigned b1[8], b2[8];
 #pragma unroll
@@ -331,6 +406,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 sl[k] = eS;
             }
         }
+        }   // screen
     }
 
     // ---- labels; deferred / stranded samples to their lists (warp-aggregated)
@@ -373,6 +449,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             const unsigned act = __ballot_sync(0xffffffffu, mine >= 0);
             if (!act) break;
             const int L = __shfl_sync(0xffffffffu, mine, __ffs(act) - 1);
+            if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 3, 1ull);
             // count; z counts (8 bits per z); t counts (16 bits per timestep)
             unsigned c = 0, zp = 0, tp = 0;
             double vs = 0.0;

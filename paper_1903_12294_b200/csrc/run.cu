@@ -669,9 +669,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
             MFSEG_CUDA(cudaStreamSynchronize(st));
             fprintf(stderr,
                     "[mfseg stats] field: bricks %llu kept/brick %.2f exact %llu | points: warp tiles %llu "
-                    "kept/tile %.2f exact %llu | stranded f %llu p %llu deferred f %llu p %llu\n",
+                    "kept/tile %.2f exact %llu | stranded f %llu p %llu deferred f %llu p %llu | records/brick %.2f\n",
                     h[8], h[8] ? (double)h[9] / h[8] : 0.0, h[10], h[12], h[12] ? (double)h[13] / h[12] : 0.0,
-                    h[14], h[0], h[1], h[2], h[3]);
+                    h[14], h[0], h[1], h[2], h[3], h[8] ? (double)h[11] / h[8] : 0.0);
         }
     }
     return 0;
