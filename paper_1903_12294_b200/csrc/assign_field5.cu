@@ -186,6 +186,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
     int sl[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) sl[k] = -1;
+    int one = -1;   // slot when a single candidate labels the whole brick (warp-uniform)
     const float fwd = C.fwd, wvf = C.wvf, slack = C.slack, cvmax = C.cvmax;
     if (!C.deferred && C.cnt > 0) {
         float fv[8];
@@ -315,6 +316,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             // dominated: it is the exact argmin of every sample
 #pragma unroll
             for (int k = 0; k < 8; ++k) sl[k] = (livem >> k & 1) ? sstar : -1;
+            one = sstar;
         } else {
         // ---- per-sample fp32 screen with packed (d, slot) keys
         unsigned b1[8], b2[8];
@@ -410,14 +412,38 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
     }
 
     // ---- labels; deferred / stranded samples to their lists (warp-aggregated)
-    int nlist = 0;
     int *lab_base = a.labels + fbase;
+    if (one >= 0) {
+        const int lab = S.id[one];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (!FULL && !(livem >> k & 1)) continue;
-        const int lab = C.deferred ? -2 : (sl[k] >= 0 ? S.id[sl[k]] : -1);
-        lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
-        if (lab < 0) ++nlist;
+        for (int k = 0; k < 8; ++k)
+            if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
+        if (a.accumulate && FULL) {
+            // whole brick -> one cluster: the count marginals are constants
+            double vs = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) vs = DADD(vs, v[k]);
+            vs = warp_sum_d(vs);
+            unsigned *h = S.hist[one];
+            if (lane < 4) atomicAdd(&h[4 * bx + lane], 32u | (32u << 16));         // 8 x, 32 each
+            else if (lane < 6) atomicAdd(&h[8 + 2 * by + (lane - 4)], 64u | (64u << 16));   // 4 y
+            else if (lane < 8) atomicAdd(&h[16 + 2 * bz + (lane - 6)], 64u | (64u << 16));  // 4 z
+            else if (lane == 8) atomicAdd(&h[24 + bt], 128u | (128u << 16));      // 2 timesteps
+            else if (lane == 9) atomicAdd(&h[26], 256u);
+            if (lane == 0) S.wsum[w][one] = DADD(S.wsum[w][one], vs);
+            return;
+        }
+        if (!a.accumulate) return;
+    }
+    int nlist = 0;
+    if (one < 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (!FULL && !(livem >> k & 1)) continue;
+            const int lab = C.deferred ? -2 : (sl[k] >= 0 ? S.id[sl[k]] : -1);
+            lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
+            if (lab < 0) ++nlist;
+        }
     }
     if (__any_sync(0xffffffffu, nlist > 0)) {
         unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
