@@ -46,7 +46,7 @@ struct PCtx {
     double o[4];
     float delta[4], Cf[4];
     float iC[4], uhi, ulo;          // 1 / Cf; 1 +- eps (box test band)
-    float Aabs, cvmax, fwd, wvf;
+    float Aabs, cvmax, fwd, wvf, slack, ndelta;
     int cnt, nrounds, len;
     long long start;
     bool deferred;
@@ -181,18 +181,20 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             vh = wmax_f(h);
         }
         // ---- warp culling (fp32 bounds over the warp-tile box, guard bands widen the box test)
-        float dl[4];
+        float dl[4], qhu[4];
         bool wf[4];
         float ubw = INF_F;
+        unsigned ubkey = 0xFFFFFFFFu;   // (ub | slot) of the best candidate valid on the whole tile
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             dl[r] = INF_F;
+            qhu[r] = INF_F;
             wf[r] = false;
             const int s = lane + 32 * r;
             if (r < C.nrounds && s < C.cnt) {
                 const float4 rc = S.rc[s];
                 const float rcv[4] = {rc.x, rc.y, rc.z, rc.w};
-                float ql = 0.f, qh = 0.f;
+                float ql = 0.f, qh = 0.f, qu = 0.f;
                 bool wfull = true, none = false;
 #pragma unroll
                 for (int d = 0; d < 4; ++d) {
@@ -203,8 +205,10 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                     const float e1 = fminf(a1, cw), e2 = fmaxf(b1, -cw);
                     const float mx = fmaxf(fabsf(e1), fabsf(e2));
                     const float mn = (e2 <= 0.f && e1 >= 0.f) ? 0.f : fminf(fabsf(e1), fabsf(e2));
+                    const float mu = fmaxf(fabsf(a1), fabsf(b1));
                     ql = fmaf(mn, mn, ql);
                     qh = fmaf(mx, mx, qh);
+                    qu = fmaf(mu, mu, qu);
                 }
                 float vtl = 0.f, vth = 0.f;
                 if (USEVAL) {
@@ -217,48 +221,17 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                     }
                 }
                 if (!none) dl[r] = fmaf(C.fwd, sqrt_approx(ql), vtl);
+                qhu[r] = qu;
                 wf[r] = wfull && !none;   // every point of the warp tile passes the box test
-                if (wfull && !none) ubw = fminf(ubw, fmaf(C.fwd, sqrt_approx(qh), vth));
+                if (wfull && !none) {
+                    const float ub = fmaf(C.fwd, sqrt_approx(qh), vth);
+                    ubw = fminf(ubw, ub);
+                    ubkey = min(ubkey, (__float_as_uint(ub) & ~SLOT_MASK) | (unsigned)s);
+                }
             }
         }
         ubw = wmin_f(ubw);
-        // Upper bound from the points themselves: screen every point against the
-        // candidate with the smallest lower bound; if it is valid for all of them,
-        // max over points of d32 bounds every point's best (box UBs need a
-        // candidate whose window covers the whole warp tile).
-        unsigned a1k = 0xFFFFFFFFu, a2k = 0xFFFFFFFFu, b1k = 0xFFFFFFFFu, b2k = 0xFFFFFFFFu;
-        bool unsure0 = false, unsure1 = false;
-        int sstar = -1;
-        {
-            unsigned mk = 0xFFFFFFFFu;
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (dl[r] < INF_F) mk = min(mk, (__float_as_uint(dl[r]) & ~SLOT_MASK) | (unsigned)(lane + 32 * r));
-            mk = __reduce_min_sync(0xffffffffu, mk);
-            if (mk != 0xFFFFFFFFu) {
-                sstar = (int)(mk & SLOT_MASK);
-                const float4 rc = S.rc[sstar];
-                float cvs = 0.f, wvs = 0.f;
-                if (USEVAL) {
-                    cvs = S.cvf[sstar];
-                    wvs = S.wvf[sstar];
-                }
-                bool un0 = false, un1 = false;
-                const float d0 = pair_d32(rc, rp0, C, false, fv0, cvs, wvs, USEVAL, un0);
-                const float d1 = pair_d32(rc, rp1, C, false, fv1, cvs, wvs, USEVAL, un1);
-                const unsigned k0 = (__float_as_uint(d0) & ~SLOT_MASK) | (unsigned)sstar;
-                const unsigned k1 = (__float_as_uint(d1) & ~SLOT_MASK) | (unsigned)sstar;
-                a1k = k0;
-                b1k = k1;
-                unsure0 = un0;
-                unsure1 = un1;
-                // per-point upper bound of d32 (INF when the box test is not certain)
-                const float u0 = (!live0) ? 0.f : (un0 ? INF_F : __uint_as_float(min(k0 & ~SLOT_MASK, INF_BITS)) * (1.f + 0x1.0p-15f));
-                const float u1 = (!live1) ? 0.f : (un1 ? INF_F : __uint_as_float(min(k1 & ~SLOT_MASK, INF_BITS)) * (1.f + 0x1.0p-15f));
-                const float um = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(u0, u1))));
-                ubw = fminf(ubw, um);
-            }
-        }
+        ubkey = __reduce_min_sync(0xffffffffu, ubkey);
         const float Wb = USEVAL ? C.wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * C.Aabs) * (1.f + 0x1.0p-15f);
         unsigned keep[4], kfull[4];
@@ -267,14 +240,84 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
             kfull[r] = __ballot_sync(0xffffffffu, wf[r]);
         }
+
+        // ---- dominance against s' = the fully valid candidate with the smallest upper
+        // bound: per axis the squared-distance difference (r_s - x)^2 - (r_s' - x)^2 is
+        // linear in x, so its minimum over the tile box is at wl or wh.  The fp32
+        // relative coordinates are within delta/2 of the exact scaled differences:
+        // exact dS >= dS32 - |delta| (sqrt Sa + sqrt Sb) - |delta|^2 / 2 - rounding.
+        // Then D_s - D_s' >= w_d dS / (sqrt S_s + sqrt S_s') - (value-term bound).
+        int sdom = -1;
+        if (ubkey != 0xFFFFFFFFu && !(a.debug & 1)) {
+            sdom = (int)(ubkey & SLOT_MASK);
+            const float4 rq = S.rc[sdom];
+            const float rqv[4] = {rq.x, rq.y, rq.z, rq.w};
+            float sb = 0.f;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const float mu = fmaxf(fabsf(rqv[d] - wl[d]), fabsf(rqv[d] - wh[d]));
+                sb = fmaf(mu, mu, sb);
+            }
+            const float rb = sqrt_approx(sb);
+            float cvq = 0.f, wvq = 0.f;
+            if (USEVAL) {
+                cvq = S.cvf[sdom];
+                wvq = S.wvf[sdom];
+            }
+            const float vabs = fmaxf(fabsf(vl), fabsf(vh));
+            const float vq = fmaxf(fabsf(vl - cvq), fabsf(vh - cvq));
+            const float nd = C.ndelta;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (keep[r] == 0u) continue;   // warp-uniform
+                const int s = lane + 32 * r;
+                bool dom = false;
+                if ((keep[r] >> lane & 1u) && s != sdom) {
+                    const float4 rc = S.rc[s];
+                    const float rcv[4] = {rc.x, rc.y, rc.z, rc.w};
+                    float dS = 0.f;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const float al = rcv[d] - wl[d], ah = rcv[d] - wh[d];
+                        const float bl = rqv[d] - wl[d], bh = rqv[d] - wh[d];
+                        dS += fminf(fmaf(al, al, -bl * bl), fmaf(ah, ah, -bh * bh));
+                    }
+                    const float sa = qhu[r], ra = sqrt_approx(sa);
+                    const float dSlb = dS - nd * (ra + rb) * (1.f + 0x1.0p-20f) - 0.5f * nd * nd -
+                                       0x1.0p-20f * (sa + sb);
+                    if (dSlb > 0.f) {
+                        const float den = (ra + rb + nd) * (1.f + 0x1.0p-20f);
+                        const float gap = __fdividef(dSlb, den) * (1.f - 0x1.0p-19f);
+                        float Vb = 0.f;
+                        if (USEVAL && wvq > 0.f) {
+                            const float cvs = S.cvf[s];
+                            const float V = S.wvf[s] > 0.f ? C.wvf * fabsf(cvs - cvq) : C.wvf * vq;
+                            Vb = V * (1.f + 0x1.0p-18f) + 0x1.0p-18f * C.wvf * (fabsf(cvs) + fabsf(cvq) + vabs);
+                        }
+                        const float rel = 0x1.0p-30f * (C.fwd * den + Wb) + C.slack;
+                        dom = C.fwd * gap * (1.f - 0x1.0p-20f) > Vb + rel;
+                    }
+                }
+                keep[r] &= ~__ballot_sync(0xffffffffu, dom);
+            }
+        }
         if ((a.debug & 8) && lane == 0) {
             atomicAdd(a.stats, 1ull);
             atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
                                                          __popc(keep[2]) + __popc(keep[3])));
         }
-        unsigned scan[4];   // kept candidates still to screen (s* already is)
+        unsigned a1k = 0xFFFFFFFFu, a2k = 0xFFFFFFFFu, b1k = 0xFFFFFFFFu, b2k = 0xFFFFFFFFu;
+        bool unsure0 = false, unsure1 = false;
+        const int nkeep = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
+        if (nkeep == 1 && sdom >= 0) {
+            // s' is valid for every point of the tile and every other candidate is
+            // culled or dominated: it is the exact argmin of every point
+            sl0 = live0 ? sdom : -1;
+            sl1 = live1 ? sdom : -1;
+        } else {
+        unsigned scan[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) scan[r] = keep[r] & ~((sstar >> 5) == r ? (1u << (sstar & 31)) : 0u);
+        for (int r = 0; r < 4; ++r) scan[r] = keep[r];
 
         // ---- per-point screen, packed (d, slot) keys
 #pragma unroll
@@ -358,6 +401,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         }
         if (!live0) sl0 = -1;
         if (!live1) sl1 = -1;
+        }   // screen
     }
 
     // ---- labels (bin-sorted order); deferred / stranded lists (warp-aggregated)
@@ -514,8 +558,9 @@ __global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
         C.uhi = 1.0f + eps;
         C.ulo = 1.0f - eps;
         const float D0 = C.delta[0], D1 = C.delta[1], D2 = C.delta[2], D3 = C.delta[3];
-        C.Aabs = 1.1f * (float)a.wd * sqrtf(D0 * D0 + D1 * D1 + D2 * D2 + D3 * D3) +
-                 3e-13f * (float)(a.wd + a.wv);
+        C.ndelta = sqrtf(D0 * D0 + D1 * D1 + D2 * D2 + D3 * D3) * 1.0001f;
+        C.slack = 3e-13f * (float)(a.wd + a.wv);
+        C.Aabs = 1.1f * (float)a.wd * C.ndelta + C.slack;
         C.cvmax = cvmax;
         C.fwd = (float)a.wd;
         C.wvf = USEVAL ? (float)a.wv : 0.f;
