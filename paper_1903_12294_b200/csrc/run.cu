@@ -374,7 +374,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         long long G = (long long)NB * P.nint;
         int gb = bits_for(G - 1);
         P.ngroups = (int)G;
-        P.sub_bits = gb + 12 <= 32 ? 12 : (32 - gb > 0 ? 32 - gb : 0);
+        P.sub_bits = gb + 8 <= 32 ? 8 : (32 - gb > 0 ? 32 - gb : 0);   // 4^4 Morton sub-cells
         P.key_bits = gb + P.sub_bits;
     }
     const int NG = P.ngroups;

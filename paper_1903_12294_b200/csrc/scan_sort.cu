@@ -139,13 +139,23 @@ __global__ void k_digit_hist(const K *keys, long long n, int shift, unsigned *co
     for (int d = threadIdx.x; d < 256; d += RS_BLOCK) counts[(long long)d * tiles + blockIdx.x] = h[d];
 }
 
+// Stable scatter of one tile: ranks from warp match masks, then the tile is
+// staged in shared memory in digit order so every digit's run is written to
+// global memory by consecutive threads (coalesced) instead of item by item.
 template <class K>
 __global__ void __launch_bounds__(RS_BLOCK) k_digit_scatter(const K *keys, const unsigned *vals,
                                                            K *ko, unsigned *vo, long long n,
                                                            int shift, const unsigned *offs,
                                                            long long tiles) {
-    __shared__ unsigned run[RS_WARPS][256];
-    __shared__ unsigned wbase[RS_WARPS][256];
+    // 32-bit keys: run[][] aliases the staging area (dead once wpre is built)
+    constexpr bool STAGE = sizeof(K) == 4;
+    constexpr int RAW = STAGE ? RS_TILE * (int)(sizeof(K) + 4) : RS_WARPS * 256 * 4;
+    __shared__ __align__(16) unsigned char raw[RAW];
+    __shared__ unsigned wpre[RS_WARPS][256];   // tile-local start of (warp, digit)
+    __shared__ unsigned loc[257];              // tile-local start of each digit
+    unsigned (*run)[256] = reinterpret_cast<unsigned (*)[256]>(raw);
+    K *sk = reinterpret_cast<K *>(raw);
+    unsigned *sv = reinterpret_cast<unsigned *>(raw + RS_TILE * sizeof(K));
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = lane; i < 256; i += 32) run[w][i] = 0;
     __syncwarp();
@@ -168,23 +178,71 @@ __global__ void __launch_bounds__(RS_BLOCK) k_digit_scatter(const K *keys, const
         __syncwarp();
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < 256; d += RS_BLOCK) {
-        unsigned acc = offs[(long long)d * tiles + blockIdx.x];
+    // per digit: tile count and the warps' prefix inside the digit
+    unsigned cnt = 0;
+    if (threadIdx.x < 256) {
+        const int d = threadIdx.x;
         for (int q = 0; q < RS_WARPS; ++q) {
-            wbase[q][d] = acc;
-            acc += run[q][d];
+            wpre[q][d] = cnt;
+            cnt += run[q][d];
         }
+        loc[d] = cnt;   // exclusive scan over digits below
     }
     __syncthreads();
+    if (threadIdx.x < 32) {   // exclusive scan of 256 digit counts by one warp
+        unsigned c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c[j] = loc[threadIdx.x * 8 + j];
+            tot += c[j];
+        }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (threadIdx.x >= o) incl += y;
+        }
+        unsigned run_s = incl - tot;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const unsigned cj = c[j];
+            loc[threadIdx.x * 8 + j] = run_s;
+            run_s += cj;
+        }
+        if (threadIdx.x == 31) loc[256] = run_s;
+    }
+    __syncthreads();
+    if (!STAGE) {   // 64-bit keys: direct scatter (link index only)
+#pragma unroll
+        for (int r = 0; r < RS_ROUNDS; ++r) {
+            long long i = base + r * 32 + lane;
+            if (i < n) {
+                unsigned d = (unsigned)(kk[r] >> shift) & 255u;
+                unsigned pos = offs[(long long)d * tiles + blockIdx.x] + wpre[w][d] + rk[r];
+                ko[pos] = kk[r];
+                vo[pos] = vv[r];
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
         long long i = base + r * 32 + lane;
         if (i < n) {
             unsigned d = (unsigned)(kk[r] >> shift) & 255u;
-            unsigned pos = wbase[w][d] + rk[r];
-            ko[pos] = kk[r];
-            vo[pos] = vv[r];
+            unsigned p = loc[d] + wpre[w][d] + rk[r];
+            sk[p] = kk[r];
+            sv[p] = vv[r];
         }
+    }
+    __syncthreads();
+    const int items = (int)min((long long)RS_TILE, n - (long long)blockIdx.x * RS_TILE);
+    for (int i = threadIdx.x; i < items; i += RS_BLOCK) {
+        const K k = sk[i];
+        const unsigned d = (unsigned)(k >> shift) & 255u;
+        const unsigned pos = offs[(long long)d * tiles + blockIdx.x] + (unsigned)i - loc[d];
+        ko[pos] = k;
+        vo[pos] = sv[i];
     }
 }
 
