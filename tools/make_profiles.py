@@ -35,7 +35,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
 traffic = {}
-for rep, name in (("fa5", "field_assign5"), ("pa4", "point_assign4")):
+for rep, name in (("fa5", "field_assign5"), ("fa5late", "field_assign5_late"), ("pa4", "point_assign4")):
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
@@ -43,7 +43,8 @@ for rep, name in (("fa5", "field_assign5"), ("pa4", "point_assign4")):
     r = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = r[0], r[1], r[2]
     m = {a: (v, u) for a, u, v in zip(hdr, units, vals)}
-    lines = [f"ncu --set full --clock-control none (one launch, pass 1 of `tools/prof_run.py c2 2`): k_{name}"]
+    which = "pass 10 of `tools/prof_run.py c2 10`" if rep.endswith("late") else "pass 1 of `tools/prof_run.py c2 2`"
+    lines = [f"ncu --set full --clock-control none (one launch, {which}): k_{name}"]
     for k in want:
         if k in m:
             lines.append(f"{k:60s} {m[k][0]} {m[k][1]}")
