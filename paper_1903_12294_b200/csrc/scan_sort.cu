@@ -120,7 +120,7 @@ int scan_impl(const T *in, T *out, long long n, void *tmp, size_t tmp_bytes, cud
 // ------------------------------------------------------------------ radix sort
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
-constexpr int RS_PER_WARP = 512;
+constexpr int RS_PER_WARP = 256;
 constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;   // 4096
 constexpr int RS_ROUNDS = RS_PER_WARP / 32;       // 16
 
@@ -143,7 +143,7 @@ __global__ void k_digit_hist(const K *keys, long long n, int shift, unsigned *co
 // staged in shared memory in digit order so every digit's run is written to
 // global memory by consecutive threads (coalesced) instead of item by item.
 template <class K>
-__global__ void __launch_bounds__(RS_BLOCK) k_digit_scatter(const K *keys, const unsigned *vals,
+__global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, const unsigned *vals,
                                                            K *ko, unsigned *vo, long long n,
                                                            int shift, const unsigned *offs,
                                                            long long tiles) {
