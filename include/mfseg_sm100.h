@@ -173,6 +173,18 @@ int mfseg_normalize_range(double *values, int64_t n, double lo, double hi, void 
  * Outputs (device): keys [n] int64 (flat key sorted ascending; flat =
  * ((k*ny + j)*nx + i)*n_int + m), members [n] int32 (point indices, stable
  * within a bucket), n_buckets_host.  Returns 2 if a point is outside the grid. */
+/* build_features' trajectory split (postproc.py:152-160, 176-191): order =
+ * point indices sorted by (traj_id, t) (np.lexsort, stable); runs of that order
+ * broken at a new trajectory, a label change or a time gap > stride * (1+1e-9)
+ * with stride = min positive difference of the unique point times (+inf when
+ * there are fewer than two).  run_start[0..n_runs] (device) delimits the runs;
+ * runs of >= 2 points are polylines, single points isolated points.
+ * label: one int32 per point (feature slot).  Synchronises the stream. */
+size_t mfseg_traj_split_workspace_size(int64_t n);
+int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const int32_t *label,
+                     int32_t *order, int32_t *run_start, int64_t *n_runs_host, double *stride_host,
+                     void *workspace, size_t workspace_bytes, void *stream);
+
 size_t mfseg_link_index_workspace_size(int64_t n);
 int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *keys,
                      int32_t *members, int64_t *n_buckets_host, void *workspace,

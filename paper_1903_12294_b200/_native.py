@@ -74,6 +74,8 @@ _SIGNATURES = {
     "mfseg_compare_centers": (C.c_int, [i32, Centers, Centers, f64, P(i32), P(f64), vp]),
     "mfseg_minmax_normalize": (C.c_int, [vp, i64, i32, P(f64), P(f64), vp]),
     "mfseg_normalize_range": (C.c_int, [vp, i64, f64, f64, vp]),
+    "mfseg_traj_split_workspace_size": (szt, [i64]),
+    "mfseg_traj_split": (C.c_int, [i64, vp, vp, vp, vp, vp, P(i64), P(f64), vp, szt, vp]),
     "mfseg_link_index_workspace_size": (szt, [i64]),
     "mfseg_link_index": (C.c_int, [P(Field), P(Points), vp, vp, P(i64), vp, szt, vp]),
     "mfseg_merge_workspace_size": (szt, [i32]),

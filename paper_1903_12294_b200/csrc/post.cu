@@ -389,6 +389,95 @@ int bits_of(unsigned long long v) {
 }
 
 }  // namespace
+
+namespace {
+
+// ------------------------------------------------------------------ trajectory split
+// build_features' polylines (postproc.py:152-160, 176-191): points ordered by
+// (traj_id, t) (np.lexsort, stable), runs broken at a new trajectory, a feature
+// change or a time gap larger than stride * (1 + 1e-9), stride = the smallest
+// positive difference of the sorted unique point times.
+
+__device__ __forceinline__ unsigned long long dkey(double x) {   // order-preserving bits
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_tkeys(long long n, const double *t, unsigned long long *k, unsigned *v) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    k[i] = dkey(t[i]);
+    v[i] = (unsigned)i;
+}
+
+// over the sorted times: unique flags and the smallest positive gap between uniques
+__global__ void k_tunique(long long n, const unsigned long long *sk, const unsigned *perm,
+                          const double *t, int *uflag, unsigned long long *min_gap) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bool u = i == 0 || sk[i] != sk[i - 1];
+    uflag[i] = u ? 1 : 0;
+    if (u && i > 0) {
+        const double g = DSUB(t[perm[i]], t[perm[i - 1]]);   // np.diff(np.unique(t))
+        if (g > 0.0) atomicMin(min_gap, (unsigned long long)__double_as_longlong(g));
+    }
+}
+
+// t rank of every point (index of its value among the sorted unique times)
+__global__ void k_trank(long long n, const int *urank_incl, const unsigned *perm, unsigned *trank) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    trank[perm[i]] = (unsigned)(urank_incl[i] - 1);
+}
+
+__global__ void k_traj_minmax(long long n, const long long *tid, unsigned long long *mm) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        lo = min(lo, tid[i]);
+        hi = max(hi, tid[i]);
+    }
+    // signed -> order-preserving unsigned for the atomics
+    atomicMin(&mm[0], (unsigned long long)lo ^ 0x8000000000000000ull);
+    atomicMax(&mm[1], (unsigned long long)hi ^ 0x8000000000000000ull);
+}
+
+__global__ void k_lex_keys(long long n, const long long *tid, const unsigned *trank, long long tmin,
+                           int tbits, unsigned long long *k, unsigned *v) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    k[i] = ((unsigned long long)(tid[i] - tmin) << tbits) | trank[i];
+    v[i] = (unsigned)i;
+}
+
+__global__ void k_traj_breaks(long long n, const unsigned *order, const long long *tid,
+                              const double *t, const int *lab, double gap_limit, int *brk) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    bool b = i == 0;
+    if (!b) {
+        const unsigned j = order[i], q = order[i - 1];
+        b = tid[j] != tid[q] || lab[j] != lab[q] || DSUB(t[j], t[q]) > gap_limit;
+    }
+    brk[i] = b ? 1 : 0;
+}
+
+__global__ void k_run_starts(long long n, const int *brk, const int *incl, int *starts) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == n) {
+        starts[incl[n - 1]] = (int)n;
+        return;
+    }
+    if (brk[i]) starts[incl[i] - 1] = (int)i;
+}
+
+__global__ void k_inclusive_from_exclusive(long long n, const int *in, const int *ex, int *incl) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) incl[i] = ex[i] + in[i];
+}
+
+}  // namespace
 }  // namespace mfseg
 
 using namespace mfseg;
@@ -653,6 +742,110 @@ int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *key
         return 2;
     }
     if (n_buckets_host) *n_buckets_host = (int64_t)nb;
+    return 0;
+}
+
+
+size_t mfseg_traj_split_workspace_size(int64_t n) {
+    Carver cv;
+    cv.take<unsigned long long>(n);
+    cv.take<unsigned>(n);
+    cv.take<unsigned long long>(n);
+    cv.take<unsigned>(n);
+    cv.take<int>(n);
+    cv.take<int>(n);
+    cv.take<int>(n);
+    cv.take<unsigned>(n);
+    cv.take<unsigned long long>(4);
+    const size_t rb = radix_tmp_bytes(n > 0 ? n : 1), sb = scan_tmp_bytes(n > 0 ? n : 1);
+    cv.take<char>(rb > sb ? rb : sb);
+    return cv.off + 256;
+}
+
+int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const int32_t *label,
+                     int32_t *order, int32_t *run_start, int64_t *n_runs_host, double *stride_host,
+                     void *workspace, size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_runs_host) *n_runs_host = 0;
+    if (n <= 0) return 0;
+    if (n >= (1ll << 31)) {
+        set_error("traj_split: more than 2^31-1 points");
+        return 2;
+    }
+    if (workspace_bytes < mfseg_traj_split_workspace_size(n)) {
+        set_error("traj_split: workspace too small");
+        return 3;
+    }
+    Carver cv(workspace, workspace_bytes);
+    unsigned long long *k0 = cv.take<unsigned long long>(n);
+    unsigned *v0 = cv.take<unsigned>(n);
+    unsigned long long *k1 = cv.take<unsigned long long>(n);
+    unsigned *v1 = cv.take<unsigned>(n);
+    int *flag = cv.take<int>(n);
+    int *ex = cv.take<int>(n);
+    int *incl = cv.take<int>(n);
+    unsigned *trank = cv.take<unsigned>(n);
+    unsigned long long *misc = cv.take<unsigned long long>(4);   // min gap, traj min, traj max
+    const size_t rb = radix_tmp_bytes(n), sb = scan_tmp_bytes(n);
+    void *tmp = cv.take<char>(rb > sb ? rb : sb);
+    const size_t tmpb = rb > sb ? rb : sb;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    const unsigned long long init[3] = {0x7FF0000000000000ull, ~0ull, 0ull};   // +inf, min, max
+    MFSEG_CUDA(cudaMemcpyAsync(misc, init, sizeof init, cudaMemcpyHostToDevice, st));
+    // 1. sorted unique times -> stride and per-point t ranks
+    ::mfseg::count_launch();
+    k_tkeys<<<g, 256, 0, st>>>(n, t, k0, v0);
+    MFSEG_TRY(radix_sort_pairs64(k0, v0, k1, v1, n, 64, tmp, tmpb, st));
+    ::mfseg::count_launch();
+    k_tunique<<<g, 256, 0, st>>>(n, k1, v1, t, flag, misc);
+    MFSEG_TRY(scan_exclusive_i32(flag, ex, n, tmp, tmpb, st));
+    ::mfseg::count_launch();
+    k_inclusive_from_exclusive<<<g, 256, 0, st>>>(n, flag, ex, incl);
+    ::mfseg::count_launch();
+    k_trank<<<g, 256, 0, st>>>(n, incl, v1, trank);
+    ::mfseg::count_launch();
+    k_traj_minmax<<<148 * 4, 256, 0, st>>>(n, (const long long *)traj_id, misc + 1);
+    MFSEG_LAUNCH("traj_split ranks");
+    unsigned long long h[3];
+    int nu = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(h, misc, sizeof h, cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaMemcpyAsync(&nu, incl + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    double stride;
+    memcpy(&stride, &h[0], sizeof stride);   // +inf when fewer than two unique times
+    const long long tmin = (long long)(h[1] ^ 0x8000000000000000ull);
+    const long long tmax = (long long)(h[2] ^ 0x8000000000000000ull);
+    const unsigned long long range = (unsigned long long)tmax - (unsigned long long)tmin;
+    int tbits = 0;
+    while ((1ll << tbits) < nu) ++tbits;
+    int rbits = 0;
+    while (rbits < 64 && (range >> rbits) != 0) ++rbits;
+    // 2. lexsort((t, traj_id)): one stable sort of (traj - min, t rank)
+    if (rbits + tbits <= 64) {
+        ::mfseg::count_launch();
+        k_lex_keys<<<g, 256, 0, st>>>(n, (const long long *)traj_id, trank, tmin, tbits, k0, v0);
+        MFSEG_TRY(radix_sort_pairs64(k0, v0, k1, v1, n, rbits + tbits > 0 ? rbits + tbits : 1, tmp,
+                                     tmpb, st));
+    } else {
+        set_error("traj_split: trajectory id range and time count exceed 64 key bits");
+        return 2;
+    }
+    // 3. run breaks along the sorted order and their compaction
+    volatile double gap_limit = stride * (1.0 + 1e-9);   // stride * (1 + 1e-9), postproc.py:182
+    ::mfseg::count_launch();
+    k_traj_breaks<<<g, 256, 0, st>>>(n, v1, (const long long *)traj_id, t, label, gap_limit, flag);
+    MFSEG_TRY(scan_exclusive_i32(flag, ex, n, tmp, tmpb, st));
+    ::mfseg::count_launch();
+    k_inclusive_from_exclusive<<<g, 256, 0, st>>>(n, flag, ex, incl);
+    ::mfseg::count_launch();
+    k_run_starts<<<(unsigned)((n + 256) / 256), 256, 0, st>>>(n, flag, incl, run_start);
+    MFSEG_CUDA(cudaMemcpyAsync(order, v1, sizeof(unsigned) * n, cudaMemcpyDeviceToDevice, st));
+    MFSEG_LAUNCH("traj_split runs");
+    int nr = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&nr, incl + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (n_runs_host) *n_runs_host = nr;
+    if (stride_host) *stride_host = stride;
     return 0;
 }
 

@@ -4,12 +4,13 @@
   merge_clusters  -> mfseg_merge        union-find over eligible pairs, smallest
                                         id root; merged rows in the reference's
                                         summation order (bit-identical)
-  build_features  -> mfseg_relabel + mfseg_voxel_csr + mfseg_feature_stats
+  build_features  -> mfseg_relabel + mfseg_traj_split + mfseg_voxel_csr +
+                     mfseg_feature_stats
   feature_stats   -> mfseg_feature_stats (exact sums; bbox exact)
 
-Trajectory splitting (postproc.py:176-191) is the one host step here: a
-sequential run-length pass over each time-ordered trajectory that only
-decides polyline vs isolated-point grouping ("next").
+Trajectory splitting (postproc.py:152-160, 176-191) orders the points by
+(traj_id, t) and finds the run breaks on the GPU; only the Python lists of
+polylines / isolated points the API returns are built on the host.
 """
 
 from __future__ import annotations
@@ -173,28 +174,39 @@ def voxel_csr_device(fslot: torch.Tensor, nt: int, ncell: int, n_slots: int):
     return seg, cells
 
 
-def _split_trajectories(flabel, traj_id, t, feats):
-    """Polylines / isolated points per time-ordered trajectory (postproc.py:152-160,176-191)."""
-    ut = np.unique(t)
-    stride = np.diff(ut).min() if len(ut) > 1 else np.inf
-    order = np.lexsort((t, traj_id))
-    tid = traj_id[order]
-    lab = flabel[order]
-    ts = t[order]
-    n = len(order)
-    # a run breaks at a new trajectory, a feature change, or a time gap
-    brk = np.ones(n + 1, bool)
-    if n > 1:
-        brk[1:n] = (tid[1:] != tid[:-1]) | (lab[1:] != lab[:-1]) | \
-                   ((ts[1:] - ts[:-1]) > stride * (1 + 1e-9))
-    starts = np.flatnonzero(brk[:n])
-    ends = np.r_[starts[1:], n]
-    for a, e in zip(starts, ends):
-        f = feats[int(lab[a])]
+def split_trajectories_device(traj_id: torch.Tensor, t: torch.Tensor, label: torch.Tensor):
+    """GPU trajectory split (postproc.py:152-160, 176-191) through mfseg_traj_split:
+    returns (order, run_start, stride) with order = point indices sorted by
+    (traj_id, t), run_start delimiting the runs (device tensors)."""
+    lib = N.load()
+    n = int(t.numel())
+    dev = t.device
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    starts = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(lib.mfseg_traj_split_workspace_size(n)), dtype=torch.uint8, device=dev)
+    nr, stride = C.c_int64(0), C.c_double(0.0)
+    tid = traj_id.to(device=dev, dtype=torch.int64).contiguous()
+    lab = label.to(device=dev, dtype=torch.int32).contiguous()
+    tt = t.to(device=dev, dtype=torch.float64).contiguous()
+    N.check(lib.mfseg_traj_split(n, N.ptr(tid), N.ptr(tt), N.ptr(lab), N.ptr(order), N.ptr(starts),
+                                 C.byref(nr), C.byref(stride), N.ptr(ws), ws.numel(), stream_ptr()),
+            "mfseg_traj_split")
+    return order[:n], starts[:nr.value + 1], stride.value
+
+
+def _split_trajectories(fid_of_slot, pslot, traj_id, t, feats):
+    """Polylines / isolated points per time-ordered trajectory (postproc.py:152-160,
+    176-191): ordering and run detection on the GPU, list building on the host."""
+    order, starts, _ = split_trajectories_device(traj_id, t, pslot)
+    order_h = order.cpu().numpy().astype(np.int64)
+    st = starts.cpu().numpy()
+    run_fid = fid_of_slot[pslot.cpu().numpy()[order_h[st[:-1]]]]
+    for a, e, fid in zip(st[:-1].tolist(), st[1:].tolist(), run_fid.tolist()):
+        f = feats[fid]
         if e - a >= 2:
-            f.polylines.append(order[a:e])
+            f.polylines.append(order_h[a:e])
         else:
-            f.isolated_points.append(int(order[a]))
+            f.isolated_points.append(int(order_h[a]))
 
 
 def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSet,
@@ -227,8 +239,9 @@ def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSe
         ps_h = pslot.cpu().numpy()
         if np.any(ps_h < 0):
             raise KeyError("point label without a merge_map entry")
-        _split_trajectories(np.asarray(fids)[ps_h], np.asarray(points.traj_id),
-                            np.asarray(points.t), feats)
+        _split_trajectories(np.asarray(fids), pslot,
+                            to_dev(np.asarray(points.traj_id, np.int64), torch.int64, dev), pts.t,
+                            feats)
     if fld.nt:
         fl = to_dev(np.asarray(seg.field_labels, np.int64), torch.int32, dev)
         fslot = feature_slots_device(fl, lut)

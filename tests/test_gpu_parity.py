@@ -479,3 +479,31 @@ def test_kernel_generations_agree(w_d, seed, monkeypatch):
     pl1, fl1 = P.assign_iteration(ps, fs, None, cs, grid, params, C)
     np.testing.assert_array_equal(fl, fl1)
     np.testing.assert_array_equal(pl, pl1)
+
+
+@pytest.mark.parametrize("seed,n,n_traj,single_time", [(0, 5000, 300, False), (1, 200000, 7000, False),
+                                                       (2, 1000, 50, True)])
+def test_traj_split_matches_numpy(seed, n, n_traj, single_time):
+    """mfseg_traj_split vs the reference's lexsort + run rules (postproc.py:152-160,
+    176-191): negative and sparse trajectory ids, repeated times, time gaps,
+    label changes; a single unique time (stride = inf)."""
+    from paper_1903_12294_b200.postproc import split_trajectories_device
+    rng = np.random.default_rng(seed)
+    tid = rng.choice(np.arange(-50, 10 * n_traj, 10), n_traj, replace=False)[rng.integers(0, n_traj, n)]
+    times = np.array([0.0]) if single_time else np.sort(rng.choice(np.arange(0, 60) * 0.25, 40,
+                                                                   replace=False))
+    t = times[rng.integers(0, len(times), n)]
+    lab = rng.integers(0, 4, n).astype(np.int32)
+    order, starts, stride = split_trajectories_device(torch.as_tensor(tid), torch.as_tensor(t).cuda(),
+                                                      torch.as_tensor(lab))
+    # numpy restatement of the reference
+    u = np.unique(t)
+    ref_stride = np.diff(u).min() if len(u) > 1 else np.inf
+    ref_order = np.lexsort((t, tid))
+    ts, ls, ids = t[ref_order], lab[ref_order], tid[ref_order]
+    brk = np.ones(n, bool)
+    brk[1:] = (ids[1:] != ids[:-1]) | (ls[1:] != ls[:-1]) | ((ts[1:] - ts[:-1]) > ref_stride * (1 + 1e-9))
+    ref_starts = np.r_[np.flatnonzero(brk), n]
+    assert stride == ref_stride
+    np.testing.assert_array_equal(order.cpu().numpy(), ref_order)
+    np.testing.assert_array_equal(starts.cpu().numpy(), ref_starts)
