@@ -26,15 +26,25 @@ __device__ __forceinline__ bool values_match(double a, double b, double eps) {
     bool na = isnan(a), nb = isnan(b);
     if (na && nb) return true;    // both lack the kind
     if (na || nb) return false;   // one-sided absence never merges
-    double pct = DDIV(DMUL(2.0, fabs(DSUB(a, b))), DADD(DADD(fabs(a), fabs(b)), DELTA));
-    return pct <= eps;
+    // pct = fl(r / s) <= eps with r, s computed exactly as the reference; the
+    // division is only needed near the threshold: r < eps s (1 - 2^-50) implies
+    // fl(r / s) <= eps, r > eps s (1 + 2^-50) implies fl(r / s) > eps
+    const double r = DMUL(2.0, fabs(DSUB(a, b))), s = DADD(DADD(fabs(a), fabs(b)), DELTA);
+    const double es = eps * s;
+    if (r < es * (1.0 - 0x1.0p-50)) return true;
+    if (r > es * (1.0 + 0x1.0p-50)) return false;
+    return DDIV(r, s) <= eps;
 }
 
 __device__ int uf_find(int *parent, int a) {
+    // path halving: every visited node is re-pointed to its grandparent (benign
+    // races: parents only ever move to smaller rows of the same component)
     int p = ((volatile int *)parent)[a];
     while (p != a) {
+        const int gp = ((volatile int *)parent)[p];
+        if (gp != p) atomicMin(&parent[a], gp);
         a = p;
-        p = ((volatile int *)parent)[a];
+        p = gp;
     }
     return a;
 }

@@ -199,14 +199,21 @@ def _split_trajectories(fid_of_slot, pslot, traj_id, t, feats):
     176-191): ordering and run detection on the GPU, list building on the host."""
     order, starts, _ = split_trajectories_device(traj_id, t, pslot)
     order_h = order.cpu().numpy().astype(np.int64)
-    st = starts.cpu().numpy()
+    st = starts.cpu().numpy().astype(np.int64)
+    if len(st) < 2:
+        return
     run_fid = fid_of_slot[pslot.cpu().numpy()[order_h[st[:-1]]]]
-    for a, e, fid in zip(st[:-1].tolist(), st[1:].tolist(), run_fid.tolist()):
-        f = feats[fid]
-        if e - a >= 2:
-            f.polylines.append(order_h[a:e])
-        else:
-            f.isolated_points.append(int(order_h[a]))
+    poly = np.diff(st) >= 2
+    by_fid = np.argsort(run_fid, kind="stable")  # runs grouped by feature, order kept
+    fs = run_fid[by_fid]
+    bounds = np.flatnonzero(np.r_[True, fs[1:] != fs[:-1], True])
+    for b0, b1 in zip(bounds[:-1].tolist(), bounds[1:].tolist()):
+        f = feats[int(fs[b0])]
+        sel = by_fid[b0:b1]
+        ps = sel[poly[sel]]
+        # polylines are views of the ordered index array (as np.split in the reference)
+        f.polylines.extend(map(order_h.__getitem__, map(slice, st[ps].tolist(), st[ps + 1].tolist())))
+        f.isolated_points.extend(order_h[st[sel[~poly[sel]]]].tolist())
 
 
 def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSet,
@@ -234,7 +241,7 @@ def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSe
     n_slots = len(fids)
     pslot = fslot = None
     if pts.n:
-        pl = to_dev(np.asarray(seg.point_labels, np.int64), torch.int32, dev)
+        pl = to_dev(np.asarray(seg.point_labels), torch.int32, dev)
         pslot = feature_slots_device(pl, lut)
         ps_h = pslot.cpu().numpy()
         if np.any(ps_h < 0):
@@ -243,7 +250,7 @@ def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSe
                             to_dev(np.asarray(points.traj_id, np.int64), torch.int64, dev), pts.t,
                             feats)
     if fld.nt:
-        fl = to_dev(np.asarray(seg.field_labels, np.int64), torch.int32, dev)
+        fl = to_dev(np.asarray(seg.field_labels), torch.int32, dev)
         fslot = feature_slots_device(fl, lut)
         ncell = int(np.prod(fld.dims))
         seg_start, cells = voxel_csr_device(fslot, fld.nt, ncell, n_slots)
