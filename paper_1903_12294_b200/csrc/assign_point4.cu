@@ -161,24 +161,16 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             rp0[d] = (float)DMUL(DSUB(P0[d], C.o[d]), sc);
             rp1[d] = (float)DMUL(DSUB(P1[d], C.o[d]), sc);
         }
-        // warp-tile box (fp32, chunk-relative) and value range
-        float wl[4], wh[4];
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            float l = INF_F, h = -INF_F;
-            if (live0) { l = rp0[d]; h = rp0[d]; }
-            if (live1) { l = fminf(l, rp1[d]); h = fmaxf(h, rp1[d]); }
-            wl[d] = wmin_f(l);
-            wh[d] = wmax_f(h);
-        }
+        // warp-tile box (fp32, chunk-relative) and value range: precomputed once per
+        // run by k_wtile_box with exactly these formulas
+        const WBox wb = a.wbox[(size_t)blockIdx.x * (POINT_CHUNK / 64) + wt];
+        const float wl[4] = {wb.lo.x, wb.lo.y, wb.lo.z, wb.lo.w};
+        const float wh[4] = {wb.hi.x, wb.hi.y, wb.hi.z, wb.hi.w};
         const float fv0 = (float)P0[4], fv1 = (float)P1[4];
         float vl = 0.f, vh = 0.f;
         if (USEVAL) {
-            float l = INF_F, h = -INF_F;
-            if (live0) { l = fv0; h = fv0; }
-            if (live1) { l = fminf(l, fv1); h = fmaxf(h, fv1); }
-            vl = wmin_f(l);
-            vh = wmax_f(h);
+            vl = wb.v.x;
+            vh = wb.v.y;
         }
         // ---- warp culling (fp32 bounds over the warp-tile box, guard bands widen the box test)
         float dl[4], qhu[4];
@@ -629,14 +621,67 @@ __global__ void k_tile_box(const int4 *tiles, const int *n_tiles, long long max_
     }
 }
 
+// chunk-relative fp32 box and fl32(value) range of every 64-point warp tile
+// (one warp per warp tile; same formulas as k_point_assign4 would use)
+__global__ void k_wtile_box(const int4 *tiles, const int *n_tiles, long long max_tiles,
+                            const double *x, const double *y, const double *z, const double *t,
+                            const double *v, double cf, const double *box, WBox *out) {
+    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long tile = wid / (POINT_CHUNK / 64);
+    const int wt = (int)(wid % (POINT_CHUNK / 64));
+    if (tile >= max_tiles || tile >= *n_tiles) return;
+    const int4 T = tiles[tile];
+    if (64 * wt >= T.z) return;
+    const double *o = box + 8 * tile;
+    float lo[5], hi[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        lo[d] = INF_F;
+        hi[d] = -INF_F;
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int off = 64 * wt + lane + 32 * q;
+        if (off >= T.z) continue;
+        const long long p = (long long)T.y + off;
+        const double P[4] = {x[p], y[p], z[p], t[p]};
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const float r = (float)DMUL(DSUB(P[d], o[d]), d == 3 ? cf : 1.0);
+            lo[d] = fminf(lo[d], r);
+            hi[d] = fmaxf(hi[d], r);
+        }
+        const float fv = (float)v[p];
+        lo[4] = fminf(lo[4], fv);
+        hi[4] = fmaxf(hi[4], fv);
+    }
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        lo[d] = wmin_f(lo[d]);
+        hi[d] = wmax_f(hi[d]);
+    }
+    if (lane == 0) {
+        WBox b;
+        b.lo = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        b.hi = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        b.v = make_float2(lo[4], hi[4]);
+        out[tile * (POINT_CHUNK / 64) + wt] = b;
+    }
+}
+
 int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,
-                    const double *y, const double *z, const double *t, double *box,
-                    cudaStream_t st) {
+                    const double *y, const double *z, const double *t, const double *v, double cf,
+                    double *box, WBox *wbox, cudaStream_t st) {
     if (max_tiles <= 0) return 0;
     ::mfseg::count_launch();
     const long long threads = max_tiles * 32;
     k_tile_box<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(tiles, n_tiles, max_tiles, x, y, z,
                                                                    t, box);
+    ::mfseg::count_launch();
+    const long long wthreads = max_tiles * (POINT_CHUNK / 64) * 32;
+    k_wtile_box<<<(unsigned)((wthreads + 255) / 256), 256, 0, st>>>(tiles, n_tiles, max_tiles, x, y,
+                                                                     z, t, v, cf, box, wbox);
     MFSEG_LAUNCH("k_tile_box");
     return 0;
 }

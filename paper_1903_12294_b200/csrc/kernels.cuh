@@ -36,12 +36,19 @@ struct FieldArgs {
     unsigned long long *stats;   // debug bit3: [0] bricks, [1] kept candidates, [2] exact samples
 };
 
+struct WBox {                 // one 64-point warp tile of a point chunk (k_point_assign4)
+    float4 lo, hi;            // chunk-relative fp32 box (t scaled by c_f)
+    float2 v;                 // range of fl32(value)
+    float2 pad;
+};
+
 struct PointArgs {
     long long n;
     const double *x, *y, *z, *t, *v;   // bin-sorted SoA
     const int4 *tiles;                 // (bin, start, len, -)
     const int *n_tiles;
     const double *tile_box;            // [tile][8]: exact lo[4], hi[4] (k_point_assign4)
+    const WBox *wbox;                  // [tile][POINT_CHUNK / 64] warp-tile boxes
     double Cx, Cy, Cz, Ct;
     double cf, wd, wv;
     CentersView c;
@@ -104,8 +111,8 @@ int field_tile_dims(int *tx, int *ty, int *tz);
 int point_tile_size();
 int point_version();
 int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,
-                    const double *y, const double *z, const double *t, double *box,
-                    cudaStream_t st);
+                    const double *y, const double *z, const double *t, const double *v, double cf,
+                    double *box, WBox *wbox, cudaStream_t st);
 int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st);
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st);
 int launch_fallback(const FallbackArgs &a, cudaStream_t st);

@@ -260,6 +260,7 @@ struct Plan {
     int ngroups, nint, sub_bits, key_bits;
     int4 *tiles;
     double *tbox;                   // exact box per point chunk (v4)
+    WBox *wbox;                     // per warp tile of a chunk (v4)
     long long max_tiles;
     long long *stranded_p, *deferred_p;
     long long cap_p;
@@ -385,6 +386,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.max_tiles = n > 0 ? (n + TP - 1) / TP + NG : 0;
     P.tiles = cv.take<int4>(P.max_tiles);
     P.tbox = cv.take<double>(8 * P.max_tiles);
+    P.wbox = cv.take<WBox>(P.max_tiles * (POINT_CHUNK / 64));
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
     P.deferred_p = cv.take<long long>(P.cap_p);
@@ -488,7 +490,7 @@ int plan_prepare(Plan &P) {
         MFSEG_LAUNCH("point tiles");
         if (point_version() == 4)
             MFSEG_TRY(launch_tile_box(P.tiles, P.tstart + NG, P.max_tiles, P.px, P.py, P.pz, P.pt,
-                                      P.tbox, st));
+                                      P.pv, p.c_f, P.tbox, P.wbox, st));
     }
     return 0;
 }
@@ -586,6 +588,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.tiles = P.tiles;
         a.n_tiles = P.tstart + P.ngroups;
         a.tile_box = P.tbox;
+        a.wbox = P.wbox;
         a.Cx = p.C[0];
         a.Cy = p.C[1];
         a.Cz = p.C[2];
