@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
     __shared__ unsigned loc[257];              // tile-local start of each digit
     unsigned (*run)[256] = reinterpret_cast<unsigned (*)[256]>(raw);
     K *sk = reinterpret_cast<K *>(raw);
-    unsigned *sv = reinterpret_cast<unsigned *>(raw + RS_TILE * sizeof(K));
+    unsigned *sv = nullptr;
+    if constexpr (STAGE) sv = reinterpret_cast<unsigned *>(raw + RS_TILE * sizeof(K));
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = lane; i < 256; i += 32) run[w][i] = 0;
     __syncwarp();
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
         if (threadIdx.x == 31) loc[256] = run_s;
     }
     __syncthreads();
-    if (!STAGE) {   // 64-bit keys: direct scatter (link index only)
+    if constexpr (!STAGE) {   // 64-bit keys: direct scatter (link index, trajectory split)
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
             long long i = base + r * 32 + lane;
@@ -223,26 +224,26 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
                 vo[pos] = vv[r];
             }
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int r = 0; r < RS_ROUNDS; ++r) {
-        long long i = base + r * 32 + lane;
-        if (i < n) {
-            unsigned d = (unsigned)(kk[r] >> shift) & 255u;
-            unsigned p = loc[d] + wpre[w][d] + rk[r];
-            sk[p] = kk[r];
-            sv[p] = vv[r];
+        for (int r = 0; r < RS_ROUNDS; ++r) {
+            long long i = base + r * 32 + lane;
+            if (i < n) {
+                unsigned d = (unsigned)(kk[r] >> shift) & 255u;
+                unsigned p = loc[d] + wpre[w][d] + rk[r];
+                sk[p] = kk[r];
+                sv[p] = vv[r];
+            }
         }
-    }
-    __syncthreads();
-    const int items = (int)min((long long)RS_TILE, n - (long long)blockIdx.x * RS_TILE);
-    for (int i = threadIdx.x; i < items; i += RS_BLOCK) {
-        const K k = sk[i];
-        const unsigned d = (unsigned)(k >> shift) & 255u;
-        const unsigned pos = offs[(long long)d * tiles + blockIdx.x] + (unsigned)i - loc[d];
-        ko[pos] = k;
-        vo[pos] = sv[i];
+        __syncthreads();
+        const int items = (int)min((long long)RS_TILE, n - (long long)blockIdx.x * RS_TILE);
+        for (int i = threadIdx.x; i < items; i += RS_BLOCK) {
+            const K k = sk[i];
+            const unsigned d = (unsigned)(k >> shift) & 255u;
+            const unsigned pos = offs[(long long)d * tiles + blockIdx.x] + (unsigned)i - loc[d];
+            ko[pos] = k;
+            vo[pos] = sv[i];
+        }
     }
 }
 
