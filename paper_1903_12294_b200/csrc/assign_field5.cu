@@ -161,7 +161,9 @@ __device__ __forceinline__ void table_row(float *e, float2 *mm, const double *co
 
 // One warp brick: lane (lx, ly) = (8 bx + lane % 8, 4 by + lane / 8), samples
 // k = 4 r + q at z = 4 bz + q, timestep 2 bt + r.  FULL: all 256 samples exist.
-template <bool USEVAL, bool FULL>
+// NR: rounds of 32 candidate slots (3 when the block has <= 96 candidates: the
+// common case gets a smaller instruction footprint)
+template <bool USEVAL, bool FULL, int NR>
 __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bx, int by,
                                       int bz, int bt, int &ovf_local) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -210,7 +212,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         float ubw = INF_F;
         unsigned ubkey = 0xFFFFFFFFu;   // (ub | slot) of the best fully valid candidate
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NR; ++r) {
             dl[r] = INF_F;
             shi[r] = INF_F;
             const int s = lane + 32 * r;
@@ -237,9 +239,9 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         ubw = warp_min_f(ubw);
         const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vwl), fabsf(vwh)) + cvmax) : 0.f) + slack;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
-        unsigned keep[4];
+        unsigned keep[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < NR; ++r)
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
 
         // ---- dominance: drop kept candidates s with D(s) > D(s*) on the whole brick,
@@ -273,7 +275,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             const float vabs = fmaxf(fabsf(vwl), fabsf(vwh));
             const float vq = fmaxf(fabsf(vwl - cvq), fabsf(vwh - cvq));
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < NR; ++r) {
                 const int s = lane + 32 * r;
                 bool dom = false;
                 if ((keep[r] >> lane & 1u) && s != sstar) {
@@ -326,7 +328,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             b2[k] = 0xFFFFFFFFu;
         }
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NR; ++r) {
             unsigned it = keep[r];
             while (it) {
                 const int s = __ffs(it) - 1 + 32 * r;
@@ -380,7 +382,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 double eD = INF_D;
                 int eI = INT_MAX, eS = -1;
 #pragma unroll 1
-                for (int r = 0; r < 4; ++r) {
+                for (int r = 0; r < NR; ++r) {
                     unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
                     while (it) {
                         const int s = __ffs(it) - 1 + 32 * r;
@@ -670,10 +672,17 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             continue;   // warp-uniform
         const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len && GZ * bz + GZ <= Z.len &&
                           GT * bt + GT <= Tm.len;
-        if (full)
-            brick<USEVAL, true>(a, S, C, bx, by, bz, bt, ovf_local);
-        else
-            brick<USEVAL, false>(a, S, C, bx, by, bz, bt, ovf_local);
+        if (C.nrounds <= 3) {
+            if (full)
+                brick<USEVAL, true, 3>(a, S, C, bx, by, bz, bt, ovf_local);
+            else
+                brick<USEVAL, false, 3>(a, S, C, bx, by, bz, bt, ovf_local);
+        } else {
+            if (full)
+                brick<USEVAL, true, 4>(a, S, C, bx, by, bz, bt, ovf_local);
+            else
+                brick<USEVAL, false, 4>(a, S, C, bx, by, bz, bt, ovf_local);
+        }
     }
 
     // ---- once per block: marginals x fixed-point coordinates -> global 128-bit sums
