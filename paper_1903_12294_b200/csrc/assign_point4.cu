@@ -137,7 +137,8 @@ __device__ __forceinline__ float pair_d32(const float4 &r, const float *rp, cons
     return d;
 }
 
-template <bool USEVAL>
+// NR: rounds of 32 candidate slots (3 for chunks with <= 96 candidates)
+template <bool USEVAL, int NR>
 __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const PCtx &C, int wt,
                                            int &ovf_local) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -178,7 +179,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         float ubw = INF_F;
         unsigned ubkey = 0xFFFFFFFFu;   // (ub | slot) of the best candidate valid on the whole tile
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NR; ++r) {
             dl[r] = INF_F;
             qhu[r] = INF_F;
             wf[r] = false;
@@ -226,9 +227,9 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         ubkey = __reduce_min_sync(0xffffffffu, ubkey);
         const float Wb = USEVAL ? C.wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb + 2.f * C.Aabs) * (1.f + 0x1.0p-15f);
-        unsigned keep[4], kfull[4];
+        unsigned keep[4] = {0u, 0u, 0u, 0u}, kfull[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NR; ++r) {
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
             kfull[r] = __ballot_sync(0xffffffffu, wf[r]);
         }
@@ -260,7 +261,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             const float vq = fmaxf(fabsf(vl - cvq), fabsf(vh - cvq));
             const float nd = C.ndelta;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < NR; ++r) {
                 if (keep[r] == 0u) continue;   // warp-uniform
                 const int s = lane + 32 * r;
                 bool dom = false;
@@ -307,13 +308,13 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             sl0 = live0 ? sdom : -1;
             sl1 = live1 ? sdom : -1;
         } else {
-        unsigned scan[4];
+        unsigned scan[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < 4; ++r) scan[r] = keep[r];
+        for (int r = 0; r < NR; ++r) scan[r] = keep[r];
 
         // ---- per-point screen, packed (d, slot) keys
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NR; ++r) {
             unsigned it = scan[r];
             while (it) {
                 const int b = __ffs(it) - 1, s = b + 32 * r;
@@ -362,7 +363,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             double eD0 = INF_D, eD1 = INF_D;
             int eI0 = INT_MAX, eI1 = INT_MAX, eS0 = -1, eS1 = -1;
 #pragma unroll 1
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < NR; ++r) {
                 unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
                 while (it) {
                     const int s = __ffs(it) - 1 + 32 * r;
@@ -564,7 +565,11 @@ __global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
     }
     __syncthreads();
     const PCtx &C = S.ctx;
-    for (int wt = w; 64 * wt < C.len; wt += NW) point_warp<USEVAL>(a, S, C, wt, ovf_local);
+    if (C.nrounds <= 3) {
+        for (int wt = w; 64 * wt < C.len; wt += NW) point_warp<USEVAL, 3>(a, S, C, wt, ovf_local);
+    } else {
+        for (int wt = w; 64 * wt < C.len; wt += NW) point_warp<USEVAL, 4>(a, S, C, wt, ovf_local);
+    }
 
     // ---- once per CTA: exact per-slot totals -> global 128-bit sums
     if (a.accumulate && !deferred && cnt > 0) {
