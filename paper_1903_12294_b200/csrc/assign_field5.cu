@@ -75,7 +75,7 @@ struct __align__(16) Smem5 {
     float tab[CAP][TE];             // 16-byte aligned rows (52 floats)
     float2 qmm[CAP][NQ];            // (min, max) of each quad of table entries
     double c[CAP][5];               // cx, cy, cz, ct, cv (0 when absent)
-    double wsum[NW][CAP];           // per-warp fp64 value sums (fixed brick order)
+    unsigned vlimb[CAP][6];         // per slot value sum: 128-bit fixed point in 24-bit limbs
     unsigned hist[CAP][HW];         // 16-bit count marginals, two per word
     unsigned long long xf[BX][2], yf[BY][2], zf[BZ][2], tf[BT][2];
     double x[BX], y[BY], z[BZ], t[BT];
@@ -85,6 +85,8 @@ struct __align__(16) Smem5 {
     unsigned char has[CAP];
     int wc[NW];
     float red[NW];
+    int lst[NW][32];                // per region: candidate slots that survive its cull
+    int nlist[NW];                  // list lengths (-1: more than 32 survivors)
     Ctx ctx;
 };
 
@@ -159,13 +161,106 @@ __device__ __forceinline__ void table_row(float *e, float2 *mm, const double *co
     }
 }
 
+
+// Add one fp64 value sum to a slot's exact 128-bit fixed-point total kept as
+// six 24-bit limbs in 32-bit shared counters (the top one signed): integer,
+// order-free, and at most 64 records per slot and block, so no counter overflows.
+__device__ __forceinline__ void add_value_limbs(unsigned *lim, double v, int &ovf) {
+    unsigned long long lo;
+    long long hi;
+    d2fix(v, lo, hi, &ovf);
+    const unsigned M = 0xFFFFFFu;
+    atomicAdd(&lim[0], (unsigned)(lo & M));
+    atomicAdd(&lim[1], (unsigned)((lo >> 24) & M));
+    atomicAdd(&lim[2], (unsigned)(((lo >> 48) | ((unsigned long long)hi << 16)) & M));
+    atomicAdd(&lim[3], (unsigned)(((unsigned long long)hi >> 8) & M));
+    atomicAdd(&lim[4], (unsigned)(((unsigned long long)hi >> 32) & M));
+    atomicAdd((int *)&lim[5], (int)(hi >> 56));
+}
+
+__device__ __forceinline__ __int128 value_limbs_total(const unsigned *lim) {
+    __int128 acc = (__int128)((int)lim[5]) << 120;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) acc += (__int128)((unsigned __int128)lim[k] << (24 * k));
+    return acc;
+}
+
 // One warp brick: lane (lx, ly) = (8 bx + lane % 8, 4 by + lane / 8), samples
 // k = 4 r + q at z = 4 bz + q, timestep 2 bt + r.  FULL: all 256 samples exist.
+
+// (min, max) over table groups [g0, g1]
+__device__ __forceinline__ float2 gmm(const float2 *m, int g0, int g1) {
+    float2 r = m[g0];
+    for (int g = g0 + 1; g <= g1; ++g) {
+        r.x = fminf(r.x, m[g].x);
+        r.y = fmaxf(r.y, m[g].y);
+    }
+    return r;
+}
+
+// Warp region = the 8 bricks of warp w: x half rbx, y quarter rby, every z and
+// timestep of the block.  Cull the block's candidates over the whole region
+// (bounds from the group tables, value range of the block) and compact the
+// survivors into S.lst[w]: a candidate culled here is beaten by the region's
+// best fully valid candidate on every sample of every brick of the region.
+// Returns the list length, or -1 when more than 32 survive.
+template <bool USEVAL, int NR>
+__device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int rby, float vl, float vh,
+                                           int debug) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int zg1 = (C.Z.len - 1) / GZ, tg1 = (C.T.len - 1) / GT;
+    const float fwd = C.fwd, wvf = C.wvf;
+    float dl[4];
+    float ubw = INF_F;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        dl[r] = INF_F;
+        const int s = lane + 32 * r;
+        if (r < C.nrounds && s < C.cnt) {
+            const float2 qx = S.qmm[s][rbx], qy = S.qmm[s][QY + rby];
+            const float2 qz = gmm(S.qmm[s] + QZ, 0, zg1), qt = gmm(S.qmm[s] + QT, 0, tg1);
+            float vtl = 0.0f, vth = 0.0f;
+            if (USEVAL) {
+                const float wvs = S.wvf[s];
+                if (wvs > 0.0f) {
+                    const float cvs = S.cvf[s];
+                    const float pl = vl - cvs, ph = vh - cvs;
+                    vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
+                    vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
+                }
+            }
+            dl[r] = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
+            ubw = fminf(ubw, fmaf(fwd, sqrt_approx((qx.y + qy.y) + (qz.y + qt.y)), vth));
+        }
+    }
+    ubw = warp_min_f(ubw);
+    const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f) + C.slack;
+    const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
+    unsigned keep[4] = {0u, 0u, 0u, 0u};
+    int total = 0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (debug & 1)));
+        total += __popc(keep[r]);
+    }
+    if (total > 32) return -1;
+    int base = 0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        if (keep[r] >> lane & 1u) S.lst[w][base + __popc(keep[r] & ((1u << lane) - 1u))] = lane + 32 * r;
+        base += __popc(keep[r]);
+    }
+    __syncwarp();
+    return total;
+}
+
 // NR: rounds of 32 candidate slots (3 when the block has <= 96 candidates: the
 // common case gets a smaller instruction footprint)
-template <bool USEVAL, bool FULL, int NR>
+// LIST: the candidates are the warp region's list S.lst[w][0..nlist) (one round,
+// bit b of a keep mask = list position b); otherwise slot = bit + 32 * round.
+template <bool USEVAL, bool FULL, int NR, bool LIST>
 __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bx, int by,
-                                      int bz, int bt, int &ovf_local) {
+                                      int bz, int bt, int region, int nlist, int &ovf_local) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
     const int z0 = GZ * bz, t0 = GT * bt;
@@ -215,8 +310,8 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         for (int r = 0; r < NR; ++r) {
             dl[r] = INF_F;
             shi[r] = INF_F;
-            const int s = lane + 32 * r;
-            if (r < C.nrounds && s < C.cnt) {
+            const int s = LIST ? (lane < nlist ? S.lst[region][lane] : -1) : lane + 32 * r;
+            if (LIST ? s >= 0 : (r < C.nrounds && s < C.cnt)) {
                 const float2 qx = S.qmm[s][bx], qy = S.qmm[s][QY + by], qz = S.qmm[s][QZ + bz],
                              qt = S.qmm[s][QT + bt];
                 float vtl = 0.0f, vth = 0.0f;
@@ -276,7 +371,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             const float vq = fmaxf(fabsf(vwl - cvq), fabsf(vwh - cvq));
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
-                const int s = lane + 32 * r;
+                const int s = LIST ? (lane < nlist ? S.lst[region][lane] : -1) : lane + 32 * r;
                 bool dom = false;
                 if ((keep[r] >> lane & 1u) && s != sstar) {
                     const float *T = S.tab[s];
@@ -331,7 +426,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         for (int r = 0; r < NR; ++r) {
             unsigned it = keep[r];
             while (it) {
-                const int s = __ffs(it) - 1 + 32 * r;
+                const int s = LIST ? S.lst[region][__ffs(it) - 1] : __ffs(it) - 1 + 32 * r;
                 it &= it - 1;
                 const float *T = S.tab[s];
                 const float axy = T[lx] + T[BX + ly];
@@ -385,7 +480,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 for (int r = 0; r < NR; ++r) {
                     unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
                     while (it) {
-                        const int s = __ffs(it) - 1 + 32 * r;
+                        const int s = LIST ? S.lst[region][__ffs(it) - 1] : __ffs(it) - 1 + 32 * r;
                         it &= it - 1;
                         const float *T = S.tab[s];
                         const float ex = T[lx], ey = T[BX + ly], ez = T[OZ + zi], et = T[OT + ti];
@@ -432,26 +527,26 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             else if (lane < 8) atomicAdd(&h[16 + 2 * bz + (lane - 6)], 64u | (64u << 16));  // 4 z
             else if (lane == 8) atomicAdd(&h[24 + bt], 128u | (128u << 16));      // 2 timesteps
             else if (lane == 9) atomicAdd(&h[26], 256u);
-            if (lane == 0) S.wsum[w][one] = DADD(S.wsum[w][one], vs);
+            if (lane == 0) add_value_limbs(S.vlimb[one], vs, ovf_local);
             return;
         }
         if (!a.accumulate) return;
     }
-    int nlist = 0;
+    int nout = 0;
     if (one < 0) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (!FULL && !(livem >> k & 1)) continue;
             const int lab = C.deferred ? -2 : (sl[k] >= 0 ? S.id[sl[k]] : -1);
             lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
-            if (lab < 0) ++nlist;
+            if (lab < 0) ++nout;
         }
     }
-    if (__any_sync(0xffffffffu, nlist > 0)) {
+    if (__any_sync(0xffffffffu, nout > 0)) {
         unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
         long long *lst = C.deferred ? a.deferred : a.stranded;
         const long long cap = C.deferred ? a.deferred_cap : a.stranded_cap;
-        long long p = warp_reserve(ctr, nlist);
+        long long p = warp_reserve(ctr, nout);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (!(livem >> k & 1)) continue;
@@ -512,7 +607,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 if (c2 | c3) atomicAdd(&h[17 + (z0 >> 1)], c2 | (c3 << 16));
                 atomicAdd(&h[24 + (t0 >> 1)], st);
                 atomicAdd(&h[26], (st & 0xFFFFu) + (st >> 16));
-                S.wsum[w][L] = DADD(S.wsum[w][L], vs);
+                add_value_limbs(S.vlimb[L], vs, ovf_local);
             }
         }
     }
@@ -642,7 +737,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         }
         if (a.accumulate) {
             for (int e = tid; e < cnt * HW; e += NT) (&S.hist[0][0])[e] = 0u;
-            for (int e = tid; e < NW * CAP; e += NT) (&S.wsum[0][0])[e] = 0.0;
+            for (int e = tid; e < cnt * 6; e += NT) (&S.vlimb[0][0])[e] = 0u;
         }
         __syncthreads();
     }
@@ -666,23 +761,51 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     }
     __syncthreads();
     const Ctx &C = S.ctx;
-    for (int bi = w; bi < 64; bi += NW) {
-        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
-        if (GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= Tm.len)
-            continue;   // warp-uniform
-        const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len && GZ * bz + GZ <= Z.len &&
-                          GT * bt + GT <= Tm.len;
-        if (C.nrounds <= 3) {
-            if (full)
-                brick<USEVAL, true, 3>(a, S, C, bx, by, bz, bt, ovf_local);
-            else
-                brick<USEVAL, false, 3>(a, S, C, bx, by, bz, bt, ovf_local);
-        } else {
-            if (full)
-                brick<USEVAL, true, 4>(a, S, C, bx, by, bz, bt, ovf_local);
-            else
-                brick<USEVAL, false, 4>(a, S, C, bx, by, bz, bt, ovf_local);
+    // warp region candidate list (see region_list)
+    {
+        int nl = -1;
+        const int rbx = w & 1, rby = (w >> 1) & 3;
+        if (!deferred && cnt > 0 && GX * rbx < X.len && GY * rby < Y.len) {
+            float vl = 0.f, vh = 0.f;
+            if (USEVAL) {
+                const float2 vr = a.vrange[blockIdx.x];
+                vl = vr.x;
+                vh = vr.y;
+            }
+            nl = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, rbx, rby, vl, vh, a.debug)
+                                : region_list<USEVAL, 4>(S, C, rbx, rby, vl, vh, a.debug);
+            if ((a.debug & 8) && lane == 0) {
+                atomicAdd(a.stats + 4, 1ull);
+                if (nl >= 0) {
+                    atomicAdd(a.stats + 5, 1ull);
+                    atomicAdd(a.stats + 6, (unsigned long long)nl);
+                }
+            }
         }
+        if (lane == 0) S.nlist[w] = nl;
+    }
+    __syncthreads();
+    // bricks: warp w takes w, w + 8, ... (the partial sums are order-free integers,
+    // so which warp takes which brick does not affect the result)
+    for (int bi = w; bi < 64;) {
+        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+        if (!(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= Tm.len)) {
+            const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len &&
+                              GZ * bz + GZ <= Z.len && GT * bt + GT <= Tm.len;
+            const int region = bi & 7, nl = S.nlist[region];
+            if (nl >= 0) {
+                if (full)
+                    brick<USEVAL, true, 1, true>(a, S, C, bx, by, bz, bt, region, nl, ovf_local);
+                else
+                    brick<USEVAL, false, 1, true>(a, S, C, bx, by, bz, bt, region, nl, ovf_local);
+            } else {
+                if (full)
+                    brick<USEVAL, true, 4, false>(a, S, C, bx, by, bz, bt, region, 0, ovf_local);
+                else
+                    brick<USEVAL, false, 4, false>(a, S, C, bx, by, bz, bt, region, 0, ovf_local);
+            }
+        }
+        bi += NW;
     }
 
     // ---- once per block: marginals x fixed-point coordinates -> global 128-bit sums
@@ -708,13 +831,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
 #pragma unroll
                 for (int i = 0; i < BT; ++i) acc += get128(S.tf[i]) * (__int128)hget(h + 24, i);
             } else if (wd == 4) {
-#pragma unroll
-                for (int q = 0; q < NW; ++q) {
-                    unsigned long long lo;
-                    long long hi;
-                    d2fix(S.wsum[q][s], lo, hi, &ovf_local);
-                    acc += (__int128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
-                }
+                acc = value_limbs_total(S.vlimb[s]);
             } else {
                 atomicAdd(dst + 13, (unsigned long long)n);
                 continue;
@@ -723,6 +840,62 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         }
     }
     if (ovf_local) *a.overflow = 1;
+}
+
+// Range of fl32(value) over every field block (once per run: values do not change
+// between passes); rounding is monotone, so these are min/max of fl32(v).
+__global__ void k_block_vrange(FieldArgs a) {
+    unsigned tile = blockIdx.x;
+    const int txi = (int)(tile % (unsigned)a.ntx);
+    tile /= (unsigned)a.ntx;
+    const int tyi = (int)(tile % (unsigned)a.nty);
+    tile /= (unsigned)a.nty;
+    const int tzi = (int)(tile % (unsigned)a.ntz);
+    const int tti = (int)(tile / (unsigned)a.ntz);
+    const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
+    const int n = X.len * Y.len * Z.len * T.len;
+    double lo = INF_D, hi = -INF_D;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        int q = e;
+        const int i = q % X.len;
+        q /= X.len;
+        const int j = q % Y.len;
+        q /= Y.len;
+        const int k = q % Z.len;
+        const int m = q / Z.len;
+        const double v = a.values[(((long long)(T.start + m) * a.nz + Z.start + k) * a.ny + Y.start + j) *
+                                      (long long)a.nx + X.start + i];
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+    }
+    __shared__ double r[2][32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        r[0][w] = lo;
+        r[1][w] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < nw; ++q) {
+            lo = fmin(lo, r[0][q]);
+            hi = fmax(hi, r[1][q]);
+        }
+        a.vrange_out[blockIdx.x] = make_float2((float)lo, (float)hi);
+    }
+}
+
+int launch_block_vrange(const FieldArgs &a, cudaStream_t st) {
+    const long long n = (long long)a.ntx * a.nty * a.ntz * a.ntt;
+    if (n <= 0 || field_version() != 5) return 0;
+    ::mfseg::count_launch();
+    k_block_vrange<<<(unsigned)n, 256, 0, st>>>(a);
+    MFSEG_LAUNCH("k_block_vrange");
+    return 0;
 }
 
 int launch_field_assign_v5(const FieldArgs &a, cudaStream_t st) {

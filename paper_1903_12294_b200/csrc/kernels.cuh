@@ -34,6 +34,8 @@ struct FieldArgs {
     int accumulate;
     int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor, bit3: stats
     unsigned long long *stats;   // debug bit3: [0] bricks, [1] kept candidates, [2] exact samples
+    const float2 *vrange;        // per field block: range of fl32(value) (k_block_vrange)
+    float2 *vrange_out;
 };
 
 struct WBox {                 // one 64-point warp tile of a point chunk (k_point_assign4)
@@ -108,6 +110,8 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
                cudaStream_t st);
 // assign.cu
 int field_tile_dims(int *tx, int *ty, int *tz);
+int field_version();
+int launch_block_vrange(const FieldArgs &a, cudaStream_t st);
 int point_tile_size();
 int point_version();
 int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,

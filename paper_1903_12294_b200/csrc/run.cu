@@ -248,6 +248,7 @@ struct Plan {
     int ntx, nty, ntz, ntt;
     int *tbin;
     AxisTile *tt;
+    float2 *vrange;                 // per field block value range (field v5)
     long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
@@ -332,7 +333,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.flags = cv.take<char>(update_flags_bytes());
     int NB = P.NB;
     P.g = grid_carve(cv, K, NB, &P.count_tmp, &P.grid_scan_tmp);
-    P.counters = cv.take<unsigned long long>(16);   // [8..16): debug stats
+    P.counters = cv.take<unsigned long long>(24);   // [8..24): debug stats
     P.overflow = cv.take<int>(4);
     // field
     P.nf = (P.f.nt > 0) ? (long long)P.f.nx * P.f.ny * P.f.nz * P.f.nt : 0;
@@ -352,6 +353,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.zt = cv.take<AxisTile>(P.ntz);
     P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
+    P.vrange = cv.take<float2>((long long)P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     P.deferred_f = cv.take<long long>(P.cap_f);
@@ -455,6 +457,25 @@ int plan_prepare(Plan &P) {
         k_tbins<<<(P.f.nt + 255) / 256, 256, 0, st>>>(P.f.nt, P.f.times, p.mins[3], p.C[3],
                                                         p.k[3], P.tbin);
         MFSEG_LAUNCH("k_tbins");
+        {   // per-block value ranges (the values are fixed for the whole run)
+            FieldArgs va;
+            memset(&va, 0, sizeof va);
+            va.nx = P.f.nx;
+            va.ny = P.f.ny;
+            va.nz = P.f.nz;
+            va.nt = P.f.nt;
+            va.values = P.f.values;
+            va.xt = P.xt;
+            va.yt = P.yt;
+            va.zt = P.zt;
+            va.tt = P.tt;
+            va.ntx = P.ntx;
+            va.nty = P.nty;
+            va.ntz = P.ntz;
+            va.ntt = P.ntt;
+            va.vrange_out = P.vrange;
+            MFSEG_TRY(launch_block_vrange(va, st));
+        }
     }
     long long n = P.np;
     if (n > 0) {
@@ -519,7 +540,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
                          P.count_tmp, P.grid_scan_tmp, st));
     mark(1, st);
-    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 16, st));
+    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 24, st));
     if (accumulate)
         MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
     if (P.nf > 0) {
@@ -545,6 +566,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.ntz = P.ntz;
         a.tbin = P.tbin;
         a.tt = P.tt;
+        a.vrange = P.vrange;
         a.ntt = P.ntt;
         a.kx = p.k[0];
         a.ky = p.k[1];
@@ -607,7 +629,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stranded_cap = P.cap_p;
         a.deferred = P.deferred_p;
         a.n_deferred = P.counters + 3;
-        a.stats = P.counters + 12;
+        a.stats = P.counters + 16;
         a.deferred_cap = P.cap_p;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
@@ -667,14 +689,17 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     mark(4, st);
     if (const char *dbg = getenv("MFSEG_DEBUG")) {
         if (atoi(dbg) & 8) {
-            unsigned long long h[16];
+            unsigned long long h[24];
             MFSEG_CUDA(cudaMemcpyAsync(h, P.counters, sizeof h, cudaMemcpyDeviceToHost, st));
             MFSEG_CUDA(cudaStreamSynchronize(st));
+            const unsigned long long *F = h + 8, *Q = h + 16;
+            auto rat = [](unsigned long long a, unsigned long long b) { return b ? (double)a / b : 0.0; };
             fprintf(stderr,
-                    "[mfseg stats] field: bricks %llu kept/brick %.2f exact %llu | points: warp tiles %llu "
-                    "kept/tile %.2f exact %llu | stranded f %llu p %llu deferred f %llu p %llu | records/brick %.2f\n",
-                    h[8], h[8] ? (double)h[9] / h[8] : 0.0, h[10], h[12], h[12] ? (double)h[13] / h[12] : 0.0,
-                    h[14], h[0], h[1], h[2], h[3], h[8] ? (double)h[11] / h[8] : 0.0);
+                    "[mfseg stats] field: bricks %llu kept/brick %.2f exact %llu records/brick %.2f "
+                    "regions %llu listed %.3f list/region %.2f | points: warp tiles %llu kept/tile %.2f "
+                    "exact %llu | stranded f %llu p %llu deferred f %llu p %llu\n",
+                    F[0], rat(F[1], F[0]), F[2], rat(F[3], F[0]), F[4], rat(F[5], F[4]), rat(F[6], F[5]),
+                    Q[0], rat(Q[1], Q[0]), Q[2], h[0], h[1], h[2], h[3]);
         }
     }
     return 0;
