@@ -334,6 +334,8 @@ def run_ours(args):
             passes.append(1 + r.iterations_used)
         e1.record(st)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     launches = lib.mfseg_launch_count() - launches0
     ms = (ctypes.c_double * 8)()
     n_timed_passes = lib.mfseg_timing_read(ms, 8)
@@ -427,7 +429,30 @@ def e2e_measure(args, fld_raw, pts_raw, params, world, rank, n_field):
     points = P.PointSet(np.zeros(pts_raw.n, np.int64), pt.numpy(), xyz.numpy(), pv.numpy())
     h2d = fv.numel() * 8 + ft.size * 8 + xyz.numel() * 8 + pt.numel() * 8 + pv.numel() * 8
     if world > 1:
-        return None    # e2e is measured on a single GPU (the public API is single-device)
+        # every rank: its slab through parallel.segment_sharded, max over ranks
+        import torch.distributed as dist
+        from paper_1903_12294_b200.parallel import segment_sharded
+        for _ in range(2):
+            seg, _ = segment_sharded(points, fields, params)
+        steps = max(3, min(args.steps, 5))
+        per = []
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            ts = time.perf_counter()
+            seg, _ = segment_sharded(points, fields, params)
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - ts], dtype=torch.float64, device="cuda")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            per.append(float(dt.item()))
+        t = sum(per) / steps
+        K = int(np.prod(params.k))
+        d2h = seg.point_labels.nbytes + seg.field_labels.nbytes + K * (6 * 8 + 3 + 2 * 8)
+        return {"value": n_field * world / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
+                "d2h_bytes_per_step": int(d2h) * world, "seconds_per_step": t,
+                "step_seconds": [round(x, 4) for x in per],
+                "api": "paper_1903_12294_b200.parallel.segment_sharded per rank (pinned host slab -> "
+                       "labels + centre table), max over ranks of the host wall clock"}
     for _ in range(2):    # warm-up: the caching allocators need two generations of outputs
         seg, _, _ = P.segment(points, fields, params)
     steps = max(3, min(args.steps, 5))

@@ -132,3 +132,18 @@ def shard_run_device(pts: DevicePoints, fld: DeviceField, extent: DomainExtent, 
 
     return run_device(pts, fld, extent, params, progress=progress, reduce=reduce_cb,
                       workspace=workspace, out=out)
+
+
+def segment_sharded(points, fields, params, group=None):
+    """pipeline.segment across ranks: this rank's host slab (whole t-bins of the
+    field timesteps and the points in them, see tbin_slabs) -> upload ->
+    global normalisation and extent -> sharded run -> this rank's labels and the
+    (replicated) centre table.  Returns (Segmentation, extent)."""
+    from .engine import device, field_to_device, points_to_device
+    from .pipeline import to_segmentation
+    dev = device()
+    pts = points_to_device(points, dev)
+    fld = field_to_device(fields, dev)
+    extent = normalize_and_extent_sharded(pts, fld, group=group)
+    r = shard_run_device(pts, fld, extent, params, group=group)
+    return to_segmentation(r, params, extent), extent

@@ -507,3 +507,33 @@ def test_traj_split_matches_numpy(seed, n, n_traj, single_time):
     assert stride == ref_stride
     np.testing.assert_array_equal(order.cpu().numpy(), ref_order)
     np.testing.assert_array_equal(starts.cpu().numpy(), ref_starts)
+
+
+def test_segment_sharded_single_rank_matches_segment():
+    """parallel.segment_sharded (NCCL process group of one rank) reproduces
+    pipeline.segment: same labels, same centre table."""
+    import socket
+    import torch.distributed as dist
+    P = pkg()
+    from paper_1903_12294_b200.parallel import segment_sharded
+    fld, pts, tid = _synthetic((40, 32, 20), 8, 1500, 9, False)
+    nt = 8
+    fs = P.FieldSet((40, 32, 20), np.zeros(3), np.ones(3), np.arange(nt, dtype=float),
+                    fld.values.cpu().numpy().reshape(nt, -1))
+    ps = P.PointSet(tid.cpu().numpy(), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(), pts.value.cpu().numpy())
+    params = P.ClusterParams(k=(5, 4, 3, 2), eps_c=1e-12, max_iterations=5)
+    ref, _, _ = P.segment(ps, fs, params)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        seg, ext = segment_sharded(ps, fs, params)
+    finally:
+        dist.destroy_process_group()
+    np.testing.assert_array_equal(seg.field_labels, ref.field_labels)
+    np.testing.assert_array_equal(seg.point_labels, ref.point_labels)
+    assert [c.id for c in seg.centers] == [c.id for c in ref.centers]
+    np.testing.assert_array_equal([c.x_c for c in seg.centers], [c.x_c for c in ref.centers])
