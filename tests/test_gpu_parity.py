@@ -537,3 +537,36 @@ def test_segment_sharded_single_rank_matches_segment():
     np.testing.assert_array_equal(seg.point_labels, ref.point_labels)
     assert [c.id for c in seg.centers] == [c.id for c in ref.centers]
     np.testing.assert_array_equal([c.x_c for c in seg.centers], [c.x_c for c in ref.centers])
+
+
+def test_kernel_generations_agree_crowded(monkeypatch):
+    """~1.4 centres per bin: candidate lists of ~100-130 exercise the 4-round
+    variants of both assignment kernels and the deferral of lists > 128."""
+    P = pkg()
+    from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
+    dims, nt, ntraj = (64, 48, 32), 12, 6000
+    fld, pts, _ = _synthetic(dims, nt, ntraj, 31, False)
+    normalize_device(pts, fld, True)
+    ext = domain_extent_device(pts, fld)
+    params = P.ClusterParams(k=(5, 4, 3, 3), w_d=0.6)
+    rng = np.random.default_rng(31)
+    C = P.interval_distances(ext, params.k)
+    seeds = P.seed_centers(ext, params.k)
+    extra = seeds[rng.integers(0, len(seeds), int(0.45 * len(seeds)))]
+    loc = np.vstack([seeds, extra]) + rng.uniform(-0.4, 0.4, (len(seeds) + len(extra), 4)) * C
+    K = len(loc)
+    cs = P.CenterState.from_seeds(loc)
+    cs.pval = np.where(rng.random(K) < 0.8, rng.random(K), np.nan)
+    cs.fval = np.where(rng.random(K) < 0.8, rng.random(K), np.nan)
+    cs.has_p, cs.has_f = ~np.isnan(cs.pval), ~np.isnan(cs.fval)
+    grid = P.CenterGrid(cs.loc, ext, C, params.k)
+    fs = P.FieldSet(dims, np.zeros(3), np.ones(3), fld.times.cpu().numpy(),
+                    fld.values.cpu().numpy().reshape(nt, -1))
+    ps = P.PointSet(np.zeros(pts.n, np.int64), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(),
+                    pts.value.cpu().numpy())
+    pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
+    monkeypatch.setenv("MFSEG_FIELD_V1", "1")
+    monkeypatch.setenv("MFSEG_POINT_V1", "1")
+    pl1, fl1 = P.assign_iteration(ps, fs, None, cs, grid, params, C)
+    np.testing.assert_array_equal(fl, fl1)
+    np.testing.assert_array_equal(pl, pl1)
