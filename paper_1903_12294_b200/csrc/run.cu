@@ -120,17 +120,37 @@ __global__ void k_point_keys(long long n, const double *xyz, const double *t, do
     vals[i] = (unsigned)i;
 }
 
+// random gather of the points into bin-sorted SoA; 4 points per thread with
+// every load issued before the stores (memory-level parallelism)
+constexpr int GATHER_PER_THREAD = 8;
 __global__ void k_point_gather(long long n, const unsigned *perm, const double *xyz,
                                const double *t, const double *value, double *px, double *py,
                                double *pz, double *pt, double *pv) {
-    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    long long j = perm[i];
-    px[i] = xyz[3 * j];
-    py[i] = xyz[3 * j + 1];
-    pz[i] = xyz[3 * j + 2];
-    pt[i] = t[j];
-    pv[i] = value[j];
+    const long long base = (blockIdx.x * (long long)blockDim.x) * GATHER_PER_THREAD + threadIdx.x;
+    double r[GATHER_PER_THREAD][5];
+#pragma unroll
+    for (int q = 0; q < GATHER_PER_THREAD; ++q) {
+        const long long i = base + (long long)q * blockDim.x;
+        if (i < n) {
+            const long long j = perm[i];
+            r[q][0] = __ldg(xyz + 3 * j);
+            r[q][1] = __ldg(xyz + 3 * j + 1);
+            r[q][2] = __ldg(xyz + 3 * j + 2);
+            r[q][3] = __ldg(t + j);
+            r[q][4] = __ldg(value + j);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < GATHER_PER_THREAD; ++q) {
+        const long long i = base + (long long)q * blockDim.x;
+        if (i < n) {
+            px[i] = r[q][0];
+            py[i] = r[q][1];
+            pz[i] = r[q][2];
+            pt[i] = r[q][3];
+            pv[i] = r[q][4];
+        }
+    }
 }
 
 // Group starts of the sorted keys by boundary detection (no atomics: sorted keys
@@ -494,8 +514,8 @@ int plan_prepare(Plan &P) {
         MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, P.key_bits, P.radix_tmp,
                                    P.radix_bytes, st));
         ::mfseg::count_launch();
-        k_point_gather<<<gb, 256, 0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px,
-                                           P.py, P.pz, P.pt, P.pv);
+        k_point_gather<<<(unsigned)((n + 256 * GATHER_PER_THREAD - 1) / (256 * GATHER_PER_THREAD)), 256, 0,
+                         st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px, P.py, P.pz, P.pt, P.pv);
         const int NG = P.ngroups;
         ::mfseg::count_launch();
         k_bin_first<<<(unsigned)((n + 256) / 256), 256, 0, st>>>(n, P.skeys, P.sub_bits, NG,
