@@ -396,6 +396,12 @@ def run_ours(args):
                    "phase_ms_per_pass": {"grid": phase_ms[0], "field_assign": phase_ms[1],
                                          "point_assign": phase_ms[2], "fallback": phase_ms[3],
                                          "update+exchange": phase_ms[4]}},
+        "stage_rooflines": {   # per pass, algorithmic bytes / CUDA-event kernel time vs measured HBM peak
+            "field_assign": {"ms": field_ms, "GB_s": achieved,
+                             "frac": (achieved / hbm) if achieved else None},
+            "point_assign": {"ms": phase_ms[2],
+                             "GB_s": (ALG_BYTES_POINT * n_point / (phase_ms[2] / 1e3) / 1e9) if phase_ms[2] > 0 else None,
+                             "frac": (ALG_BYTES_POINT * n_point / (phase_ms[2] / 1e3) / 1e9 / hbm) if phase_ms[2] > 0 else None}},
         "roofline": {"bound": "hbm", "kernel": "k_field_assign", "achieved": achieved,
                      "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
