@@ -912,21 +912,13 @@ int launch_field_assign_v5(const FieldArgs &a, cudaStream_t st) {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<false, 3>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<true, 2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MFSEG_CUDA(cudaFuncSetAttribute(k_field_assign5<false, 2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    const bool two = getenv("MFSEG_F5_MINB2") != nullptr;
     ::mfseg::count_launch();
-    if (a.wv > 0.0) {
-        if (two) k_field_assign5<true, 2><<<(unsigned)n, NT, smem, st>>>(a);
-        else k_field_assign5<true, 3><<<(unsigned)n, NT, smem, st>>>(a);
-    } else {
-        if (two) k_field_assign5<false, 2><<<(unsigned)n, NT, smem, st>>>(a);
-        else k_field_assign5<false, 3><<<(unsigned)n, NT, smem, st>>>(a);
-    }
+    if (a.wv > 0.0)
+        k_field_assign5<true, 3><<<(unsigned)n, NT, smem, st>>>(a);
+    else
+        k_field_assign5<false, 3><<<(unsigned)n, NT, smem, st>>>(a);
     MFSEG_LAUNCH("k_field_assign5");
     return 0;
 }
