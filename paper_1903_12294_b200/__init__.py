@@ -18,6 +18,7 @@ from .ingest import (IngestError, LinkIndex, NormalizationRecord, build_link_ind
 from .postproc import (Feature, FeatureStats, build_features, feature_stats, merge_clusters,
                        merge_eligible)
 from .pipeline import segment
+from . import artifacts
 
 __all__ = [
     "CenterGrid", "CenterState", "ClusterCenter", "ClusterParams", "DomainExtent", "Feature",
@@ -26,7 +27,7 @@ __all__ = [
     "build_features", "build_link_index", "domain_extent", "feature_stats", "field_distance",
     "has_converged", "initial_assignment", "interval_distances", "max_center_delta",
     "merge_clusters", "merge_eligible", "normalize_variables", "point_distance", "run",
-    "seed_centers", "segment", "space_time_distance", "update_centers",
+    "seed_centers", "segment", "space_time_distance", "update_centers", "artifacts",
 ]
 
 __version__ = "0.1.0"

@@ -250,7 +250,28 @@ def frontend_subset():
     }
 
 
+def artifacts_case():
+    """The reference's own artifact writer (artifacts.py) on the frontend
+    configuration: segmentation.json + label files, merge.json, features.json
+    -> tests/golden/artifacts_slab2/ (byte-level goldens for our writer)."""
+    from mfseg import artifacts
+    out = os.path.join(HERE, "artifacts_slab2")
+    os.makedirs(out, exist_ok=True)
+    pts, fld = load_via_files(spec_slabs(2))
+    params = ClusterParams(k=(3, 1, 1, 1), w_d=0.05, eps_m=0.01, normalize=True)
+    seg, norm, _ = pipeline.segment(pts, fld, params)
+    artifacts.save_segmentation(out, seg, norm)
+    mm, merged = postproc.merge_clusters(seg.centers, 0.01)
+    artifacts.save_merge(out, 0.01, mm, merged)
+    p_n, f_n, _ = ingest.normalize_variables(pts, fld, True)
+    feats = postproc.build_features(seg, mm, p_n, f_n)
+    artifacts.save_features(out, feats, merged, mm)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "artifacts":
+        artifacts_case()
+        return
     # 1. the frontend golden configuration (pkg/frontend/test/fixtures/*):
     #    slab_spec(2), k=(3,1,1,1), w_d=0.05, eps_m=0.01, normalize on
     pts, fld = load_via_files(spec_slabs(2))
