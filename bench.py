@@ -47,6 +47,10 @@ CONFIGS = {
     "c1": dict(dims=(64, 64, 64), nt=8, n_traj=100_000, k=(8, 8, 8, 4),
                label="configs[0]: synthetic 64^3 x 8 timesteps, 100k particles"),
     "small": dict(dims=(64, 64, 32), nt=8, n_traj=20_000, k=(8, 8, 4, 4), label="smoke size"),
+    # configs[2] per GPU: one 8-timestep slab of the 512^3 x 64 field and its 16M
+    # trajectories (k_t = 16 over 64 steps -> 2 t-bins per GPU); --gpus 8 = the full box
+    "c3": dict(dims=(512, 512, 512), nt=8, n_traj=16_000_000, k=(16, 16, 16, 2),
+               label="configs[2]: 512^3 x 64 timesteps, 16M particles, time slabs of 8 steps per B200"),
 }
 METRIC = "voxel-timesteps segmented/sec"
 UNIT = "voxel-timesteps/s"
