@@ -259,8 +259,8 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
 // LIST: the candidates are the warp region's list S.lst[w][0..nlist) (one round,
 // bit b of a keep mask = list position b); otherwise slot = bit + 32 * round.
 template <bool USEVAL, bool FULL, int NR, bool LIST>
-__device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bx, int by,
-                                      int bz, int bt, int region, int nlist, int &ovf_local) {
+__device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bi, int bx,
+                                      int by, int bz, int bt, int region, int nlist, int &ovf_local) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
     const int z0 = GZ * bz, t0 = GT * bt;
@@ -275,10 +275,19 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 if (z0 + (k & 3) < C.Z.len && t0 + (k >> 2) < C.T.len) livem |= 1u << k;
         }
     }
+    // Values are loaded only where they are needed: bricks left with several
+    // candidates (per-sample screen) and bricks cut by the block edge.  Bricks
+    // labelled by one candidate use the per-run brick value range and value
+    // sum (k_brick_pre: the field values do not change between passes).
+    const size_t bidx = (size_t)blockIdx.x * 64 + bi;
     double v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * C.plane + (k >> 2) * C.vol) : 0.0;
+    for (int k = 0; k < 8; ++k) v[k] = 0.0;
+    if (!FULL) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * C.plane + (k >> 2) * C.vol) : 0.0;
+    }
 
     int sl[8];
 #pragma unroll
@@ -286,21 +295,12 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
     int one = -1;   // slot when a single candidate labels the whole brick (warp-uniform)
     const float fwd = C.fwd, wvf = C.wvf, slack = C.slack, cvmax = C.cvmax;
     if (!C.deferred && C.cnt > 0) {
-        float fv[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            fv[k] = (FULL || (livem >> k & 1)) ? (float)v[k] : __int_as_float(0x7fffffff);
         // brick value range: min/max of fl(v) = fl(min/max of v) (rounding is monotone)
         float vwl = 0.0f, vwh = 0.0f;
         if (USEVAL) {
-            float lo = INF_F, hi = -INF_F;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                lo = fminf(lo, fv[k]);   // NaN (missing sample) ignored
-                hi = fmaxf(hi, fv[k]);
-            }
-            vwl = warp_min_f(lo);
-            vwh = warp_max_f(hi);
+            const float2 r = a.brange[bidx];
+            vwl = r.x;
+            vwh = r.y;
         }
         // ---- warp culling from the group (min, max) tables
         float dl[4], shi[4];
@@ -415,6 +415,14 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             for (int k = 0; k < 8; ++k) sl[k] = (livem >> k & 1) ? sstar : -1;
             one = sstar;
         } else {
+        if (FULL) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(a.values + fbase + (k & 3) * C.plane + (k >> 2) * C.vol);
+        }
+        float fv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            fv[k] = (FULL || (livem >> k & 1)) ? (float)v[k] : __int_as_float(0x7fffffff);
         // ---- per-sample fp32 screen with packed (d, slot) keys
         unsigned b1[8], b2[8];
 #pragma unroll
@@ -516,11 +524,9 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         for (int k = 0; k < 8; ++k)
             if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
         if (a.accumulate && FULL) {
-            // whole brick -> one cluster: the count marginals are constants
-            double vs = 0.0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) vs = DADD(vs, v[k]);
-            vs = warp_sum_d(vs);
+            // whole brick -> one cluster: the count marginals are constants and the
+            // value sum is the brick's (fixed-order warp sum, computed once per run)
+            const double vs = a.bsum[bidx];
             unsigned *h = S.hist[one];
             if (lane < 4) atomicAdd(&h[4 * bx + lane], 32u | (32u << 16));         // 8 x, 32 each
             else if (lane < 6) atomicAdd(&h[8 + 2 * by + (lane - 4)], 64u | (64u << 16));   // 4 y
@@ -795,14 +801,14 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             const int region = bi & 7, nl = S.nlist[region];
             if (nl >= 0) {
                 if (full)
-                    brick<USEVAL, true, 1, true>(a, S, C, bx, by, bz, bt, region, nl, ovf_local);
+                    brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nl, ovf_local);
                 else
-                    brick<USEVAL, false, 1, true>(a, S, C, bx, by, bz, bt, region, nl, ovf_local);
+                    brick<USEVAL, false, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nl, ovf_local);
             } else {
                 if (full)
-                    brick<USEVAL, true, 4, false>(a, S, C, bx, by, bz, bt, region, 0, ovf_local);
+                    brick<USEVAL, true, 4, false>(a, S, C, bi, bx, by, bz, bt, region, 0, ovf_local);
                 else
-                    brick<USEVAL, false, 4, false>(a, S, C, bx, by, bz, bt, region, 0, ovf_local);
+                    brick<USEVAL, false, 4, false>(a, S, C, bi, bx, by, bz, bt, region, 0, ovf_local);
             }
         }
         bi += NW;
@@ -895,6 +901,58 @@ int launch_block_vrange(const FieldArgs &a, cudaStream_t st) {
     ::mfseg::count_launch();
     k_block_vrange<<<(unsigned)n, 256, 0, st>>>(a);
     MFSEG_LAUNCH("k_block_vrange");
+    return 0;
+}
+
+// Per brick, once per run: range of fl32(value) and the fixed-order value sum
+// (each lane sums its samples in k order, then the fp64 warp butterfly) --
+// exactly what k_field_assign5 would compute from the same samples.
+__global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
+    unsigned tile = blockIdx.x;
+    const int txi = (int)(tile % (unsigned)a.ntx);
+    tile /= (unsigned)a.ntx;
+    const int tyi = (int)(tile % (unsigned)a.nty);
+    tile /= (unsigned)a.nty;
+    const int tzi = (int)(tile % (unsigned)a.ntz);
+    const int tti = (int)(tile / (unsigned)a.ntz);
+    const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long plane = (long long)a.ny * a.nx, vol = plane * a.nz;
+    for (int bi = w; bi < 64; bi += NW) {
+        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+        if (GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= T.len) continue;
+        const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
+        const int z0 = GZ * bz, t0 = GT * bt;
+        const long long fbase = (((long long)(T.start + t0) * a.nz + Z.start + z0) * a.ny +
+                                 (Y.start + ly)) * (long long)a.nx + (X.start + lx);
+        float lo = INF_F, hi = -INF_F;
+        double vs = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const bool live = lx < X.len && ly < Y.len && z0 + (k & 3) < Z.len && t0 + (k >> 2) < T.len;
+            const double v = live ? a.values[fbase + (k & 3) * plane + (k >> 2) * vol] : 0.0;
+            vs = DADD(vs, v);
+            if (live) {
+                lo = fminf(lo, (float)v);
+                hi = fmaxf(hi, (float)v);
+            }
+        }
+        vs = warp_sum_d(vs);
+        lo = warp_min_f(lo);
+        hi = warp_max_f(hi);
+        if (lane == 0) {
+            a.brange_out[(size_t)blockIdx.x * 64 + bi] = make_float2(lo, hi);
+            a.bsum_out[(size_t)blockIdx.x * 64 + bi] = vs;
+        }
+    }
+}
+
+int launch_brick_pre(const FieldArgs &a, cudaStream_t st) {
+    const long long n = (long long)a.ntx * a.nty * a.ntz * a.ntt;
+    if (n <= 0 || field_version() != 5) return 0;
+    ::mfseg::count_launch();
+    k_brick_pre<<<(unsigned)n, NT, 0, st>>>(a);
+    MFSEG_LAUNCH("k_brick_pre");
     return 0;
 }
 

@@ -269,6 +269,8 @@ struct Plan {
     int *tbin;
     AxisTile *tt;
     float2 *vrange;                 // per field block value range (field v5)
+    float2 *brange;                 // per brick value range (field v5)
+    double *bsum;                   // per brick value sum (field v5)
     long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
@@ -374,6 +376,8 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
     P.vrange = cv.take<float2>((long long)P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
+    P.brange = cv.take<float2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
+    P.bsum = cv.take<double>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     P.deferred_f = cv.take<long long>(P.cap_f);
@@ -494,7 +498,10 @@ int plan_prepare(Plan &P) {
             va.ntz = P.ntz;
             va.ntt = P.ntt;
             va.vrange_out = P.vrange;
+            va.brange_out = P.brange;
+            va.bsum_out = P.bsum;
             MFSEG_TRY(launch_block_vrange(va, st));
+            MFSEG_TRY(launch_brick_pre(va, st));
         }
     }
     long long n = P.np;
@@ -587,6 +594,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.tbin = P.tbin;
         a.tt = P.tt;
         a.vrange = P.vrange;
+        a.brange = P.brange;
+        a.bsum = P.bsum;
         a.ntt = P.ntt;
         a.kx = p.k[0];
         a.ky = p.k[1];
