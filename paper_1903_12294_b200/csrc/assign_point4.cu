@@ -146,32 +146,24 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     const int off0 = 64 * wt + lane, off1 = off0 + 32;
     const bool live0 = off0 < C.len, live1 = off1 < C.len;
     const long long p0 = C.start + off0, p1 = C.start + off1;
+    // The point records are loaded only for tiles left with several candidates;
+    // a tile labelled by one candidate uses its per-run box and sums (k_wtile_box:
+    // the points do not change between passes).
     double P0[5] = {0, 0, 0, 0, 0}, P1[5] = {0, 0, 0, 0, 0};
-    if (live0) {
-        P0[0] = a.x[p0]; P0[1] = a.y[p0]; P0[2] = a.z[p0]; P0[3] = a.t[p0]; P0[4] = a.v[p0];
-    }
-    if (live1) {
-        P1[0] = a.x[p1]; P1[1] = a.y[p1]; P1[2] = a.z[p1]; P1[3] = a.t[p1]; P1[4] = a.v[p1];
-    }
+    const WBox *wbp = a.wbox + (size_t)blockIdx.x * (POINT_CHUNK / 64) + wt;
     int sl0 = -1, sl1 = -1;
+    int one = -1;   // slot labelling the whole tile (warp-uniform)
     if (!C.deferred && C.cnt > 0) {
-        float rp0[4], rp1[4];
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const double sc = d == 3 ? a.cf : 1.0;
-            rp0[d] = (float)DMUL(DSUB(P0[d], C.o[d]), sc);
-            rp1[d] = (float)DMUL(DSUB(P1[d], C.o[d]), sc);
-        }
         // warp-tile box (fp32, chunk-relative) and value range: precomputed once per
-        // run by k_wtile_box with exactly these formulas
-        const WBox wb = a.wbox[(size_t)blockIdx.x * (POINT_CHUNK / 64) + wt];
-        const float wl[4] = {wb.lo.x, wb.lo.y, wb.lo.z, wb.lo.w};
-        const float wh[4] = {wb.hi.x, wb.hi.y, wb.hi.z, wb.hi.w};
-        const float fv0 = (float)P0[4], fv1 = (float)P1[4];
+        // run by k_wtile_box with exactly the formulas used for rp / fv below
+        const float4 blo = wbp->lo, bhi = wbp->hi;
+        const float2 bv = wbp->v;
+        const float wl[4] = {blo.x, blo.y, blo.z, blo.w};
+        const float wh[4] = {bhi.x, bhi.y, bhi.z, bhi.w};
         float vl = 0.f, vh = 0.f;
         if (USEVAL) {
-            vl = wb.v.x;
-            vh = wb.v.y;
+            vl = bv.x;
+            vh = bv.y;
         }
         // ---- warp culling (fp32 bounds over the warp-tile box, guard bands widen the box test)
         float dl[4], qhu[4];
@@ -307,7 +299,22 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             // culled or dominated: it is the exact argmin of every point
             sl0 = live0 ? sdom : -1;
             sl1 = live1 ? sdom : -1;
+            one = sdom;
         } else {
+        if (live0) {
+            P0[0] = a.x[p0]; P0[1] = a.y[p0]; P0[2] = a.z[p0]; P0[3] = a.t[p0]; P0[4] = a.v[p0];
+        }
+        if (live1) {
+            P1[0] = a.x[p1]; P1[1] = a.y[p1]; P1[2] = a.z[p1]; P1[3] = a.t[p1]; P1[4] = a.v[p1];
+        }
+        float rp0[4], rp1[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const double sc = d == 3 ? a.cf : 1.0;
+            rp0[d] = (float)DMUL(DSUB(P0[d], C.o[d]), sc);
+            rp1[d] = (float)DMUL(DSUB(P1[d], C.o[d]), sc);
+        }
+        const float fv0 = (float)P0[4], fv1 = (float)P1[4];
         unsigned scan[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int r = 0; r < NR; ++r) scan[r] = keep[r];
@@ -424,6 +431,14 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     }
 
     // ---- partial sums: per-warp fp64 running sums + shared counts
+    if (a.accumulate && one >= 0) {   // the whole tile -> one cluster: per-run tile sums
+        if (lane == 0) {
+#pragma unroll
+            for (int d = 0; d < 5; ++d) S.wsum[w][d][one] = DADD(S.wsum[w][d][one], wbp->s[d]);
+            atomicAdd(&S.n[one], (unsigned)min(64, C.len - 64 * wt));
+        }
+        return;
+    }
     if (a.accumulate && !C.deferred && C.cnt > 0) {
         unsigned m0 = __ballot_sync(0xffffffffu, sl0 >= 0), m1 = __ballot_sync(0xffffffffu, sl1 >= 0);
         while (m0 | m1) {
@@ -640,6 +655,7 @@ __global__ void k_wtile_box(const int4 *tiles, const int *n_tiles, long long max
     if (64 * wt >= T.z) return;
     const double *o = box + 8 * tile;
     float lo[5], hi[5];
+    double sm[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // point_warp's record order: P0, then + P1
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
         lo[d] = INF_F;
@@ -651,6 +667,9 @@ __global__ void k_wtile_box(const int4 *tiles, const int *n_tiles, long long max
         if (off >= T.z) continue;
         const long long p = (long long)T.y + off;
         const double P[4] = {x[p], y[p], z[p], t[p]};
+        const double Pv[5] = {P[0], P[1], P[2], P[3], v[p]};
+#pragma unroll
+        for (int d = 0; d < 5; ++d) sm[d] = q == 0 ? Pv[d] : DADD(sm[d], Pv[d]);
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
             const float r = (float)DMUL(DSUB(P[d], o[d]), d == 3 ? cf : 1.0);
@@ -665,12 +684,17 @@ __global__ void k_wtile_box(const int4 *tiles, const int *n_tiles, long long max
     for (int d = 0; d < 5; ++d) {
         lo[d] = wmin_f(lo[d]);
         hi[d] = wmax_f(hi[d]);
+        sm[d] = warp_sum_d(sm[d]);
     }
     if (lane == 0) {
         WBox b;
         b.lo = make_float4(lo[0], lo[1], lo[2], lo[3]);
         b.hi = make_float4(hi[0], hi[1], hi[2], hi[3]);
         b.v = make_float2(lo[4], hi[4]);
+        b.pad = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) b.s[d] = sm[d];
+        b.pad2 = 0.0;
         out[tile * (POINT_CHUNK / 64) + wt] = b;
     }
 }

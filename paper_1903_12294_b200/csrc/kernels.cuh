@@ -46,6 +46,8 @@ struct WBox {                 // one 64-point warp tile of a point chunk (k_poin
     float4 lo, hi;            // chunk-relative fp32 box (t scaled by c_f)
     float2 v;                 // range of fl32(value)
     float2 pad;
+    double s[5];              // fixed-order warp sums of x, y, z, t, value (whole tile)
+    double pad2;
 };
 
 struct PointArgs {
