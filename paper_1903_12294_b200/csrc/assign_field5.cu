@@ -773,10 +773,19 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         const int rbx = w & 1, rby = (w >> 1) & 3;
         if (!deferred && cnt > 0 && GX * rbx < X.len && GY * rby < Y.len) {
             float vl = 0.f, vh = 0.f;
-            if (USEVAL) {
-                const float2 vr = a.vrange[blockIdx.x];
-                vl = vr.x;
-                vh = vr.y;
+            if (USEVAL) {   // value range of the region = union of its bricks' ranges
+                float lo = INF_F, hi = -INF_F;
+                if (lane < 8) {
+                    const int bi = w + NW * lane;
+                    const int bz = (bi >> 3) & 3, bt = bi >> 5;
+                    if (GZ * bz < Z.len && GT * bt < Tm.len) {
+                        const float2 r = a.brange[(size_t)blockIdx.x * 64 + bi];
+                        lo = r.x;
+                        hi = r.y;
+                    }
+                }
+                vl = warp_min_f(lo);
+                vh = warp_max_f(hi);
             }
             nl = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, rbx, rby, vl, vh, a.debug)
                                 : region_list<USEVAL, 4>(S, C, rbx, rby, vl, vh, a.debug);
@@ -846,62 +855,6 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         }
     }
     if (ovf_local) *a.overflow = 1;
-}
-
-// Range of fl32(value) over every field block (once per run: values do not change
-// between passes); rounding is monotone, so these are min/max of fl32(v).
-__global__ void k_block_vrange(FieldArgs a) {
-    unsigned tile = blockIdx.x;
-    const int txi = (int)(tile % (unsigned)a.ntx);
-    tile /= (unsigned)a.ntx;
-    const int tyi = (int)(tile % (unsigned)a.nty);
-    tile /= (unsigned)a.nty;
-    const int tzi = (int)(tile % (unsigned)a.ntz);
-    const int tti = (int)(tile / (unsigned)a.ntz);
-    const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
-    const int n = X.len * Y.len * Z.len * T.len;
-    double lo = INF_D, hi = -INF_D;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        int q = e;
-        const int i = q % X.len;
-        q /= X.len;
-        const int j = q % Y.len;
-        q /= Y.len;
-        const int k = q % Z.len;
-        const int m = q / Z.len;
-        const double v = a.values[(((long long)(T.start + m) * a.nz + Z.start + k) * a.ny + Y.start + j) *
-                                      (long long)a.nx + X.start + i];
-        lo = fmin(lo, v);
-        hi = fmax(hi, v);
-    }
-    __shared__ double r[2][32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (lane == 0) {
-        r[0][w] = lo;
-        r[1][w] = hi;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int q = 1; q < nw; ++q) {
-            lo = fmin(lo, r[0][q]);
-            hi = fmax(hi, r[1][q]);
-        }
-        a.vrange_out[blockIdx.x] = make_float2((float)lo, (float)hi);
-    }
-}
-
-int launch_block_vrange(const FieldArgs &a, cudaStream_t st) {
-    const long long n = (long long)a.ntx * a.nty * a.ntz * a.ntt;
-    if (n <= 0 || field_version() != 5) return 0;
-    ::mfseg::count_launch();
-    k_block_vrange<<<(unsigned)n, 256, 0, st>>>(a);
-    MFSEG_LAUNCH("k_block_vrange");
-    return 0;
 }
 
 // Per brick, once per run: range of fl32(value) and the fixed-order value sum

@@ -34,8 +34,6 @@ struct FieldArgs {
     int accumulate;
     int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor, bit3: stats
     unsigned long long *stats;   // debug bit3: [0] bricks, [1] kept candidates, [2] exact samples
-    const float2 *vrange;        // per field block: range of fl32(value) (k_block_vrange)
-    float2 *vrange_out;
     const float2 *brange;        // per brick (block * 64 + brick): range of fl32(value)
     const double *bsum;          // per brick: fixed-order value sum (k_brick_pre)
     float2 *brange_out;
@@ -117,7 +115,6 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
 // assign.cu
 int field_tile_dims(int *tx, int *ty, int *tz);
 int field_version();
-int launch_block_vrange(const FieldArgs &a, cudaStream_t st);
 int launch_brick_pre(const FieldArgs &a, cudaStream_t st);
 int point_tile_size();
 int point_version();

@@ -268,7 +268,6 @@ struct Plan {
     int ntx, nty, ntz, ntt;
     int *tbin;
     AxisTile *tt;
-    float2 *vrange;                 // per field block value range (field v5)
     float2 *brange;                 // per brick value range (field v5)
     double *bsum;                   // per brick value sum (field v5)
     long long *stranded_f, *deferred_f;
@@ -375,7 +374,6 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.zt = cv.take<AxisTile>(P.ntz);
     P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
-    P.vrange = cv.take<float2>((long long)P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     P.brange = cv.take<float2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     P.bsum = cv.take<double>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
@@ -481,7 +479,7 @@ int plan_prepare(Plan &P) {
         k_tbins<<<(P.f.nt + 255) / 256, 256, 0, st>>>(P.f.nt, P.f.times, p.mins[3], p.C[3],
                                                         p.k[3], P.tbin);
         MFSEG_LAUNCH("k_tbins");
-        {   // per-block value ranges (the values are fixed for the whole run)
+        {   // per-brick value ranges and sums (the values are fixed for the whole run)
             FieldArgs va;
             memset(&va, 0, sizeof va);
             va.nx = P.f.nx;
@@ -497,10 +495,8 @@ int plan_prepare(Plan &P) {
             va.nty = P.nty;
             va.ntz = P.ntz;
             va.ntt = P.ntt;
-            va.vrange_out = P.vrange;
             va.brange_out = P.brange;
             va.bsum_out = P.bsum;
-            MFSEG_TRY(launch_block_vrange(va, st));
             MFSEG_TRY(launch_brick_pre(va, st));
         }
     }
@@ -593,7 +589,6 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.ntz = P.ntz;
         a.tbin = P.tbin;
         a.tt = P.tt;
-        a.vrange = P.vrange;
         a.brange = P.brange;
         a.bsum = P.bsum;
         a.ntt = P.ntt;
