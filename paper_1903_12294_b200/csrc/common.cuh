@@ -201,6 +201,12 @@ struct AxisTile {         // field tile along one axis: index range inside one s
     int start, len, bin, pad;
 };
 
+// 256 bytes of device scratch (plus a pinned host mirror) per host thread and
+// device, allocated once: the small flag / min-max buffers of the synchronous
+// ABI calls.  (cudaMallocAsync/cudaFreeAsync on the default pool took up to a
+// second per call next to the caching allocator's multi-GB blocks.)
+int tiny_scratch(void **dev, void **host);
+
 // host-side internal entry points shared between translation units
 int scan_exclusive_i32(const int *in, int *out, long long n, void *tmp, size_t tmp_bytes,
                        cudaStream_t st);

@@ -46,6 +46,27 @@ static void harvest() {
 
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_err;
+int tiny_scratch(void **dev, void **host) {
+    struct Slot {
+        void *d = nullptr, *h = nullptr;
+    };
+    static thread_local Slot slots[64];
+    int id = 0;
+    MFSEG_CUDA(cudaGetDevice(&id));
+    if (id < 0 || id >= 64) {
+        set_error("device ordinal out of range");
+        return 1;
+    }
+    Slot &sl = slots[id];
+    if (!sl.d) {
+        MFSEG_CUDA(cudaMalloc(&sl.d, 256));
+        MFSEG_CUDA(cudaMallocHost(&sl.h, 256));
+    }
+    *dev = sl.d;
+    *host = sl.h;
+    return 0;
+}
+
 void set_error(const std::string &msg) { g_err = msg; }
 int fail(const char *where, cudaError_t e) {
     g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -884,8 +905,8 @@ int mfseg_accumulate(int32_t K, const mfseg_field *f, const mfseg_points *pts,
                      const int32_t *point_labels, const int32_t *field_labels, int64_t *acc,
                      void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    int *ovf = nullptr;
-    MFSEG_CUDA(cudaMallocAsync((void **)&ovf, sizeof(int), st));
+    int *ovf = nullptr, *ovf_h = nullptr;
+    MFSEG_TRY(tiny_scratch((void **)&ovf, (void **)&ovf_h));
     MFSEG_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
     MFSEG_CUDA(cudaMemsetAsync(acc, 0, sizeof(int64_t) * K * MFSEG_ACC_WORDS, st));
     if (pts && pts->n > 0)
@@ -894,11 +915,9 @@ int mfseg_accumulate(int32_t K, const mfseg_field *f, const mfseg_points *pts,
         long long n = (long long)f->nx * f->ny * f->nz * f->nt;
         MFSEG_TRY(launch_accumulate_field(n, f, field_labels, (unsigned long long *)acc, ovf, st));
     }
-    int h = 0;
-    MFSEG_CUDA(cudaMemcpyAsync(&h, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-    MFSEG_CUDA(cudaFreeAsync(ovf, st));
+    MFSEG_CUDA(cudaMemcpyAsync(ovf_h, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
-    if (h) {
+    if (*ovf_h) {
         set_error("fixed-point accumulator overflow");
         return 4;
     }
@@ -915,13 +934,11 @@ int mfseg_update_centers(int32_t K, const int64_t *acc, mfseg_centers old_state,
                          mfseg_centers new_state, double eps_c, int32_t *conv_host,
                          double *delta_host, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    void *flags = nullptr;
-    MFSEG_CUDA(cudaMallocAsync(&flags, 64, st));
+    void *flags = nullptr, *h = nullptr;
+    MFSEG_TRY(tiny_scratch(&flags, &h));
     MFSEG_TRY(launch_update(K, (const unsigned long long *)acc, old_state, new_state, eps_c,
                             flags, st));
-    alignas(16) char h[64];
     MFSEG_CUDA(cudaMemcpyAsync(h, flags, update_flags_bytes(), cudaMemcpyDeviceToHost, st));
-    MFSEG_CUDA(cudaFreeAsync(flags, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
     int conv;
     double delta;
@@ -938,16 +955,14 @@ int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_
         set_error("minmax of an empty array");
         return 2;
     }
-    unsigned long long *mm = nullptr;
-    MFSEG_CUDA(cudaMallocAsync((void **)&mm, 16, st));
-    unsigned long long init[2] = {~0ull, 0ull};
+    unsigned long long *mm = nullptr, *h = nullptr;
+    MFSEG_TRY(tiny_scratch((void **)&mm, (void **)&h));
+    const unsigned long long init[2] = {~0ull, 0ull};
     MFSEG_CUDA(cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
     ::mfseg::count_launch();
     k_minmax<<<148 * 4, 256, 0, st>>>(values, n, mm);
     MFSEG_LAUNCH("k_minmax");
-    unsigned long long h[2];
     MFSEG_CUDA(cudaMemcpyAsync(h, mm, 16, cudaMemcpyDeviceToHost, st));
-    MFSEG_CUDA(cudaFreeAsync(mm, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
     double lo = unkey(h[0]), hi = unkey(h[1]);
     if (lo_host) *lo_host = lo;

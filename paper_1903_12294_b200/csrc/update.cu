@@ -285,21 +285,20 @@ int mfseg_update_centers_f64(int32_t K, const double *sums, const double *psum, 
 int mfseg_compare_centers(int32_t K, mfseg_centers old_state, mfseg_centers new_state,
                           double eps_c, int32_t *conv_host, double *delta_host, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    Flags *fl = nullptr;
-    MFSEG_CUDA(cudaMallocAsync((void **)&fl, sizeof(Flags), st));
+    Flags *fl = nullptr, *hf = nullptr;
+    static_assert(sizeof(Flags) <= 256, "tiny scratch");
+    MFSEG_TRY(tiny_scratch((void **)&fl, (void **)&hf));
     MFSEG_CUDA(cudaMemsetAsync(fl, 0, sizeof(Flags), st));
     if (K > 0) {
         ::mfseg::count_launch();
         k_compare<<<(K + 255) / 256, 256, 0, st>>>(K, old_state, new_state, eps_c, fl);
     }
     MFSEG_LAUNCH("k_compare");
-    Flags h;
-    MFSEG_CUDA(cudaMemcpyAsync(&h, fl, sizeof(Flags), cudaMemcpyDeviceToHost, st));
-    MFSEG_CUDA(cudaFreeAsync(fl, st));
+    MFSEG_CUDA(cudaMemcpyAsync(hf, fl, sizeof(Flags), cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
     int conv;
     double delta;
-    decode_flags(&h, &conv, &delta);
+    decode_flags(hf, &conv, &delta);
     if (conv_host) *conv_host = conv;
     if (delta_host) *delta_host = delta;
     return 0;
