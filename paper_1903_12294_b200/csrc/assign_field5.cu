@@ -61,6 +61,7 @@ constexpr int QY = BX / GX, QZ = QY + BY / GY, QT = QZ + BZ / GZ;
 constexpr int NQ = QT + BT / GT;                   // brick-row groups: x 2, y 4, z 4, t 2
 constexpr int HW = 27;                             // histogram words: x 8, y 8, z 8, t 2, n 1
 constexpr float KSCR = 0x1.0p-18f;
+static_assert(MULTI_MAX <= 32, "one lane per kept candidate in k_field_screen");
 constexpr float KCULL = 0x1.0p-16f;
 
 struct Ctx {
@@ -415,105 +416,48 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             for (int k = 0; k < 8; ++k) sl[k] = (livem >> k & 1) ? sstar : -1;
             one = sstar;
         } else {
-        if (FULL) {
+            // several survivors: the per-sample screen runs in k_field_screen (one
+            // warp per brick, kept candidates by global id), keeping this kernel lean;
+            // more than MULTI_MAX survivors or a full queue: exact per-sample path
+            unsigned long long item = ~0ull;
+            if (lane == 0 && nkeep <= MULTI_MAX) item = atomicAdd(a.n_multi, 1ull);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item < (unsigned long long)a.multi_cap) {
+            MultiItem &it = a.multi[item];
+            int pos = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = __ldg(a.values + fbase + (k & 3) * C.plane + (k >> 2) * C.vol);
-        }
-        float fv[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            fv[k] = (FULL || (livem >> k & 1)) ? (float)v[k] : __int_as_float(0x7fffffff);
-        // ---- per-sample fp32 screen with packed (d, slot) keys
-        unsigned b1[8], b2[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            b1[k] = 0xFFFFFFFFu;
-            b2[k] = 0xFFFFFFFFu;
-        }
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            unsigned it = keep[r];
-            while (it) {
-                const int s = LIST ? S.lst[region][__ffs(it) - 1] : __ffs(it) - 1 + 32 * r;
-                it &= it - 1;
-                const float *T = S.tab[s];
-                const float axy = T[lx] + T[BX + ly];
-                const float4 tz = *reinterpret_cast<const float4 *>(T + OZ + z0);
-                const float2 tt = *reinterpret_cast<const float2 *>(T + OT + t0);
-                const float az[4] = {axy + tz.x, axy + tz.y, axy + tz.z, axy + tz.w};
-                float cvs = 0.0f, wvs = 0.0f;
-                if (USEVAL) {
-                    cvs = S.cvf[s];
-                    wvs = S.wvf[s];
+            for (int r = 0; r < NR; ++r) {
+                const unsigned kr = keep[r];
+                if (kr >> lane & 1u) {
+                    const int slot = LIST ? S.lst[region][lane] : lane + 32 * r;
+                    it.id[pos + __popc(kr & ((1u << lane) - 1u))] = S.id[slot];
                 }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const float sq = az[k & 3] + ((k >> 2) ? tt.y : tt.x);
-                    const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf(fv[k] - cvs))
-                                           : fwd * sqrt_approx(sq);
-                    const unsigned key = (__float_as_uint(d) & ~SLOT_MASK) | (unsigned)s;
-                    b2[k] = min(b2[k], max(b1[k], key));
-                    b1[k] = min(b1[k], key);
-                }
+                pos += __popc(kr);
             }
-        }
-        // ---- certify, or resolve exactly
-        unsigned need = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float t1 = __uint_as_float(min(b1[k] & ~SLOT_MASK, INF_BITS));
-            const float t2 = __uint_as_float(min(b2[k] & ~SLOT_MASK, INF_BITS));
-            const float u1 = t1 * (1.f + 0x1.0p-15f);
-            const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
-            const bool ok = !(a.debug & 2) && b1[k] < INF_BITS &&
-                            t2 * (1.f - KSCR) > u1 * (1.f + KSCR) + 2.f * KSCR * W;
-            sl[k] = ok ? (int)(b1[k] & SLOT_MASK) : -1;
-            if (!ok && (livem >> k & 1)) need |= 1u << k;
-        }
-        if ((a.debug & 8) && need) atomicAdd(a.stats + 2, (unsigned long long)__popc(need));
-        if (__any_sync(0xffffffffu, need != 0) && need) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (!(need >> k & 1)) continue;
-                const int zi = z0 + (k & 3), ti = t0 + (k >> 2);
-                const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
-                const float u1 = __uint_as_float(b1[k] & ~SLOT_MASK) * (1.f + 0x1.0p-15f);
-                const float thrk = b1[k] < INF_BITS
-                                       ? (u1 * (1.f + KSCR) + 2.f * KSCR * W) * (1.f + 0x1.0p-17f)
-                                       : INF_F;
-                const double px = S.x[lx], py = S.y[ly], pz = S.z[zi];
-                double eD = INF_D;
-                int eI = INT_MAX, eS = -1;
-#pragma unroll 1
-                for (int r = 0; r < NR; ++r) {
-                    unsigned it = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
-                    while (it) {
-                        const int s = LIST ? S.lst[region][__ffs(it) - 1] : __ffs(it) - 1 + 32 * r;
-                        it &= it - 1;
-                        const float *T = S.tab[s];
-                        const float ex = T[lx], ey = T[BX + ly], ez = T[OZ + zi], et = T[OT + ti];
-                        if (ex == INF_F || ey == INF_F || ez == INF_F || et == INF_F) continue;
-                        const float sq = ((ex + ey) + ez) + et;
-                        const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), S.wvf[s] * fabsf(fv[k] - S.cvf[s]))
-                                               : fwd * sqrt_approx(sq);
-                        if (d > thrk) continue;
-                        const double dx = DSUB(S.c[s][0], px), dy = DSUB(S.c[s][1], py),
-                                     dz = DSUB(S.c[s][2], pz);
-                        const double ct = DMUL(a.cf, DSUB(S.c[s][3], S.t[ti]));
-                        const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
-                        const double D = metric_tail(qq, DMUL(ct, ct), v[k], S.c[s][4], S.has[s],
-                                                     a.wv, a.wd);
-                        if (better(D, S.id[s], eD, eI)) {
-                            eD = D;
-                            eI = S.id[s];
-                            eS = s;
-                        }
-                    }
-                }
-                sl[k] = eS;
+            if (lane == 0) {
+                it.tile = (int)blockIdx.x;
+                it.bi = bi;
+                it.nk = nkeep;
             }
+            return;
+            }
+            int nd = 0;
+            int *lab_base = a.labels + fbase;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (livem >> k & 1) {
+                    lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = -2;
+                    ++nd;
+                }
+            long long p = warp_reserve(a.n_deferred, nd);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (livem >> k & 1) {
+                    if (p < a.deferred_cap) a.deferred[p] = fbase + (k & 3) * C.plane + (k >> 2) * C.vol;
+                    ++p;
+                }
+            return;
         }
-        }   // screen
     }
 
     // ---- labels; deferred / stranded samples to their lists (warp-aggregated)

@@ -1,0 +1,365 @@
+// k_field_screen — per-sample resolution of the field bricks that
+// k_field_assign5 left with several candidates (cell boundaries and value
+// edges run through them).  One warp per brick, candidates by global id.
+//
+// Every number here is computed exactly as in k_field_assign5: the fp32
+// per-axis entries fl32((c - s)^2) (fp64 difference and square, one rounding,
+// +inf outside the validity window), d32 = fwd sqrt(((Tx + Ty) + Tz) + Tt)
+// + w_v |fl(v) - fl(cv)|, packed (d | candidate) keys, the certification
+// t2 (1-K) > u1 (1+K) + 2 K W and the exact fp64 re-evaluation within the
+// margin (error analysis: assign_field5.cu header).  W uses the largest |cv|
+// among the kept candidates, the only ones compared.
+//
+// Partial sums: per (brick, cluster) record, x / y / z / t sums as count
+// marginals x 128-bit fixed-point coordinates (exact), reduced over the warp
+// in 128-bit integer arithmetic; the value sum as the fixed-order fp64 warp sum
+// converted exactly; one 128-bit integer atomic per word.  Integer sums are
+// order-free, so the result does not depend on which warp takes which brick.
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace mfseg {
+namespace {
+
+constexpr double INF_D = __builtin_huge_val();
+constexpr float INF_F = __builtin_huge_valf();
+constexpr float FLT_BIG = 3.4028234663852886e38f;
+constexpr unsigned INF_BITS = 0x7F800000u;
+constexpr unsigned KEY_MASK = 127u;   // same key truncation as k_field_assign5
+constexpr float KSCR = 0x1.0p-18f;
+constexpr int GX = 8, GY = 4, GZ = 4, GT = 2;
+constexpr int ACC_FV = 10, ACC_NF = 13;   // accumulator words (assign.cu)
+constexpr int SCREEN_MINB = 2;
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float to_f(double x) { return fminf(__double2float_rn(x), FLT_BIG); }
+
+__device__ __forceinline__ long long warp_reserve(unsigned long long *counter, int n) {
+    const int lane = threadIdx.x & 31;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total > 0) base = atomicAdd(counter, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return (long long)base + incl - n;
+}
+
+}  // namespace
+
+struct ScreenCand {            // one warp's kept candidates, staged in shared memory
+    double c[4][MULTI_MAX];
+    double cv[MULTI_MAX];
+    int4 b0[MULTI_MAX], b1[MULTI_MAX];
+    float cvf[MULTI_MAX], wvf[MULTI_MAX];
+    int id[MULTI_MAX], has[MULTI_MAX];
+};
+
+template <bool USEVAL>
+__global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) {
+    __shared__ ScreenCand SC[8];
+    const int lane = threadIdx.x & 31;
+    ScreenCand &Q = SC[threadIdx.x >> 5];
+    const long long n_items = min((long long)*a.n_multi, a.multi_cap);
+    const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+    int ovf_local = 0;
+    const long long plane = (long long)a.ny * a.nx, vol = plane * a.nz;
+    const float fwd = (float)a.wd;
+    const float wvf = USEVAL ? (float)a.wv : 0.0f;
+    const float slack = 3e-13f * (float)(a.wd + a.wv);
+    for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; item < n_items;
+         item += nwarps) {
+        const MultiItem &it = a.multi[item];
+        const int nk = it.nk, bi = it.bi;
+        unsigned tile = (unsigned)it.tile;
+        const int txi = (int)(tile % (unsigned)a.ntx);
+        tile /= (unsigned)a.ntx;
+        const int tyi = (int)(tile % (unsigned)a.nty);
+        tile /= (unsigned)a.nty;
+        const int tzi = (int)(tile % (unsigned)a.ntz);
+        const int tti = (int)(tile / (unsigned)a.ntz);
+        const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
+        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+        const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
+        const int z0 = GZ * bz, t0 = GT * bt;
+        const int gx = X.start + lx, gy = Y.start + ly, gz0 = Z.start + z0, gt0 = T.start + t0;
+        const long long fbase = (((long long)gt0 * a.nz + gz0) * a.ny + gy) * (long long)a.nx + gx;
+        unsigned livem = 0;
+        if (lx < X.len && ly < Y.len) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (z0 + (k & 3) < Z.len && t0 + (k >> 2) < T.len) livem |= 1u << k;
+        }
+        double v[8];   // dead samples: 0 (their keys are never used)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
+        // sample coordinates (reference formula); index clamped for dead lanes
+        const double px = cell_coord(a.ox, a.sx, X.start + min(lx, X.len - 1));
+        const double py = cell_coord(a.oy, a.sy, Y.start + min(ly, Y.len - 1));
+        double pz[4], pt[2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pz[q] = cell_coord(a.oz, a.sz, Z.start + min(z0 + q, Z.len - 1));
+#pragma unroll
+        for (int r = 0; r < 2; ++r) pt[r] = a.times[T.start + min(t0 + r, T.len - 1)];
+        // stage the kept candidates; largest |cv| among them (certification's W)
+        float cvmax = 0.f;
+        __syncwarp();
+        if (lane < nk) {
+            const int id = it.id[lane];
+            const bool has = a.chas[id] != 0;
+            const double cv = has ? a.cval[id] : 0.0;
+            Q.id[lane] = id;
+            Q.has[lane] = has;
+            Q.cv[lane] = cv;
+            Q.cvf[lane] = (float)cv;
+            Q.wvf[lane] = (USEVAL && has) ? (float)a.wv : 0.f;
+            Q.c[0][lane] = a.c.x[id];
+            Q.c[1][lane] = a.c.y[id];
+            Q.c[2][lane] = a.c.z[id];
+            Q.c[3][lane] = a.c.t[id];
+            Q.b0[lane] = a.g.vbox[2 * id];
+            Q.b1[lane] = a.g.vbox[2 * id + 1];
+            if (USEVAL && has) cvmax = fabsf((float)cv);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cvmax = fmaxf(cvmax, __shfl_xor_sync(0xffffffffu, cvmax, o));
+
+        // ---- screen over the kept candidates
+        unsigned b1[8], b2[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            b1[k] = 0xFFFFFFFFu;
+            b2[k] = 0xFFFFFFFFu;
+        }
+#pragma unroll 1
+        for (int j = 0; j < nk; ++j) {
+            const int4 b0 = Q.b0[j], bb = Q.b1[j];
+            const double cx = Q.c[0][j], cy = Q.c[1][j], cz = Q.c[2][j], ct = Q.c[3][j];
+            float tx = INF_F, ty = INF_F, tz[4], tt[2];
+            if (gx >= b0.x && gx <= b0.y) {
+                const double d = DSUB(cx, px);
+                tx = to_f(DMUL(d, d));
+            }
+            if (gy >= b0.z && gy <= b0.w) {
+                const double d = DSUB(cy, py);
+                ty = to_f(DMUL(d, d));
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                tz[q] = INF_F;
+                if (gz0 + q >= bb.x && gz0 + q <= bb.y) {
+                    const double d = DSUB(cz, pz[q]);
+                    tz[q] = to_f(DMUL(d, d));
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                tt[r] = INF_F;
+                if (gt0 + r >= bb.z && gt0 + r <= bb.w) {
+                    const double d = DMUL(a.cf, DSUB(ct, pt[r]));
+                    tt[r] = to_f(DMUL(d, d));
+                }
+            }
+            const float cvs = USEVAL ? Q.cvf[j] : 0.f, wvs = USEVAL ? Q.wvf[j] : 0.f;
+            const float axy = tx + ty;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float sq = (axy + tz[k & 3]) + tt[k >> 2];
+                const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf((float)v[k] - cvs))
+                                       : fwd * sqrt_approx(sq);
+                const unsigned key = (__float_as_uint(d) & ~KEY_MASK) | (unsigned)j;
+                b2[k] = min(b2[k], max(b1[k], key));
+                b1[k] = min(b1[k], key);
+            }
+        }
+        // ---- certify, or resolve exactly
+        int sl[8];
+        unsigned need = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float t1 = __uint_as_float(min(b1[k] & ~KEY_MASK, INF_BITS));
+            const float t2 = __uint_as_float(min(b2[k] & ~KEY_MASK, INF_BITS));
+            const float u1 = t1 * (1.f + 0x1.0p-15f);
+            const float W = USEVAL ? fmaf(wvf, fabsf((float)v[k]) + cvmax, slack) : slack;
+            const bool ok = !(a.debug & 2) && b1[k] < INF_BITS &&
+                            t2 * (1.f - KSCR) > u1 * (1.f + KSCR) + 2.f * KSCR * W;
+            sl[k] = ok ? (int)(b1[k] & KEY_MASK) : -1;
+            if (!ok && (livem >> k & 1)) need |= 1u << k;
+        }
+        if (need) {
+#pragma unroll 1
+            for (int k = 0; k < 8; ++k) {
+                if (!(need >> k & 1)) continue;
+                double vk = v[0], pzk = pz[0], ptk = pt[0];
+                unsigned b1k = b1[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q)
+                    if (q == k) {
+                        vk = v[q];
+                        b1k = b1[q];
+                    }
+#pragma unroll
+                for (int q = 1; q < 4; ++q)
+                    if (q == (k & 3)) pzk = pz[q];
+                if (k >> 2) ptk = pt[1];
+                const float fvk = (float)vk;
+                const float W = USEVAL ? fmaf(wvf, fabsf(fvk) + cvmax, slack) : slack;
+                const float u1 = __uint_as_float(b1k & ~KEY_MASK) * (1.f + 0x1.0p-15f);
+                const float thrk = b1k < INF_BITS
+                                       ? (u1 * (1.f + KSCR) + 2.f * KSCR * W) * (1.f + 0x1.0p-17f)
+                                       : INF_F;
+                const int gz = gz0 + (k & 3), gt = gt0 + (k >> 2);
+                double eD = INF_D;
+                int eI = INT_MAX, eJ = -1;
+                for (int j = 0; j < nk; ++j) {
+                    const int id = Q.id[j];
+                    const int4 b0 = Q.b0[j], bb = Q.b1[j];
+                    if (!(gx >= b0.x && gx <= b0.y && gy >= b0.z && gy <= b0.w && gz >= bb.x &&
+                          gz <= bb.y && gt >= bb.z && gt <= bb.w))
+                        continue;
+                    const double cx = Q.c[0][j], cy = Q.c[1][j], cz = Q.c[2][j], ct = Q.c[3][j];
+                    const double dx = DSUB(cx, px), dy = DSUB(cy, py), dz = DSUB(cz, pzk);
+                    const double dt = DMUL(a.cf, DSUB(ct, ptk));
+                    // fp32 screen value of this pair (prune outside the margin)
+                    const float sq = ((to_f(DMUL(dx, dx)) + to_f(DMUL(dy, dy))) + to_f(DMUL(dz, dz))) +
+                                     to_f(DMUL(dt, dt));
+                    const bool has = Q.has[j] != 0;
+                    const float cvs = Q.cvf[j];
+                    const float wvs = USEVAL ? Q.wvf[j] : 0.f;
+                    const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf(fvk - cvs))
+                                           : fwd * sqrt_approx(sq);
+                    if (d > thrk) continue;
+                    const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
+                    const double D = metric_tail(qq, DMUL(dt, dt), vk, Q.cv[j], has,
+                                                 a.wv, a.wd);
+                    if (better(D, id, eD, eI)) {
+                        eD = D;
+                        eI = id;
+                        eJ = j;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q == k) sl[q] = eJ;
+            }
+        }
+
+        // ---- labels; stranded samples (no kept candidate valid) to the fallback list
+        int nout = 0;
+        int *lab_base = a.labels + fbase;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (!(livem >> k & 1)) continue;
+            const int lab = sl[k] >= 0 ? Q.id[sl[k]] : -1;
+            lab_base[(k & 3) * plane + (k >> 2) * vol] = lab;
+            if (lab < 0) ++nout;
+        }
+        if (__any_sync(0xffffffffu, nout > 0)) {
+            long long p = warp_reserve(a.n_stranded, nout);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (!(livem >> k & 1) || sl[k] >= 0) continue;
+                if (p < a.stranded_cap) a.stranded[p] = fbase + (k & 3) * plane + (k >> 2) * vol;
+                ++p;
+            }
+        }
+
+        // ---- partial sums: one record per cluster present in the brick.  Group
+        // lanes hold one fixed-point coordinate each: x columns on lanes 0-7, y rows
+        // on 8-11, z planes on 16-19, timesteps on 24-25 (others 0); per record the
+        // count-weighted products are summed inside each 8-lane group.
+        if (a.accumulate) {
+            const int grp = lane >> 3, gi = lane & 7;
+            double gc = 0.0;
+            {
+                const double pyr = __shfl_sync(0xffffffffu, py, (gi & 3) << 3);
+                double pzq = pz[0];
+#pragma unroll
+                for (int q = 1; q < 4; ++q)
+                    if (q == (gi & 3)) pzq = pz[q];
+                gc = grp == 0 ? px : grp == 1 ? pyr : grp == 2 ? pzq : (gi & 1) ? pt[1] : pt[0];
+            }
+            const bool gl = grp == 0 || gi < (grp == 3 ? 2 : 4);
+            unsigned long long flo = 0;
+            long long fhi = 0;
+            if (gl) d2fix(gc, flo, fhi, &ovf_local);
+            unsigned todo = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (sl[k] >= 0 && (livem >> k & 1)) todo |= 1u << k;
+            const unsigned MX = 0x01010101u << (lane & 7);
+            const unsigned MY = 0xFFu << (8 * (lane >> 3));
+            while (true) {
+                int mine = -1;
+#pragma unroll
+                for (int k = 7; k >= 0; --k)
+                    if (todo >> k & 1) mine = sl[k];
+                const unsigned act = __ballot_sync(0xffffffffu, mine >= 0);
+                if (!act) break;
+                const int L = __shfl_sync(0xffffffffu, mine, __ffs(act) - 1);
+                unsigned c = 0, zp = 0, tp = 0;
+                double vs = 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if ((todo >> k & 1) && sl[k] == L) {
+                        todo &= ~(1u << k);
+                        ++c;
+                        zp += 1u << (8 * (k & 3));
+                        tp += 1u << (16 * (k >> 2));
+                        vs = DADD(vs, v[k]);
+                    }
+                }
+                const unsigned sx = __reduce_add_sync(MX, c);
+                const unsigned sy = __reduce_add_sync(MY, c);
+                const unsigned sz = __reduce_add_sync(0xffffffffu, zp);
+                const unsigned st = __reduce_add_sync(0xffffffffu, tp);
+                vs = warp_sum_d(vs);
+                const unsigned syr = __shfl_sync(0xffffffffu, sy, (gi & 3) << 3);
+                unsigned cnt = grp == 0 ? sx : grp == 1 ? syr
+                             : grp == 2 ? (sz >> (8 * (gi & 3))) & 0xFFu
+                                        : (st >> (16 * (gi & 1))) & 0xFFFFu;
+                if (!gl) cnt = 0;
+                // 128-bit (flo, fhi) * cnt, then the sum over the 8 lanes of the group
+                unsigned long long lo = flo * cnt;
+                long long hi = fhi * (long long)cnt + (long long)__umul64hi(flo, cnt);
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+                    const long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+                    const unsigned long long n = lo + l2;
+                    hi = hi + h2 + (n < lo ? 1 : 0);
+                    lo = n;
+                }
+                unsigned long long *dst = a.acc + (size_t)Q.id[L] * MFSEG_ACC_WORDS;
+                if (lane == 1) d2fix(vs, lo, hi, &ovf_local);
+                if (gi == 0 || lane == 1) atomic_add_fix(dst + (lane == 1 ? ACC_FV : 2 * grp), lo, hi);
+                if (lane == 2) atomicAdd(dst + ACC_NF, (unsigned long long)((st & 0xFFFFu) + (st >> 16)));
+            }
+        }
+    }
+    if (ovf_local) *a.overflow = 1;
+}
+
+int launch_field_screen(const FieldArgs &a, cudaStream_t st) {
+    if (!a.multi) return 0;
+    ::mfseg::count_launch();
+    if (a.wv > 0.0)
+        k_field_screen<true><<<148 * 8, 256, 0, st>>>(a);
+    else
+        k_field_screen<false><<<148 * 8, 256, 0, st>>>(a);
+    MFSEG_LAUNCH("k_field_screen");
+    return 0;
+}
+
+}  // namespace mfseg

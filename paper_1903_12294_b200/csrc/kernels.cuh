@@ -6,6 +6,14 @@
 
 namespace mfseg {
 
+// A field brick left with several candidates after culling and dominance:
+// resolved per sample by k_field_screen (one warp per item).
+constexpr int MULTI_MAX = 16;
+struct MultiItem {
+    int tile, bi, nk, pad;
+    int id[MULTI_MAX];        // kept candidates (global centre ids)
+};
+
 struct FieldArgs {
     int nx, ny, nz, nt;
     double ox, oy, oz, sx, sy, sz;
@@ -38,6 +46,9 @@ struct FieldArgs {
     const double *bsum;          // per brick: fixed-order value sum (k_brick_pre)
     float2 *brange_out;
     double *bsum_out;
+    MultiItem *multi;            // queue of bricks for k_field_screen (capacity: all bricks)
+    unsigned long long *n_multi;
+    long long multi_cap;
 };
 
 struct WBox {                 // one 64-point warp tile of a point chunk (k_point_assign4)
@@ -116,6 +127,7 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
 int field_tile_dims(int *tx, int *ty, int *tz);
 int field_version();
 int launch_brick_pre(const FieldArgs &a, cudaStream_t st);
+int launch_field_screen(const FieldArgs &a, cudaStream_t st);
 int point_tile_size();
 int point_version();
 int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,

@@ -291,6 +291,8 @@ struct Plan {
     AxisTile *tt;
     float2 *brange;                 // per brick value range (field v5)
     double *bsum;                   // per brick value sum (field v5)
+    MultiItem *multi;               // multi-candidate bricks for k_field_screen
+    long long multi_cap;
     long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
@@ -397,6 +399,11 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
     P.brange = cv.take<float2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     P.bsum = cv.take<double>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
+    {
+        const long long bricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
+        P.multi_cap = P.nf > 0 ? (bricks < (1ll << 21) ? bricks : (1ll << 21)) : 0;
+        P.multi = cv.take<MultiItem>(P.multi_cap);
+    }
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     P.deferred_f = cv.take<long long>(P.cap_f);
@@ -633,6 +640,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.n_deferred = P.counters + 2;
         a.stats = P.counters + 8;
         a.deferred_cap = P.cap_f;
+        a.multi = P.multi;
+        a.n_multi = P.counters + 4;
+        a.multi_cap = P.multi_cap;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
         {
@@ -641,6 +651,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         }
         long long ntiles = (long long)P.ntx * P.nty * P.ntz * P.f.nt;
         MFSEG_TRY(launch_field_assign(a, ntiles, st));
+        if (field_version() >= 5) MFSEG_TRY(launch_field_screen(a, st));
     }
     mark(2, st);
     if (P.np > 0) {
