@@ -435,9 +435,12 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 pos += __popc(kr);
             }
             if (lane == 0) {
-                it.tile = (int)blockIdx.x;
-                it.bi = bi;
-                it.nk = nkeep;
+                it.x0 = C.X.start + GX * bx;
+                it.y0 = C.Y.start + GY * by;
+                it.z0 = C.Z.start + GZ * bz;
+                it.t0 = C.T.start + GT * bt;
+                it.meta = nkeep | min(GX, C.X.len - GX * bx) << 8 | min(GY, C.Y.len - GY * by) << 12 |
+                          min(GZ, C.Z.len - GZ * bz) << 16 | min(GT, C.T.len - GT * bt) << 20;
             }
             return;
             }
@@ -512,8 +515,6 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (sl[k] >= 0 && (FULL || (livem >> k & 1))) todo |= 1u << k;
-        const unsigned MX = 0x01010101u << (lane & 7);
-        const unsigned MY = 0xFFu << (8 * (lane >> 3));
         while (true) {
             int mine = -1;
 #pragma unroll
@@ -536,8 +537,11 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                     vs = DADD(vs, v[k]);
                 }
             }
-            const unsigned sx = __reduce_add_sync(MX, c);
-            const unsigned sy = __reduce_add_sync(MY, c);
+            unsigned sx = c + __shfl_xor_sync(0xffffffffu, c, 8);   // column sums
+            sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+            unsigned sy = c + __shfl_xor_sync(0xffffffffu, c, 1);    // row sums
+            sy += __shfl_xor_sync(0xffffffffu, sy, 2);
+            sy += __shfl_xor_sync(0xffffffffu, sy, 4);
             const unsigned sz = __reduce_add_sync(0xffffffffu, zp);
             const unsigned st = __reduce_add_sync(0xffffffffu, tp);
             vs = warp_sum_d(vs);

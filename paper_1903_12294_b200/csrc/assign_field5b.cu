@@ -79,38 +79,30 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
     for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; item < n_items;
          item += nwarps) {
         const MultiItem &it = a.multi[item];
-        const int nk = it.nk, bi = it.bi;
-        unsigned tile = (unsigned)it.tile;
-        const int txi = (int)(tile % (unsigned)a.ntx);
-        tile /= (unsigned)a.ntx;
-        const int tyi = (int)(tile % (unsigned)a.nty);
-        tile /= (unsigned)a.nty;
-        const int tzi = (int)(tile % (unsigned)a.ntz);
-        const int tti = (int)(tile / (unsigned)a.ntz);
-        const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
-        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
-        const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
-        const int z0 = GZ * bz, t0 = GT * bt;
-        const int gx = X.start + lx, gy = Y.start + ly, gz0 = Z.start + z0, gt0 = T.start + t0;
+        const int meta = it.meta, nk = meta & 0xFF;
+        const int ex = (meta >> 8) & 15, ey = (meta >> 12) & 15, ez = (meta >> 16) & 15,
+                  et = (meta >> 20) & 15;
+        const int lxr = lane & 7, lyr = lane >> 3;
+        const int gx = it.x0 + lxr, gy = it.y0 + lyr, gz0 = it.z0, gt0 = it.t0;
         const long long fbase = (((long long)gt0 * a.nz + gz0) * a.ny + gy) * (long long)a.nx + gx;
         unsigned livem = 0;
-        if (lx < X.len && ly < Y.len) {
+        if (lxr < ex && lyr < ey) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (z0 + (k & 3) < Z.len && t0 + (k >> 2) < T.len) livem |= 1u << k;
+                if ((k & 3) < ez && (k >> 2) < et) livem |= 1u << k;
         }
         double v[8];   // dead samples: 0 (their keys are never used)
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
         // sample coordinates (reference formula); index clamped for dead lanes
-        const double px = cell_coord(a.ox, a.sx, X.start + min(lx, X.len - 1));
-        const double py = cell_coord(a.oy, a.sy, Y.start + min(ly, Y.len - 1));
+        const double px = cell_coord(a.ox, a.sx, it.x0 + min(lxr, ex - 1));
+        const double py = cell_coord(a.oy, a.sy, it.y0 + min(lyr, ey - 1));
         double pz[4], pt[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pz[q] = cell_coord(a.oz, a.sz, Z.start + min(z0 + q, Z.len - 1));
+        for (int q = 0; q < 4; ++q) pz[q] = cell_coord(a.oz, a.sz, gz0 + min(q, ez - 1));
 #pragma unroll
-        for (int r = 0; r < 2; ++r) pt[r] = a.times[T.start + min(t0 + r, T.len - 1)];
+        for (int r = 0; r < 2; ++r) pt[r] = a.times[gt0 + min(r, et - 1)];
         // stage the kept candidates; largest |cv| among them (certification's W)
         float cvmax = 0.f;
         __syncwarp();
@@ -298,8 +290,6 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 if (sl[k] >= 0 && (livem >> k & 1)) todo |= 1u << k;
-            const unsigned MX = 0x01010101u << (lane & 7);
-            const unsigned MY = 0xFFu << (8 * (lane >> 3));
             while (true) {
                 int mine = -1;
 #pragma unroll
@@ -320,8 +310,11 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
                         vs = DADD(vs, v[k]);
                     }
                 }
-                const unsigned sx = __reduce_add_sync(MX, c);
-                const unsigned sy = __reduce_add_sync(MY, c);
+                unsigned sx = c + __shfl_xor_sync(0xffffffffu, c, 8);   // column sums
+                sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+                unsigned sy = c + __shfl_xor_sync(0xffffffffu, c, 1);    // row sums
+                sy += __shfl_xor_sync(0xffffffffu, sy, 2);
+                sy += __shfl_xor_sync(0xffffffffu, sy, 4);
                 const unsigned sz = __reduce_add_sync(0xffffffffu, zp);
                 const unsigned st = __reduce_add_sync(0xffffffffu, tp);
                 vs = warp_sum_d(vs);

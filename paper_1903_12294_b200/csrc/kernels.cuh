@@ -10,7 +10,9 @@ namespace mfseg {
 // resolved per sample by k_field_screen (one warp per item).
 constexpr int MULTI_MAX = 16;
 struct MultiItem {
-    int tile, bi, nk, pad;
+    int x0, y0, z0, t0;       // brick origin (global sample indices)
+    int meta;                 // nk | live extent x << 8 | y << 12 | z << 16 | t << 20
+    int pad[3];
     int id[MULTI_MAX];        // kept candidates (global centre ids)
 };
 
