@@ -46,6 +46,7 @@ struct PCtx {
     double o[4];
     float delta[4], Cf[4];
     float iC[4], uhi, ulo;          // 1 / Cf; 1 +- eps (box test band)
+    float cw[4], cn[4];             // Cf +- delta (guard-banded box half-widths)
     float Aabs, cvmax, fwd, wvf, slack, ndelta;
     int cnt, nrounds, len;
     long long start;
@@ -183,7 +184,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                 bool wfull = true, none = false;
 #pragma unroll
                 for (int d = 0; d < 4; ++d) {
-                    const float cw = C.Cf[d] + C.delta[d], cn = C.Cf[d] - C.delta[d];
+                    const float cw = C.cw[d], cn = C.cn[d];
                     const float a1 = rcv[d] - wl[d], b1 = rcv[d] - wh[d];   // a1 >= b1
                     if (a1 < -cw || b1 > cw) none = true;
                     if (!(a1 <= cn && b1 >= -cn)) wfull = false;
@@ -287,6 +288,9 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             }
         }
         if ((a.debug & 8) && lane == 0) {
+            const int nk = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
+            if (nk == 1 && sdom >= 0) atomicAdd(a.stats + 3, 1ull);
+            atomicAdd(a.stats + 4 + min(nk, 7), 1ull);
             atomicAdd(a.stats, 1ull);
             atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
                                                          __popc(keep[2]) + __popc(keep[3])));
@@ -560,6 +564,8 @@ __global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
         float eps = 0.f;
         for (int d = 0; d < 4; ++d) {
             C.iC[d] = 1.0f / C.Cf[d];
+            C.cw[d] = C.Cf[d] + C.delta[d];
+            C.cn[d] = C.Cf[d] - C.delta[d];
             eps = fmaxf(eps, C.delta[d] / C.Cf[d]);
         }
         eps = eps * 1.0001f + 0x1.0p-22f;

@@ -377,7 +377,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.flags = cv.take<char>(update_flags_bytes());
     int NB = P.NB;
     P.g = grid_carve(cv, K, NB, &P.count_tmp, &P.grid_scan_tmp);
-    P.counters = cv.take<unsigned long long>(24);   // [8..24): debug stats
+    P.counters = cv.take<unsigned long long>(32);   // [8..32): debug stats
     P.overflow = cv.take<int>(4);
     // field
     P.nf = (P.f.nt > 0) ? (long long)P.f.nx * P.f.ny * P.f.nz * P.f.nt : 0;
@@ -591,7 +591,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
                          P.count_tmp, P.grid_scan_tmp, st));
     mark(1, st);
-    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 24, st));
+    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 32, st));
     if (accumulate)
         MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
     if (P.nf > 0) {
@@ -745,7 +745,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     mark(4, st);
     if (const char *dbg = getenv("MFSEG_DEBUG")) {
         if (atoi(dbg) & 8) {
-            unsigned long long h[24];
+            unsigned long long h[32];
             MFSEG_CUDA(cudaMemcpyAsync(h, P.counters, sizeof h, cudaMemcpyDeviceToHost, st));
             MFSEG_CUDA(cudaStreamSynchronize(st));
             const unsigned long long *F = h + 8, *Q = h + 16;
@@ -756,6 +756,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                     "exact %llu | stranded f %llu p %llu deferred f %llu p %llu\n",
                     F[0], rat(F[1], F[0]), F[2], rat(F[3], F[0]), F[4], rat(F[5], F[4]), rat(F[6], F[5]),
                     Q[0], rat(Q[1], Q[0]), Q[2], h[0], h[1], h[2], h[3]);
+            fprintf(stderr, "[mfseg stats] point tiles single %.3f kept hist", rat(Q[3], Q[0]));
+            for (int q = 0; q < 8; ++q) fprintf(stderr, " %.3f", rat(Q[4 + q], Q[0]));
+            fprintf(stderr, "\n");
         }
     }
     return 0;
