@@ -166,10 +166,7 @@ __device__ __forceinline__ void table_row(float *e, float2 *mm, const double *co
 // Add one fp64 value sum to a slot's exact 128-bit fixed-point total kept as
 // six 24-bit limbs in 32-bit shared counters (the top one signed): integer,
 // order-free, and at most 64 records per slot and block, so no counter overflows.
-__device__ __forceinline__ void add_value_limbs(unsigned *lim, double v, int &ovf) {
-    unsigned long long lo;
-    long long hi;
-    d2fix(v, lo, hi, &ovf);
+__device__ __forceinline__ void add_fix_limbs(unsigned *lim, unsigned long long lo, long long hi) {
     const unsigned M = 0xFFFFFFu;
     atomicAdd(&lim[0], (unsigned)(lo & M));
     atomicAdd(&lim[1], (unsigned)((lo >> 24) & M));
@@ -177,6 +174,13 @@ __device__ __forceinline__ void add_value_limbs(unsigned *lim, double v, int &ov
     atomicAdd(&lim[3], (unsigned)(((unsigned long long)hi >> 8) & M));
     atomicAdd(&lim[4], (unsigned)(((unsigned long long)hi >> 32) & M));
     atomicAdd((int *)&lim[5], (int)(hi >> 56));
+}
+
+__device__ __forceinline__ void add_value_limbs(unsigned *lim, double v, int &ovf) {
+    unsigned long long lo;
+    long long hi;
+    d2fix(v, lo, hi, &ovf);
+    add_fix_limbs(lim, lo, hi);
 }
 
 __device__ __forceinline__ __int128 value_limbs_total(const unsigned *lim) {
@@ -348,6 +352,11 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         // least dS / (sqrt S_s,max + sqrt S_s*,max); the value terms differ by at
         // most w_v |cv_s - cv_s*| (both have values) or w_v max|v - cv_s*| (only s*).
         ubkey = __reduce_min_sync(0xffffffffu, ubkey);
+        if ((a.debug & 8) && lane == 0) {
+            const int nc = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
+            atomicAdd(a.stats + 7, (unsigned long long)nc);
+            if (nc == 1) atomicAdd(a.stats + 2, 1ull);
+        }
         int sstar = -1;
         if (ubkey != 0xFFFFFFFFu && !(a.debug & 1)) {
             sstar = (int)(ubkey & SLOT_MASK);
@@ -473,14 +482,22 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         if (a.accumulate && FULL) {
             // whole brick -> one cluster: the count marginals are constants and the
             // value sum is the brick's (fixed-order warp sum, computed once per run)
-            const double vs = a.bsum[bidx];
+            const ulonglong2 vs = a.bsum[bidx];
             unsigned *h = S.hist[one];
             if (lane < 4) atomicAdd(&h[4 * bx + lane], 32u | (32u << 16));         // 8 x, 32 each
             else if (lane < 6) atomicAdd(&h[8 + 2 * by + (lane - 4)], 64u | (64u << 16));   // 4 y
             else if (lane < 8) atomicAdd(&h[16 + 2 * bz + (lane - 6)], 64u | (64u << 16));  // 4 z
             else if (lane == 8) atomicAdd(&h[24 + bt], 128u | (128u << 16));      // 2 timesteps
             else if (lane == 9) atomicAdd(&h[26], 256u);
-            if (lane == 0) add_value_limbs(S.vlimb[one], vs, ovf_local);
+            else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
+                const int q = lane - 10;
+                const unsigned long long lo = vs.x, hi = vs.y;
+                const unsigned long long bits = q < 2 ? lo >> (24 * q)
+                                              : q == 2 ? (lo >> 48) | (hi << 16)
+                                                       : hi >> (24 * q - 64);
+                atomicAdd(&S.vlimb[one][q], q < 5 ? (unsigned)(bits & 0xFFFFFFu) : (unsigned)(bits & 0xFFu) |
+                                                        ((bits & 0x80u) ? 0xFFFFFF00u : 0u));
+            }
             return;
         }
         if (!a.accumulate) return;
@@ -843,7 +860,12 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
         hi = warp_max_f(hi);
         if (lane == 0) {
             a.brange_out[(size_t)blockIdx.x * 64 + bi] = make_float2(lo, hi);
-            a.bsum_out[(size_t)blockIdx.x * 64 + bi] = vs;
+            unsigned long long flo;
+            long long fhi;
+            int ovf = 0;
+            d2fix(vs, flo, fhi, &ovf);
+            if (ovf) *a.overflow = 1;
+            a.bsum_out[(size_t)blockIdx.x * 64 + bi] = make_ulonglong2(flo, (unsigned long long)fhi);
         }
     }
 }

@@ -45,9 +45,9 @@ struct FieldArgs {
     int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor, bit3: stats
     unsigned long long *stats;   // debug bit3: [0] bricks, [1] kept candidates, [2] exact samples
     const float2 *brange;        // per brick (block * 64 + brick): range of fl32(value)
-    const double *bsum;          // per brick: fixed-order value sum (k_brick_pre)
+    const ulonglong2 *bsum;      // per brick: fixed-order value sum as 128-bit fixed point (k_brick_pre)
     float2 *brange_out;
-    double *bsum_out;
+    ulonglong2 *bsum_out;
     MultiItem *multi;            // queue of bricks for k_field_screen (capacity: all bricks)
     unsigned long long *n_multi;
     long long multi_cap;

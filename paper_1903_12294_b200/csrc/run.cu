@@ -290,7 +290,7 @@ struct Plan {
     int *tbin;
     AxisTile *tt;
     float2 *brange;                 // per brick value range (field v5)
-    double *bsum;                   // per brick value sum (field v5)
+    ulonglong2 *bsum;               // per brick value sum, fixed point (field v5)
     MultiItem *multi;               // multi-candidate bricks for k_field_screen
     long long multi_cap;
     long long *stranded_f, *deferred_f;
@@ -398,7 +398,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
     P.brange = cv.take<float2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
-    P.bsum = cv.take<double>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
+    P.bsum = cv.take<ulonglong2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     {
         const long long bricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
         P.multi_cap = P.nf > 0 ? (bricks < (1ll << 21) ? bricks : (1ll << 21)) : 0;
@@ -525,6 +525,7 @@ int plan_prepare(Plan &P) {
             va.ntt = P.ntt;
             va.brange_out = P.brange;
             va.bsum_out = P.bsum;
+            va.overflow = P.overflow;
             MFSEG_TRY(launch_brick_pre(va, st));
         }
     }
@@ -756,6 +757,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                     "exact %llu | stranded f %llu p %llu deferred f %llu p %llu\n",
                     F[0], rat(F[1], F[0]), F[2], rat(F[3], F[0]), F[4], rat(F[5], F[4]), rat(F[6], F[5]),
                     Q[0], rat(Q[1], Q[0]), Q[2], h[0], h[1], h[2], h[3]);
+            fprintf(stderr, "[mfseg stats] field bricks: kept after cull %.3f, single after cull %.3f\n",
+                    rat(F[7], F[0]), rat(F[2], F[0]));
             fprintf(stderr, "[mfseg stats] point tiles single %.3f kept hist", rat(Q[3], Q[0]));
             for (int q = 0; q < 8; ++q) fprintf(stderr, " %.3f", rat(Q[4 + q], Q[0]));
             fprintf(stderr, "\n");
