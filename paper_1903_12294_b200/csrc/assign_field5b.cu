@@ -30,7 +30,7 @@ constexpr unsigned KEY_MASK = 127u;   // same key truncation as k_field_assign5
 constexpr float KSCR = 0x1.0p-18f;
 constexpr int GX = 8, GY = 4, GZ = 4, GT = 2;
 constexpr int ACC_FV = 10, ACC_NF = 13;   // accumulator words (assign.cu)
-constexpr int SCREEN_MINB = 2;
+constexpr int SCREEN_MINB = 3;
 
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;
@@ -62,6 +62,8 @@ struct ScreenCand {            // one warp's kept candidates, staged in shared m
     int4 b0[MULTI_MAX], b1[MULTI_MAX];
     float cvf[MULTI_MAX], wvf[MULTI_MAX];
     int id[MULTI_MAX], has[MULTI_MAX];
+    double v[8][32];          // the brick's samples (k, lane)
+    double pz[4], pt[2];      // its z-plane and timestep coordinates
 };
 
 template <bool USEVAL>
@@ -91,18 +93,22 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             for (int k = 0; k < 8; ++k)
                 if ((k & 3) < ez && (k >> 2) < et) livem |= 1u << k;
         }
-        double v[8];   // dead samples: 0 (their keys are never used)
+        // samples to shared memory (dead samples: 0, their keys are never used);
+        // fp32 copies stay in registers for the screen
+        __syncwarp();
+        float fv[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-            v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
+        for (int k = 0; k < 8; ++k) {
+            const double vk = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
+            Q.v[k][lane] = vk;
+            fv[k] = (float)vk;
+        }
         // sample coordinates (reference formula); index clamped for dead lanes
         const double px = cell_coord(a.ox, a.sx, it.x0 + min(lxr, ex - 1));
         const double py = cell_coord(a.oy, a.sy, it.y0 + min(lyr, ey - 1));
-        double pz[4], pt[2];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pz[q] = cell_coord(a.oz, a.sz, gz0 + min(q, ez - 1));
-#pragma unroll
-        for (int r = 0; r < 2; ++r) pt[r] = a.times[gt0 + min(r, et - 1)];
+        if (lane < 4) Q.pz[lane] = cell_coord(a.oz, a.sz, gz0 + min(lane, ez - 1));
+        else if (lane < 6) Q.pt[lane - 4] = a.times[gt0 + min(lane - 4, et - 1)];
+        const double *pz = Q.pz, *pt = Q.pt;
         // stage the kept candidates; largest |cv| among them (certification's W)
         float cvmax = 0.f;
         __syncwarp();
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const float sq = (axy + tz[k & 3]) + tt[k >> 2];
-                const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf((float)v[k] - cvs))
+                const float d = USEVAL ? fmaf(fwd, sqrt_approx(sq), wvs * fabsf(fv[k] - cvs))
                                        : fwd * sqrt_approx(sq);
                 const unsigned key = (__float_as_uint(d) & ~KEY_MASK) | (unsigned)j;
                 b2[k] = min(b2[k], max(b1[k], key));
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             const float t1 = __uint_as_float(min(b1[k] & ~KEY_MASK, INF_BITS));
             const float t2 = __uint_as_float(min(b2[k] & ~KEY_MASK, INF_BITS));
             const float u1 = t1 * (1.f + 0x1.0p-15f);
-            const float W = USEVAL ? fmaf(wvf, fabsf((float)v[k]) + cvmax, slack) : slack;
+            const float W = USEVAL ? fmaf(wvf, fabsf(fv[k]) + cvmax, slack) : slack;
             const bool ok = !(a.debug & 2) && b1[k] < INF_BITS &&
                             t2 * (1.f - KSCR) > u1 * (1.f + KSCR) + 2.f * KSCR * W;
             sl[k] = ok ? (int)(b1[k] & KEY_MASK) : -1;
@@ -193,18 +199,14 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
 #pragma unroll 1
             for (int k = 0; k < 8; ++k) {
                 if (!(need >> k & 1)) continue;
-                double vk = v[0], pzk = pz[0], ptk = pt[0];
+                const double vk = Q.v[k][lane], pzk = pz[k & 3], ptk = pt[k >> 2];
                 unsigned b1k = b1[0];
 #pragma unroll
                 for (int q = 1; q < 8; ++q)
                     if (q == k) {
-                        vk = v[q];
                         b1k = b1[q];
                     }
 #pragma unroll
-                for (int q = 1; q < 4; ++q)
-                    if (q == (k & 3)) pzk = pz[q];
-                if (k >> 2) ptk = pt[1];
                 const float fvk = (float)vk;
                 const float W = USEVAL ? fmaf(wvf, fabsf(fvk) + cvmax, slack) : slack;
                 const float u1 = __uint_as_float(b1k & ~KEY_MASK) * (1.f + 0x1.0p-15f);
@@ -276,10 +278,7 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             double gc = 0.0;
             {
                 const double pyr = __shfl_sync(0xffffffffu, py, (gi & 3) << 3);
-                double pzq = pz[0];
-#pragma unroll
-                for (int q = 1; q < 4; ++q)
-                    if (q == (gi & 3)) pzq = pz[q];
+                const double pzq = pz[gi & 3];
                 gc = grp == 0 ? px : grp == 1 ? pyr : grp == 2 ? pzq : (gi & 1) ? pt[1] : pt[0];
             }
             const bool gl = grp == 0 || gi < (grp == 3 ? 2 : 4);
@@ -307,7 +306,7 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
                         ++c;
                         zp += 1u << (8 * (k & 3));
                         tp += 1u << (16 * (k >> 2));
-                        vs = DADD(vs, v[k]);
+                        vs = DADD(vs, Q.v[k][lane]);
                     }
                 }
                 unsigned sx = c + __shfl_xor_sync(0xffffffffu, c, 8);   // column sums
