@@ -618,90 +618,116 @@ __global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
     if (ovf_local) *a.overflow = 1;
 }
 
-// exact fp64 bounding box of every point chunk (once per run): one warp per chunk
-__global__ void k_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles,
-                           const double *x, const double *y, const double *z, const double *t,
-                           double *box) {
-    const long long tile = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (tile >= max_tiles || tile >= *n_tiles) return;
+// Once per run, one CTA per point chunk: the exact fp64 bounding box of the
+// chunk, then for each 64-point warp tile (warp w takes tiles w, w + 8, ...)
+// the chunk-relative fp32 box, the fl32(value) range and the fixed-order sums
+// -- the same formulas k_point_assign4 uses.  The second read of the chunk's
+// points hits the cache.
+__global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const int *n_tiles,
+                                                      const double *x, const double *y,
+                                                      const double *z, const double *t,
+                                                      const double *v, double cf, double *box,
+                                                      WBox *out) {
+    constexpr int TPW = POINT_CHUNK / 64 / 8;   // warp tiles per warp
+    __shared__ double red[8][8];
+    __shared__ double o[4];
+    const long long tile = blockIdx.x;
+    if (tile >= *n_tiles) return;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int4 T = tiles[tile];
-    double lo[4] = {INF_D, INF_D, INF_D, INF_D}, hi[4] = {-INF_D, -INF_D, -INF_D, -INF_D};
-    for (int i = lane; i < T.z; i += 32) {
-        const long long p = (long long)T.y + i;
-        const double v[4] = {x[p], y[p], z[p], t[p]};
+    // every point of the chunk once, in registers: warp w holds its warp tiles
+    // w + 8 j, lane l points l and l + 32 of each
+    double P[TPW][2][5];
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            lo[d] = fmin(lo[d], v[d]);
-            hi[d] = fmax(hi[d], v[d]);
+    for (int j = 0; j < TPW; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int off = 64 * (w + 8 * j) + lane + 32 * q;
+            const long long p = (long long)T.y + min(off, T.z - 1);   // clamped: box unaffected
+            P[j][q][0] = x[p];
+            P[j][q][1] = y[p];
+            P[j][q][2] = z[p];
+            P[j][q][3] = t[p];
+            P[j][q][4] = v[p];
         }
-    }
+    double lo[4], hi[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
+        lo[d] = P[0][0][d];
+        hi[d] = P[0][0][d];
+#pragma unroll
+        for (int j = 0; j < TPW; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                lo[d] = fmin(lo[d], P[j][q][d]);
+                hi[d] = fmax(hi[d], P[j][q][d]);
+            }
         lo[d] = wmin_d(lo[d]);
         hi[d] = wmax_d(hi[d]);
     }
     if (lane < 4) {
-        box[8 * tile + lane] = lo[lane];
-        box[8 * tile + 4 + lane] = hi[lane];
+        double l = lo[0], h = hi[0];
+#pragma unroll
+        for (int d = 1; d < 4; ++d)
+            if (lane == d) {
+                l = lo[d];
+                h = hi[d];
+            }
+        red[w][lane] = l;
+        red[w][4 + lane] = h;
     }
-}
-
-// chunk-relative fp32 box and fl32(value) range of every 64-point warp tile
-// (one warp per warp tile; same formulas as k_point_assign4 would use)
-__global__ void k_wtile_box(const int4 *tiles, const int *n_tiles, long long max_tiles,
-                            const double *x, const double *y, const double *z, const double *t,
-                            const double *v, double cf, const double *box, WBox *out) {
-    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const long long tile = wid / (POINT_CHUNK / 64);
-    const int wt = (int)(wid % (POINT_CHUNK / 64));
-    if (tile >= max_tiles || tile >= *n_tiles) return;
-    const int4 T = tiles[tile];
-    if (64 * wt >= T.z) return;
-    const double *o = box + 8 * tile;
-    float lo[5], hi[5];
-    double sm[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // point_warp's record order: P0, then + P1
-#pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        lo[d] = INF_F;
-        hi[d] = -INF_F;
+    __syncthreads();
+    if (tid < 8) {
+        double r = red[0][tid];
+        for (int q = 1; q < 8; ++q) r = tid < 4 ? fmin(r, red[q][tid]) : fmax(r, red[q][tid]);
+        box[8 * tile + tid] = r;
+        if (tid < 4) o[tid] = r;
     }
+    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int off = 64 * wt + lane + 32 * q;
-        if (off >= T.z) continue;
-        const long long p = (long long)T.y + off;
-        const double P[4] = {x[p], y[p], z[p], t[p]};
-        const double Pv[5] = {P[0], P[1], P[2], P[3], v[p]};
+    for (int j = 0; j < TPW; ++j) {
+        const int wt = w + 8 * j;
+        if (64 * wt >= T.z) break;   // warp-uniform
+        float flo[5], fhi[5];
+        double sm[5];   // point_warp's record order: P0, then + P1
 #pragma unroll
-        for (int d = 0; d < 5; ++d) sm[d] = q == 0 ? Pv[d] : DADD(sm[d], Pv[d]);
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const float r = (float)DMUL(DSUB(P[d], o[d]), d == 3 ? cf : 1.0);
-            lo[d] = fminf(lo[d], r);
-            hi[d] = fmaxf(hi[d], r);
+        for (int d = 0; d < 5; ++d) {
+            flo[d] = INF_F;
+            fhi[d] = -INF_F;
+            sm[d] = 0.0;
         }
-        const float fv = (float)v[p];
-        lo[4] = fminf(lo[4], fv);
-        hi[4] = fmaxf(hi[4], fv);
-    }
 #pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        lo[d] = wmin_f(lo[d]);
-        hi[d] = wmax_f(hi[d]);
-        sm[d] = warp_sum_d(sm[d]);
-    }
-    if (lane == 0) {
-        WBox b;
-        b.lo = make_float4(lo[0], lo[1], lo[2], lo[3]);
-        b.hi = make_float4(hi[0], hi[1], hi[2], hi[3]);
-        b.v = make_float2(lo[4], hi[4]);
-        b.pad = make_float2(0.f, 0.f);
+        for (int q = 0; q < 2; ++q) {
+            if (64 * wt + lane + 32 * q >= T.z) continue;
 #pragma unroll
-        for (int d = 0; d < 5; ++d) b.s[d] = sm[d];
-        b.pad2 = 0.0;
-        out[tile * (POINT_CHUNK / 64) + wt] = b;
+            for (int d = 0; d < 5; ++d) sm[d] = q == 0 ? P[j][q][d] : DADD(sm[d], P[j][q][d]);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const float r = (float)DMUL(DSUB(P[j][q][d], o[d]), d == 3 ? cf : 1.0);
+                flo[d] = fminf(flo[d], r);
+                fhi[d] = fmaxf(fhi[d], r);
+            }
+            const float fv = (float)P[j][q][4];
+            flo[4] = fminf(flo[4], fv);
+            fhi[4] = fmaxf(fhi[4], fv);
+        }
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            flo[d] = wmin_f(flo[d]);
+            fhi[d] = wmax_f(fhi[d]);
+            sm[d] = warp_sum_d(sm[d]);
+        }
+        if (lane == 0) {
+            WBox b;
+            b.lo = make_float4(flo[0], flo[1], flo[2], flo[3]);
+            b.hi = make_float4(fhi[0], fhi[1], fhi[2], fhi[3]);
+            b.v = make_float2(flo[4], fhi[4]);
+            b.pad = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d = 0; d < 5; ++d) b.s[d] = sm[d];
+            b.pad2 = 0.0;
+            out[tile * (POINT_CHUNK / 64) + wt] = b;
+        }
     }
 }
 
@@ -709,15 +735,13 @@ int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, 
                     const double *y, const double *z, const double *t, const double *v, double cf,
                     double *box, WBox *wbox, cudaStream_t st) {
     if (max_tiles <= 0) return 0;
+    if (max_tiles > 0x7fffffffll) {
+        set_error("point chunk grid too large");
+        return 3;
+    }
     ::mfseg::count_launch();
-    const long long threads = max_tiles * 32;
-    k_tile_box<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(tiles, n_tiles, max_tiles, x, y, z,
-                                                                   t, box);
-    ::mfseg::count_launch();
-    const long long wthreads = max_tiles * (POINT_CHUNK / 64) * 32;
-    k_wtile_box<<<(unsigned)((wthreads + 255) / 256), 256, 0, st>>>(tiles, n_tiles, max_tiles, x, y,
-                                                                     z, t, v, cf, box, wbox);
-    MFSEG_LAUNCH("k_tile_box");
+    k_chunk_boxes<<<(unsigned)max_tiles, 256, 0, st>>>(tiles, n_tiles, x, y, z, t, v, cf, box, wbox);
+    MFSEG_LAUNCH("k_chunk_boxes");
     return 0;
 }
 
