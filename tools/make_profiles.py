@@ -35,7 +35,14 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
 traffic = {}
-for rep, name in (("fa5", "field_assign5"), ("fa5late", "field_assign5_late"), ("pa4", "point_assign4")):
+CAPS = (("fa5", "field_assign5", "pass 1 of `tools/prof_run.py c2 2`"),
+        ("fa5mid", "field_assign5_mid", "pass 5 of `tools/prof_run.py c2 10`"),
+        ("screenmid", "field_screen_mid", "pass 5 of `tools/prof_run.py c2 10`"),
+        ("fa5late", "field_assign5_late", "pass 10 of `tools/prof_run.py c2 10`"),
+        ("screenlate", "field_screen_late", "pass 10 of `tools/prof_run.py c2 10`"),
+        ("pa4", "point_assign4", "pass 1 of `tools/prof_run.py c2 2`"),
+        ("pa4mid", "point_assign4_mid", "pass 5 of `tools/prof_run.py c2 10`"))
+for rep, name, which in CAPS:
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
         continue
@@ -43,7 +50,6 @@ for rep, name in (("fa5", "field_assign5"), ("fa5late", "field_assign5_late"), (
     r = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = r[0], r[1], r[2]
     m = {a: (v, u) for a, u, v in zip(hdr, units, vals)}
-    which = "pass 10 of `tools/prof_run.py c2 10`" if rep.endswith("late") else "pass 1 of `tools/prof_run.py c2 2`"
     lines = [f"ncu --set full --clock-control none (one launch, {which}): k_{name}"]
     for k in want:
         if k in m:
@@ -58,11 +64,15 @@ for rep, name in (("fa5", "field_assign5"), ("fa5late", "field_assign5_late"), (
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         return v * scale
     traffic[name] = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
-if "field_assign5" in traffic:
-    json.dump({"k_field_assign_dram_bytes_per_launch": traffic["field_assign5"],
-               "k_point_assign_dram_bytes_per_launch": traffic.get("point_assign4"),
-               "source": f"profiles/{R}_field_assign5_ncu.txt, profiles/{R}_point_assign4_ncu.txt "
-                         "(dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full)"},
+if "field_assign5_mid" in traffic and "field_screen_mid" in traffic:
+    # the field phase of a pass = k_field_assign5 + k_field_screen (same pass)
+    json.dump({"k_field_assign_dram_bytes_per_launch": traffic["field_assign5_mid"] + traffic["field_screen_mid"],
+               "k_field_assign5_dram_bytes": traffic["field_assign5_mid"],
+               "k_field_screen_dram_bytes": traffic["field_screen_mid"],
+               "k_point_assign_dram_bytes_per_launch": traffic.get("point_assign4_mid"),
+               "source": f"profiles/{R}_field_assign5_mid_ncu.txt + profiles/{R}_field_screen_mid_ncu.txt, "
+                         f"profiles/{R}_point_assign4_mid_ncu.txt (pass 5 of 11; dram__bytes_read.sum + "
+                         "dram__bytes_write.sum, ncu --set full)"},
               open(os.path.join(PR, "traffic_c2.json"), "w"), indent=1)
 print(open(os.path.join(PR, f"{R}_launches_c2.md")).read())
 print(json.dumps(traffic))
