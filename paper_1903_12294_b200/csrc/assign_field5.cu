@@ -13,16 +13,19 @@
 //    block gets fp32 tables (dx^2[16] | dy^2[16] | dz^2[16] | (cf dt)^2[4],
 //    each computed in fp64 exactly like the reference and rounded once; +inf
 //    where |c - s| <= C fails) plus per-quad (min, max) of every axis;
-//  * each warp walks 8 bricks of 4x4x4 voxels x 4 timesteps (8 samples per
-//    lane).  Warp culling uses the quad tables (O(1) per candidate and brick);
-//  * the fp32 screen tracks best/second best as packed 32-bit keys
-//    (float bits of d with the low 7 mantissa bits replaced by the slot), so
-//    the top-2 update is three integer min/max;
+//  * each warp walks the 8 bricks of its region (bricks of 8x4x4 voxels x 2
+//    timesteps, 8 samples per lane): warp culling from the group tables, then
+//    the linear dominance test against the best fully valid candidate.  A
+//    brick left with one candidate is labelled here; a brick with several
+//    (<= MULTI_MAX) is queued for k_field_screen (assign_field5b.cu), which
+//    runs the per-sample fp32 screen below (packed 32-bit keys: float bits of
+//    d with the low 7 mantissa bits replaced by the candidate, so the top-2
+//    update is three integer min/max) and the certification;
 //  * partial sums: per slot 16-bit count marginals in shared memory (x, y, z,
-//    t indices; shared-memory integer atomics), value sums as per-warp fp64
-//    running sums in the warp's fixed brick order; once per block the
-//    marginals x 128-bit fixed-point coordinates and the warp value sums
-//    (converted exactly) go to the global 128-bit sums.
+//    t indices; shared-memory integer atomics) and the value sums as 24-bit
+//    shared limbs of the bricks' per-run fixed-point sums; once per block the
+//    marginals x 128-bit fixed-point coordinates and the limbs go to the
+//    global 128-bit sums.
 //
 // Error analysis of the screen (all table terms >= 0):
 //   s = (((Tx + Ty) + Tz) + Tt) has 4 fp32 rounded table terms and 3 fp32
