@@ -35,7 +35,9 @@ constexpr double INF_D = __builtin_huge_val();
 constexpr float INF_F = __builtin_huge_valf();
 constexpr unsigned INF_BITS = 0x7F800000u;
 
-constexpr int NT = 256, NW = 8;
+constexpr int NT = 128, NW = 4;   // 4 warps: a short per-CTA tail, 6 CTAs per SM
+constexpr int CR = 2;             // raw candidate rounds of NT (up to 256 per bin)
+constexpr int MINB = 6;
 constexpr int CAP = 128;
 constexpr unsigned SLOT_MASK = 127u;
 constexpr float KSCR = 0x1.0p-18f;
@@ -61,7 +63,7 @@ struct __align__(16) PSmem4 {
     int id[CAP];
     float cvf[CAP], wvf[CAP];
     unsigned char has[CAP], full[CAP];
-    int wc[NW];
+    int wc[CR * NW];
     float red[NW];
     PCtx ctx;
 };
@@ -473,7 +475,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
 }  // namespace
 
 template <bool USEVAL>
-__global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
+__global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
     if ((int)blockIdx.x >= *a.n_tiles) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PSmem4 &S = *reinterpret_cast<PSmem4 *>(smem_raw);
@@ -491,59 +493,74 @@ __global__ void __launch_bounds__(NT, 3) k_point_assign4(PointArgs a) {
     }
     __syncthreads();
     const int L0 = a.g.cand_start[T.x], L1 = a.g.cand_start[T.x + 1];
-    bool deferred = (L1 - L0) > NT;
+    bool deferred = (L1 - L0) > CR * NT;
     int cnt = 0;
     float cvmax = 0.f;
     if (!deferred) {
         // ---- candidates classified against the chunk box (exact fp64), compacted
-        const int ci = L0 + tid;
-        bool have = ci < L1, full = false;
-        int id = 0;
-        double c4[4] = {0, 0, 0, 0};
-        if (have) {
-            id = a.g.cand_ids[ci];
-            c4[0] = a.c.x[id];
-            c4[1] = a.c.y[id];
-            c4[2] = a.c.z[id];
-            c4[3] = a.c.t[id];
-            full = true;
+        bool have[CR], full[CR];
+        int id[CR];
+        double c4[CR][4];
+        unsigned bal[CR];
 #pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const double da = DSUB(c4[d], box[d]), db = DSUB(c4[d], box[4 + d]);   // da >= db
-                if (da < -Cd[d] || db > Cd[d]) have = false;    // no sample passes
-                if (!(da <= Cd[d] && db >= -Cd[d])) full = false;   // not every sample
+        for (int r = 0; r < CR; ++r) {
+            const int ci = L0 + tid + NT * r;
+            have[r] = ci < L1;
+            full[r] = false;
+            id[r] = 0;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) c4[r][d] = 0.0;
+            if (have[r]) {
+                id[r] = a.g.cand_ids[ci];
+                c4[r][0] = a.c.x[id[r]];
+                c4[r][1] = a.c.y[id[r]];
+                c4[r][2] = a.c.z[id[r]];
+                c4[r][3] = a.c.t[id[r]];
+                full[r] = true;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const double da = DSUB(c4[r][d], box[d]), db = DSUB(c4[r][d], box[4 + d]);   // da >= db
+                    if (da < -Cd[d] || db > Cd[d]) have[r] = false;    // no sample passes
+                    if (!(da <= Cd[d] && db >= -Cd[d])) full[r] = false;   // not every sample
+                }
+                if (!have[r]) full[r] = false;
             }
-            if (!have) full = false;
+            bal[r] = __ballot_sync(0xffffffffu, have[r]);
+            if (lane == 0) S.wc[r * NW + w] = __popc(bal[r]);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, have);
-        if (lane == 0) S.wc[w] = __popc(bal);
         __syncthreads();
-        int off = 0;
+        int off[CR];
 #pragma unroll
-        for (int q = 0; q < NW; ++q) {
-            off += q < w ? S.wc[q] : 0;
+        for (int r = 0; r < CR; ++r) off[r] = 0;
+#pragma unroll
+        for (int q = 0; q < CR * NW; ++q) {
+#pragma unroll
+            for (int r = 0; r < CR; ++r) off[r] += q < r * NW + w ? S.wc[q] : 0;
             cnt += S.wc[q];
         }
         deferred = cnt > CAP;
         float mycv = 0.f;
-        if (!deferred && have) {
-            const int p = off + __popc(bal & ((1u << lane) - 1u));
-            const bool chas = a.chas[id] != 0;
-            const double cv = chas ? a.cval[id] : 0.0;
-            S.id[p] = id;
-            S.c[p][0] = c4[0];
-            S.c[p][1] = c4[1];
-            S.c[p][2] = c4[2];
-            S.c[p][3] = c4[3];
-            S.c[p][4] = cv;
-            S.rc[p] = make_float4((float)DSUB(c4[0], S.ctx.o[0]), (float)DSUB(c4[1], S.ctx.o[1]),
-                                  (float)DSUB(c4[2], S.ctx.o[2]),
-                                  (float)DMUL(DSUB(c4[3], S.ctx.o[3]), a.cf));
-            S.cvf[p] = (float)cv;
-            S.wvf[p] = (USEVAL && chas) ? (float)a.wv : 0.f;
-            S.has[p] = chas;
-            S.full[p] = full;
-            if (USEVAL && chas) mycv = fabsf((float)cv);
+#pragma unroll
+        for (int r = 0; r < CR; ++r) {
+            if (!deferred && have[r]) {
+                const int p = off[r] + __popc(bal[r] & ((1u << lane) - 1u));
+                const bool chas = a.chas[id[r]] != 0;
+                const double cv = chas ? a.cval[id[r]] : 0.0;
+                S.id[p] = id[r];
+                S.c[p][0] = c4[r][0];
+                S.c[p][1] = c4[r][1];
+                S.c[p][2] = c4[r][2];
+                S.c[p][3] = c4[r][3];
+                S.c[p][4] = cv;
+                S.rc[p] = make_float4((float)DSUB(c4[r][0], S.ctx.o[0]), (float)DSUB(c4[r][1], S.ctx.o[1]),
+                                      (float)DSUB(c4[r][2], S.ctx.o[2]),
+                                      (float)DMUL(DSUB(c4[r][3], S.ctx.o[3]), a.cf));
+                S.cvf[p] = (float)cv;
+                S.wvf[p] = (USEVAL && chas) ? (float)a.wv : 0.f;
+                S.has[p] = chas;
+                S.full[p] = full[r];
+                if (USEVAL && chas) mycv = fmaxf(mycv, fabsf((float)cv));
+            }
         }
         if (USEVAL) {
             mycv = wmax_f(mycv);
