@@ -110,6 +110,27 @@ __device__ __forceinline__ float warp_max_f(float v) {
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
+// warp min / max by one REDUX: non-negative floats order like their bit
+// patterns; general floats through an order-preserving bit transform
+__device__ __forceinline__ float warp_min_nn(float v) {
+    return __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(v)));
+}
+__device__ __forceinline__ float warp_max_nn(float v) {
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
+}
+__device__ __forceinline__ unsigned f2ord(float v) {
+    const unsigned b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ float warp_min_any(float v) {
+    return ord2f(__reduce_min_sync(0xffffffffu, f2ord(v)));
+}
+__device__ __forceinline__ float warp_max_any(float v) {
+    return ord2f(__reduce_max_sync(0xffffffffu, f2ord(v)));
+}
 __device__ __forceinline__ __int128 get128(const unsigned long long *p) {
     return (__int128)(((unsigned __int128)p[1] << 64) | (unsigned __int128)p[0]);
 }
@@ -241,7 +262,7 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
             ubw = fminf(ubw, fmaf(fwd, sqrt_approx((qx.y + qy.y) + (qz.y + qt.y)), vth));
         }
     }
-    ubw = warp_min_f(ubw);
+    ubw = warp_min_nn(ubw);
     const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f) + C.slack;
     const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
     unsigned keep[4] = {0u, 0u, 0u, 0u};
@@ -339,7 +360,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 if (ub < INF_F) ubkey = min(ubkey, (__float_as_uint(ub) & ~SLOT_MASK) | (unsigned)s);
             }
         }
-        ubw = warp_min_f(ubw);
+        ubw = warp_min_nn(ubw);
         const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vwl), fabsf(vwh)) + cvmax) : 0.f) + slack;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
         unsigned keep[4] = {0u, 0u, 0u, 0u};
@@ -681,7 +702,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             if (USEVAL && chas) mycv = fabsf((float)cv);
         }
         if (USEVAL) {
-            mycv = warp_max_f(mycv);
+            mycv = warp_max_nn(mycv);
             if (lane == 0) S.red[w] = mycv;
         }
         __syncthreads();
@@ -752,8 +773,8 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                         hi = r.y;
                     }
                 }
-                vl = warp_min_f(lo);
-                vh = warp_max_f(hi);
+                vl = warp_min_any(lo);
+                vh = warp_max_any(hi);
             }
             nl = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, rbx, rby, vl, vh, a.debug)
                                 : region_list<USEVAL, 4>(S, C, rbx, rby, vl, vh, a.debug);
