@@ -644,6 +644,10 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.multi = P.multi;
         a.n_multi = P.counters + 4;
         a.multi_cap = P.multi_cap;
+        if (const char *mc = getenv("MFSEG_MULTI_CAP")) {   // test knob: a smaller brick queue
+            const long long cap = atoll(mc);
+            if (cap >= 0 && cap < a.multi_cap) a.multi_cap = cap;
+        }
         a.overflow = P.overflow;
         a.accumulate = accumulate;
         {

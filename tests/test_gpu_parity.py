@@ -481,6 +481,40 @@ def test_kernel_generations_agree(w_d, seed, monkeypatch):
     np.testing.assert_array_equal(pl, pl1)
 
 
+@pytest.mark.parametrize("env", [{"MFSEG_MULTI_CAP": "0"}, {"MFSEG_MULTI_CAP": "37"},
+                                 {"MFSEG_DEBUG": "2"}, {"MFSEG_DEBUG": "1"}])
+def test_field_brick_queue_paths_agree(env, monkeypatch):
+    """k_field_assign5 queues multi-candidate bricks for k_field_screen; a full
+    queue (capacity 0 or 37 items) sends the rest to the exact per-sample path
+    (k_deferred), MFSEG_DEBUG=2 resolves every queued sample in exact fp64 and
+    MFSEG_DEBUG=1 disables culling and dominance (most bricks then exceed the
+    16-candidate queue limit).  A 3-pass run: labels and centre positions
+    bit-identical (integer sums), field means within fp64 rounding (the value
+    sums are rounded per record or per sample depending on the path)."""
+    P = pkg()
+    dims, nt, ntraj = (64, 48, 40), 8, 2000
+    fld, pts, _ = _synthetic(dims, nt, ntraj, 31, False)
+    fs = P.FieldSet(dims, np.zeros(3), np.ones(3), fld.times.cpu().numpy(),
+                    fld.values.cpu().numpy().reshape(nt, -1))
+    ps = P.PointSet(np.zeros(pts.n, np.int64), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(),
+                    pts.value.cpu().numpy())
+    ext = P.domain_extent(ps, fs)
+    params = P.ClusterParams(k=(5, 4, 3, 2), w_d=0.3, max_iterations=2, eps_c=1e-12)
+    a = P.run(ps, fs, ext, params)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    b = P.run(ps, fs, ext, params)
+    np.testing.assert_array_equal(a.field_labels, b.field_labels)
+    np.testing.assert_array_equal(a.point_labels, b.point_labels)
+    assert [c.id for c in a.centers] == [c.id for c in b.centers]
+    for ca, cb in zip(a.centers, b.centers):
+        assert (ca.x_c, ca.y_c, ca.z_c, ca.t_c) == (cb.x_c, cb.y_c, cb.z_c, cb.t_c)
+        assert (ca.n_points, ca.n_fields, ca.p_c) == (cb.n_points, cb.n_fields, cb.p_c)
+        assert (ca.f_c is None) == (cb.f_c is None)
+        if ca.f_c is not None:
+            assert ca.f_c == pytest.approx(cb.f_c, rel=1e-12, abs=1e-15)
+
+
 @pytest.mark.parametrize("seed,n,n_traj,single_time", [(0, 5000, 300, False), (1, 200000, 7000, False),
                                                        (2, 1000, 50, True)])
 def test_traj_split_matches_numpy(seed, n, n_traj, single_time):
