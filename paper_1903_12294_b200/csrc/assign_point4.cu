@@ -597,6 +597,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         C.wvf = USEVAL ? (float)a.wv : 0.f;
         C.cnt = cnt;
         C.nrounds = (cnt + 31) >> 5;
+        if (a.debug & 8) atomicAdd(a.stats + 12 + min(C.nrounds, 3), 1ull);
         C.len = T.z;
         C.start = T.y;
         C.deferred = deferred;
