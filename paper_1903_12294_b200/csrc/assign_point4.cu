@@ -255,12 +255,14 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             const float vabs = fmaxf(fabsf(vl), fabsf(vh));
             const float vq = fmaxf(fabsf(vl - cvq), fabsf(vh - cvq));
             const float nd = C.ndelta;
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                if (keep[r] == 0u) continue;   // warp-uniform
+#pragma unroll 1
+            for (int r = 0; r < NR; ++r) {   // rolled: a small hot loop for the instruction cache
+                const unsigned kr = r == 0 ? keep[0] : r == 1 ? keep[1] : r == 2 ? keep[2] : keep[3];
+                if (kr == 0u) continue;   // warp-uniform
+                const float sa = r == 0 ? qhu[0] : r == 1 ? qhu[1] : r == 2 ? qhu[2] : qhu[3];
                 const int s = lane + 32 * r;
                 bool dom = false;
-                if ((keep[r] >> lane & 1u) && s != sdom) {
+                if ((kr >> lane & 1u) && s != sdom) {
                     const float4 rc = S.rc[s];
                     const float rcv[4] = {rc.x, rc.y, rc.z, rc.w};
                     float dS = 0.f;
@@ -270,7 +272,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                         const float bl = rqv[d] - wl[d], bh = rqv[d] - wh[d];
                         dS += fminf(fmaf(al, al, -bl * bl), fmaf(ah, ah, -bh * bh));
                     }
-                    const float sa = qhu[r], ra = sqrt_approx(sa);
+                    const float ra = sqrt_approx(sa);
                     const float dSlb = dS - nd * (ra + rb) * (1.f + 0x1.0p-20f) - 0.5f * nd * nd -
                                        0x1.0p-20f * (sa + sb);
                     if (dSlb > 0.f) {
@@ -286,7 +288,11 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                         dom = C.fwd * gap * (1.f - 0x1.0p-20f) > Vb + rel;
                     }
                 }
-                keep[r] &= ~__ballot_sync(0xffffffffu, dom);
+                const unsigned db = __ballot_sync(0xffffffffu, dom);
+                if (r == 0) keep[0] &= ~db;
+                else if (r == 1) keep[1] &= ~db;
+                else if (r == 2) keep[2] &= ~db;
+                else keep[3] &= ~db;
             }
         }
         if ((a.debug & 8) && lane == 0) {
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         C.wvf = USEVAL ? (float)a.wv : 0.f;
         C.cnt = cnt;
         C.nrounds = (cnt + 31) >> 5;
-        if (a.debug & 8) atomicAdd(a.stats + 12 + min(C.nrounds, 3), 1ull);
+        if (a.debug & 8) atomicAdd(a.stats + 11 + min(max(C.nrounds, 1), 4), 1ull);
         C.len = T.z;
         C.start = T.y;
         C.deferred = deferred;

@@ -765,7 +765,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                     rat(F[7], F[0]), rat(F[2], F[0]));
             fprintf(stderr, "[mfseg stats] point tiles single %.3f kept hist", rat(Q[3], Q[0]));
             for (int q = 0; q < 8; ++q) fprintf(stderr, " %.3f", rat(Q[4 + q], Q[0]));
-            fprintf(stderr, " | chunks by candidate rounds 0/1/2/3+: %llu %llu %llu %llu", Q[12], Q[13],
+            fprintf(stderr, " | chunks by candidate rounds 1/2/3/4: %llu %llu %llu %llu", Q[12], Q[13],
                     Q[14], Q[15]);
             fprintf(stderr, "\n");
         }
