@@ -332,14 +332,15 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         for (int r = 0; r < NR; ++r) scan[r] = keep[r];
 
         // ---- per-point screen, packed (d, slot) keys
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            unsigned it = scan[r];
+#pragma unroll 1
+        for (int r = 0; r < NR; ++r) {   // rolled: a small hot loop for the instruction cache
+            unsigned it = r == 0 ? scan[0] : r == 1 ? scan[1] : r == 2 ? scan[2] : scan[3];
+            const unsigned kf = r == 0 ? kfull[0] : r == 1 ? kfull[1] : r == 2 ? kfull[2] : kfull[3];
             while (it) {
                 const int b = __ffs(it) - 1, s = b + 32 * r;
                 it &= it - 1;
                 const float4 rc = S.rc[s];
-                const bool fl = (kfull[r] >> b) & 1u;
+                const bool fl = (kf >> b) & 1u;
                 float cvs = 0.f, wvs = 0.f;
                 if (USEVAL) {
                     cvs = S.cvf[s];
