@@ -239,11 +239,11 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int zg1 = (C.Z.len - 1) / GZ, tg1 = (C.T.len - 1) / GT;
     const float fwd = C.fwd, wvf = C.wvf;
-    float dl[4];
+    float dl[4] = {INF_F, INF_F, INF_F, INF_F};
     float ubw = INF_F;
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-        dl[r] = INF_F;
+#pragma unroll 1
+    for (int r = 0; r < NR; ++r) {   // rolled: smaller code next to the hot brick loop
+        float dlr = INF_F;
         const int s = lane + 32 * r;
         if (r < C.nrounds && s < C.cnt) {
             const float2 qx = S.qmm[s][rbx], qy = S.qmm[s][QY + rby];
@@ -258,9 +258,13 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
                     vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
                 }
             }
-            dl[r] = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
+            dlr = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
             ubw = fminf(ubw, fmaf(fwd, sqrt_approx((qx.y + qy.y) + (qz.y + qt.y)), vth));
         }
+        if (r == 0) dl[0] = dlr;
+        else if (r == 1) dl[1] = dlr;
+        else if (r == 2) dl[2] = dlr;
+        else dl[3] = dlr;
     }
     ubw = warp_min_nn(ubw);
     const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vl), fabsf(vh)) + C.cvmax) : 0.f) + C.slack;
