@@ -143,7 +143,7 @@ __global__ void k_point_keys(long long n, const double *xyz, const double *t, do
 
 // random gather of the points into bin-sorted SoA; 4 points per thread with
 // every load issued before the stores (memory-level parallelism)
-constexpr int GATHER_PER_THREAD = 8;
+constexpr int GATHER_PER_THREAD = 16;
 __global__ void k_point_gather(long long n, const unsigned *perm, const double *xyz,
                                const double *t, const double *value, double *px, double *py,
                                double *pz, double *pt, double *pv) {
