@@ -91,6 +91,7 @@ struct __align__(16) Smem5 {
     float red[NW];
     int lst[NW][32];                // per region: candidate slots that survive its cull
     int nlist[NW];                  // list lengths (-1: more than 32 survivors)
+    unsigned char bslot[64];        // reused bricks: slot of their label (255: recompute)
     Ctx ctx;
 };
 
@@ -291,6 +292,29 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
 // common case gets a smaller instruction footprint)
 // LIST: the candidates are the warp region's list S.lst[w][0..nlist) (one round,
 // bit b of a keep mask = list position b); otherwise slot = bit + 32 * round.
+// A whole brick labelled by one slot: the count marginals are constants and the
+// value sum is the brick's (fixed-order warp sum, computed once per run).
+__device__ __forceinline__ void single_brick_sums(const FieldArgs &a, Smem5 &S, size_t bidx, int one,
+                                                  int bx, int by, int bz, int bt) {
+    const int lane = threadIdx.x & 31;
+    unsigned *h = S.hist[one];
+    if (lane < 4) atomicAdd(&h[4 * bx + lane], 32u | (32u << 16));         // 8 x, 32 each
+    else if (lane < 6) atomicAdd(&h[8 + 2 * by + (lane - 4)], 64u | (64u << 16));   // 4 y
+    else if (lane < 8) atomicAdd(&h[16 + 2 * bz + (lane - 6)], 64u | (64u << 16));  // 4 z
+    else if (lane == 8) atomicAdd(&h[24 + bt], 128u | (128u << 16));      // 2 timesteps
+    else if (lane == 9) atomicAdd(&h[26], 256u);
+    else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
+        const ulonglong2 vs = a.bsum[bidx];
+        const int q = lane - 10;
+        const unsigned long long lo = vs.x, hi = vs.y;
+        const unsigned long long bits = q < 2 ? lo >> (24 * q)
+                                      : q == 2 ? (lo >> 48) | (hi << 16)
+                                               : hi >> (24 * q - 64);
+        atomicAdd(&S.vlimb[one][q], q < 5 ? (unsigned)(bits & 0xFFFFFFu) : (unsigned)(bits & 0xFFu) |
+                                                ((bits & 0x80u) ? 0xFFFFFF00u : 0u));
+    }
+}
+
 template <bool USEVAL, bool FULL, int NR, bool LIST>
 __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bi, int bx,
                                       int by, int bz, int bt, int region, int nlist, int &ovf_local) {
@@ -507,25 +531,9 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
+        if (FULL && lane == 0 && a.bslot) a.bslot[bidx] = (unsigned char)one;
         if (a.accumulate && FULL) {
-            // whole brick -> one cluster: the count marginals are constants and the
-            // value sum is the brick's (fixed-order warp sum, computed once per run)
-            const ulonglong2 vs = a.bsum[bidx];
-            unsigned *h = S.hist[one];
-            if (lane < 4) atomicAdd(&h[4 * bx + lane], 32u | (32u << 16));         // 8 x, 32 each
-            else if (lane < 6) atomicAdd(&h[8 + 2 * by + (lane - 4)], 64u | (64u << 16));   // 4 y
-            else if (lane < 8) atomicAdd(&h[16 + 2 * bz + (lane - 6)], 64u | (64u << 16));  // 4 z
-            else if (lane == 8) atomicAdd(&h[24 + bt], 128u | (128u << 16));      // 2 timesteps
-            else if (lane == 9) atomicAdd(&h[26], 256u);
-            else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
-                const int q = lane - 10;
-                const unsigned long long lo = vs.x, hi = vs.y;
-                const unsigned long long bits = q < 2 ? lo >> (24 * q)
-                                              : q == 2 ? (lo >> 48) | (hi << 16)
-                                                       : hi >> (24 * q - 64);
-                atomicAdd(&S.vlimb[one][q], q < 5 ? (unsigned)(bits & 0xFFFFFFu) : (unsigned)(bits & 0xFFu) |
-                                                        ((bits & 0x80u) ? 0xFFFFFF00u : 0u));
-            }
+            single_brick_sums(a, S, bidx, one, bx, by, bz, bt);
             return;
         }
         if (!a.accumulate) return;
@@ -716,7 +724,28 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         }
     }
 
-    if (!deferred && cnt > 0) {
+    // ---- reuse: in a stable block (no candidate changed since the last pass) a
+    // brick labelled by one slot then keeps its labels; the tables and region
+    // lists are built only if some brick must be recomputed
+    const bool stable = a.reuse && !deferred && cnt > 0 && a.bin_stable[sbin];
+    bool need_full = true;
+    if (stable) {
+        int need = 0;
+        if (tid < 64) {
+            const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
+            const unsigned char sl = a.bslot[(size_t)blockIdx.x * 64 + tid];
+            S.bslot[tid] = sl;
+            need = sl == 255 && !(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len ||
+                                  GT * bt >= Tm.len);
+        }
+        need_full = __syncthreads_or(need) != 0;
+    }
+    if (!deferred && cnt > 0 && !need_full && a.accumulate) {
+        for (int e = tid; e < cnt * HW; e += NT) (&S.hist[0][0])[e] = 0u;
+        for (int e = tid; e < cnt * 6; e += NT) (&S.vlimb[0][0])[e] = 0u;
+        __syncthreads();
+    }
+    if (!deferred && cnt > 0 && need_full) {
         // ---- fp32 tables + group (min, max): one (axis, candidate) row per thread
         for (int j = tid; j < 4 * cnt; j += NT) {
             const int ax = j / cnt, p = j - ax * cnt;   // axis-major: warps stay on one axis
@@ -764,7 +793,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     {
         int nl = -1;
         const int rbx = w & 1, rby = (w >> 1) & 3;
-        if (!deferred && cnt > 0 && GX * rbx < X.len && GY * rby < Y.len) {
+        if (!deferred && cnt > 0 && need_full && GX * rbx < X.len && GY * rby < Y.len) {
             float vl = 0.f, vh = 0.f;
             if (USEVAL) {   // value range of the region = union of its bricks' ranges
                 float lo = INF_F, hi = -INF_F;
@@ -801,6 +830,15 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len &&
                               GZ * bz + GZ <= Z.len && GT * bt + GT <= Tm.len;
             const int region = bi & 7, nl = S.nlist[region];
+            const size_t bidx = (size_t)blockIdx.x * 64 + bi;
+            if (stable && S.bslot[bi] != 255) {
+                // unchanged since the last pass: labels stay, sums are constants
+                if (a.accumulate) single_brick_sums(a, S, bidx, S.bslot[bi], bx, by, bz, bt);
+                if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
+                bi += NW;
+                continue;
+            }
+            if (lane == 0 && a.bslot) a.bslot[bidx] = 255;
             if (nl >= 0) {
                 if (full)
                     brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nl, ovf_local);

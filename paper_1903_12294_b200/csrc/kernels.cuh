@@ -51,6 +51,12 @@ struct FieldArgs {
     MultiItem *multi;            // queue of bricks for k_field_screen (capacity: all bricks)
     unsigned long long *n_multi;
     long long multi_cap;
+    // reuse of the previous pass: a block whose 3^4 neighbour bins hold no
+    // centre changed by the last update (bin_stable) keeps the labels of its
+    // single-candidate bricks (bslot: slot, 255 = none)
+    const unsigned char *bin_stable;
+    unsigned char *bslot;
+    int reuse;
 };
 
 struct WBox {                 // one 64-point warp tile of a point chunk (k_point_assign4)

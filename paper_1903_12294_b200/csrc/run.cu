@@ -293,6 +293,8 @@ struct Plan {
     ulonglong2 *bsum;               // per brick value sum, fixed point (field v5)
     MultiItem *multi;               // multi-candidate bricks for k_field_screen
     long long multi_cap;
+    unsigned char *bslot;           // per brick: slot of its single label last pass (255: none)
+    unsigned char *bmark, *bstable; // per sample bin: changed centres / stable neighbourhood
     long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
@@ -377,7 +379,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.flags = cv.take<char>(update_flags_bytes());
     int NB = P.NB;
     P.g = grid_carve(cv, K, NB, &P.count_tmp, &P.grid_scan_tmp);
-    P.counters = cv.take<unsigned long long>(32);   // [8..32): debug stats
+    P.counters = cv.take<unsigned long long>(40);   // [8..40): debug stats
     P.overflow = cv.take<int>(4);
     // field
     P.nf = (P.f.nt > 0) ? (long long)P.f.nx * P.f.ny * P.f.nz * P.f.nt : 0;
@@ -403,7 +405,10 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         const long long bricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
         P.multi_cap = P.nf > 0 ? (bricks < (1ll << 21) ? bricks : (1ll << 21)) : 0;
         P.multi = cv.take<MultiItem>(P.multi_cap);
+        P.bslot = cv.take<unsigned char>(P.nf > 0 ? bricks : 0);
     }
+    P.bmark = cv.take<unsigned char>(P.nf > 0 ? NB : 0);
+    P.bstable = cv.take<unsigned char>(P.nf > 0 ? NB : 0);
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     P.deferred_f = cv.take<long long>(P.cap_f);
@@ -528,6 +533,9 @@ int plan_prepare(Plan &P) {
             va.overflow = P.overflow;
             MFSEG_TRY(launch_brick_pre(va, st));
         }
+        if (P.bslot)
+            MFSEG_CUDA(cudaMemsetAsync(P.bslot, 255,
+                                       64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1), st));
     }
     long long n = P.np;
     if (n > 0) {
@@ -581,9 +589,61 @@ CentersView view_of(const mfseg_centers &s, int K) {
     return v;
 }
 
-// one assignment pass for centre state `c` (grid rebuilt here)
+// Centres changed by the last update (position, field value or its presence,
+// bitwise): mark the sample bins they left and entered.
+__global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, double4 mins, double4 C,
+                               int4 k, unsigned char *mark) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= K) return;
+    bool ch = cur.has_f[c] != old.has_f[c] ||
+              __double_as_longlong(cur.fval[c]) != __double_as_longlong(old.fval[c]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        ch |= __double_as_longlong(cur.loc[(size_t)q * K + c]) != __double_as_longlong(old.loc[(size_t)q * K + c]);
+    if (!ch) return;
+    const double mn[4] = {mins.x, mins.y, mins.z, mins.w}, CC[4] = {C.x, C.y, C.z, C.w};
+    const int kk[4] = {k.x, k.y, k.z, k.w};
+    int bn[4], bo[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        bn[q] = bin_coord(cur.loc[(size_t)q * K + c], mn[q], CC[q], kk[q]);
+        bo[q] = bin_coord(old.loc[(size_t)q * K + c], mn[q], CC[q], kk[q]);
+    }
+    mark[((bn[3] * k.z + bn[2]) * k.y + bn[1]) * k.x + bn[0]] = 1;
+    mark[((bo[3] * k.z + bo[2]) * k.y + bo[1]) * k.x + bo[0]] = 1;
+}
+
+// A sample bin is stable when none of its 3^4 neighbour bins is marked: its
+// candidate list and every candidate's state equal the last pass's.
+__global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned char *stable) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= NB) return;
+    int r = b;
+    const int bx = r % k.x;
+    r /= k.x;
+    const int by = r % k.y;
+    r /= k.y;
+    const int bz = r % k.z;
+    const int bt = r / k.z;
+    bool ok = true;
+    for (int dt = -1; dt <= 1; ++dt)
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int qx = bx + dx, qy = by + dy, qz = bz + dz, qt = bt + dt;
+                    if (qx < 0 || qy < 0 || qz < 0 || qt < 0 || qx >= k.x || qy >= k.y || qz >= k.z ||
+                        qt >= k.w)
+                        continue;
+                    ok = ok && !mark[((qt * k.z + qz) * k.y + qy) * k.x + qx];
+                }
+    stable[b] = ok;
+}
+
+// one assignment pass for centre state `c` (grid rebuilt here); `prev`: the
+// state of the previous pass when it used the same weights (labels of stable
+// field blocks are reused), else null
 int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, int32_t *flabels,
-              int accumulate) {
+              int accumulate, const mfseg_centers *prev) {
     cudaStream_t st = P.st;
     const mfseg_params &p = P.p;
     int K = P.K;
@@ -592,7 +652,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
                          P.count_tmp, P.grid_scan_tmp, st));
     mark(1, st);
-    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 32, st));
+    MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 40, st));
     if (accumulate)
         MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
     if (P.nf > 0) {
@@ -644,6 +704,23 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.multi = P.multi;
         a.n_multi = P.counters + 4;
         a.multi_cap = P.multi_cap;
+        a.bslot = field_version() == 5 ? P.bslot : nullptr;
+        const bool no_reuse = getenv("MFSEG_NO_REUSE") != nullptr;
+        if (prev && a.bslot && accumulate && !no_reuse) {
+            const int NB = P.NB;
+            MFSEG_CUDA(cudaMemsetAsync(P.bmark, 0, NB, st));
+            ::mfseg::count_launch();
+            k_mark_changed<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(
+                K, c, *prev, make_double4(p.mins[0], p.mins[1], p.mins[2], p.mins[3]),
+                make_double4(p.C[0], p.C[1], p.C[2], p.C[3]), make_int4(p.k[0], p.k[1], p.k[2], p.k[3]),
+                P.bmark);
+            ::mfseg::count_launch();
+            k_bin_stable<<<(unsigned)((NB + 255) / 256), 256, 0, st>>>(
+                NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable);
+            MFSEG_LAUNCH("stable bins");
+            a.reuse = 1;
+            a.bin_stable = P.bstable;
+        }
         if (const char *mc = getenv("MFSEG_MULTI_CAP")) {   // test knob: a smaller brick queue
             const long long cap = atoll(mc);
             if (cap >= 0 && cap < a.multi_cap) a.multi_cap = cap;
@@ -750,7 +827,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     mark(4, st);
     if (const char *dbg = getenv("MFSEG_DEBUG")) {
         if (atoi(dbg) & 8) {
-            unsigned long long h[32];
+            unsigned long long h[40];
             MFSEG_CUDA(cudaMemcpyAsync(h, P.counters, sizeof h, cudaMemcpyDeviceToHost, st));
             MFSEG_CUDA(cudaStreamSynchronize(st));
             const unsigned long long *F = h + 8, *Q = h + 16;
@@ -761,8 +838,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                     "exact %llu | stranded f %llu p %llu deferred f %llu p %llu\n",
                     F[0], rat(F[1], F[0]), F[2], rat(F[3], F[0]), F[4], rat(F[5], F[4]), rat(F[6], F[5]),
                     Q[0], rat(Q[1], Q[0]), Q[2], h[0], h[1], h[2], h[3]);
-            fprintf(stderr, "[mfseg stats] field bricks: kept after cull %.3f, single after cull %.3f\n",
-                    rat(F[7], F[0]), rat(F[2], F[0]));
+            fprintf(stderr, "[mfseg stats] field bricks: kept after cull %.3f, single after cull %.3f, "
+                    "reused %llu\n", rat(F[7], F[0]), rat(F[2], F[0]), h[32]);
             fprintf(stderr, "[mfseg stats] point tiles single %.3f kept hist", rat(Q[3], Q[0]));
             for (int q = 0; q < 8; ++q) fprintf(stderr, " %.3f", rat(Q[4 + q], Q[0]));
             fprintf(stderr, " | chunks by candidate rounds 1/2/3/4: %llu %llu %llu %llu", Q[12], Q[13],
@@ -860,7 +937,8 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
         bool initial = pass == 0;
         // initial assignment: pure space-time nearest seed (engine.py:346-351)
         double wd = initial ? 1.0 : p->w_d, wp = initial ? 0.0 : p->w_p, wf = initial ? 0.0 : p->w_f;
-        MFSEG_TRY(plan_pass(P, P.s[cur], wd, wp, wf, field_labels, 1));
+        // from the second weighted pass on, stable field blocks reuse the last labels
+        MFSEG_TRY(plan_pass(P, P.s[cur], wd, wp, wf, field_labels, 1, pass >= 2 ? &P.s[cur ^ 1] : nullptr));
         if (reduce) {
             long long npairs = (long long)K * MFSEG_ACC_WORDS / 2;
             MFSEG_TRY(launch_to_limbs(npairs, P.acc, P.limbs, st));
@@ -911,7 +989,7 @@ int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
     MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
     MFSEG_TRY(plan_prepare(P));
-    MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1));
+    MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr));
     if (P.np > 0) {
         ::mfseg::count_launch();
         k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,

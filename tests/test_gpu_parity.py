@@ -482,14 +482,17 @@ def test_kernel_generations_agree(w_d, seed, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"MFSEG_MULTI_CAP": "0"}, {"MFSEG_MULTI_CAP": "37"},
-                                 {"MFSEG_DEBUG": "2"}, {"MFSEG_DEBUG": "1"}])
+                                 {"MFSEG_DEBUG": "2"}, {"MFSEG_DEBUG": "1"},
+                                 {"MFSEG_NO_REUSE": "1"}])
 def test_field_brick_queue_paths_agree(env, monkeypatch):
     """k_field_assign5 queues multi-candidate bricks for k_field_screen; a full
     queue (capacity 0 or 37 items) sends the rest to the exact per-sample path
     (k_deferred), MFSEG_DEBUG=2 resolves every queued sample in exact fp64 and
     MFSEG_DEBUG=1 disables culling and dominance (most bricks then exceed the
-    16-candidate queue limit).  A 3-pass run: labels and centre positions
-    bit-identical (integer sums), field means within fp64 rounding (the value
+    16-candidate queue limit); MFSEG_NO_REUSE=1 recomputes the blocks whose
+    candidates did not change since the last pass.  A 6-pass run: labels and
+    centre positions bit-identical (integer sums), field means within fp64
+    rounding (the value
     sums are rounded per record or per sample depending on the path)."""
     P = pkg()
     dims, nt, ntraj = (64, 48, 40), 8, 2000
@@ -499,7 +502,7 @@ def test_field_brick_queue_paths_agree(env, monkeypatch):
     ps = P.PointSet(np.zeros(pts.n, np.int64), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(),
                     pts.value.cpu().numpy())
     ext = P.domain_extent(ps, fs)
-    params = P.ClusterParams(k=(5, 4, 3, 2), w_d=0.3, max_iterations=2, eps_c=1e-12)
+    params = P.ClusterParams(k=(5, 4, 3, 2), w_d=0.3, max_iterations=5, eps_c=1e-12)
     a = P.run(ps, fs, ext, params)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
