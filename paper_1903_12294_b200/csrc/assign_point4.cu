@@ -53,6 +53,7 @@ struct PCtx {
     int cnt, nrounds, len;
     long long start;
     bool deferred;
+    bool stable;                    // no candidate changed since the last pass
 };
 
 struct __align__(16) PSmem4 {
@@ -154,6 +155,19 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     // the points do not change between passes).
     double P0[5] = {0, 0, 0, 0, 0}, P1[5] = {0, 0, 0, 0, 0};
     const WBox *wbp = a.wbox + (size_t)blockIdx.x * (POINT_CHUNK / 64) + wt;
+    const size_t tidx = (size_t)blockIdx.x * (POINT_CHUNK / 64) + wt;
+    if (C.stable) {   // unchanged since the last pass: a tile with one label keeps it
+        const unsigned char ts = a.tslot[tidx];
+        if (ts != 255) {
+            if (a.accumulate && lane == 0) {
+#pragma unroll
+                for (int d = 0; d < 5; ++d) S.wsum[w][d][ts] = DADD(S.wsum[w][d][ts], wbp->s[d]);
+                atomicAdd(&S.n[ts], (unsigned)min(64, C.len - 64 * wt));
+            }
+            return;
+        }
+    }
+    if (lane == 0 && a.tslot) a.tslot[tidx] = 255;
     int sl0 = -1, sl1 = -1;
     int one = -1;   // slot labelling the whole tile (warp-uniform)
     if (!C.deferred && C.cnt > 0) {
@@ -312,6 +326,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             sl0 = live0 ? sdom : -1;
             sl1 = live1 ? sdom : -1;
             one = sdom;
+            if (lane == 0 && a.tslot) a.tslot[tidx] = (unsigned char)sdom;
         } else {
         if (live0) {
             P0[0] = a.x[p0]; P0[1] = a.y[p0]; P0[2] = a.z[p0]; P0[3] = a.t[p0]; P0[4] = a.v[p0];
@@ -608,6 +623,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         C.len = T.z;
         C.start = T.y;
         C.deferred = deferred;
+        C.stable = a.reuse && !deferred && cnt > 0 && a.bin_stable[T.x];
     }
     __syncthreads();
     const PCtx &C = S.ctx;

@@ -92,6 +92,10 @@ struct PointArgs {
     int accumulate;
     int debug;
     unsigned long long *stats;   // debug bit3: [0] warp tiles, [1] kept candidates, [2] exact points
+    // reuse (as FieldArgs): per warp tile the slot of its single label last pass (255: none)
+    const unsigned char *bin_stable;
+    unsigned char *tslot;
+    int reuse;
 };
 
 // Stranded-sample fallback (engine.py:195-205): field samples (kind 1) are

@@ -295,6 +295,7 @@ struct Plan {
     long long multi_cap;
     unsigned char *bslot;           // per brick: slot of its single label last pass (255: none)
     unsigned char *bmark, *bstable; // per sample bin: changed centres / stable neighbourhood
+    unsigned char *tslot;           // per point warp tile: slot of its single label last pass
     long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
@@ -407,8 +408,8 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         P.multi = cv.take<MultiItem>(P.multi_cap);
         P.bslot = cv.take<unsigned char>(P.nf > 0 ? bricks : 0);
     }
-    P.bmark = cv.take<unsigned char>(P.nf > 0 ? NB : 0);
-    P.bstable = cv.take<unsigned char>(P.nf > 0 ? NB : 0);
+    P.bmark = cv.take<unsigned char>(NB);
+    P.bstable = cv.take<unsigned char>(NB);
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     P.deferred_f = cv.take<long long>(P.cap_f);
@@ -444,6 +445,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tiles = cv.take<int4>(P.max_tiles);
     P.tbox = cv.take<double>(8 * P.max_tiles);
     P.wbox = cv.take<WBox>(P.max_tiles * (POINT_CHUNK / 64));
+    P.tslot = cv.take<unsigned char>(P.max_tiles * (POINT_CHUNK / 64));
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
     P.deferred_p = cv.take<long long>(P.cap_p);
@@ -572,6 +574,7 @@ int plan_prepare(Plan &P) {
         if (point_version() == 4)
             MFSEG_TRY(launch_tile_box(P.tiles, P.tstart + NG, P.max_tiles, P.px, P.py, P.pz, P.pt,
                                       P.pv, p.c_f, P.tbox, P.wbox, st));
+        MFSEG_CUDA(cudaMemsetAsync(P.tslot, 255, P.max_tiles * (POINT_CHUNK / 64), st));
     }
     return 0;
 }
@@ -589,14 +592,15 @@ CentersView view_of(const mfseg_centers &s, int K) {
     return v;
 }
 
-// Centres changed by the last update (position, field value or its presence,
-// bitwise): mark the sample bins they left and entered.
+// Centres changed by the last update (position, point or field value or their
+// presence, bitwise): mark the sample bins they left and entered.
 __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, double4 mins, double4 C,
                                int4 k, unsigned char *mark) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= K) return;
-    bool ch = cur.has_f[c] != old.has_f[c] ||
-              __double_as_longlong(cur.fval[c]) != __double_as_longlong(old.fval[c]);
+    bool ch = cur.has_f[c] != old.has_f[c] || cur.has_p[c] != old.has_p[c] ||
+              __double_as_longlong(cur.fval[c]) != __double_as_longlong(old.fval[c]) ||
+              __double_as_longlong(cur.pval[c]) != __double_as_longlong(old.pval[c]);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         ch |= __double_as_longlong(cur.loc[(size_t)q * K + c]) != __double_as_longlong(old.loc[(size_t)q * K + c]);
@@ -653,6 +657,21 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                          P.count_tmp, P.grid_scan_tmp, st));
     mark(1, st);
     MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 40, st));
+    // reuse of the previous pass: sample bins whose candidates did not change
+    const bool reuse = prev && accumulate && getenv("MFSEG_NO_REUSE") == nullptr;
+    if (reuse) {
+        const int NB = P.NB;
+        MFSEG_CUDA(cudaMemsetAsync(P.bmark, 0, NB, st));
+        ::mfseg::count_launch();
+        k_mark_changed<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(
+            K, c, *prev, make_double4(p.mins[0], p.mins[1], p.mins[2], p.mins[3]),
+            make_double4(p.C[0], p.C[1], p.C[2], p.C[3]), make_int4(p.k[0], p.k[1], p.k[2], p.k[3]),
+            P.bmark);
+        ::mfseg::count_launch();
+        k_bin_stable<<<(unsigned)((NB + 255) / 256), 256, 0, st>>>(
+            NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable);
+        MFSEG_LAUNCH("stable bins");
+    }
     if (accumulate)
         MFSEG_CUDA(cudaMemsetAsync(P.acc, 0, sizeof(unsigned long long) * K * MFSEG_ACC_WORDS, st));
     if (P.nf > 0) {
@@ -705,19 +724,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.n_multi = P.counters + 4;
         a.multi_cap = P.multi_cap;
         a.bslot = field_version() == 5 ? P.bslot : nullptr;
-        const bool no_reuse = getenv("MFSEG_NO_REUSE") != nullptr;
-        if (prev && a.bslot && accumulate && !no_reuse) {
-            const int NB = P.NB;
-            MFSEG_CUDA(cudaMemsetAsync(P.bmark, 0, NB, st));
-            ::mfseg::count_launch();
-            k_mark_changed<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(
-                K, c, *prev, make_double4(p.mins[0], p.mins[1], p.mins[2], p.mins[3]),
-                make_double4(p.C[0], p.C[1], p.C[2], p.C[3]), make_int4(p.k[0], p.k[1], p.k[2], p.k[3]),
-                P.bmark);
-            ::mfseg::count_launch();
-            k_bin_stable<<<(unsigned)((NB + 255) / 256), 256, 0, st>>>(
-                NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable);
-            MFSEG_LAUNCH("stable bins");
+        if (reuse && a.bslot) {
             a.reuse = 1;
             a.bin_stable = P.bstable;
         }
@@ -769,6 +776,11 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.n_deferred = P.counters + 3;
         a.stats = P.counters + 16;
         a.deferred_cap = P.cap_p;
+        a.tslot = point_version() == 4 ? P.tslot : nullptr;
+        if (reuse && a.tslot) {
+            a.reuse = 1;
+            a.bin_stable = P.bstable;
+        }
         a.overflow = P.overflow;
         a.accumulate = accumulate;
         {
