@@ -165,25 +165,25 @@ template <int N, int G>
 __device__ __forceinline__ void table_row(float *e, float2 *mm, const double *coord, double cc,
                                           double scale, bool scaled, unsigned lo, unsigned hi,
                                           int len) {
-    float mn = INF_F, mx = 0.0f;
+#pragma unroll 1
+    for (int g = 0; g < N / G; ++g) {   // rolled over groups: small setup code (I-cache)
+        float mn = INF_F, mx = 0.0f;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-        float val = INF_F;
-        if ((unsigned)i >= lo && (unsigned)i <= hi) {
-            double d = DSUB(cc, coord[i]);
-            if (scaled) d = DMUL(scale, d);
-            val = to_f(DMUL(d, d));
+        for (int j = 0; j < G; ++j) {
+            const int i = g * G + j;
+            float val = INF_F;
+            if ((unsigned)i >= lo && (unsigned)i <= hi) {
+                double d = DSUB(cc, coord[i]);
+                if (scaled) d = DMUL(scale, d);
+                val = to_f(DMUL(d, d));
+            }
+            e[i] = val;
+            if (i < len) {
+                mn = fminf(mn, val);
+                mx = fmaxf(mx, val);
+            }
         }
-        e[i] = val;
-        if (i < len) {
-            mn = fminf(mn, val);
-            mx = fmaxf(mx, val);
-        }
-        if (i % G == G - 1) {
-            mm[i / G] = make_float2(mn, mx);
-            mn = INF_F;
-            mx = 0.0f;
-        }
+        mm[g] = make_float2(mn, mx);
     }
 }
 
