@@ -864,18 +864,12 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             if (n == 0) continue;
             unsigned long long *dst = a.acc + (size_t)S.id[s] * MFSEG_ACC_WORDS;
             __int128 acc = 0;
-            if (wd == 0) {
-#pragma unroll
-                for (int i = 0; i < BX; ++i) acc += get128(S.xf[i]) * (__int128)hget(h, i);
-            } else if (wd == 1) {
-#pragma unroll
-                for (int i = 0; i < BY; ++i) acc += get128(S.yf[i]) * (__int128)hget(h + 8, i);
-            } else if (wd == 2) {
-#pragma unroll
-                for (int i = 0; i < BZ; ++i) acc += get128(S.zf[i]) * (__int128)hget(h + 16, i);
-            } else if (wd == 3) {
-#pragma unroll
-                for (int i = 0; i < BT; ++i) acc += get128(S.tf[i]) * (__int128)hget(h + 24, i);
+            if (wd < 4) {   // one rolled loop for the four axes (small code)
+                static_assert(BX == BY && BY == BZ, "x, y, z marginals share one loop");
+                const unsigned long long(*F)[2] = wd == 0 ? S.xf : wd == 1 ? S.yf : wd == 2 ? S.zf : S.tf;
+                const int nn = wd == 3 ? BT : BX;
+#pragma unroll 4
+                for (int i = 0; i < nn; ++i) acc += get128(F[i]) * (__int128)hget(h + 8 * wd, i);
             } else if (wd == 4) {
                 acc = value_limbs_total(S.vlimb[s]);
             } else {
