@@ -235,10 +235,9 @@ __device__ __forceinline__ float2 gmm(const float2 *m, int g0, int g1) {
 // best fully valid candidate on every sample of every brick of the region.
 // Returns the list length, or -1 when more than 32 survive.
 template <bool USEVAL, int NR>
-__device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int rby, float vl, float vh,
-                                           int debug) {
+__device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int rby, int zg0, int zg1,
+                                           int tg0, int tg1, float vl, float vh, int debug) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int zg1 = (C.Z.len - 1) / GZ, tg1 = (C.T.len - 1) / GT;
     const float fwd = C.fwd, wvf = C.wvf;
     float dl[4] = {INF_F, INF_F, INF_F, INF_F};
     float ubw = INF_F;
@@ -248,7 +247,7 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
         const int s = lane + 32 * r;
         if (r < C.nrounds && s < C.cnt) {
             const float2 qx = S.qmm[s][rbx], qy = S.qmm[s][QY + rby];
-            const float2 qz = gmm(S.qmm[s] + QZ, 0, zg1), qt = gmm(S.qmm[s] + QT, 0, tg1);
+            const float2 qz = gmm(S.qmm[s] + QZ, zg0, zg1), qt = gmm(S.qmm[s] + QT, tg0, tg1);
             float vtl = 0.0f, vth = 0.0f;
             if (USEVAL) {
                 const float wvs = S.wvf[s];
@@ -313,6 +312,32 @@ __device__ __forceinline__ void single_brick_sums(const FieldArgs &a, Smem5 &S, 
         atomicAdd(&S.vlimb[one][q], q < 5 ? (unsigned)(bits & 0xFFFFFFu) : (unsigned)(bits & 0xFFu) |
                                                 ((bits & 0x80u) ? 0xFFFFFF00u : 0u));
     }
+}
+
+// Every sample of a brick to the exact per-sample path (k_deferred, label -2).
+__device__ __forceinline__ void defer_brick(const FieldArgs &a, const Ctx &C, int bx, int by, int bz, int bt) {
+    const int lane = threadIdx.x & 31;
+    const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
+    const int z0 = GZ * bz, t0 = GT * bt;
+    const long long fbase = (((long long)(C.T.start + t0) * a.nz + C.Z.start + z0) * a.ny +
+                             (C.Y.start + ly)) * (long long)a.nx + (C.X.start + lx);
+    unsigned livem = 0;
+    if (lx < C.X.len && ly < C.Y.len) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (z0 + (k & 3) < C.Z.len && t0 + (k >> 2) < C.T.len) livem |= 1u << k;
+    }
+    int *lab_base = a.labels + fbase;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (livem >> k & 1) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = -2;
+    long long p = warp_reserve(a.n_deferred, __popc(livem));
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (livem >> k & 1) {
+            if (p < a.deferred_cap) a.deferred[p] = fbase + (k & 3) * C.plane + (k >> 2) * C.vol;
+            ++p;
+        }
 }
 
 template <bool USEVAL, bool FULL, int NR, bool LIST>
@@ -809,8 +834,9 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 vl = warp_min_any(lo);
                 vh = warp_max_any(hi);
             }
-            nl = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, rbx, rby, vl, vh, a.debug)
-                                : region_list<USEVAL, 4>(S, C, rbx, rby, vl, vh, a.debug);
+            const int zg1 = (Z.len - 1) / GZ, tg1 = (Tm.len - 1) / GT;
+            nl = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, rbx, rby, 0, zg1, 0, tg1, vl, vh, a.debug)
+                                : region_list<USEVAL, 4>(S, C, rbx, rby, 0, zg1, 0, tg1, vl, vh, a.debug);
             if ((a.debug & 8) && lane == 0) {
                 atomicAdd(a.stats + 4, 1ull);
                 if (nl >= 0) {
@@ -839,16 +865,26 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 continue;
             }
             if (lane == 0 && a.bslot) a.bslot[bidx] = 255;
-            if (nl >= 0) {
+            int nlb = nl;
+            if (nl < 0) {
+                // more than 32 survivors in the region: a list for this brick alone
+                // (one code path for every brick keeps the hot code small)
+                float vl = 0.f, vh = 0.f;
+                if (USEVAL) {
+                    const float2 r = a.brange[bidx];
+                    vl = r.x;
+                    vh = r.y;
+                }
+                nlb = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, bx, by, bz, bz, bt, bt, vl, vh, a.debug)
+                                     : region_list<USEVAL, 4>(S, C, bx, by, bz, bz, bt, bt, vl, vh, a.debug);
+            }
+            if (nlb >= 0) {
                 if (full)
-                    brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nl, ovf_local);
+                    brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb, ovf_local);
                 else
-                    brick<USEVAL, false, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nl, ovf_local);
+                    brick<USEVAL, false, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb, ovf_local);
             } else {
-                if (full)
-                    brick<USEVAL, true, 4, false>(a, S, C, bi, bx, by, bz, bt, region, 0, ovf_local);
-                else
-                    brick<USEVAL, false, 4, false>(a, S, C, bi, bx, by, bz, bt, region, 0, ovf_local);
+                defer_brick(a, C, bx, by, bz, bt);   // > 32 survivors in one brick: exact path
             }
         }
         bi += NW;
