@@ -518,6 +518,31 @@ def test_field_brick_queue_paths_agree(env, monkeypatch):
             assert ca.f_c == pytest.approx(cb.f_c, rel=1e-12, abs=1e-15)
 
 
+def test_reuse_of_unchanged_blocks_is_exact(monkeypatch):
+    """A 10-iteration run on a mid-size case where, in the later passes, many
+    field blocks and point chunks have no changed candidate and reuse the
+    previous pass's labels: labels and centres must equal a run that recomputes
+    everything (MFSEG_NO_REUSE)."""
+    P = pkg()
+    from paper_1903_12294_b200.engine import run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
+    dims, nt, ntraj = (128, 96, 64), 24, 20000
+    fld, pts, _ = _synthetic(dims, nt, ntraj, 5, False, n_blobs=3)
+    normalize_device(pts, fld, True)
+    ext = domain_extent_device(pts, fld)
+    params = P.ClusterParams(k=(8, 6, 4, 6), eps_c=1e-12, max_iterations=10)
+    a = run_device(pts, fld, ext, params)
+    monkeypatch.setenv("MFSEG_NO_REUSE", "1")
+    b = run_device(pts, fld, ext, params)
+    assert a.iterations_used == b.iterations_used
+    assert torch.equal(a.field_labels, b.field_labels)
+    assert torch.equal(a.point_labels, b.point_labels)
+    sa, sb = P.CenterState.from_device(a.state), P.CenterState.from_device(b.state)
+    np.testing.assert_array_equal(np.asarray(sa.loc), np.asarray(sb.loc))
+    np.testing.assert_array_equal(np.asarray(sa.fval), np.asarray(sb.fval))
+    np.testing.assert_array_equal(np.asarray(sa.pval), np.asarray(sb.pval))
+
+
 @pytest.mark.parametrize("seed,n,n_traj,single_time", [(0, 5000, 300, False), (1, 200000, 7000, False),
                                                        (2, 1000, 50, True)])
 def test_traj_split_matches_numpy(seed, n, n_traj, single_time):
