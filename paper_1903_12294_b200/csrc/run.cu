@@ -851,7 +851,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                     F[0], rat(F[1], F[0]), F[2], rat(F[3], F[0]), F[4], rat(F[5], F[4]), rat(F[6], F[5]),
                     Q[0], rat(Q[1], Q[0]), Q[2], h[0], h[1], h[2], h[3]);
             fprintf(stderr, "[mfseg stats] field bricks: kept after cull %.3f, single after cull %.3f, "
-                    "reused %llu\n", rat(F[7], F[0]), rat(F[2], F[0]), h[32]);
+                    "reused %llu, screen items %llu exact samples %llu\n", rat(F[7], F[0]), rat(F[2], F[0]),
+                    h[32], h[33], h[34]);
             fprintf(stderr, "[mfseg stats] point tiles single %.3f kept hist", rat(Q[3], Q[0]));
             for (int q = 0; q < 8; ++q) fprintf(stderr, " %.3f", rat(Q[4 + q], Q[0]));
             fprintf(stderr, " | chunks by candidate rounds 1/2/3/4: %llu %llu %llu %llu", Q[12], Q[13],
