@@ -92,6 +92,9 @@ struct __align__(16) Smem5 {
     int lst[NW][32];                // per region: candidate slots that survive its cull
     int nlist[NW];                  // list lengths (-1: more than 32 survivors)
     unsigned char bslot[64];        // reused bricks: slot of their label (255: recompute)
+    float rcg[NW];                  // per region: min over its culled candidates of dl (1-2^-16) - 2^-15 Wb
+    float red2[NW];
+    float dmax;                     // largest metric change of the block's candidates
     Ctx ctx;
 };
 
@@ -271,11 +274,16 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
     const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
     unsigned keep[4] = {0u, 0u, 0u, 0u};
     int total = 0;
+    float rc = INF_F;   // smallest lower bound among the culled candidates (margin reuse)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-        keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (debug & 1)));
+        const bool k = dl[r] < INF_F && (dl[r] <= thr || (debug & 1));
+        keep[r] = __ballot_sync(0xffffffffu, k);
         total += __popc(keep[r]);
+        if (!k && dl[r] < INF_F) rc = fminf(rc, dl[r]);
     }
+    rc = warp_min_nn(rc);
+    if (lane == 0) S.rcg[w] = rc < INF_F ? rc * (1.f - 0x1.0p-16f) - 0x1.0p-15f * Wb : INF_F;
     if (total > 32) return -1;
     int base = 0;
 #pragma unroll
@@ -416,10 +424,12 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         ubw = warp_min_nn(ubw);
         const float Wb = (USEVAL ? wvf * (fmaxf(fabsf(vwl), fabsf(vwh)) + cvmax) : 0.f) + slack;
         const float thr = (ubw * (1.f + KCULL) + 2.f * KCULL * Wb) * (1.f + 0x1.0p-15f);
-        unsigned keep[4] = {0u, 0u, 0u, 0u};
+        unsigned keep[4] = {0u, 0u, 0u, 0u}, keep0[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < NR; ++r)
+        for (int r = 0; r < NR; ++r) {
             keep[r] = __ballot_sync(0xffffffffu, dl[r] < INF_F && (dl[r] <= thr || (a.debug & 1)));
+            keep0[r] = keep[r];
+        }
 
         // ---- dominance: drop kept candidates s with D(s) > D(s*) on the whole brick,
         // s* = the fully valid candidate with the smallest upper bound.  The squared
@@ -435,6 +445,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             if (nc == 1) atomicAdd(a.stats + 2, 1ull);
         }
         int sstar = -1;
+        float gmin = INF_F;   // smallest proven gap D_s - D_s* among the dominated candidates
         if (ubkey != 0xFFFFFFFFu && !(a.debug & 1)) {
             sstar = (int)(ubkey & SLOT_MASK);
             const int xa = GX * bx, ya = GY * by, za = GZ * bz, ta = GT * bt;
@@ -460,6 +471,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
             for (int r = 0; r < NR; ++r) {
                 const int s = LIST ? (lane < nlist ? S.lst[region][lane] : -1) : lane + 32 * r;
                 bool dom = false;
+                float gd = INF_F;
                 if ((keep[r] >> lane & 1u) && s != sstar) {
                     const float *T = S.tab[s];
                     const float ex0 = T[xa], ex1 = T[xb], ey0 = T[BX + ya], ey1 = T[BX + yb];
@@ -481,11 +493,13 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                                      0x1.0p-18f * wvf * (fabsf(cvs) + fabsf(cvq) + vabs);
                             }
                             const float rel = 0x1.0p-30f * (fwd * den + Wb) + slack;
-                            dom = fwd * gap * (1.f - 0x1.0p-20f) > Vb + rel;
+                            gd = fwd * gap * (1.f - 0x1.0p-20f) - (Vb + rel);
+                            dom = gd > 0.f;
                         }
                     }
                 }
                 keep[r] &= ~__ballot_sync(0xffffffffu, dom);
+                if (dom) gmin = fminf(gmin, gd);
             }
         }
         if ((a.debug & 8) && lane == 0) {
@@ -501,6 +515,23 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
             for (int k = 0; k < 8; ++k) sl[k] = (livem >> k & 1) ? sstar : -1;
             one = sstar;
+            if (FULL && a.bmargin) {
+                // proven lower bound of D_s - D_s* over the brick for every other
+                // candidate: culled (lower bound minus s*'s upper bound, with the
+                // cull's error allowances), region-culled, or dominated (its gap)
+                float cm = INF_F;
+#pragma unroll
+                for (int r = 0; r < NR; ++r)
+                    if (!(keep0[r] >> lane & 1u) && dl[r] < INF_F) cm = fminf(cm, dl[r]);
+                cm = warp_min_nn(cm);
+                gmin = warp_min_nn(gmin);
+                const float ubs = ubw * (1.f + 0x1.0p-15f) * (1.f + 0x1.0p-16f);
+                float m = gmin;
+                if (cm < INF_F) m = fminf(m, cm * (1.f - 0x1.0p-16f) - ubs - 0x1.0p-15f * Wb);
+                const float rg = S.rcg[region];
+                if (rg < INF_F) m = fminf(m, rg - ubs - 0x1.0p-15f * Wb);
+                if (lane == 0) a.bmargin[bidx] = m - 1e-6f * (fwd + wvf) - slack;
+            }
         } else {
             // several survivors: the per-sample screen runs in k_field_screen (one
             // warp per brick, kept candidates by global id), keeping this kernel lean;
@@ -742,6 +773,10 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             mycv = warp_max_nn(mycv);
             if (lane == 0) S.red[w] = mycv;
         }
+        if (a.reuse) {   // largest metric change among the block's candidates
+            const float md = warp_max_nn((!deferred && have) ? a.cdelta[id] : 0.f);
+            if (lane == 0) S.red2[w] = md;
+        }
         __syncthreads();
         if (USEVAL) {
 #pragma unroll
@@ -752,13 +787,25 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     // ---- reuse: in a stable block (no candidate changed since the last pass) a
     // brick labelled by one slot then keeps its labels; the tables and region
     // lists are built only if some brick must be recomputed
-    const bool stable = a.reuse && !deferred && cnt > 0 && a.bin_stable[sbin];
+    // stable: nothing changed (labels reusable as they are); sstable: only bounded
+    // moves (a brick's label is reusable while its proven margin exceeds twice the
+    // largest metric change of the block's candidates; the margin is carried on)
+    const bool sstable = a.reuse && !deferred && cnt > 0 && a.bin_sstable[sbin];
+    const bool stable = sstable && a.bin_stable[sbin];
     bool need_full = true;
-    if (stable) {
+    float dmax = 0.f;
+    if (sstable) {
+        if (!stable) {
+#pragma unroll
+            for (int q = 0; q < NW; ++q) dmax = fmaxf(dmax, S.red2[q]);
+        }
+        const float lim = 2.f * dmax * (1.f + 0x1.0p-20f);
         int need = 0;
         if (tid < 64) {
             const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
-            const unsigned char sl = a.bslot[(size_t)blockIdx.x * 64 + tid];
+            const size_t bidx = (size_t)blockIdx.x * 64 + tid;
+            unsigned char sl = a.bslot[bidx];
+            if (sl != 255 && !stable && !(a.bmargin[bidx] > lim)) sl = 255;
             S.bslot[tid] = sl;
             need = sl == 255 && !(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len ||
                                   GT * bt >= Tm.len);
@@ -857,9 +904,12 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                               GZ * bz + GZ <= Z.len && GT * bt + GT <= Tm.len;
             const int region = bi & 7, nl = S.nlist[region];
             const size_t bidx = (size_t)blockIdx.x * 64 + bi;
-            if (stable && S.bslot[bi] != 255) {
-                // unchanged since the last pass: labels stay, sums are constants
+            if (sstable && S.bslot[bi] != 255) {
+                // label provably unchanged since the last pass: labels stay, sums are
+                // constants; the margin shrinks by the bound of this pass's moves
                 if (a.accumulate) single_brick_sums(a, S, bidx, S.bslot[bi], bx, by, bz, bt);
+                if (!stable && lane == 0)
+                    a.bmargin[bidx] = (a.bmargin[bidx] - 2.f * dmax) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
                 if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
                 bi += NW;
                 continue;

@@ -57,6 +57,13 @@ struct FieldArgs {
     const unsigned char *bin_stable;
     unsigned char *bslot;
     int reuse;
+    // margin reuse: bins whose neighbourhood's candidate lists, validity boxes and
+    // has-flags did not change (bin_sstable); per centre an upper bound of the
+    // change of its metric anywhere (cdelta = w_d |delta c| + w_v |delta cv|);
+    // per brick a proven lower bound of D_s - D_s* over its samples (bmargin)
+    const unsigned char *bin_sstable;
+    const float *cdelta;
+    float *bmargin;
 };
 
 struct WBox {                 // one 64-point warp tile of a point chunk (k_point_assign4)

@@ -295,6 +295,10 @@ struct Plan {
     long long multi_cap;
     unsigned char *bslot;           // per brick: slot of its single label last pass (255: none)
     unsigned char *bmark, *bstable; // per sample bin: changed centres / stable neighbourhood
+    unsigned char *smark, *sstable; // per sample bin: structural changes (bin, validity box, has)
+    float *cdelta;                  // per centre: bound of its metric change in the last update
+    float *bmargin;                 // per brick: proven margin of its single label
+    int4 *vbox_prev;                // validity boxes of the previous pass
     unsigned char *tslot;           // per point warp tile: slot of its single label last pass
     long long *stranded_f, *deferred_f;
     long long cap_f;
@@ -407,9 +411,14 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         P.multi_cap = P.nf > 0 ? (bricks < (1ll << 21) ? bricks : (1ll << 21)) : 0;
         P.multi = cv.take<MultiItem>(P.multi_cap);
         P.bslot = cv.take<unsigned char>(P.nf > 0 ? bricks : 0);
+        P.bmargin = cv.take<float>(P.nf > 0 ? bricks : 0);
     }
     P.bmark = cv.take<unsigned char>(NB);
     P.bstable = cv.take<unsigned char>(NB);
+    P.smark = cv.take<unsigned char>(NB);
+    P.sstable = cv.take<unsigned char>(NB);
+    P.cdelta = cv.take<float>(K);
+    P.vbox_prev = cv.take<int4>(P.nf > 0 ? 2ll * K : 0);
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
     P.deferred_f = cv.take<long long>(P.cap_f);
@@ -593,9 +602,14 @@ CentersView view_of(const mfseg_centers &s, int K) {
 }
 
 // Centres changed by the last update (position, point or field value or their
-// presence, bitwise): mark the sample bins they left and entered.
+// presence, bitwise): mark the sample bins they left and entered (mark).  A
+// centre whose bin, field validity box or field has-flag changed also marks
+// them in smark (structural change).  cdelta: an upper bound of how much its
+// field metric w_d sst + w_f |v - cv| can change at any sample.
 __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, double4 mins, double4 C,
-                               int4 k, unsigned char *mark) {
+                               int4 k, double cf, double wd, double wf, const int4 *vbox,
+                               const int4 *vbox_prev, unsigned char *mark, unsigned char *smark,
+                               float *cdelta) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= K) return;
     bool ch = cur.has_f[c] != old.has_f[c] || cur.has_p[c] != old.has_p[c] ||
@@ -604,6 +618,20 @@ __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, doub
 #pragma unroll
     for (int q = 0; q < 4; ++q)
         ch |= __double_as_longlong(cur.loc[(size_t)q * K + c]) != __double_as_longlong(old.loc[(size_t)q * K + c]);
+    float delta = 0.f;
+    if (ch) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double d = cur.loc[(size_t)q * K + c] - old.loc[(size_t)q * K + c];
+            if (q == 3) d *= cf;
+            d2 += d * d;
+        }
+        double dv = 0.0;
+        if (cur.has_f[c] && old.has_f[c]) dv = fabs(cur.fval[c] - old.fval[c]);
+        delta = __double2float_ru((wd * sqrt(d2) + wf * dv) * (1.0 + 0x1.0p-30) + 1e-300);
+    }
+    cdelta[c] = delta;
     if (!ch) return;
     const double mn[4] = {mins.x, mins.y, mins.z, mins.w}, CC[4] = {C.x, C.y, C.z, C.w};
     const int kk[4] = {k.x, k.y, k.z, k.w};
@@ -613,13 +641,26 @@ __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, doub
         bn[q] = bin_coord(cur.loc[(size_t)q * K + c], mn[q], CC[q], kk[q]);
         bo[q] = bin_coord(old.loc[(size_t)q * K + c], mn[q], CC[q], kk[q]);
     }
-    mark[((bn[3] * k.z + bn[2]) * k.y + bn[1]) * k.x + bn[0]] = 1;
-    mark[((bo[3] * k.z + bo[2]) * k.y + bo[1]) * k.x + bo[0]] = 1;
+    const int fn = ((bn[3] * k.z + bn[2]) * k.y + bn[1]) * k.x + bn[0];
+    const int fo = ((bo[3] * k.z + bo[2]) * k.y + bo[1]) * k.x + bo[0];
+    mark[fn] = 1;
+    mark[fo] = 1;
+    bool sch = fn != fo || cur.has_f[c] != old.has_f[c];
+    if (vbox) {
+        const int4 a0 = vbox[2 * c], a1 = vbox[2 * c + 1], b0 = vbox_prev[2 * c], b1 = vbox_prev[2 * c + 1];
+        sch |= a0.x != b0.x || a0.y != b0.y || a0.z != b0.z || a0.w != b0.w || a1.x != b1.x ||
+               a1.y != b1.y || a1.z != b1.z || a1.w != b1.w;
+    }
+    if (sch) {
+        smark[fn] = 1;
+        smark[fo] = 1;
+    }
 }
 
 // A sample bin is stable when none of its 3^4 neighbour bins is marked: its
 // candidate list and every candidate's state equal the last pass's.
-__global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned char *stable) {
+__global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned char *stable,
+                             const unsigned char *smark, unsigned char *sstable) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= NB) return;
     int r = b;
@@ -629,7 +670,7 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
     r /= k.y;
     const int bz = r % k.z;
     const int bt = r / k.z;
-    bool ok = true;
+    bool ok = true, sok = true;
     for (int dt = -1; dt <= 1; ++dt)
         for (int dz = -1; dz <= 1; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
@@ -638,9 +679,12 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
                     if (qx < 0 || qy < 0 || qz < 0 || qt < 0 || qx >= k.x || qy >= k.y || qz >= k.z ||
                         qt >= k.w)
                         continue;
-                    ok = ok && !mark[((qt * k.z + qz) * k.y + qy) * k.x + qx];
+                    const int q = ((qt * k.z + qz) * k.y + qy) * k.x + qx;
+                    ok = ok && !mark[q];
+                    sok = sok && !smark[q];
                 }
     stable[b] = ok;
+    sstable[b] = sok;
 }
 
 // one assignment pass for centre state `c` (grid rebuilt here); `prev`: the
@@ -653,23 +697,29 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     int K = P.K;
     CentersView cv = view_of(c, K);
     mark(0, st);
+    // validity boxes of the previous pass (structural-change test of the reuse)
+    const bool reuse = prev && accumulate && getenv("MFSEG_NO_REUSE") == nullptr;
+    if (P.vbox_prev && P.nf > 0 && accumulate)
+        MFSEG_CUDA(cudaMemcpyAsync(P.vbox_prev, P.g.vbox, sizeof(int4) * 2 * K, cudaMemcpyDeviceToDevice, st));
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
                          P.count_tmp, P.grid_scan_tmp, st));
     mark(1, st);
     MFSEG_CUDA(cudaMemsetAsync(P.counters, 0, sizeof(unsigned long long) * 40, st));
     // reuse of the previous pass: sample bins whose candidates did not change
-    const bool reuse = prev && accumulate && getenv("MFSEG_NO_REUSE") == nullptr;
+    // (exactly, or only by bounded moves: see k_mark_changed)
     if (reuse) {
         const int NB = P.NB;
         MFSEG_CUDA(cudaMemsetAsync(P.bmark, 0, NB, st));
+        MFSEG_CUDA(cudaMemsetAsync(P.smark, 0, NB, st));
         ::mfseg::count_launch();
         k_mark_changed<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(
             K, c, *prev, make_double4(p.mins[0], p.mins[1], p.mins[2], p.mins[3]),
             make_double4(p.C[0], p.C[1], p.C[2], p.C[3]), make_int4(p.k[0], p.k[1], p.k[2], p.k[3]),
-            P.bmark);
+            p.c_f, wd, wf, P.nf > 0 ? P.g.vbox : nullptr, P.nf > 0 ? P.vbox_prev : nullptr, P.bmark,
+            P.smark, P.cdelta);
         ::mfseg::count_launch();
         k_bin_stable<<<(unsigned)((NB + 255) / 256), 256, 0, st>>>(
-            NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable);
+            NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable, P.smark, P.sstable);
         MFSEG_LAUNCH("stable bins");
     }
     if (accumulate)
@@ -724,9 +774,12 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.n_multi = P.counters + 4;
         a.multi_cap = P.multi_cap;
         a.bslot = field_version() == 5 ? P.bslot : nullptr;
+        a.bmargin = a.bslot ? P.bmargin : nullptr;
         if (reuse && a.bslot) {
             a.reuse = 1;
             a.bin_stable = P.bstable;
+            a.bin_sstable = getenv("MFSEG_NO_MARGIN_REUSE") ? P.bstable : P.sstable;
+            a.cdelta = P.cdelta;
         }
         if (const char *mc = getenv("MFSEG_MULTI_CAP")) {   // test knob: a smaller brick queue
             const long long cap = atoll(mc);
