@@ -95,6 +95,7 @@ struct __align__(16) Smem5 {
     float rcg[NW];                  // per region: min over its culled candidates of dl (1-2^-16) - 2^-15 Wb
     float red2[NW];
     float dmax;                     // largest metric change of the block's candidates
+    float bdec[64];                 // per reused brick: the margin it uses up this pass
     Ctx ctx;
 };
 
@@ -799,13 +800,18 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
 #pragma unroll
             for (int q = 0; q < NW; ++q) dmax = fmaxf(dmax, S.red2[q]);
         }
-        const float lim = 2.f * dmax * (1.f + 0x1.0p-20f);
         int need = 0;
         if (tid < 64) {
             const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
             const size_t bidx = (size_t)blockIdx.x * 64 + tid;
             unsigned char sl = a.bslot[bidx];
-            if (sl != 255 && !stable && !(a.bmargin[bidx] > lim)) sl = 255;
+            if (sl != 255 && !stable) {
+                // the margin must exceed the change of s* plus the largest change of
+                // any other candidate of the block
+                const float dec = (a.cdelta[S.id[sl]] + dmax) * (1.f + 0x1.0p-20f);
+                S.bdec[tid] = dec;
+                if (!(a.bmargin[bidx] > dec)) sl = 255;
+            }
             S.bslot[tid] = sl;
             need = sl == 255 && !(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len ||
                                   GT * bt >= Tm.len);
@@ -909,7 +915,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 // constants; the margin shrinks by the bound of this pass's moves
                 if (a.accumulate) single_brick_sums(a, S, bidx, S.bslot[bi], bx, by, bz, bt);
                 if (!stable && lane == 0)
-                    a.bmargin[bidx] = (a.bmargin[bidx] - 2.f * dmax) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
+                    a.bmargin[bidx] = (a.bmargin[bidx] - S.bdec[bi]) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
                 if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
                 bi += NW;
                 continue;
