@@ -156,9 +156,11 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     double P0[5] = {0, 0, 0, 0, 0}, P1[5] = {0, 0, 0, 0, 0};
     const WBox *wbp = a.wbox + (size_t)blockIdx.x * (POINT_CHUNK / 64) + wt;
     const size_t tidx = (size_t)blockIdx.x * (POINT_CHUNK / 64) + wt;
-    if (C.stable) {   // unchanged since the last pass: a tile with one label keeps it
+    int sl0 = -1, sl1 = -1;
+    bool reused = false;   // several labels kept from the last pass: sums only
+    if (C.stable) {   // unchanged since the last pass: the tile keeps its labels
         const unsigned char ts = a.tslot[tidx];
-        if (ts != 255) {
+        if (ts < 254) {   // one label: the per-run tile sums
             if (a.accumulate && lane == 0) {
 #pragma unroll
                 for (int d = 0; d < 5; ++d) S.wsum[w][d][ts] = DADD(S.wsum[w][d][ts], wbp->s[d]);
@@ -166,10 +168,44 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             }
             return;
         }
+        if (ts == 254) {   // several labels (none stranded): slots from the labels
+            if (!a.accumulate) return;
+            const int lab0 = live0 ? a.labels[p0] : -1, lab1 = live1 ? a.labels[p1] : -1;
+            int todo0 = lab0, todo1 = lab1;
+            while (true) {
+                const unsigned m0 = __ballot_sync(0xffffffffu, todo0 >= 0),
+                               m1 = __ballot_sync(0xffffffffu, todo1 >= 0);
+                if (!(m0 | m1)) break;
+                const int L = m0 ? __shfl_sync(0xffffffffu, todo0, __ffs(m0) - 1)
+                                 : __shfl_sync(0xffffffffu, todo1, __ffs(m1) - 1);
+                int slot = -1;
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const int s = lane + 32 * r;
+                    const unsigned f = __ballot_sync(0xffffffffu, s < C.cnt && S.id[s] == L);
+                    if (f && slot < 0) slot = __ffs(f) - 1 + 32 * r;
+                }
+                if (todo0 == L) {
+                    sl0 = slot;
+                    todo0 = -1;
+                }
+                if (todo1 == L) {
+                    sl1 = slot;
+                    todo1 = -1;
+                }
+            }
+            if (live0) {
+                P0[0] = a.x[p0]; P0[1] = a.y[p0]; P0[2] = a.z[p0]; P0[3] = a.t[p0]; P0[4] = a.v[p0];
+            }
+            if (live1) {
+                P1[0] = a.x[p1]; P1[1] = a.y[p1]; P1[2] = a.z[p1]; P1[3] = a.t[p1]; P1[4] = a.v[p1];
+            }
+            reused = true;
+        }
     }
-    if (lane == 0 && a.tslot) a.tslot[tidx] = 255;
-    int sl0 = -1, sl1 = -1;
+    if (!reused && lane == 0 && a.tslot) a.tslot[tidx] = 255;
     int one = -1;   // slot labelling the whole tile (warp-uniform)
+    if (!reused) {
     if (!C.deferred && C.cnt > 0) {
         // warp-tile box (fp32, chunk-relative) and value range: precomputed once per
         // run by k_wtile_box with exactly the formulas used for rp / fv below
@@ -444,7 +480,8 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         a.labels[p1] = lab;
         if (lab < 0) ++nlist;
     }
-    if (__any_sync(0xffffffffu, nlist > 0)) {
+    const bool listed = __any_sync(0xffffffffu, nlist > 0);
+    if (listed) {
         unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
         long long *lst = C.deferred ? a.deferred : a.stranded;
         const long long cap = C.deferred ? a.deferred_cap : a.stranded_cap;
@@ -457,6 +494,9 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             if (p < cap) lst[p] = p1;
         }
     }
+    // several labels, none stranded: reusable while the chunk's candidates stay
+    if (one < 0 && !listed && !C.deferred && C.cnt > 0 && lane == 0 && a.tslot) a.tslot[tidx] = 254;
+    }   // !reused
 
     // ---- partial sums: per-warp fp64 running sums + shared counts
     if (a.accumulate && one >= 0) {   // the whole tile -> one cluster: per-run tile sums
