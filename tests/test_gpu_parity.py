@@ -518,11 +518,13 @@ def test_field_brick_queue_paths_agree(env, monkeypatch):
             assert ca.f_c == pytest.approx(cb.f_c, rel=1e-12, abs=1e-15)
 
 
-def test_reuse_of_unchanged_blocks_is_exact(monkeypatch):
+@pytest.mark.parametrize("weights", [dict(), dict(c_f=0.5, w_d=0.3, w_p=1.5, w_f=2.0)])
+def test_reuse_of_unchanged_blocks_is_exact(weights, monkeypatch):
     """A 10-iteration run on a mid-size case where, in the later passes, many
-    field blocks and point chunks have no changed candidate and reuse the
-    previous pass's labels: labels and centres must equal a run that recomputes
-    everything (MFSEG_NO_REUSE)."""
+    field blocks and point chunks reuse the previous pass's labels (unchanged
+    candidates, or field bricks whose proven margin exceeds the centre moves):
+    labels and centres must equal a run that recomputes everything
+    (MFSEG_NO_REUSE), with default and with non-unit weights and time scale."""
     P = pkg()
     from paper_1903_12294_b200.engine import run_device
     from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
@@ -530,7 +532,7 @@ def test_reuse_of_unchanged_blocks_is_exact(monkeypatch):
     fld, pts, _ = _synthetic(dims, nt, ntraj, 5, False, n_blobs=3)
     normalize_device(pts, fld, True)
     ext = domain_extent_device(pts, fld)
-    params = P.ClusterParams(k=(8, 6, 4, 6), eps_c=1e-12, max_iterations=10)
+    params = P.ClusterParams(k=(8, 6, 4, 6), eps_c=1e-12, max_iterations=10, **weights)
     a = run_device(pts, fld, ext, params)
     monkeypatch.setenv("MFSEG_NO_REUSE", "1")
     b = run_device(pts, fld, ext, params)
