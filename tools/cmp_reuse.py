@@ -12,7 +12,11 @@ if len(sys.argv) > 3:   # child: one run, save outputs
     fld, pts, _ = synthetic_device(cfg["dims"], cfg["nt"], cfg["n_traj"], seed=0)
     normalize_device(pts, fld, True)
     ext = domain_extent_device(pts, fld)
-    params = ClusterParams(k=cfg["k"], eps_c=1e-12, max_iterations=int(sys.argv[2]))
+    extra = {}
+    for kv in filter(None, os.environ.get("CMP_WEIGHTS", "").split(",")):   # e.g. c_f=0.5,w_f=2
+        key, val = kv.split("=")
+        extra[key] = float(val)
+    params = ClusterParams(k=cfg["k"], eps_c=1e-12, max_iterations=int(sys.argv[2]), **extra)
     r = run_device(pts, fld, ext, params)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
