@@ -48,10 +48,8 @@
 namespace mfseg {
 namespace {
 
-constexpr double INF_D = __builtin_huge_val();
 constexpr float INF_F = __builtin_huge_valf();
 constexpr float FLT_BIG = 3.4028234663852886e38f;
-constexpr unsigned INF_BITS = 0x7F800000u;
 
 constexpr int BX = 16, BY = 16, BZ = 16, BT = 4;   // block = one bin's 16^3 x 4 samples (at most)
 constexpr int NT = 256, NW = 8;
@@ -63,7 +61,6 @@ constexpr int GX = 8, GY = 4, GZ = 4, GT = 2;      // brick: 8x4x4 voxels x 2 ti
 constexpr int QY = BX / GX, QZ = QY + BY / GY, QT = QZ + BZ / GZ;
 constexpr int NQ = QT + BT / GT;                   // brick-row groups: x 2, y 4, z 4, t 2
 constexpr int HW = 27;                             // histogram words: x 8, y 8, z 8, t 2, n 1
-constexpr float KSCR = 0x1.0p-18f;
 static_assert(MULTI_MAX <= 32, "one lane per kept candidate in k_field_screen");
 constexpr float KCULL = 0x1.0p-16f;
 
@@ -352,7 +349,7 @@ __device__ __forceinline__ void defer_brick(const FieldArgs &a, const Ctx &C, in
 template <bool USEVAL, bool FULL, int NR, bool LIST>
 __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bi, int bx,
                                       int by, int bz, int bt, int region, int nlist, int &ovf_local) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
     const int z0 = GZ * bz, t0 = GT * bt;
     const long long fbase = (((long long)(C.T.start + t0) * a.nz + C.Z.start + z0) * a.ny +

@@ -28,7 +28,6 @@ constexpr float FLT_BIG = 3.4028234663852886e38f;
 constexpr unsigned INF_BITS = 0x7F800000u;
 constexpr unsigned KEY_MASK = 127u;   // same key truncation as k_field_assign5
 constexpr float KSCR = 0x1.0p-18f;
-constexpr int GX = 8, GY = 4, GZ = 4, GT = 2;
 constexpr int ACC_FV = 10, ACC_NF = 13;   // accumulator words (assign.cu)
 constexpr int SCREEN_MINB = 3;
 
@@ -210,7 +209,6 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
                     if (q == k) {
                         b1k = b1[q];
                     }
-#pragma unroll
                 const float fvk = (float)vk;
                 const float W = USEVAL ? fmaf(wvf, fabsf(fvk) + cvmax, slack) : slack;
                 const float u1 = __uint_as_float(b1k & ~KEY_MASK) * (1.f + 0x1.0p-15f);
