@@ -868,7 +868,10 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     {
         int nl = -1;
         const int rbx = w & 1, rby = (w >> 1) & 3;
-        if (!deferred && cnt > 0 && need_full && GX * rbx < X.len && GY * rby < Y.len) {
+        // (skipped when every brick of this warp keeps its labels)
+        bool wneed = need_full;
+        if (sstable && need_full) wneed = __any_sync(0xffffffffu, lane < 8 && S.bslot[w + NW * lane] == 255);
+        if (!deferred && cnt > 0 && wneed && GX * rbx < X.len && GY * rby < Y.len) {
             float vl = 0.f, vh = 0.f;
             if (USEVAL) {   // value range of the region = union of its bricks' ranges
                 float lo = INF_F, hi = -INF_F;
