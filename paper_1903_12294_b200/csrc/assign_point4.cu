@@ -704,10 +704,15 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
 // the chunk-relative fp32 box, the fl32(value) range and the fixed-order sums
 // -- the same formulas k_point_assign4 uses.  The second read of the chunk's
 // points hits the cache.
+// GATHER: the chunk's points are first gathered from the caller's arrays through
+// the sort permutation (and written to the bin-sorted SoA), so the sorted points
+// are read from HBM once, here, instead of by a separate gather pass.
+template <bool GATHER>
 __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const int *n_tiles,
-                                                      const double *x, const double *y,
-                                                      const double *z, const double *t,
-                                                      const double *v, double cf, double *box,
+                                                      double *x, double *y, double *z, double *t,
+                                                      double *v, const unsigned *perm,
+                                                      const double *gxyz, const double *gt,
+                                                      const double *gv, double cf, double *box,
                                                       WBox *out) {
     constexpr int TPW = POINT_CHUNK / 64 / 8;   // warp tiles per warp
     __shared__ double red[8][8];
@@ -725,12 +730,37 @@ __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const in
         for (int q = 0; q < 2; ++q) {
             const int off = 64 * (w + 8 * j) + lane + 32 * q;
             const long long p = (long long)T.y + min(off, T.z - 1);   // clamped: box unaffected
-            P[j][q][0] = x[p];
-            P[j][q][1] = y[p];
-            P[j][q][2] = z[p];
-            P[j][q][3] = t[p];
-            P[j][q][4] = v[p];
+            if (GATHER) {
+                const long long src = perm[p];
+                P[j][q][0] = __ldg(gxyz + 3 * src);
+                P[j][q][1] = __ldg(gxyz + 3 * src + 1);
+                P[j][q][2] = __ldg(gxyz + 3 * src + 2);
+                P[j][q][3] = __ldg(gt + src);
+                P[j][q][4] = __ldg(gv + src);
+            } else {
+                P[j][q][0] = x[p];
+                P[j][q][1] = y[p];
+                P[j][q][2] = z[p];
+                P[j][q][3] = t[p];
+                P[j][q][4] = v[p];
+            }
         }
+    if (GATHER) {
+#pragma unroll
+        for (int j = 0; j < TPW; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int off = 64 * (w + 8 * j) + lane + 32 * q;
+                if (off < T.z) {
+                    const long long p = (long long)T.y + off;
+                    x[p] = P[j][q][0];
+                    y[p] = P[j][q][1];
+                    z[p] = P[j][q][2];
+                    t[p] = P[j][q][3];
+                    v[p] = P[j][q][4];
+                }
+            }
+    }
     double lo[4], hi[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
@@ -812,16 +842,22 @@ __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const in
     }
 }
 
-int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,
-                    const double *y, const double *z, const double *t, const double *v, double cf,
-                    double *box, WBox *wbox, cudaStream_t st) {
+int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, double *x, double *y,
+                    double *z, double *t, double *v, double cf, double *box, WBox *wbox,
+                    const unsigned *perm, const double *gxyz, const double *gt, const double *gv,
+                    cudaStream_t st) {
     if (max_tiles <= 0) return 0;
     if (max_tiles > 0x7fffffffll) {
         set_error("point chunk grid too large");
         return 3;
     }
     ::mfseg::count_launch();
-    k_chunk_boxes<<<(unsigned)max_tiles, 256, 0, st>>>(tiles, n_tiles, x, y, z, t, v, cf, box, wbox);
+    if (perm)
+        k_chunk_boxes<true><<<(unsigned)max_tiles, 256, 0, st>>>(tiles, n_tiles, x, y, z, t, v, perm, gxyz,
+                                                                 gt, gv, cf, box, wbox);
+    else
+        k_chunk_boxes<false><<<(unsigned)max_tiles, 256, 0, st>>>(tiles, n_tiles, x, y, z, t, v, nullptr,
+                                                                  nullptr, nullptr, nullptr, cf, box, wbox);
     MFSEG_LAUNCH("k_chunk_boxes");
     return 0;
 }

@@ -149,9 +149,10 @@ int launch_brick_pre(const FieldArgs &a, cudaStream_t st);
 int launch_field_screen(const FieldArgs &a, cudaStream_t st);
 int point_tile_size();
 int point_version();
-int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, const double *x,
-                    const double *y, const double *z, const double *t, const double *v, double cf,
-                    double *box, WBox *wbox, cudaStream_t st);
+int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, double *x, double *y,
+                    double *z, double *t, double *v, double cf, double *box, WBox *wbox,
+                    const unsigned *perm, const double *gxyz, const double *gt, const double *gv,
+                    cudaStream_t st);
 int launch_field_assign(const FieldArgs &a, long long ntiles, cudaStream_t st);
 int launch_point_assign(const PointArgs &a, long long max_tiles, cudaStream_t st);
 int launch_fallback(const FallbackArgs &a, cudaStream_t st);

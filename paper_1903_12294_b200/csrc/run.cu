@@ -564,9 +564,13 @@ int plan_prepare(Plan &P) {
         }
         MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, P.key_bits, P.radix_tmp,
                                    P.radix_bytes, st));
-        ::mfseg::count_launch();
-        k_point_gather<<<(unsigned)((n + 256 * GATHER_PER_THREAD - 1) / (256 * GATHER_PER_THREAD)), 256, 0,
-                         st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px, P.py, P.pz, P.pt, P.pv);
+        const bool fused_gather = point_version() == 4;   // gathered chunk by chunk in k_chunk_boxes
+        if (!fused_gather) {
+            ::mfseg::count_launch();
+            k_point_gather<<<(unsigned)((n + 256 * GATHER_PER_THREAD - 1) / (256 * GATHER_PER_THREAD)), 256,
+                             0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px, P.py, P.pz, P.pt,
+                                      P.pv);
+        }
         const int NG = P.ngroups;
         ::mfseg::count_launch();
         k_bin_first<<<(unsigned)((n + 256) / 256), 256, 0, st>>>(n, P.skeys, P.sub_bits, NG,
@@ -580,9 +584,10 @@ int plan_prepare(Plan &P) {
         ::mfseg::count_launch();
         k_make_tiles<<<gk, 256, 0, st>>>(NG, P.bcnt, P.bfirst, P.tstart, TP, P.nint, P.tiles);
         MFSEG_LAUNCH("point tiles");
-        if (point_version() == 4)
+        if (fused_gather)
             MFSEG_TRY(launch_tile_box(P.tiles, P.tstart + NG, P.max_tiles, P.px, P.py, P.pz, P.pt,
-                                      P.pv, p.c_f, P.tbox, P.wbox, st));
+                                      P.pv, p.c_f, P.tbox, P.wbox, P.perm, P.pts.xyz, P.pts.t,
+                                      P.pts.value, st));
         MFSEG_CUDA(cudaMemsetAsync(P.tslot, 255, P.max_tiles * (POINT_CHUNK / 64), st));
     }
     return 0;
