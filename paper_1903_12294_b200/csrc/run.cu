@@ -202,9 +202,19 @@ __global__ void k_make_tiles(int ng, const int *cnt, const int *first, const int
         tiles[o + q] = make_int4(g / per_bin, f + q * tp, min(tp, n - q * tp), g);
 }
 
+// labels back to the caller's point order: 4 per thread (vector loads), scattered stores
 __global__ void k_unpermute(long long n, const unsigned *perm, const int *src, int *dst) {
-    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < n) dst[perm[i]] = src[i];
+    const long long i = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    if (i + 3 < n) {
+        const uint4 pm = *reinterpret_cast<const uint4 *>(perm + i);
+        const int4 sv = *reinterpret_cast<const int4 *>(src + i);
+        dst[pm.x] = sv.x;
+        dst[pm.y] = sv.y;
+        dst[pm.z] = sv.z;
+        dst[pm.w] = sv.w;
+    } else {
+        for (long long q = i; q < n; ++q) dst[perm[q]] = src[q];
+    }
 }
 
 __global__ void k_copy_state(int K, mfseg_centers s, mfseg_centers d) {
@@ -1040,7 +1050,7 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
     MFSEG_TRY(check_overflow(P));
     if (P.np > 0) {
         ::mfseg::count_launch();
-        k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,
+        k_unpermute<<<(unsigned)((P.np + 1023) / 1024), 256, 0, st>>>(P.np, P.perm, P.plabels,
                                                                      point_labels);
         MFSEG_LAUNCH("k_unpermute");
     }
@@ -1063,7 +1073,7 @@ int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr));
     if (P.np > 0) {
         ::mfseg::count_launch();
-        k_unpermute<<<(unsigned)((P.np + 255) / 256), 256, 0, st>>>(P.np, P.perm, P.plabels,
+        k_unpermute<<<(unsigned)((P.np + 1023) / 1024), 256, 0, st>>>(P.np, P.perm, P.plabels,
                                                                      point_labels);
         MFSEG_LAUNCH("k_unpermute");
     }
