@@ -988,7 +988,8 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
     const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long plane = (long long)a.ny * a.nx, vol = plane * a.nz;
-    for (int bi = w; bi < 64; bi += NW) {
+#pragma unroll 4
+    for (int bi = w; bi < 64; bi += NW) {   // unrolled: several bricks' loads in flight
         const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
         if (GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= T.len) continue;
         const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
@@ -1000,7 +1001,7 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const bool live = lx < X.len && ly < Y.len && z0 + (k & 3) < Z.len && t0 + (k >> 2) < T.len;
-            const double v = live ? a.values[fbase + (k & 3) * plane + (k >> 2) * vol] : 0.0;
+            const double v = live ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
             vs = DADD(vs, v);
             if (live) {
                 lo = fminf(lo, (float)v);
