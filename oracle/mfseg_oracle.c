@@ -10,8 +10,11 @@
  * SSE2), so every floating-point operation below rounds exactly like numpy's.
  *
  *   oracle_assign   engine._assign_chunk + _fallback_assign  (engine.py:164-205)
+ *   oracle_assign_field  the same for field cells given by the grid geometry
  *   oracle_run      engine.run incl. np.bincount's sequential
  *                   sums (engine.py:244-263) and update/converge (266-320)
+ *   oracle_run_grid engine.run with field locations derived from the geometry
+ *                   (model.py:137-150) instead of a materialised loc4 array
  *
  * Pinned against the reference's own outputs by tests/test_oracle_golden.py.
  */
@@ -137,10 +140,65 @@ static int assign_one(const grid_t *g, const double *s, double v, double wv, dou
     }
 }
 
+/* Samples: either an n x 4 location array, or field cells whose locations are
+ * derived from the grid geometry exactly as FieldSet.cell_centers / loc4 do
+ * (model.py:137-150: origin + (i + 0.5) * spacing, two roundings; timestep-major,
+ * x fastest), optionally restricted to a list of flat indices. */
+typedef struct {
+    const double *loc;    /* n x 4, or NULL: field geometry below */
+    const double *val;    /* per sample (loc mode) or the whole field (geometry mode) */
+    int nx, ny, nz;
+    long long ncell;
+    double origin[3], spacing[3];
+    const double *times;
+    const int64_t *idx;   /* geometry mode: flat indices of the samples, or NULL = all */
+} src_t;
+
+static void src_sample(const src_t *s, long long i, double out[4], double *v) {
+    if (s->loc) {
+        memcpy(out, s->loc + 4 * i, 4 * sizeof(double));
+        *v = s->val[i];
+        return;
+    }
+    long long q = s->idx ? s->idx[i] : i;
+    long long m = q / s->ncell, r = q % s->ncell;
+    long long ii = r % s->nx, jj = (r / s->nx) % s->ny, kk = r / ((long long)s->nx * s->ny);
+    out[0] = s->origin[0] + ((double)ii + 0.5) * s->spacing[0];
+    out[1] = s->origin[1] + ((double)jj + 0.5) * s->spacing[1];
+    out[2] = s->origin[2] + ((double)kk + 0.5) * s->spacing[2];
+    out[3] = s->times[m];
+    *v = s->val[q];
+}
+
+static src_t loc_src(const double *loc, const double *val) {
+    src_t s;
+    memset(&s, 0, sizeof s);
+    s.loc = loc;
+    s.val = val;
+    return s;
+}
+
+static src_t grid_src(const int *dims, const double *origin, const double *spacing,
+                      const double *times, const double *values, const int64_t *idx) {
+    src_t s;
+    memset(&s, 0, sizeof s);
+    s.val = values;
+    s.nx = dims[0];
+    s.ny = dims[1];
+    s.nz = dims[2];
+    s.ncell = (long long)dims[0] * dims[1] * dims[2];
+    for (int d = 0; d < 3; ++d) {
+        s.origin[d] = origin[d];
+        s.spacing[d] = spacing[d];
+    }
+    s.times = times;
+    s.idx = idx;
+    return s;
+}
+
 typedef struct {
     const grid_t *g;
-    const double *loc;
-    const double *val;
+    const src_t *src;
     int64_t *out;
     long long lo, hi;
     double wv, wd, cf;
@@ -148,12 +206,15 @@ typedef struct {
 
 static void *worker(void *arg) {
     job_t *j = (job_t *)arg;
-    for (long long i = j->lo; i < j->hi; ++i)
-        j->out[i] = assign_one(j->g, j->loc + 4 * i, j->val[i], j->wv, j->wd, j->cf);
+    double s[4], v;
+    for (long long i = j->lo; i < j->hi; ++i) {
+        src_sample(j->src, i, s, &v);
+        j->out[i] = assign_one(j->g, s, v, j->wv, j->wd, j->cf);
+    }
     return NULL;
 }
 
-static void assign_all(const grid_t *g, long long n, const double *loc, const double *val,
+static void assign_all(const grid_t *g, long long n, const src_t *src,
                        double wv, double wd, double cf, int64_t *out, int threads) {
     if (threads < 1) threads = 1;
     if (threads > 256) threads = 256;
@@ -164,7 +225,7 @@ static void assign_all(const grid_t *g, long long n, const double *loc, const do
     for (int t = 0; t < threads; ++t) {
         long long lo = per * t, hi = lo + per < n ? lo + per : n;
         if (lo > n) lo = n;
-        jobs[t] = (job_t){g, loc, val, out, lo, hi, wv, wd, cf};
+        jobs[t] = (job_t){g, src, out, lo, hi, wv, wd, cf};
         if (threads == 1) worker(&jobs[t]);
         else pthread_create(&th[t], NULL, worker, &jobs[t]);
     }
@@ -183,16 +244,37 @@ int oracle_assign(long long n, const double *loc, const double *val, int K, cons
         g.k[d] = k[d];
     }
     if (grid_build(&g)) return -1;
-    assign_all(&g, n, loc, val, wv, wd, cf, out, threads);
+    src_t s = loc_src(loc, val);
+    assign_all(&g, n, &s, wv, wd, cf, out, threads);
+    grid_free(&g);
+    return 0;
+}
+
+/* The same for field cells given by the grid geometry: the samples are the
+ * flat indices idx[0..n) (or all nt * ncell cells when idx is NULL). */
+int oracle_assign_field(long long n, const int64_t *idx, const int *dims, const double *origin,
+                        const double *spacing, const double *times, const double *values, int K,
+                        const double *cloc, const double *cval, const uint8_t *chas,
+                        const double *mins, const double *C, const int *k, double wv, double wd,
+                        double cf, int64_t *out, int threads) {
+    grid_t g = {K, cloc, cval, chas, {0}, {0}, {0}, NULL, NULL};
+    for (int d = 0; d < 4; ++d) {
+        g.mins[d] = mins[d];
+        g.C[d] = C[d];
+        g.k[d] = k[d];
+    }
+    if (grid_build(&g)) return -1;
+    src_t s = grid_src(dims, origin, spacing, times, values, idx);
+    assign_all(&g, n, &s, wv, wd, cf, out, threads);
     grid_free(&g);
     return 0;
 }
 
 /* Sequential per-cluster sums in sample-index order (np.bincount)  engine.py:244-263 */
-static void accumulate(int K, long long np_, const double *ploc, const double *pval,
-                       const int64_t *pl, long long nf, const double *floc, const double *fval,
-                       const int64_t *fl, double *sums, double *psum, double *fsum,
-                       int64_t *n_p, int64_t *n_f) {
+static void accumulate(int K, long long np_, const src_t *ps, const int64_t *pl, long long nf,
+                       const src_t *fs, const int64_t *fl, double *sums, double *psum,
+                       double *fsum, int64_t *n_p, int64_t *n_f) {
+    double s[4], v;
     double *P = (double *)calloc((size_t)K * 4, sizeof(double));
     double *F = (double *)calloc((size_t)K * 4, sizeof(double));
     memset(psum, 0, sizeof(double) * K);
@@ -201,14 +283,16 @@ static void accumulate(int K, long long np_, const double *ploc, const double *p
     memset(n_f, 0, sizeof(int64_t) * K);
     for (long long i = 0; i < np_; ++i) {
         int64_t c = pl[i];
-        for (int d = 0; d < 4; ++d) P[4 * c + d] += ploc[4 * i + d];
-        psum[c] += pval[i];
+        src_sample(ps, i, s, &v);
+        for (int d = 0; d < 4; ++d) P[4 * c + d] += s[d];
+        psum[c] += v;
         n_p[c]++;
     }
     for (long long i = 0; i < nf; ++i) {
         int64_t c = fl[i];
-        for (int d = 0; d < 4; ++d) F[4 * c + d] += floc[4 * i + d];
-        fsum[c] += fval[i];
+        src_sample(fs, i, s, &v);
+        for (int d = 0; d < 4; ++d) F[4 * c + d] += s[d];
+        fsum[c] += v;
         n_f[c]++;
     }
     for (long long j = 0; j < 4LL * K; ++j) sums[j] = (0.0 + P[j]) + F[j];
@@ -225,13 +309,12 @@ static double rel(double o, double n) { return fabs(n - o) / (fabs(o) + 1e-12); 
  * are outputs; progress_delta[max_iter] receives the per-iteration max delta.
  * Returns iterations_used, converged via pointers.
  */
-int oracle_run(long long np_, const double *ploc, const double *pval, long long nf,
-               const double *floc, const double *fval, const double *mins, const double *maxs,
-               const int *k, double cf, double wd, double wp, double wf, double eps_c,
-               int max_iter, int threads, int32_t *pl_out, int32_t *fl_out, double *cloc,
-               double *cpv, double *cfv, uint8_t *has_p, uint8_t *has_f, int64_t *n_points,
-               int64_t *n_fields, uint8_t *dormant, int *iters_used, int *converged,
-               double *progress_delta) {
+static int run_impl(long long np_, const src_t *ps, long long nf, const src_t *fs,
+                    const double *mins, const double *maxs, const int *k, double cf, double wd,
+                    double wp, double wf, double eps_c, int max_iter, int threads,
+                    int32_t *pl_out, int32_t *fl_out, double *cloc, double *cpv, double *cfv,
+                    uint8_t *has_p, uint8_t *has_f, int64_t *n_points, int64_t *n_fields,
+                    uint8_t *dormant, int *iters_used, int *converged, double *progress_delta) {
     double C[4];
     for (int d = 0; d < 4; ++d) C[d] = (maxs[d] - mins[d]) / k[d];
     int K = k[0] * k[1] * k[2] * k[3];
@@ -271,12 +354,12 @@ int oracle_run(long long np_, const double *ploc, const double *pval, long long 
             g.k[d] = k[d];
         }
         if (grid_build(&g)) return -1;
-        assign_all(&g, np_, ploc, pval, pw, dw, cf, pl, threads);
+        assign_all(&g, np_, ps, pw, dw, cf, pl, threads);
         g.cval = cfv;
         g.chas = has_f;
-        assign_all(&g, nf, floc, fval, fw, dw, cf, fl, threads);
+        assign_all(&g, nf, fs, fw, dw, cf, fl, threads);
         grid_free(&g);
-        accumulate(K, np_, ploc, pval, pl, nf, floc, fval, fl, sums, psum, fsum, cnp, cnf);
+        accumulate(K, np_, ps, pl, nf, fs, fl, sums, psum, fsum, cnp, cnf);
         memcpy(oloc, cloc, sizeof(double) * 4 * K);
         memcpy(opv, cpv, sizeof(double) * K);
         memcpy(ofv, cfv, sizeof(double) * K);
@@ -346,4 +429,36 @@ int oracle_run(long long np_, const double *ploc, const double *pval, long long 
     free(pl); free(fl); free(sums); free(psum); free(fsum); free(cnp); free(cnf);
     free(oloc); free(opv); free(ofv); free(ohp); free(ohf);
     return 0;
+}
+
+int oracle_run(long long np_, const double *ploc, const double *pval, long long nf,
+               const double *floc, const double *fval, const double *mins, const double *maxs,
+               const int *k, double cf, double wd, double wp, double wf, double eps_c,
+               int max_iter, int threads, int32_t *pl_out, int32_t *fl_out, double *cloc,
+               double *cpv, double *cfv, uint8_t *has_p, uint8_t *has_f, int64_t *n_points,
+               int64_t *n_fields, uint8_t *dormant, int *iters_used, int *converged,
+               double *progress_delta) {
+    src_t ps = loc_src(ploc, pval), fs = loc_src(floc, fval);
+    return run_impl(np_, &ps, nf, &fs, mins, maxs, k, cf, wd, wp, wf, eps_c, max_iter, threads,
+                    pl_out, fl_out, cloc, cpv, cfv, has_p, has_f, n_points, n_fields, dormant,
+                    iters_used, converged, progress_delta);
+}
+
+/* engine.run with the field given by its grid geometry (dims, origin, spacing,
+ * times, values [nt][ncell]): field locations are derived per cell (model.py:137-150)
+ * instead of a materialised loc4 array, so bench-scale fields fit in host memory. */
+int oracle_run_grid(long long np_, const double *ploc, const double *pval, int nt,
+                    const int *dims, const double *origin, const double *spacing,
+                    const double *times, const double *fval, const double *mins,
+                    const double *maxs, const int *k, double cf, double wd, double wp, double wf,
+                    double eps_c, int max_iter, int threads, int32_t *pl_out, int32_t *fl_out,
+                    double *cloc, double *cpv, double *cfv, uint8_t *has_p, uint8_t *has_f,
+                    int64_t *n_points, int64_t *n_fields, uint8_t *dormant, int *iters_used,
+                    int *converged, double *progress_delta) {
+    src_t ps = loc_src(ploc, pval);
+    src_t fs = grid_src(dims, origin, spacing, times, fval, NULL);
+    long long nf = nt > 0 ? (long long)nt * fs.ncell : 0;
+    return run_impl(np_, &ps, nf, &fs, mins, maxs, k, cf, wd, wp, wf, eps_c, max_iter, threads,
+                    pl_out, fl_out, cloc, cpv, cfv, has_p, has_f, n_points, n_fields, dormant,
+                    iters_used, converged, progress_delta);
 }

@@ -33,9 +33,13 @@ def _oracle_run(case, impl):
         ids, loc, pc, fc = _table_arrays(r.centres)
         return (r.point_labels, r.field_labels, ids, loc, pc, fc, r.iterations_used,
                 r.converged, [d for _, d in r.progress])
-    floc = O.field_locations(dims, origin, spacing, times) if values.size else np.zeros((0, 4))
-    r = c_oracle.run(case.p_loc, case["in_p_value"], floc, values.reshape(-1), mins, maxs,
-                     p["k"], threads=4, **kw)
+    if impl == "c_grid":
+        r = c_oracle.run_grid(case.p_loc, case["in_p_value"], dims, origin, spacing, times,
+                              values.reshape(-1), mins, maxs, p["k"], threads=4, **kw)
+    else:
+        floc = O.field_locations(dims, origin, spacing, times) if values.size else np.zeros((0, 4))
+        r = c_oracle.run(case.p_loc, case["in_p_value"], floc, values.reshape(-1), mins, maxs,
+                         p["k"], threads=4, **kw)
     ids = np.flatnonzero(r["n_points"] + r["n_fields"] > 0)
     pc = np.where(r["has_p"][ids], r["pval"][ids], np.nan)
     fc = np.where(r["has_f"][ids], r["fval"][ids], np.nan)
@@ -43,7 +47,7 @@ def _oracle_run(case, impl):
             r["iterations_used"], r["converged"], list(r["progress"]))
 
 
-@pytest.mark.parametrize("impl", ["numpy", "c"])
+@pytest.mark.parametrize("impl", ["numpy", "c", "c_grid"])
 @pytest.mark.parametrize("name", RUNS)
 def test_run_matches_reference_bit_exact(name, impl):
     case = Case(name)
@@ -81,6 +85,16 @@ def test_assign_matches_reference(name):
                           mins, C, p["k"], p["w_f"], p["w_d"], p["c_f"])
     np.testing.assert_array_equal(cpl, case["out_point_labels"])
     np.testing.assert_array_equal(cfl, case["out_field_labels"])
+    if values.size:   # field cells from the geometry, all and a shuffled subset
+        gfl = c_oracle.assign_field(dims, origin, spacing, times, values, cloc, case["in_c_fval"],
+                                    case["in_c_has_f"], mins, C, p["k"], p["w_f"], p["w_d"],
+                                    p["c_f"])
+        np.testing.assert_array_equal(gfl, case["out_field_labels"])
+        idx = np.random.default_rng(0).permutation(values.size)[: max(values.size // 3, 1)]
+        sfl = c_oracle.assign_field(dims, origin, spacing, times, values, cloc, case["in_c_fval"],
+                                    case["in_c_has_f"], mins, C, p["k"], p["w_f"], p["w_d"],
+                                    p["c_f"], idx=idx)
+        np.testing.assert_array_equal(sfl, case["out_field_labels"][idx])
     # accumulate + update with the reference's labels
     K = len(cloc)
     sums = O.cluster_sums(case["out_point_labels"], case.p_loc, case["in_p_value"],
