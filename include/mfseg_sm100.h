@@ -10,7 +10,11 @@
  *   - Plain C types only: pointers, sizes, POD structs.  No torch types.
  *   - All array pointers are DEVICE pointers unless a name ends in `_host`.
  *     The caller owns every buffer, including the workspace sized by the
- *     matching *_workspace_size() query.  The library never frees caller memory.
+ *     matching *_workspace_size() query (any alignment; the library aligns its
+ *     carvings itself).  The library never frees caller memory.
+ *   - Inputs must be finite: NaN / inf values, coordinates or
+ *     times are rejected with status 2, as are inputs whose per-cluster sums
+ *     could exceed the exact 128-bit accumulators (max |x| * samples >= 2^62).
  *   - Every call is stream-ordered on the caller's `stream` (a cudaStream_t
  *     passed as void*; NULL = legacy default stream).  Calls that return host
  *     values synchronise that stream.
@@ -32,7 +36,7 @@
 extern "C" {
 #endif
 
-#define MFSEG_ABI_VERSION 1
+#define MFSEG_ABI_VERSION 2
 
 /* Clustering geometry and weights: ClusterParams (model.py:198-228) plus the
  * extent minima and interval distances C = extent/k (model.py:275-280). */
@@ -47,13 +51,17 @@ typedef struct mfseg_params {
 } mfseg_params;
 
 /* FieldSet (model.py:108-157).  values: [nt][nz][ny][nx] fp64 (already
- * normalized, ingest.py:321-335), times: [nt]. */
+ * normalized, ingest.py:321-335), times: [nt].  offset: global cell index of
+ * the first local cell per axis (0 for a whole grid; a spatial slab of a larger
+ * grid keeps the grid's origin and sets offset, so that cell centres are
+ * origin + (offset + i + 0.5) * spacing with the reference's roundings). */
 typedef struct mfseg_field {
     int32_t nx, ny, nz, nt;
     double origin[3];
     double spacing[3];
     const double *times;
     const double *values;
+    int32_t offset[3];
 } mfseg_field;
 
 /* PointSet (model.py:78-105): xyz [n][3], t [n], value [n] (normalized). */
@@ -101,8 +109,24 @@ int mfseg_abi_version(void);
  * assign, 3 stranded fallback, 4 exchange + update).  mfseg_timing_read fills
  * ms_out[0..n) with accumulated milliseconds and returns the pass count. */
 long long mfseg_launch_count(void);
+
 void mfseg_timing_enable(int32_t on);
 int32_t mfseg_timing_read(double *ms_out, int32_t n);
+
+/* Diagnostics / test knobs for the calling thread (defaults 0 / -1 are the
+ * product behaviour; no environment variable is read by the library):
+ * flags: bit 0 no tile culling, bit 1 exact fp64 for every surviving
+ * candidate, bit 3 per-pass statistics on stderr, bit 4 no reuse of unchanged
+ * blocks / chunks across passes, bit 5 exact reuse only (no margin reuse);
+ * multi_cap >= 0 caps the multi-candidate brick queue (the overflow takes the
+ * exact per-sample path).  Results are identical for every setting. */
+#define MFSEG_DEBUG_NO_CULL 1
+#define MFSEG_DEBUG_EXACT 2
+#define MFSEG_DEBUG_STATS 8
+#define MFSEG_DEBUG_KERNEL_BITS 11
+#define MFSEG_DEBUG_NO_REUSE 16
+#define MFSEG_DEBUG_NO_MARGIN_REUSE 32
+int mfseg_set_debug_options(int32_t flags, int64_t multi_cap);
 
 /* ---------------------------------------------------------------- full run
  * engine.run (engine.py:323-381): seed -> initial pass -> iterate
@@ -185,6 +209,13 @@ int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const i
                      int32_t *order, int32_t *run_start, int64_t *n_runs_host, double *stride_host,
                      void *workspace, size_t workspace_bytes, void *stream);
 
+/* The same split with a caller-given stride (multi-GPU: the ranks' common
+ * stride over all point times; the points of each trajectory are all local). */
+int mfseg_traj_split_stride(int64_t n, const int64_t *traj_id, const double *t,
+                            const int32_t *label, double stride, int32_t *order,
+                            int32_t *run_start, int64_t *n_runs_host, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
 size_t mfseg_link_index_workspace_size(int64_t n);
 int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *keys,
                      int32_t *members, int64_t *n_buckets_host, void *workspace,
@@ -228,6 +259,25 @@ int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *fi
                         const mfseg_points *pts, const int32_t *point_slot, double *stats,
                         void *workspace, size_t workspace_bytes, void *stream);
 
+/* feature_stats in steps, for samples sharded over ranks (the caller reduces
+ * `partial` across ranks between the steps).  partial [n_slots][18] uint64:
+ *   [0..1] point-value sum, [2..3] field-value sum (128-bit fixed point, lo/hi),
+ *   [4..5] point, [6..7] field sums of squared deviations from the mean (same),
+ *   [8] n_points, [9] n_fields, [10..13] bbox minima, [14..17] bbox maxima as
+ *   order-preserving keys of the doubles (unsigned min / max).
+ * pass 0 initialises `partial` and adds sums, counts and bbox; pass 1 adds the
+ * squared deviations from `mean` [n_slots][2] (point, field), which
+ * mfseg_feature_stats_means derives from the (reduced) pass-0 words;
+ * mfseg_feature_stats_final writes the MFSEG_STAT_WORDS rows.  Integer sums make
+ * the result independent of the sharding.  Synchronises (pass). */
+#define MFSEG_STAT_PARTIAL_WORDS 18
+int mfseg_feature_stats_pass(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
+                             const mfseg_points *pts, const int32_t *point_slot, int32_t pass,
+                             const double *mean, uint64_t *partial, void *stream);
+int mfseg_feature_stats_means(int32_t n_slots, const uint64_t *partial, double *mean, void *stream);
+int mfseg_feature_stats_final(int32_t n_slots, const uint64_t *partial, const double *mean,
+                              double *stats, void *stream);
+
 /* ---------------------------------------------------------------- multi-GPU
  * acc [n_words] 128-bit (lo,hi) pairs <-> 3 limbs of 42 bits, for SUM
  * all-reduce across ranks (exact for up to 2^20 ranks). */
@@ -249,6 +299,13 @@ typedef struct mfseg_synth {
 int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream);
 int mfseg_synth_points(const mfseg_synth *s, int64_t *traj_id, double *t, double *xyz,
                        double *value, void *stream);
+/* Windows of the same datasets (multi-GPU slabs generate only their share):
+ * timesteps [m0, m1) x z-planes [z0, z1) of the field ([m][z][y][x], x fastest),
+ * trajectories [p0, p1) x timesteps [m0, m1) of the points (trajectory-major). */
+int mfseg_synth_field_window(const mfseg_synth *s, int32_t m0, int32_t m1, int32_t z0, int32_t z1,
+                             double *values, void *stream);
+int mfseg_synth_points_window(const mfseg_synth *s, int64_t p0, int64_t p1, int32_t m0, int32_t m1,
+                              int64_t *traj_id, double *t, double *xyz, double *value, void *stream);
 
 #ifdef __cplusplus
 }

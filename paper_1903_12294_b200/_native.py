@@ -8,6 +8,7 @@ raises.  Device buffers are torch tensors; only raw pointers cross the ABI.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -15,9 +16,10 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmfseg_sm100.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 ACC_WORDS = 16
 STAT_WORDS = 14
+STAT_PARTIAL_WORDS = 18
 
 vp = C.c_void_p
 i32 = C.c_int32
@@ -34,7 +36,7 @@ class Params(C.Structure):
 
 class Field(C.Structure):
     _fields_ = [("nx", i32), ("ny", i32), ("nz", i32), ("nt", i32), ("origin", f64 * 3),
-                ("spacing", f64 * 3), ("times", vp), ("values", vp)]
+                ("spacing", f64 * 3), ("times", vp), ("values", vp), ("offset", i32 * 3)]
 
 
 class Points(C.Structure):
@@ -60,6 +62,7 @@ _SIGNATURES = {
     "mfseg_last_error": (C.c_char_p, []),
     "mfseg_abi_version": (C.c_int, []),
     "mfseg_launch_count": (C.c_longlong, []),
+    "mfseg_set_debug_options": (C.c_int, [i32, i64]),
     "mfseg_timing_enable": (None, [i32]),
     "mfseg_timing_read": (i32, [P(f64), i32]),
     "mfseg_run_workspace_size": (szt, [P(Params), P(Field), P(Points)]),
@@ -86,10 +89,16 @@ _SIGNATURES = {
     "mfseg_voxel_csr": (C.c_int, [vp, i32, i64, vp, i32, i32, vp, vp, vp, szt, vp]),
     "mfseg_feature_stats_workspace_size": (szt, [i32]),
     "mfseg_feature_stats": (C.c_int, [i32, P(Field), vp, P(Points), vp, vp, vp, szt, vp]),
+    "mfseg_traj_split_stride": (C.c_int, [i64, vp, vp, vp, f64, vp, vp, P(i64), vp, szt, vp]),
+    "mfseg_feature_stats_pass": (C.c_int, [i32, P(Field), vp, P(Points), vp, i32, vp, vp, vp]),
+    "mfseg_feature_stats_means": (C.c_int, [i32, vp, vp, vp]),
+    "mfseg_feature_stats_final": (C.c_int, [i32, vp, vp, vp, vp]),
     "mfseg_acc_to_limbs": (C.c_int, [vp, i64, vp, vp]),
     "mfseg_limbs_to_acc": (C.c_int, [vp, i64, vp, vp]),
     "mfseg_synth_field": (C.c_int, [P(Synth), vp, vp]),
     "mfseg_synth_points": (C.c_int, [P(Synth), vp, vp, vp, vp, vp]),
+    "mfseg_synth_field_window": (C.c_int, [P(Synth), i32, i32, i32, i32, vp, vp]),
+    "mfseg_synth_points_window": (C.c_int, [P(Synth), i64, i64, i32, i32, vp, vp, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -129,6 +138,36 @@ def check(rc: int, what: str) -> None:
         if rc == 2:
             raise ValueError(f"{what}: {msg}")
         raise NativeError(f"{what} failed (code {rc}): {msg}")
+
+
+# mfseg_set_debug_options flags (include/mfseg_sm100.h); results never depend on them
+DEBUG_NO_CULL = 1
+DEBUG_EXACT = 2
+DEBUG_STATS = 8
+DEBUG_NO_REUSE = 16
+DEBUG_NO_MARGIN_REUSE = 32
+
+
+@contextlib.contextmanager
+def debug_options(flags: int = 0, multi_cap: int = -1):
+    """Diagnostics / test knobs for library calls made by this thread inside the
+    block (the library itself reads no environment variables)."""
+    lib = load()
+    lib.mfseg_set_debug_options(int(flags), int(multi_cap))
+    try:
+        yield
+    finally:
+        lib.mfseg_set_debug_options(0, -1)
+
+
+def debug_options_from_env() -> None:
+    """tools/: map the MFSEG_DEBUG / MFSEG_NO_REUSE / MFSEG_NO_MARGIN_REUSE /
+    MFSEG_MULTI_CAP environment variables onto this thread's debug options."""
+    env = os.environ
+    flags = int(env.get("MFSEG_DEBUG", "0") or 0)
+    flags |= DEBUG_NO_REUSE if env.get("MFSEG_NO_REUSE") else 0
+    flags |= DEBUG_NO_MARGIN_REUSE if env.get("MFSEG_NO_MARGIN_REUSE") else 0
+    load().mfseg_set_debug_options(flags, int(env.get("MFSEG_MULTI_CAP", "-1")))
 
 
 def ptr(t) -> int:

@@ -694,17 +694,17 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         double cv;
         unsigned long long *dst;
         if (tid < BX) {
-            cv = cell_coord(a.ox, a.sx, X.start + min(tid, X.len - 1));
+            cv = cell_coord(a.ox, a.sx, a.x0 + X.start + min(tid, X.len - 1));
             S.x[tid] = cv;
             dst = S.xf[tid];
         } else if (tid < OZ) {
             const int i = tid - BX;
-            cv = cell_coord(a.oy, a.sy, Y.start + min(i, Y.len - 1));
+            cv = cell_coord(a.oy, a.sy, a.y0 + Y.start + min(i, Y.len - 1));
             S.y[i] = cv;
             dst = S.yf[i];
         } else if (tid < OT) {
             const int i = tid - OZ;
-            cv = cell_coord(a.oz, a.sz, Z.start + min(i, Z.len - 1));
+            cv = cell_coord(a.oz, a.sz, a.z0 + Z.start + min(i, Z.len - 1));
             S.z[i] = cv;
             dst = S.zf[i];
         } else {
@@ -988,6 +988,8 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
     const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], T = a.tt[tti];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long plane = (long long)a.ny * a.nx, vol = plane * a.nz;
+    double amax = 0.0;   // max |value| and non-finite flag (range check of the fixed-point sums)
+    bool bad = false;
 #pragma unroll 4
     for (int bi = w; bi < 64; bi += NW) {   // unrolled: several bricks' loads in flight
         const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
@@ -1006,6 +1008,8 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
             if (live) {
                 lo = fminf(lo, (float)v);
                 hi = fmaxf(hi, (float)v);
+                amax = fmax(amax, fabs(v));
+                bad |= !isfinite(v);
             }
         }
         vs = warp_sum_d(vs);
@@ -1021,11 +1025,18 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
             a.bsum_out[(size_t)blockIdx.x * 64 + bi] = make_ulonglong2(flo, (unsigned long long)fhi);
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0 && a.absmax) {
+        atomicMax(a.absmax + 5, (unsigned long long)__double_as_longlong(amax));
+        if (bad) atomicOr(a.absmax + 6, 1ull);
+    }
 }
 
 int launch_brick_pre(const FieldArgs &a, cudaStream_t st) {
     const long long n = (long long)a.ntx * a.nty * a.ntz * a.ntt;
-    if (n <= 0 || field_version() != 5) return 0;
+    if (n <= 0) return 0;
     ::mfseg::count_launch();
     k_brick_pre<<<(unsigned)n, NT, 0, st>>>(a);
     MFSEG_LAUNCH("k_brick_pre");

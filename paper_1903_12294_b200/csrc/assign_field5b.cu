@@ -103,9 +103,9 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             fv[k] = (float)vk;
         }
         // sample coordinates (reference formula); index clamped for dead lanes
-        const double px = cell_coord(a.ox, a.sx, it.x0 + min(lxr, ex - 1));
-        const double py = cell_coord(a.oy, a.sy, it.y0 + min(lyr, ey - 1));
-        if (lane < 4) Q.pz[lane] = cell_coord(a.oz, a.sz, gz0 + min(lane, ez - 1));
+        const double px = cell_coord(a.ox, a.sx, a.x0 + it.x0 + min(lxr, ex - 1));
+        const double py = cell_coord(a.oy, a.sy, a.y0 + it.y0 + min(lyr, ey - 1));
+        if (lane < 4) Q.pz[lane] = cell_coord(a.oz, a.sz, a.z0 + gz0 + min(lane, ez - 1));
         else if (lane < 6) Q.pt[lane - 4] = a.times[gt0 + min(lane - 4, et - 1)];
         const double *pz = Q.pz, *pt = Q.pt;
         // stage the kept candidates; largest |cv| among them (certification's W)

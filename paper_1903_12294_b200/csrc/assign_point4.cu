@@ -713,9 +713,11 @@ __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const in
                                                       double *v, const unsigned *perm,
                                                       const double *gxyz, const double *gt,
                                                       const double *gv, double cf, double *box,
-                                                      WBox *out) {
+                                                      WBox *out, unsigned long long *absmax) {
     constexpr int TPW = POINT_CHUNK / 64 / 8;   // warp tiles per warp
     __shared__ double red[8][8];
+    __shared__ double amax_s[8][5];
+    __shared__ int bad_s;
     __shared__ double o[4];
     const long long tile = blockIdx.x;
     if (tile >= *n_tiles) return;
@@ -760,6 +762,32 @@ __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const in
                     v[p] = P[j][q][4];
                 }
             }
+    }
+    {   // range check of the fixed-point sums: max |x|, |y|, |z|, |t|, |v| and non-finite inputs
+        if (tid == 0) bad_s = 0;
+        bool bad = false;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            double m = 0.0;
+#pragma unroll
+            for (int j = 0; j < TPW; ++j)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    m = fmax(m, fabs(P[j][q][d]));
+                    bad |= !isfinite(P[j][q][d]);
+                }
+            m = wmax_d(m);
+            if (lane == 0) amax_s[w][d] = m;
+        }
+        __syncthreads();
+        if (bad) bad_s = 1;
+        __syncthreads();
+        if (tid < 5) {
+            double m = amax_s[0][tid];
+            for (int q = 1; q < 8; ++q) m = fmax(m, amax_s[q][tid]);
+            atomicMax(absmax + tid, (unsigned long long)__double_as_longlong(m));
+        }
+        if (tid == 0 && bad_s) atomicOr(absmax + 6, 1ull);
     }
     double lo[4], hi[4];
 #pragma unroll
@@ -842,7 +870,7 @@ __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const in
     }
 }
 
-int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, double *x, double *y,
+int launch_tile_box(unsigned long long *absmax, const int4 *tiles, const int *n_tiles, long long max_tiles, double *x, double *y,
                     double *z, double *t, double *v, double cf, double *box, WBox *wbox,
                     const unsigned *perm, const double *gxyz, const double *gt, const double *gv,
                     cudaStream_t st) {
@@ -854,10 +882,10 @@ int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, 
     ::mfseg::count_launch();
     if (perm)
         k_chunk_boxes<true><<<(unsigned)max_tiles, 256, 0, st>>>(tiles, n_tiles, x, y, z, t, v, perm, gxyz,
-                                                                 gt, gv, cf, box, wbox);
+                                                                 gt, gv, cf, box, wbox, absmax);
     else
         k_chunk_boxes<false><<<(unsigned)max_tiles, 256, 0, st>>>(tiles, n_tiles, x, y, z, t, v, nullptr,
-                                                                  nullptr, nullptr, nullptr, cf, box, wbox);
+                                                                  nullptr, nullptr, nullptr, cf, box, wbox, absmax);
     MFSEG_LAUNCH("k_chunk_boxes");
     return 0;
 }

@@ -50,9 +50,12 @@ struct Carver {
     char *base;
     size_t off, cap;
     explicit Carver(void *b = nullptr, size_t c = 0) : base((char *)b), off(0), cap(c) {}
+    // every carving is 256-byte aligned in absolute address (the caller's
+    // workspace pointer need not be aligned: the size queries include 256 B of slack)
     template <class T>
     T *take(size_t n) {
-        size_t a = (off + 255) & ~size_t(255);
+        const size_t b = (size_t)(uintptr_t)base;
+        size_t a = ((b + off + 255) & ~size_t(255)) - b;
         off = a + sizeof(T) * (n > 0 ? n : 1);
         return base ? (T *)(base + a) : nullptr;
     }

@@ -31,20 +31,20 @@ __global__ void k_center_bins(int K, const double *x, const double *y, const dou
 }
 
 // first index i in [0, n) with fl(c - x_i) <= C  (n if none)
-__device__ int first_le(double c, double C, double o, double s, int n) {
+__device__ int first_le(double c, double C, double o, double s, int off, int n) {
     int a = 0, b = n;
     while (a < b) {
         int mid = (a + b) >> 1;
-        if (DSUB(c, cell_coord(o, s, mid)) <= C) b = mid; else a = mid + 1;
+        if (DSUB(c, cell_coord(o, s, (long long)off + mid)) <= C) b = mid; else a = mid + 1;
     }
     return a;
 }
 // last index i with fl(c - x_i) >= -C  (-1 if none)
-__device__ int last_ge(double c, double C, double o, double s, int n) {
+__device__ int last_ge(double c, double C, double o, double s, int off, int n) {
     int a = 0, b = n;   // first i with fl(c - x_i) < -C
     while (a < b) {
         int mid = (a + b) >> 1;
-        if (DSUB(c, cell_coord(o, s, mid)) < -C) b = mid; else a = mid + 1;
+        if (DSUB(c, cell_coord(o, s, (long long)off + mid)) < -C) b = mid; else a = mid + 1;
     }
     return a - 1;
 }
@@ -68,6 +68,7 @@ __device__ int last_ge_t(double c, double C, const double *tt, int n) {
 struct FieldGeom {
     int nx, ny, nz, nt;
     double ox, oy, oz, sx, sy, sz;
+    int x0, y0, z0;   // global index of the first cell (spatial slabs); vbox is local
     const double *times;
 };
 
@@ -76,12 +77,12 @@ __global__ void k_center_vbox(int K, const double *x, const double *y, const dou
     int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= K) return;
     int4 a, b;
-    a.x = first_le(x[c], C.x, fg.ox, fg.sx, fg.nx);
-    a.y = last_ge(x[c], C.x, fg.ox, fg.sx, fg.nx);
-    a.z = first_le(y[c], C.y, fg.oy, fg.sy, fg.ny);
-    a.w = last_ge(y[c], C.y, fg.oy, fg.sy, fg.ny);
-    b.x = first_le(z[c], C.z, fg.oz, fg.sz, fg.nz);
-    b.y = last_ge(z[c], C.z, fg.oz, fg.sz, fg.nz);
+    a.x = first_le(x[c], C.x, fg.ox, fg.sx, fg.x0, fg.nx);
+    a.y = last_ge(x[c], C.x, fg.ox, fg.sx, fg.x0, fg.nx);
+    a.z = first_le(y[c], C.y, fg.oy, fg.sy, fg.y0, fg.ny);
+    a.w = last_ge(y[c], C.y, fg.oy, fg.sy, fg.y0, fg.ny);
+    b.x = first_le(z[c], C.z, fg.oz, fg.sz, fg.z0, fg.nz);
+    b.y = last_ge(z[c], C.z, fg.oz, fg.sz, fg.z0, fg.nz);
     b.z = first_le_t(t[c], C.w, fg.times, fg.nt);
     b.w = last_ge_t(t[c], C.w, fg.times, fg.nt);
     vbox[2 * c] = a;
@@ -228,7 +229,8 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
     k_cand_fill<<<gb, B, 0, st>>>(NB, k, g.bin_start, g.bin_ids, g.cand_start, g.cand_ids);
     if (f && f->nt > 0 && K > 0) {
         FieldGeom fg{f->nx, f->ny, f->nz, f->nt, f->origin[0], f->origin[1], f->origin[2],
-                     f->spacing[0], f->spacing[1], f->spacing[2], f->times};
+                     f->spacing[0], f->spacing[1], f->spacing[2], f->offset[0], f->offset[1],
+                     f->offset[2], f->times};
         ::mfseg::count_launch();
         k_center_vbox<<<gk, B, 0, st>>>(K, x, y, z, t, C, fg, g.vbox);
     }

@@ -19,6 +19,7 @@ struct MultiItem {
 struct FieldArgs {
     int nx, ny, nz, nt;
     double ox, oy, oz, sx, sy, sz;
+    int x0, y0, z0;       // global cell index of the field's first cell (spatial slabs)
     const double *times;
     const double *values;
     const AxisTile *xt, *yt, *zt;
@@ -41,6 +42,7 @@ struct FieldArgs {
     unsigned long long *n_deferred;
     long long deferred_cap;
     int *overflow;
+    unsigned long long *absmax;   // k_brick_pre: [5] max |value| (double bits), [6] non-finite flag
     int accumulate;
     int debug;   // bit0: no warp culling, bit1: exact evaluation of every survivor, bit3: stats
     unsigned long long *stats;   // debug bit3: [0] bricks, [1] kept candidates, [2] exact samples
@@ -119,6 +121,7 @@ struct FallbackArgs {
     int nx, ny, nz, nt;
     double ox, oy, oz, sx, sy, sz;
     const double *times, *values;
+    int x0, y0, z0;                    // global cell index of the field's first cell (slabs)
     const double *px, *py, *pz, *pt, *pv;
     long long n_samples;
     int *labels;
@@ -130,9 +133,6 @@ struct FallbackArgs {
     int accumulate;
 };
 
-// points per point tile: k_point_assign3 = 128 threads x 2 points (and the
-// v1 kernel's 128 x 2); the runtime cuts tiles with this size.
-constexpr int POINT_TILE = 256;
 // points per chunk of k_point_assign4 (8 warps x 4 warp tiles of 64 points)
 constexpr int POINT_CHUNK = 2048;
 
@@ -143,13 +143,16 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
                const mfseg_params *p, const mfseg_field *f, int *count_tmp, void *scan_tmp,
                cudaStream_t st);
 // assign.cu
+struct DebugOptions {   // mfseg_set_debug_options (thread-local; defaults = product behaviour)
+    int flags = 0;
+    long long multi_cap = -1;
+};
+const DebugOptions &debug_options();
 int field_tile_dims(int *tx, int *ty, int *tz);
-int field_version();
 int launch_brick_pre(const FieldArgs &a, cudaStream_t st);
 int launch_field_screen(const FieldArgs &a, cudaStream_t st);
 int point_tile_size();
-int point_version();
-int launch_tile_box(const int4 *tiles, const int *n_tiles, long long max_tiles, double *x, double *y,
+int launch_tile_box(unsigned long long *absmax, const int4 *tiles, const int *n_tiles, long long max_tiles, double *x, double *y,
                     double *z, double *t, double *v, double cf, double *box, WBox *wbox,
                     const unsigned *perm, const double *gxyz, const double *gt, const double *gv,
                     cudaStream_t st);

@@ -268,6 +268,7 @@ struct StatArgs {
     long long nf, ncell;
     int nx, ny, nz;
     double ox, oy, oz, sx, sy, sz;
+    int x0, y0, z0;   // global index of the first cell (spatial slabs)
     const double *times, *values;
     const int *fslot;
     long long np;
@@ -292,9 +293,9 @@ __global__ void k_stats(StatArgs a, int pass) {
                 if (slot >= 0) {
                     long long r = q % a.ncell;
                     long long m = q / a.ncell;
-                    x = cell_coord(a.ox, a.sx, r % a.nx);
-                    y = cell_coord(a.oy, a.sy, (r / a.nx) % a.ny);
-                    z = cell_coord(a.oz, a.sz, r / ((long long)a.nx * a.ny));
+                    x = cell_coord(a.ox, a.sx, a.x0 + r % a.nx);
+                    y = cell_coord(a.oy, a.sy, a.y0 + (r / a.nx) % a.ny);
+                    z = cell_coord(a.oz, a.sz, a.z0 + r / ((long long)a.nx * a.ny));
                     t = a.times[m];
                     v = a.values[q];
                 }
@@ -662,6 +663,9 @@ int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *fi
         a.ox = f->origin[0];
         a.oy = f->origin[1];
         a.oz = f->origin[2];
+        a.x0 = f->offset[0];
+        a.y0 = f->offset[1];
+        a.z0 = f->offset[2];
         a.sx = f->spacing[0];
         a.sy = f->spacing[1];
         a.sz = f->spacing[2];
@@ -699,6 +703,91 @@ int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *fi
     return 0;
 }
 
+static void stat_args(StatArgs &a, int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
+                      const mfseg_points *pts, const int32_t *point_slot) {
+    memset(&a, 0, sizeof a);
+    a.n_slots = n_slots;
+    if (f && f->nt > 0 && field_slot) {
+        a.ncell = (long long)f->nx * f->ny * f->nz;
+        a.nf = a.ncell * f->nt;
+        a.nx = f->nx;
+        a.ny = f->ny;
+        a.nz = f->nz;
+        a.ox = f->origin[0];
+        a.oy = f->origin[1];
+        a.oz = f->origin[2];
+        a.x0 = f->offset[0];
+        a.y0 = f->offset[1];
+        a.z0 = f->offset[2];
+        a.sx = f->spacing[0];
+        a.sy = f->spacing[1];
+        a.sz = f->spacing[2];
+        a.times = f->times;
+        a.values = f->values;
+        a.fslot = field_slot;
+    }
+    if (pts && pts->n > 0 && point_slot) {
+        a.np = pts->n;
+        a.xyz = pts->xyz;
+        a.pt = pts->t;
+        a.pv = pts->value;
+        a.pslot = point_slot;
+    }
+}
+
+int mfseg_feature_stats_pass(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
+                             const mfseg_points *pts, const int32_t *point_slot, int32_t pass,
+                             const double *mean, uint64_t *partial, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_slots <= 0) return 0;
+    if (pass != 0 && pass != 1) {
+        set_error("feature_stats_pass: pass must be 0 or 1");
+        return 2;
+    }
+    int *ovf = nullptr, *ovf_h = nullptr;
+    MFSEG_TRY(tiny_scratch((void **)&ovf, (void **)&ovf_h));
+    StatArgs a;
+    stat_args(a, n_slots, f, field_slot, pts, point_slot);
+    a.S = (unsigned long long *)partial;
+    a.mean = mean;
+    a.ovf = ovf;
+    unsigned gs = (unsigned)((n_slots + 255) / 256);
+    MFSEG_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+    if (pass == 0) {
+        ::mfseg::count_launch();
+        k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
+    }
+    ::mfseg::count_launch();
+    k_stats<<<148 * 8, 256, 0, st>>>(a, pass);
+    MFSEG_LAUNCH("feature_stats_pass");
+    MFSEG_CUDA(cudaMemcpyAsync(ovf_h, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (*ovf_h) {
+        set_error("feature_stats: fixed-point overflow");
+        return 4;
+    }
+    return 0;
+}
+
+int mfseg_feature_stats_means(int32_t n_slots, const uint64_t *partial, double *mean, void *stream) {
+    if (n_slots <= 0) return 0;
+    ::mfseg::count_launch();
+    k_stats_means<<<(unsigned)((n_slots + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n_slots, (const unsigned long long *)partial, mean);
+    MFSEG_LAUNCH("k_stats_means");
+    return 0;
+}
+
+int mfseg_feature_stats_final(int32_t n_slots, const uint64_t *partial, const double *mean,
+                              double *stats, void *stream) {
+    if (n_slots <= 0) return 0;
+    ::mfseg::count_launch();
+    k_stats_final<<<(unsigned)((n_slots + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n_slots, (const unsigned long long *)partial, mean, stats);
+    MFSEG_LAUNCH("k_stats_final");
+    return 0;
+}
+
 size_t mfseg_link_index_workspace_size(int64_t n) {
     Carver cv;
     cv.take<unsigned long long>(n);
@@ -716,6 +805,10 @@ int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *key
     long long n = pts ? pts->n : 0;
     if (n_buckets_host) *n_buckets_host = 0;
     if (n <= 0) return 0;
+    if (f->offset[0] || f->offset[1] || f->offset[2]) {
+        set_error("link_index: the field must be a whole grid (offset 0)");
+        return 2;
+    }
     if (workspace_bytes < mfseg_link_index_workspace_size(n)) {
         set_error("link_index: workspace too small");
         return 3;
@@ -772,9 +865,10 @@ size_t mfseg_traj_split_workspace_size(int64_t n) {
     return cv.off + 256;
 }
 
-int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const int32_t *label,
-                     int32_t *order, int32_t *run_start, int64_t *n_runs_host, double *stride_host,
-                     void *workspace, size_t workspace_bytes, void *stream) {
+static int traj_split_impl(int64_t n, const int64_t *traj_id, const double *t,
+                           const int32_t *label, const double *stride_in, int32_t *order,
+                           int32_t *run_start, int64_t *n_runs_host, double *stride_host,
+                           void *workspace, size_t workspace_bytes, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n_runs_host) *n_runs_host = 0;
     if (n <= 0) return 0;
@@ -823,6 +917,7 @@ int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const i
     MFSEG_CUDA(cudaStreamSynchronize(st));
     double stride;
     memcpy(&stride, &h[0], sizeof stride);   // +inf when fewer than two unique times
+    if (stride_in) stride = *stride_in;      // sharded: the stride of all ranks' times
     const long long tmin = (long long)(h[1] ^ 0x8000000000000000ull);
     const long long tmax = (long long)(h[2] ^ 0x8000000000000000ull);
     const unsigned long long range = (unsigned long long)tmax - (unsigned long long)tmin;
@@ -857,6 +952,21 @@ int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const i
     if (n_runs_host) *n_runs_host = nr;
     if (stride_host) *stride_host = stride;
     return 0;
+}
+
+int mfseg_traj_split(int64_t n, const int64_t *traj_id, const double *t, const int32_t *label,
+                     int32_t *order, int32_t *run_start, int64_t *n_runs_host, double *stride_host,
+                     void *workspace, size_t workspace_bytes, void *stream) {
+    return traj_split_impl(n, traj_id, t, label, nullptr, order, run_start, n_runs_host,
+                           stride_host, workspace, workspace_bytes, stream);
+}
+
+int mfseg_traj_split_stride(int64_t n, const int64_t *traj_id, const double *t,
+                            const int32_t *label, double stride, int32_t *order,
+                            int32_t *run_start, int64_t *n_runs_host, void *workspace,
+                            size_t workspace_bytes, void *stream) {
+    return traj_split_impl(n, traj_id, t, label, &stride, order, run_start, n_runs_host, nullptr,
+                           workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

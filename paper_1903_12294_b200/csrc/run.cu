@@ -1,6 +1,7 @@
 // Host-side runtime of the segmentation core: workspace plan, point binning,
 // field tiling, the pass loop of engine.run (engine.py:323-381) and the C ABI.
 #include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -43,6 +44,12 @@ static void harvest() {
         if (cudaEventElapsedTime(&t, g_ev[i], g_ev[i + 1]) == cudaSuccess) g_timer.ms[i] += t;
     g_timer.passes++;
 }
+
+// ------------------------------------------------------------------ debug options
+// Diagnostics and test knobs (mfseg_set_debug_options), per calling thread;
+// the defaults are the product behaviour.
+static thread_local DebugOptions g_dbg;
+const DebugOptions &debug_options() { return g_dbg; }
 
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_err;
@@ -141,39 +148,6 @@ __global__ void k_point_keys(long long n, const double *xyz, const double *t, do
     vals[i] = (unsigned)i;
 }
 
-// random gather of the points into bin-sorted SoA; 4 points per thread with
-// every load issued before the stores (memory-level parallelism)
-constexpr int GATHER_PER_THREAD = 16;
-__global__ void k_point_gather(long long n, const unsigned *perm, const double *xyz,
-                               const double *t, const double *value, double *px, double *py,
-                               double *pz, double *pt, double *pv) {
-    const long long base = (blockIdx.x * (long long)blockDim.x) * GATHER_PER_THREAD + threadIdx.x;
-    double r[GATHER_PER_THREAD][5];
-#pragma unroll
-    for (int q = 0; q < GATHER_PER_THREAD; ++q) {
-        const long long i = base + (long long)q * blockDim.x;
-        if (i < n) {
-            const long long j = perm[i];
-            r[q][0] = __ldg(xyz + 3 * j);
-            r[q][1] = __ldg(xyz + 3 * j + 1);
-            r[q][2] = __ldg(xyz + 3 * j + 2);
-            r[q][3] = __ldg(t + j);
-            r[q][4] = __ldg(value + j);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < GATHER_PER_THREAD; ++q) {
-        const long long i = base + (long long)q * blockDim.x;
-        if (i < n) {
-            px[i] = r[q][0];
-            py[i] = r[q][1];
-            pz[i] = r[q][2];
-            pt[i] = r[q][3];
-            pv[i] = r[q][4];
-        }
-    }
-}
-
 // Group starts of the sorted keys by boundary detection (no atomics: sorted keys
 // would serialise a histogram on the same counters).  Thread i in [0, n] writes
 // first[q] = i for every group q in (group(i-1), group(i)]; group(n) = ng.
@@ -232,13 +206,17 @@ __global__ void k_copy_state(int K, mfseg_centers s, mfseg_centers d) {
 
 __global__ void k_minmax(const double *v, long long n, unsigned long long *mm) {
     // mm[0] = ordered-bits min, mm[1] = ordered-bits max (total order on doubles)
+    // mm[2] = non-zero when a value is NaN or +-inf
     double lo = __builtin_huge_val(), hi = -__builtin_huge_val();
+    bool bad = false;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         double x = v[i];
         lo = fmin(lo, x);
         hi = fmax(hi, x);
+        bad |= !isfinite(x);
     }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&mm[2], 1ull);
     for (int o = 16; o > 0; o >>= 1) {
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -312,6 +290,8 @@ struct Plan {
     unsigned char *tslot;           // per point warp tile: slot of its single label last pass
     long long *stranded_f, *deferred_f;
     long long cap_f;
+    unsigned long long *absmax;     // [0..3] max |point x, y, z, t|, [4] |point v|, [5] |field v|
+                                    // (double bits), [6] non-finite input flag
     unsigned long long *counters;   // [0] field stranded, [1] point stranded
     int *overflow;
     // points
@@ -332,21 +312,24 @@ struct Plan {
     size_t scan_bytes;
 };
 
-std::vector<AxisTile> axis_tiles(int n, double o, double s, double mn, double C, int k, int T) {
+// tiles of <= T cells along one axis that never straddle a bin boundary; `off` =
+// global index of the first local cell (spatial slabs: a slab that starts on a
+// bin boundary gets exactly the tiles of the whole grid)
+std::vector<AxisTile> axis_tiles(int n, double o, double s, int off, double mn, double C, int k, int T) {
     std::vector<AxisTile> v;
     int i = 0;
     while (i < n) {
-        int b = bin_coord(cell_coord(o, s, i), mn, C, k);
+        int b = bin_coord(cell_coord(o, s, (long long)off + i), mn, C, k);
         int j = i;
-        while (j < n && j - i < T && bin_coord(cell_coord(o, s, j), mn, C, k) == b) ++j;
+        while (j < n && j - i < T && bin_coord(cell_coord(o, s, (long long)off + j), mn, C, k) == b) ++j;
         v.push_back(AxisTile{i, j - i, b, 0});
         i = j;
     }
     return v;
 }
 
-long long axis_tile_count(int n, double o, double s, double mn, double C, int k, int T) {
-    return (long long)axis_tiles(n, o, s, mn, C, k, T).size();
+long long axis_tile_count(int n, double o, double s, int off, double mn, double C, int k, int T) {
+    return (long long)axis_tiles(n, o, s, off, mn, C, k, T).size();
 }
 
 int check_inputs(const mfseg_params *p, const mfseg_field *f, const mfseg_points *pts) {
@@ -366,6 +349,10 @@ int check_inputs(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     }
     if (f && f->nt > 0 && (f->nx < 1 || f->ny < 1 || f->nz < 1)) {
         set_error("invalid field dims");
+        return 2;
+    }
+    if (f && f->nt > 0 && (f->offset[0] < 0 || f->offset[1] < 0 || f->offset[2] < 0)) {
+        set_error("invalid field offset (global index of the first cell must be >= 0)");
         return 2;
     }
     if (pts && pts->n >= (1ll << 31)) {
@@ -395,6 +382,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     int NB = P.NB;
     P.g = grid_carve(cv, K, NB, &P.count_tmp, &P.grid_scan_tmp);
     P.counters = cv.take<unsigned long long>(40);   // [8..40): debug stats
+    P.absmax = cv.take<unsigned long long>(8);
     P.overflow = cv.take<int>(4);
     // field
     P.nf = (P.f.nt > 0) ? (long long)P.f.nx * P.f.ny * P.f.nz * P.f.nt : 0;
@@ -402,11 +390,11 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     field_tile_dims(&TX, &TY, &TZ);
     P.ntx = P.nty = P.ntz = 0;
     if (P.nf > 0) {
-        P.ntx = (int)axis_tile_count(P.f.nx, P.f.origin[0], P.f.spacing[0], P.p.mins[0], P.p.C[0],
+        P.ntx = (int)axis_tile_count(P.f.nx, P.f.origin[0], P.f.spacing[0], P.f.offset[0], P.p.mins[0], P.p.C[0],
                                      P.p.k[0], TX);
-        P.nty = (int)axis_tile_count(P.f.ny, P.f.origin[1], P.f.spacing[1], P.p.mins[1], P.p.C[1],
+        P.nty = (int)axis_tile_count(P.f.ny, P.f.origin[1], P.f.spacing[1], P.f.offset[1], P.p.mins[1], P.p.C[1],
                                      P.p.k[1], TY);
-        P.ntz = (int)axis_tile_count(P.f.nz, P.f.origin[2], P.f.spacing[2], P.p.mins[2], P.p.C[2],
+        P.ntz = (int)axis_tile_count(P.f.nz, P.f.origin[2], P.f.spacing[2], P.f.offset[2], P.p.mins[2], P.p.C[2],
                                      P.p.k[2], TZ);
     }
     P.xt = cv.take<AxisTile>(P.ntx);
@@ -495,16 +483,44 @@ int plan_init(Plan &P, const mfseg_params *p, const mfseg_field *f, const mfseg_
     return 0;
 }
 
+// Inputs must be finite, and every per-cluster sum must fit the
+// 128-bit fixed-point accumulators (2^-64 units, |sum| < 2^63): with m = the
+// largest |input| of a sum and n its sample count, m * n < 2^62 is required.
+int check_ranges(Plan &P, double field_coord_max) {
+    unsigned long long *h = nullptr;
+    void *d = nullptr;
+    MFSEG_TRY(tiny_scratch(&d, (void **)&h));
+    MFSEG_CUDA(cudaMemcpyAsync(h, P.absmax, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, P.st));
+    MFSEG_CUDA(cudaStreamSynchronize(P.st));
+    if (h[6]) {
+        set_error("non-finite (NaN or inf) sample value or coordinate");
+        return 2;
+    }
+    double m[6];
+    for (int i = 0; i < 6; ++i) memcpy(&m[i], &h[i], sizeof(double));
+    const double n = (double)(P.np + P.nf), lim = 0x1.0p62;
+    double coord = field_coord_max;
+    for (int i = 0; i < 4; ++i) coord = std::fmax(coord, m[i]);
+    if (coord * n >= lim || m[4] * (double)P.np >= lim || m[5] * (double)P.nf >= lim) {
+        set_error("sample coordinates or values too large for the exact 128-bit cluster sums "
+                  "(max |x| * samples must stay below 2^62): rescale or shift the inputs");
+        return 2;
+    }
+    return 0;
+}
+
 // once per run: field axis tiles, timestep bins, point binning + sort + tiles
 int plan_prepare(Plan &P) {
     cudaStream_t st = P.st;
     const mfseg_params &p = P.p;
+    MFSEG_CUDA(cudaMemsetAsync(P.absmax, 0, sizeof(unsigned long long) * 8, st));
+    double field_coord_max = 0.0;   // max |cell centre| and |time| of the field (host)
     if (P.nf > 0) {
         int TX, TY, TZ;
         field_tile_dims(&TX, &TY, &TZ);
-        auto xt = axis_tiles(P.f.nx, P.f.origin[0], P.f.spacing[0], p.mins[0], p.C[0], p.k[0], TX);
-        auto yt = axis_tiles(P.f.ny, P.f.origin[1], P.f.spacing[1], p.mins[1], p.C[1], p.k[1], TY);
-        auto zt = axis_tiles(P.f.nz, P.f.origin[2], P.f.spacing[2], p.mins[2], p.C[2], p.k[2], TZ);
+        auto xt = axis_tiles(P.f.nx, P.f.origin[0], P.f.spacing[0], P.f.offset[0], p.mins[0], p.C[0], p.k[0], TX);
+        auto yt = axis_tiles(P.f.ny, P.f.origin[1], P.f.spacing[1], P.f.offset[1], p.mins[1], p.C[1], p.k[1], TY);
+        auto zt = axis_tiles(P.f.nz, P.f.origin[2], P.f.spacing[2], P.f.offset[2], p.mins[2], p.C[2], p.k[2], TZ);
         MFSEG_CUDA(cudaMemcpyAsync(P.xt, xt.data(), sizeof(AxisTile) * xt.size(),
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaMemcpyAsync(P.yt, yt.data(), sizeof(AxisTile) * yt.size(),
@@ -526,6 +542,22 @@ int plan_prepare(Plan &P) {
             m0 = m1;
         }
         P.ntt = (int)tts.size();
+        for (int m = 0; m < P.f.nt; ++m) {
+            if (!std::isfinite(th[m])) {
+                set_error("non-finite field time");
+                return 2;
+            }
+            field_coord_max = std::fmax(field_coord_max, std::fabs(th[m]));
+        }
+        for (int d = 0; d < 3; ++d) {
+            const int n = d == 0 ? P.f.nx : d == 1 ? P.f.ny : P.f.nz;
+            if (!std::isfinite(P.f.origin[d]) || !std::isfinite(P.f.spacing[d])) {
+                set_error("non-finite field origin or spacing");
+                return 2;
+            }
+            field_coord_max = std::fmax(field_coord_max, std::fabs(cell_coord(P.f.origin[d], P.f.spacing[d], P.f.offset[d])));
+            field_coord_max = std::fmax(field_coord_max, std::fabs(cell_coord(P.f.origin[d], P.f.spacing[d], (long long)P.f.offset[d] + n - 1)));
+        }
         MFSEG_CUDA(cudaMemcpyAsync(P.tt, tts.data(), sizeof(AxisTile) * tts.size(),
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaStreamSynchronize(st));   // host vectors die at scope exit
@@ -552,6 +584,7 @@ int plan_prepare(Plan &P) {
             va.brange_out = P.brange;
             va.bsum_out = P.bsum;
             va.overflow = P.overflow;
+            va.absmax = P.absmax;
             MFSEG_TRY(launch_brick_pre(va, st));
         }
         if (P.bslot)
@@ -574,13 +607,6 @@ int plan_prepare(Plan &P) {
         }
         MFSEG_TRY(radix_sort_pairs(P.keys, P.vals, P.skeys, P.perm, n, P.key_bits, P.radix_tmp,
                                    P.radix_bytes, st));
-        const bool fused_gather = point_version() == 4;   // gathered chunk by chunk in k_chunk_boxes
-        if (!fused_gather) {
-            ::mfseg::count_launch();
-            k_point_gather<<<(unsigned)((n + 256 * GATHER_PER_THREAD - 1) / (256 * GATHER_PER_THREAD)), 256,
-                             0, st>>>(n, P.perm, P.pts.xyz, P.pts.t, P.pts.value, P.px, P.py, P.pz, P.pt,
-                                      P.pv);
-        }
         const int NG = P.ngroups;
         ::mfseg::count_launch();
         k_bin_first<<<(unsigned)((n + 256) / 256), 256, 0, st>>>(n, P.skeys, P.sub_bits, NG,
@@ -594,13 +620,13 @@ int plan_prepare(Plan &P) {
         ::mfseg::count_launch();
         k_make_tiles<<<gk, 256, 0, st>>>(NG, P.bcnt, P.bfirst, P.tstart, TP, P.nint, P.tiles);
         MFSEG_LAUNCH("point tiles");
-        if (fused_gather)
-            MFSEG_TRY(launch_tile_box(P.tiles, P.tstart + NG, P.max_tiles, P.px, P.py, P.pz, P.pt,
+        // the points are gathered into the bin-sorted SoA chunk by chunk here
+        MFSEG_TRY(launch_tile_box(P.absmax, P.tiles, P.tstart + NG, P.max_tiles, P.px, P.py, P.pz, P.pt,
                                       P.pv, p.c_f, P.tbox, P.wbox, P.perm, P.pts.xyz, P.pts.t,
                                       P.pts.value, st));
         MFSEG_CUDA(cudaMemsetAsync(P.tslot, 255, P.max_tiles * (POINT_CHUNK / 64), st));
     }
-    return 0;
+    return check_ranges(P, field_coord_max);
 }
 
 CentersView view_of(const mfseg_centers &s, int K) {
@@ -713,7 +739,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     CentersView cv = view_of(c, K);
     mark(0, st);
     // validity boxes of the previous pass (structural-change test of the reuse)
-    const bool reuse = prev && accumulate && getenv("MFSEG_NO_REUSE") == nullptr;
+    const DebugOptions &dbg = debug_options();
+    const bool reuse = prev && accumulate && !(dbg.flags & MFSEG_DEBUG_NO_REUSE);
     if (P.vbox_prev && P.nf > 0 && accumulate)
         MFSEG_CUDA(cudaMemcpyAsync(P.vbox_prev, P.g.vbox, sizeof(int4) * 2 * K, cudaMemcpyDeviceToDevice, st));
     MFSEG_TRY(grid_build(P.g, cv.x, cv.y, cv.z, cv.t, &p, P.nf > 0 ? &P.f : nullptr,
@@ -749,6 +776,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.ox = P.f.origin[0];
         a.oy = P.f.origin[1];
         a.oz = P.f.origin[2];
+        a.x0 = P.f.offset[0];
+        a.y0 = P.f.offset[1];
+        a.z0 = P.f.offset[2];
         a.sx = P.f.spacing[0];
         a.sy = P.f.spacing[1];
         a.sz = P.f.spacing[2];
@@ -788,27 +818,21 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.multi = P.multi;
         a.n_multi = P.counters + 4;
         a.multi_cap = P.multi_cap;
-        a.bslot = field_version() == 5 ? P.bslot : nullptr;
+        a.bslot = P.bslot;
         a.bmargin = a.bslot ? P.bmargin : nullptr;
         if (reuse && a.bslot) {
             a.reuse = 1;
             a.bin_stable = P.bstable;
-            a.bin_sstable = getenv("MFSEG_NO_MARGIN_REUSE") ? P.bstable : P.sstable;
+            a.bin_sstable = (dbg.flags & MFSEG_DEBUG_NO_MARGIN_REUSE) ? P.bstable : P.sstable;
             a.cdelta = P.cdelta;
         }
-        if (const char *mc = getenv("MFSEG_MULTI_CAP")) {   // test knob: a smaller brick queue
-            const long long cap = atoll(mc);
-            if (cap >= 0 && cap < a.multi_cap) a.multi_cap = cap;
-        }
+        if (dbg.multi_cap >= 0 && dbg.multi_cap < a.multi_cap) a.multi_cap = dbg.multi_cap;   // test knob
         a.overflow = P.overflow;
         a.accumulate = accumulate;
-        {
-            const char *dbg = getenv("MFSEG_DEBUG");
-            a.debug = dbg ? atoi(dbg) : 0;
-        }
+        a.debug = dbg.flags & MFSEG_DEBUG_KERNEL_BITS;
         long long ntiles = (long long)P.ntx * P.nty * P.ntz * P.f.nt;
         MFSEG_TRY(launch_field_assign(a, ntiles, st));
-        if (field_version() >= 5) MFSEG_TRY(launch_field_screen(a, st));
+        MFSEG_TRY(launch_field_screen(a, st));
     }
     mark(2, st);
     if (P.np > 0) {
@@ -844,17 +868,14 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.n_deferred = P.counters + 3;
         a.stats = P.counters + 16;
         a.deferred_cap = P.cap_p;
-        a.tslot = point_version() == 4 ? P.tslot : nullptr;
+        a.tslot = P.tslot;
         if (reuse && a.tslot) {
             a.reuse = 1;
             a.bin_stable = P.bstable;
         }
         a.overflow = P.overflow;
         a.accumulate = accumulate;
-        {
-            const char *dbg = getenv("MFSEG_DEBUG");
-            a.debug = dbg ? atoi(dbg) : 0;
-        }
+        a.debug = dbg.flags & MFSEG_DEBUG_KERNEL_BITS;
         MFSEG_TRY(launch_point_assign(a, P.max_tiles, st));
     }
     mark(3, st);
@@ -880,6 +901,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.ox = P.f.origin[0];
         a.oy = P.f.origin[1];
         a.oz = P.f.origin[2];
+        a.x0 = P.f.offset[0];
+        a.y0 = P.f.offset[1];
+        a.z0 = P.f.offset[2];
         a.sx = P.f.spacing[0];
         a.sy = P.f.spacing[1];
         a.sz = P.f.spacing[2];
@@ -905,8 +929,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         MFSEG_TRY(launch_fallback(a, st));
     }
     mark(4, st);
-    if (const char *dbg = getenv("MFSEG_DEBUG")) {
-        if (atoi(dbg) & 8) {
+    {
+        if (dbg.flags & MFSEG_DEBUG_STATS) {
             unsigned long long h[40];
             MFSEG_CUDA(cudaMemcpyAsync(h, P.counters, sizeof h, cudaMemcpyDeviceToHost, st));
             MFSEG_CUDA(cudaStreamSynchronize(st));
@@ -965,6 +989,12 @@ int32_t mfseg_timing_read(double *ms_out, int32_t n) {
     return mfseg::g_timer.passes;
 }
 int mfseg_abi_version(void) { return MFSEG_ABI_VERSION; }
+
+int mfseg_set_debug_options(int32_t flags, int64_t multi_cap) {
+    mfseg::g_dbg.flags = flags;
+    mfseg::g_dbg.multi_cap = multi_cap;
+    return 0;
+}
 
 size_t mfseg_run_workspace_size(const mfseg_params *p, const mfseg_field *f,
                                 const mfseg_points *pts) {
@@ -1139,13 +1169,17 @@ int mfseg_minmax_normalize(double *values, int64_t n, int32_t apply, double *lo_
     }
     unsigned long long *mm = nullptr, *h = nullptr;
     MFSEG_TRY(tiny_scratch((void **)&mm, (void **)&h));
-    const unsigned long long init[2] = {~0ull, 0ull};
-    MFSEG_CUDA(cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, st));
+    const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+    MFSEG_CUDA(cudaMemcpyAsync(mm, init, 24, cudaMemcpyHostToDevice, st));
     ::mfseg::count_launch();
     k_minmax<<<148 * 4, 256, 0, st>>>(values, n, mm);
     MFSEG_LAUNCH("k_minmax");
-    MFSEG_CUDA(cudaMemcpyAsync(h, mm, 16, cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaMemcpyAsync(h, mm, 24, cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (h[2]) {   // samples are finite
+        set_error("non-finite (NaN or inf) sample value");
+        return 2;
+    }
     double lo = unkey(h[0]), hi = unkey(h[1]);
     if (lo_host) *lo_host = lo;
     if (hi_host) *hi_host = hi;

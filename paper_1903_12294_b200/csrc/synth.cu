@@ -82,33 +82,39 @@ __device__ double noisy(double base, unsigned long long seed, unsigned long long
     return v;
 }
 
-__global__ void k_synth_field(mfseg_synth s, Blobs B, double *values) {
-    long long ncell = (long long)s.nx * s.ny * s.nz;
-    long long n = ncell * s.nt;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
-         q += (long long)gridDim.x * blockDim.x) {
-        long long r = q;
+// window [m0, m0 + wt) x [z0, z0 + wz) of the dataset's timesteps x z-planes;
+// every value depends only on its GLOBAL flat index q
+__global__ void k_synth_field(mfseg_synth s, Blobs B, int m0, int wt, int z0, int wz, double *values) {
+    const long long plane = (long long)s.nx * s.ny, ncell = plane * s.nz;
+    const long long n = plane * wz * wt;
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < n;
+         w += (long long)gridDim.x * blockDim.x) {
+        long long r = w;
         int i = (int)(r % s.nx);
         r /= s.nx;
         int j = (int)(r % s.ny);
         r /= s.ny;
-        int k = (int)(r % s.nz);
-        int m = (int)(r / s.nz);
+        int k = z0 + (int)(r % wz);
+        int m = m0 + (int)(r / wz);
+        const long long q = (long long)m * ncell + ((long long)k * s.ny + j) * s.nx + i;
         int b = blob_at(B, (double)i + 0.5, (double)j + 0.5, (double)k + 0.5, (double)m);
         double v = noisy(b >= 0 ? B.b[b].fv : 0.0, s.seed, (unsigned long long)q, s.noise, s.dyadic);
         if (s.dyadic && q < 2) v = (double)q;   // pin min 0 / max 1: normalization is the identity
-        values[q] = v;
+        values[w] = v;
     }
 }
 
-__global__ void k_synth_points(mfseg_synth s, Blobs B, long long *traj_id, double *t, double *xyz,
-                               double *value) {
-    long long n = s.n_traj * s.nt;
+// trajectories [p0, p0 + wp) x timesteps [m0, m0 + wt), trajectory-major; every
+// sample depends only on its GLOBAL record index q = p * nt + m
+__global__ void k_synth_points(mfseg_synth s, Blobs B, long long p0, long long wp, int m0, int wt,
+                               long long *traj_id, double *t, double *xyz, double *value) {
+    long long n = wp * wt;
     double ex = s.nx, ey = s.ny, ez = s.nz;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
-         q += (long long)gridDim.x * blockDim.x) {
-        long long p = q / s.nt;
-        int m = (int)(q % s.nt);
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < n;
+         w += (long long)gridDim.x * blockDim.x) {
+        long long p = p0 + w / wt;
+        int m = m0 + (int)(w % wt);
+        const long long q = p * s.nt + m;
         unsigned long long sp = s.seed ^ 0x5bd1e995ull;
         double x0 = DMUL(ex, u01(h3(sp, p, 11))), y0 = DMUL(ey, u01(h3(sp, p, 12))),
                z0 = DMUL(ez, u01(h3(sp, p, 13)));
@@ -129,12 +135,12 @@ __global__ void k_synth_points(mfseg_synth s, Blobs B, long long *traj_id, doubl
         int b = blob_at(B, x, y, z, mm);
         double v = noisy(b >= 0 ? B.b[b].pv : 0.0, sp, (unsigned long long)q, s.noise, s.dyadic);
         if (s.dyadic && q < 2) v = (double)q;
-        traj_id[q] = p;
-        t[q] = mm;
-        xyz[3 * q] = x;
-        xyz[3 * q + 1] = y;
-        xyz[3 * q + 2] = z;
-        value[q] = v;
+        traj_id[w] = p;
+        t[w] = mm;
+        xyz[3 * w] = x;
+        xyz[3 * w + 1] = y;
+        xyz[3 * w + 2] = z;
+        value[w] = v;
     }
 }
 
@@ -145,22 +151,42 @@ using namespace mfseg;
 
 extern "C" {
 
-int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream) {
+int mfseg_synth_field_window(const mfseg_synth *s, int32_t m0, int32_t m1, int32_t z0, int32_t z1,
+                             double *values, void *stream) {
+    if (m0 < 0 || m1 > s->nt || m0 > m1 || z0 < 0 || z1 > s->nz || z0 > z1) {
+        set_error("synth_field_window: window outside the dataset");
+        return 2;
+    }
+    if (m1 == m0 || z1 == z0) return 0;
     Blobs B = make_blobs(s);
     ::mfseg::count_launch();
-    k_synth_field<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, values);
+    k_synth_field<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, m0, m1 - m0, z0, z1 - z0, values);
     MFSEG_LAUNCH("k_synth_field");
+    return 0;
+}
+
+int mfseg_synth_field(const mfseg_synth *s, double *values, void *stream) {
+    return mfseg_synth_field_window(s, 0, s->nt, 0, s->nz, values, stream);
+}
+
+int mfseg_synth_points_window(const mfseg_synth *s, int64_t p0, int64_t p1, int32_t m0, int32_t m1,
+                              int64_t *traj_id, double *t, double *xyz, double *value, void *stream) {
+    if (p0 < 0 || p1 > s->n_traj || p0 > p1 || m0 < 0 || m1 > s->nt || m0 > m1) {
+        set_error("synth_points_window: window outside the dataset");
+        return 2;
+    }
+    if (p1 == p0 || m1 == m0) return 0;
+    Blobs B = make_blobs(s);
+    ::mfseg::count_launch();
+    k_synth_points<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, p0, p1 - p0, m0, m1 - m0,
+                                                               (long long *)traj_id, t, xyz, value);
+    MFSEG_LAUNCH("k_synth_points");
     return 0;
 }
 
 int mfseg_synth_points(const mfseg_synth *s, int64_t *traj_id, double *t, double *xyz,
                        double *value, void *stream) {
-    Blobs B = make_blobs(s);
-    ::mfseg::count_launch();
-    k_synth_points<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, (long long *)traj_id, t,
-                                                               xyz, value);
-    MFSEG_LAUNCH("k_synth_points");
-    return 0;
+    return mfseg_synth_points_window(s, 0, s->n_traj, 0, s->nt, traj_id, t, xyz, value, stream);
 }
 
 }  // extern "C"

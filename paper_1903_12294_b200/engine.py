@@ -96,6 +96,7 @@ class DeviceField:
     spacing: np.ndarray
     times: torch.Tensor      # (T,) f64
     values: torch.Tensor     # (T * ncell,) f64
+    offset: tuple = (0, 0, 0)   # global cell index of the first cell (spatial slabs)
 
     @property
     def nt(self):
@@ -114,6 +115,8 @@ class DeviceField:
             f.spacing[d] = float(self.spacing[d])
         f.times = N.ptr(self.times)
         f.values = N.ptr(self.values)
+        for d in range(3):
+            f.offset[d] = int(self.offset[d])
         return f
 
 

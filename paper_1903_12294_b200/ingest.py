@@ -208,3 +208,58 @@ def synthetic_device(dims, nt, n_traj, seed=0, noise=0.05, n_blobs=6, dyadic=Fal
     fld = DeviceField(tuple(int(d) for d in dims), np.zeros(3), np.ones(3),
                       torch.arange(nt, dtype=torch.float64, device=dev), values)
     return fld, DevicePoints(xyz, t, v), tid
+
+
+def synthetic_field_window(dims, nt, seed=0, noise=0.05, n_blobs=6, dyadic=False, dev=None,
+                           m0=0, m1=None, z0=0, z1=None) -> DeviceField:
+    """Timesteps [m0, m1) x z-planes [z0, z1) of `synthetic_device`'s field (a
+    time or spatial slab; values bit-identical to the whole dataset's)."""
+    lib = N.load()
+    dev = dev or device()
+    m1 = nt if m1 is None else m1
+    z1 = dims[2] if z1 is None else z1
+    s = synth_spec(dims, nt, 0, seed, noise, n_blobs, dyadic)
+    values = torch.empty(int(dims[0]) * int(dims[1]) * (z1 - z0) * (m1 - m0), dtype=torch.float64,
+                         device=dev)
+    N.check(lib.mfseg_synth_field_window(C.byref(s), m0, m1, z0, z1, N.ptr(values), stream_ptr()),
+            "mfseg_synth_field_window")
+    return DeviceField((int(dims[0]), int(dims[1]), z1 - z0), np.zeros(3), np.ones(3),
+                       torch.arange(m0, m1, dtype=torch.float64, device=dev), values, (0, 0, z0))
+
+
+def synthetic_points_window(dims, nt, n_traj, seed=0, noise=0.05, n_blobs=6, dyadic=False,
+                            dev=None, m0=0, m1=None, keep=None, chunk=1 << 22):
+    """Point samples of `synthetic_device` at timesteps [m0, m1) (all
+    trajectories, trajectory-major), optionally only those for which
+    keep(xyz, t) (a device mask function, e.g. a z-bin range) holds; generated in
+    chunks of trajectories so a slab never materialises the whole set.
+    Returns (DevicePoints, traj_id)."""
+    lib = N.load()
+    dev = dev or device()
+    m1 = nt if m1 is None else m1
+    s = synth_spec(dims, nt, n_traj, seed, noise, n_blobs, dyadic)
+    w = m1 - m0
+    parts = []
+    for p0 in range(0, int(n_traj), chunk if keep is not None else max(int(n_traj), 1)):
+        p1 = min(int(n_traj), p0 + (chunk if keep is not None else int(n_traj)))
+        n = (p1 - p0) * w
+        tid = torch.empty(n, dtype=torch.int64, device=dev)
+        t = torch.empty(n, dtype=torch.float64, device=dev)
+        xyz = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        v = torch.empty(n, dtype=torch.float64, device=dev)
+        if n:
+            N.check(lib.mfseg_synth_points_window(C.byref(s), p0, p1, m0, m1, N.ptr(tid), N.ptr(t),
+                                                  N.ptr(xyz), N.ptr(v), stream_ptr()),
+                    "mfseg_synth_points_window")
+        if keep is not None:
+            sel = keep(xyz, t)
+            tid, t, xyz, v = tid[sel], t[sel], xyz[sel], v[sel]
+        parts.append((tid, t, xyz, v))
+    if not parts:
+        z = torch.zeros(0, dtype=torch.float64, device=dev)
+        return DevicePoints(z.reshape(0, 3), z, z), torch.zeros(0, dtype=torch.int64, device=dev)
+    if len(parts) == 1:
+        tid, t, xyz, v = parts[0]
+    else:
+        tid, t, xyz, v = (torch.cat([p[i] for p in parts]) for i in range(4))
+    return DevicePoints(xyz.contiguous(), t.contiguous(), v.contiguous()), tid

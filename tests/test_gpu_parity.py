@@ -13,6 +13,8 @@ import torch
 
 from golden_io import Case, names
 
+from paper_1903_12294_b200 import _native as N
+
 pytestmark = pytest.mark.gpu
 
 RUNS = names("run_")
@@ -447,11 +449,22 @@ def test_limb_kernels_match_python_encoding():
     assert torch.equal(back, acc)
 
 
+def _oracle_labels(ps, fs, cs, ext, C, params):
+    """The C oracle's windowed assignment (engine.py:164-218) of both kinds."""
+    from oracle import c_oracle
+    ploc = np.column_stack([ps.xyz, ps.t])
+    pl = c_oracle.assign(ploc, ps.value, cs.loc, cs.pval, cs.has_p, ext.mins, C, params.k,
+                         params.w_p, params.w_d, params.c_f)
+    fl = c_oracle.assign_field(fs.dims, fs.origin, fs.spacing, fs.times, fs.values, cs.loc,
+                               cs.fval, cs.has_f, ext.mins, C, params.k, params.w_f, params.w_d,
+                               params.c_f)
+    return pl, fl
+
+
 @pytest.mark.parametrize("w_d,seed", [(1.0, 21), (0.15, 22)])
-def test_kernel_generations_agree(w_d, seed, monkeypatch):
-    """The v5 field / v4 point kernels (dominance pruning, packed-key screen)
-    against the first-generation kernels (exhaustive per-sample fp64 over the
-    tile survivors) on drifted centres with and without values: one
+def test_assign_drifted_centres_vs_oracle(w_d, seed):
+    """The field (block culling, dominance, packed-key screen) and point kernels
+    against the C oracle on drifted centres with and without values: one
     assignment pass over ~6M voxel-timesteps and 150k points, labels bit-exact.
     A small w_d makes the value term large (dominance's value bound)."""
     P = pkg()
@@ -474,23 +487,20 @@ def test_kernel_generations_agree(w_d, seed, monkeypatch):
     ps = P.PointSet(np.zeros(pts.n, np.int64), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(),
                     pts.value.cpu().numpy())
     pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
-    monkeypatch.setenv("MFSEG_FIELD_V1", "1")
-    monkeypatch.setenv("MFSEG_POINT_V1", "1")
-    pl1, fl1 = P.assign_iteration(ps, fs, None, cs, grid, params, C)
-    np.testing.assert_array_equal(fl, fl1)
-    np.testing.assert_array_equal(pl, pl1)
+    want_p, want_f = _oracle_labels(ps, fs, cs, ext, C, params)
+    np.testing.assert_array_equal(fl, want_f)
+    np.testing.assert_array_equal(pl, want_p)
 
 
-@pytest.mark.parametrize("env", [{"MFSEG_MULTI_CAP": "0"}, {"MFSEG_MULTI_CAP": "37"},
-                                 {"MFSEG_DEBUG": "2"}, {"MFSEG_DEBUG": "1"},
-                                 {"MFSEG_NO_REUSE": "1"}])
-def test_field_brick_queue_paths_agree(env, monkeypatch):
+@pytest.mark.parametrize("opts", [dict(multi_cap=0), dict(multi_cap=37), dict(flags=2),
+                                  dict(flags=1), dict(flags=16), dict(flags=32)])
+def test_field_brick_queue_paths_agree(opts):
     """k_field_assign5 queues multi-candidate bricks for k_field_screen; a full
     queue (capacity 0 or 37 items) sends the rest to the exact per-sample path
-    (k_deferred), MFSEG_DEBUG=2 resolves every queued sample in exact fp64 and
-    MFSEG_DEBUG=1 disables culling and dominance (most bricks then exceed the
-    16-candidate queue limit); MFSEG_NO_REUSE=1 recomputes the blocks whose
-    candidates did not change since the last pass.  A 6-pass run: labels and
+    (k_deferred), debug flag 2 resolves every queued sample in exact fp64 and
+    flag 1 disables culling and dominance (most bricks then exceed the
+    16-candidate queue limit); flag 16 recomputes the blocks whose candidates
+    did not change since the last pass, flag 32 keeps only exact reuse.  A 6-pass run: labels and
     centre positions bit-identical (integer sums), field means within fp64
     rounding (the value
     sums are rounded per record or per sample depending on the path)."""
@@ -504,9 +514,8 @@ def test_field_brick_queue_paths_agree(env, monkeypatch):
     ext = P.domain_extent(ps, fs)
     params = P.ClusterParams(k=(5, 4, 3, 2), w_d=0.3, max_iterations=5, eps_c=1e-12)
     a = P.run(ps, fs, ext, params)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    b = P.run(ps, fs, ext, params)
+    with N.debug_options(**opts):
+        b = P.run(ps, fs, ext, params)
     np.testing.assert_array_equal(a.field_labels, b.field_labels)
     np.testing.assert_array_equal(a.point_labels, b.point_labels)
     assert [c.id for c in a.centers] == [c.id for c in b.centers]
@@ -519,12 +528,12 @@ def test_field_brick_queue_paths_agree(env, monkeypatch):
 
 
 @pytest.mark.parametrize("weights", [dict(), dict(c_f=0.5, w_d=0.3, w_p=1.5, w_f=2.0)])
-def test_reuse_of_unchanged_blocks_is_exact(weights, monkeypatch):
+def test_reuse_of_unchanged_blocks_is_exact(weights):
     """A 10-iteration run on a mid-size case where, in the later passes, many
     field blocks and point chunks reuse the previous pass's labels (unchanged
     candidates, or field bricks whose proven margin exceeds the centre moves):
     labels and centres must equal a run that recomputes everything
-    (MFSEG_NO_REUSE), with default and with non-unit weights and time scale."""
+    (debug flag NO_REUSE), with default and with non-unit weights and time scale."""
     P = pkg()
     from paper_1903_12294_b200.engine import run_device
     from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
@@ -534,8 +543,8 @@ def test_reuse_of_unchanged_blocks_is_exact(weights, monkeypatch):
     ext = domain_extent_device(pts, fld)
     params = P.ClusterParams(k=(8, 6, 4, 6), eps_c=1e-12, max_iterations=10, **weights)
     a = run_device(pts, fld, ext, params)
-    monkeypatch.setenv("MFSEG_NO_REUSE", "1")
-    b = run_device(pts, fld, ext, params)
+    with N.debug_options(N.DEBUG_NO_REUSE):
+        b = run_device(pts, fld, ext, params)
     assert a.iterations_used == b.iterations_used
     assert torch.equal(a.field_labels, b.field_labels)
     assert torch.equal(a.point_labels, b.point_labels)
@@ -573,9 +582,10 @@ def test_traj_split_matches_numpy(seed, n, n_traj, single_time):
     np.testing.assert_array_equal(starts.cpu().numpy(), ref_starts)
 
 
-def test_segment_sharded_single_rank_matches_segment():
+@pytest.mark.parametrize("normalize", [True, False])
+def test_segment_sharded_single_rank_matches_segment(normalize):
     """parallel.segment_sharded (NCCL process group of one rank) reproduces
-    pipeline.segment: same labels, same centre table."""
+    pipeline.segment: same labels, centre table and NormalizationRecord."""
     import socket
     import torch.distributed as dist
     P = pkg()
@@ -585,8 +595,8 @@ def test_segment_sharded_single_rank_matches_segment():
     fs = P.FieldSet((40, 32, 20), np.zeros(3), np.ones(3), np.arange(nt, dtype=float),
                     fld.values.cpu().numpy().reshape(nt, -1))
     ps = P.PointSet(tid.cpu().numpy(), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(), pts.value.cpu().numpy())
-    params = P.ClusterParams(k=(5, 4, 3, 2), eps_c=1e-12, max_iterations=5)
-    ref, _, _ = P.segment(ps, fs, params)
+    params = P.ClusterParams(k=(5, 4, 3, 2), eps_c=1e-12, max_iterations=5, normalize=normalize)
+    ref, rnorm, _ = P.segment(ps, fs, params)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -594,18 +604,20 @@ def test_segment_sharded_single_rank_matches_segment():
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
     try:
-        seg, ext = segment_sharded(ps, fs, params)
+        seg, norm, _ = segment_sharded(ps, fs, params)
     finally:
         dist.destroy_process_group()
+    assert norm == rnorm
     np.testing.assert_array_equal(seg.field_labels, ref.field_labels)
     np.testing.assert_array_equal(seg.point_labels, ref.point_labels)
     assert [c.id for c in seg.centers] == [c.id for c in ref.centers]
     np.testing.assert_array_equal([c.x_c for c in seg.centers], [c.x_c for c in ref.centers])
 
 
-def test_kernel_generations_agree_crowded(monkeypatch):
+def test_assign_crowded_vs_oracle():
     """~1.4 centres per bin: candidate lists of ~100-130 exercise the 4-round
-    variants of both assignment kernels and the deferral of lists > 128."""
+    variants of both assignment kernels and the deferral of lists > 128;
+    labels bit-exact against the C oracle."""
     P = pkg()
     from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
     dims, nt, ntraj = (64, 48, 32), 12, 6000
@@ -629,8 +641,6 @@ def test_kernel_generations_agree_crowded(monkeypatch):
     ps = P.PointSet(np.zeros(pts.n, np.int64), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(),
                     pts.value.cpu().numpy())
     pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
-    monkeypatch.setenv("MFSEG_FIELD_V1", "1")
-    monkeypatch.setenv("MFSEG_POINT_V1", "1")
-    pl1, fl1 = P.assign_iteration(ps, fs, None, cs, grid, params, C)
-    np.testing.assert_array_equal(fl, fl1)
-    np.testing.assert_array_equal(pl, pl1)
+    want_p, want_f = _oracle_labels(ps, fs, cs, ext, C, params)
+    np.testing.assert_array_equal(fl, want_f)
+    np.testing.assert_array_equal(pl, want_p)

@@ -173,3 +173,170 @@ def test_sharded_exact_sums_match_single_rank():
     two = run_ranks(_shard_fn, world=2)
     one = run_ranks(_shard_fn, world=1)
     assert two[0] == two[1] == one[0]
+
+
+# ------------------------------------------------------------------ z-slabs, bin ranges, points
+
+def test_zbin_slabs_and_bin_ranges_partition():
+    """z-plane slabs of whole z-bins; the per-rank bin ranges give every point
+    exactly one owner (also points outside the field's bins)."""
+    from paper_1903_12294_b200.parallel import (bins_of, cell_centres, select_points_for_slab,
+                                                slab_bin_ranges, zbin_slabs)
+    rng = np.random.default_rng(3)
+    for nz, k_z, world, origin, spacing in ((64, 8, 2, 0.0, 1.0), (128, 32, 8, -3.7, 0.31),
+                                            (10, 3, 4, 0.0, 1.0), (33, 4, 3, 1e6, 0.125)):
+        z_min = origin - 0.01
+        C_z = (nz * spacing + 0.02) / k_z
+        slabs = zbin_slabs(nz, origin, spacing, z_min, C_z, k_z, world)
+        zc = cell_centres(nz, origin, spacing)
+        b = bins_of(zc, z_min, C_z, k_z)
+        covered = [k for k0, k1 in slabs for k in range(k0, k1)]
+        assert covered == list(range(nz))
+        for k0, k1 in slabs:
+            if 0 < k0 < nz and k1 > k0:
+                assert b[k0] != b[k0 - 1]
+        ranges = slab_bin_ranges(zc, z_min, C_z, k_z, slabs)
+        pz = rng.uniform(z_min - 5 * C_z, z_min + (k_z + 5) * C_z, 5000)
+        owners = np.zeros(len(pz), int)
+        for r, (b0, b1) in enumerate(ranges):
+            owners += select_points_for_slab(pz, z_min, C_z, k_z, b0, b1).astype(int)
+            for k0, k1 in [slabs[r]]:
+                if k1 > k0:   # the rank's own cells are inside its bin range
+                    assert np.all((b[k0:k1] >= b0) & (b[k0:k1] < b1))
+        assert np.all(owners == 1)
+
+
+def _extent_fn(rank, world):
+    """normalize_and_extent_sharded (values untouched: normalize off) on CPU
+    tensors equals the host extent of the union."""
+    from paper_1903_12294_b200.engine import DeviceField, DevicePoints
+    from paper_1903_12294_b200.parallel import normalize_and_extent_sharded
+    rng = np.random.default_rng(10 + rank)
+    n = 50 + 30 * rank
+    xyz = torch.as_tensor(rng.uniform(-2, 9, (n, 3)))
+    t = torch.as_tensor(rng.uniform(0, 5, n))
+    v = torch.as_tensor(rng.normal(size=n))
+    nz_local = 3
+    fld = DeviceField((4, 5, nz_local), np.array([0.5, -1.0, 2.0]), np.array([0.25, 0.5, 1.0]),
+                      torch.arange(3, dtype=torch.float64) * 2.0,
+                      torch.as_tensor(rng.normal(size=3 * 4 * 5 * nz_local)), (0, 0, nz_local * rank))
+    ext, norm = normalize_and_extent_sharded(DevicePoints(xyz, t, v), fld, False,
+                                             grid_dims=(4, 5, nz_local * world))
+    return (ext.mins.tolist(), ext.maxs.tolist(), norm.enabled,
+            xyz.numpy(), t.numpy())
+
+
+def test_normalize_and_extent_sharded_gloo():
+    res = run_ranks(_extent_fn)
+    assert res[0][:3] == res[1][:3]
+    xyz = np.vstack([r[3] for r in res])
+    t = np.concatenate([r[4] for r in res])
+    mins, maxs, enabled = res[0][:3]
+    assert enabled is False
+    field_lo = np.array([0.5, -1.0, 2.0, 0.0])
+    field_hi = np.array([0.5 + 4 * 0.25, -1.0 + 5 * 0.5, 2.0 + 6 * 1.0, 4.0])
+    want_lo = np.minimum(field_lo, np.r_[xyz.min(0), t.min()])
+    want_hi = np.maximum(field_hi, np.r_[xyz.max(0), t.max()])
+    assert mins == want_lo.tolist() and maxs == want_hi.tolist()
+
+
+def _nonfinite_fn(rank, world):
+    from paper_1903_12294_b200.engine import DeviceField, DevicePoints
+    from paper_1903_12294_b200.parallel import normalize_and_extent_sharded
+    v = torch.tensor([0.0, float("nan") if rank == 1 else 1.0], dtype=torch.float64)
+    pts = DevicePoints(torch.zeros((2, 3), dtype=torch.float64), torch.zeros(2, dtype=torch.float64), v)
+    fld = DeviceField((1, 1, 1), np.zeros(3), np.ones(3), torch.zeros(0, dtype=torch.float64),
+                      torch.zeros(0, dtype=torch.float64))
+    try:
+        normalize_and_extent_sharded(pts, fld, False)
+    except ValueError as e:
+        return str(e)
+    return None
+
+
+def test_sharded_non_finite_rejected_on_every_rank():
+    res = run_ranks(_nonfinite_fn)
+    assert all(r is not None and "non-finite" in r for r in res)
+
+
+# ------------------------------------------------------------------ sharded feature materialisation
+
+def test_fix128_limb_roundtrip():
+    from paper_1903_12294_b200.postproc import fix128_to_limbs, limbs_to_fix128
+    rng = np.random.default_rng(0)
+    vals = [int(x) * (1 << 50) + int(y) for x, y in zip(rng.integers(-2**62, 2**62, 64),
+                                                          rng.integers(0, 2**50, 64))]
+    def pair(v):
+        u = v & ((1 << 128) - 1)
+        lo, hi = u & ((1 << 64) - 1), u >> 64
+        return [lo - (1 << 64) if lo >> 63 else lo, hi - (1 << 64) if hi >> 63 else hi]
+    w = torch.tensor([pair(v) for v in vals], dtype=torch.int64)
+    L = fix128_to_limbs(w)
+    assert torch.equal(limbs_to_fix128(L), w)
+    # sums of several values through the limbs
+    L3 = L[:16] + L[16:32] + L[32:48]
+    back = limbs_to_fix128(L3)
+    for i in range(16):
+        lo, hi = int(back[i, 0]) & ((1 << 64) - 1), int(back[i, 1])
+        assert hi * (1 << 64) + lo == vals[i] + vals[16 + i] + vals[32 + i]
+
+
+def _stat_fn(rank, world):
+    from paper_1903_12294_b200.postproc import reduce_stat_partials
+    rng = np.random.default_rng(20 + rank)
+    n = 5
+    S = torch.zeros((n, 18), dtype=torch.int64)
+    S[:, 0:8] = torch.as_tensor(rng.integers(-2**40, 2**40, (n, 8)))
+    S[:, 1::2][:, :4] = torch.as_tensor(rng.integers(-3, 3, (n, 4)))   # hi words
+    S[:, 8:10] = torch.as_tensor(rng.integers(0, 100, (n, 2)))
+    keys = rng.integers(-2**63, 2**63 - 1, (n, 8), dtype=np.int64)
+    S[:, 10:18] = torch.as_tensor(keys)
+    before = S.clone()
+    reduce_stat_partials(S)
+    return before, S
+
+
+def test_reduce_stat_partials_gloo():
+    res = run_ranks(_stat_fn)
+    a, b = res[0][0], res[1][0]
+    for r in range(2):
+        S = res[r][1]
+        for i in range(a.shape[0]):
+            for w in range(4):
+                def val(T):
+                    return int(T[i, 2 * w + 1]) * (1 << 64) + (int(T[i, 2 * w]) & ((1 << 64) - 1))
+                assert val(S) == val(a) + val(b)
+        assert torch.equal(S[:, 8:10], a[:, 8:10] + b[:, 8:10])
+        ua, ub = a[:, 10:18].numpy().view(np.uint64), b[:, 10:18].numpy().view(np.uint64)
+        us = S[:, 10:18].numpy().view(np.uint64)
+        assert np.array_equal(us[:, :4], np.minimum(ua[:, :4], ub[:, :4]))
+        assert np.array_equal(us[:, 4:], np.maximum(ua[:, 4:], ub[:, 4:]))
+
+
+def _traj_fn(rank, world):
+    from paper_1903_12294_b200.postproc import exchange_by_trajectory, global_stride
+    rng = np.random.default_rng(30 + rank)
+    n = 200 + 50 * rank
+    tid = torch.as_tensor(rng.integers(-20, 60, n), dtype=torch.int64)
+    t = torch.as_tensor(rng.integers(0, 10, n) * 0.5 + 0.25 * rank)
+    gidx = torch.arange(n, dtype=torch.int64) + 1000 * rank
+    o_tid, (o_t, o_g) = exchange_by_trajectory(tid, [t, gidx])
+    return tid.numpy(), gidx.numpy(), o_tid.numpy(), o_t.numpy(), o_g.numpy(), global_stride(t)
+
+
+def test_exchange_by_trajectory_gloo():
+    res = run_ranks(_traj_fn)
+    all_tid = np.concatenate([r[0] for r in res])
+    all_g = np.concatenate([r[1] for r in res])
+    got_g = np.concatenate([r[4] for r in res])
+    assert sorted(got_g.tolist()) == sorted(all_g.tolist())      # every sample once
+    owners = {}
+    for r, rr in enumerate(res):
+        for tr in rr[2].tolist():
+            assert owners.setdefault(tr, r) == r                # a trajectory has one owner
+        if r and len(rr[2]) and len(res[r - 1][2]):
+            assert rr[2].min() > res[r - 1][2].max()            # owner ranges increase with rank
+        # every received sample keeps its own (traj, t, index)
+        g2t = dict(zip(all_g.tolist(), all_tid.tolist()))
+        assert all(g2t[g] == tr for g, tr in zip(rr[4].tolist(), rr[2].tolist()))
+    assert res[0][5] == res[1][5] == 0.25

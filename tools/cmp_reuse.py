@@ -6,6 +6,7 @@ if len(sys.argv) > 3:   # child: one run, save outputs
     import numpy as np, torch
     from bench import CONFIGS
     from paper_1903_12294_b200 import ClusterParams
+    from paper_1903_12294_b200 import _native as _N; _N.debug_options_from_env()  # MFSEG_* knobs
     from paper_1903_12294_b200.engine import run_device, CenterState
     from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device, synthetic_device
     cfg = CONFIGS[sys.argv[1]]

@@ -5,6 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from bench import CONFIGS
 from paper_1903_12294_b200 import ClusterParams
+from paper_1903_12294_b200 import _native as _N; _N.debug_options_from_env()  # MFSEG_* knobs
 from paper_1903_12294_b200.engine import run_device
 from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device, synthetic_device
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]

@@ -3,6 +3,7 @@ sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 os.environ["MFSEG_DEBUG"] = "8"
 import numpy as np
 import paper_1903_12294_b200 as P
+from paper_1903_12294_b200 import _native as _N; _N.debug_options_from_env()  # MFSEG_* knobs
 from paper_1903_12294_b200.ingest import synthetic_device
 dims, nt, ntraj = (64, 48, 40), 8, 2000
 fld, pts, _ = synthetic_device(dims, nt, ntraj, seed=31, noise=0.05, n_blobs=5, dyadic=False)
