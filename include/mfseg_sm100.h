@@ -306,6 +306,13 @@ int mfseg_synth_field_window(const mfseg_synth *s, int32_t m0, int32_t m1, int32
                              double *values, void *stream);
 int mfseg_synth_points_window(const mfseg_synth *s, int64_t p0, int64_t p1, int32_t m0, int32_t m1,
                               int64_t *traj_id, double *t, double *xyz, double *value, void *stream);
+/* Taxi-like 2D+t points (configs[3]): trajectories [p0, p1), each `steps`
+ * consecutive samples from a uniform random start step; a fraction `skew` of
+ * them drive along road rows / columns (a fraction `road_frac` of all rows /
+ * columns), z = 0.5 * nz.  Output (p1 - p0) * steps samples, trajectory-major. */
+int mfseg_synth_taxi_points(const mfseg_synth *s, int32_t steps, double skew, double road_frac,
+                            int64_t p0, int64_t p1, int64_t *traj_id, double *t, double *xyz,
+                            double *value, void *stream);
 
 #ifdef __cplusplus
 }

@@ -127,3 +127,45 @@ def points(dims, nt, n_traj, seed=0, noise=0.05, n_blobs=6, dyadic=False, traj=N
     if dyadic:
         v = np.where(q < 2, q.astype(float), v)
     return p.astype(np.int64), m, np.column_stack([x, y, z]), v
+
+
+def taxi_points(dims, nt, n_traj, steps=8, skew=0.7, road_frac=0.02, seed=0, noise=0.05,
+                n_blobs=6, traj=None):
+    """(traj_id, t, xyz, value) of the taxi-like generator (csrc/synth.cu
+    k_synth_taxi) for the requested trajectories (default: all)."""
+    nx, ny, nz = (float(d) for d in dims)
+    B = blobs(dims, nt, seed, n_blobs)
+    traj = np.arange(n_traj) if traj is None else np.asarray(traj)
+    n_rows = max(int(road_frac * ny), 1)
+    n_cols = max(int(road_frac * nx), 1)
+    span = max(nt - steps + 1, 1)
+    p = np.repeat(traj.astype(np.uint64), steps)
+    j = np.tile(np.arange(steps), len(traj)).astype(float)
+    sp = np.uint64(seed) ^ np.uint64(0x7a3c5e91)
+    s0 = np.minimum((_u01(_h3(sp, p, 21)) * span).astype(np.int64), span - 1)
+    m = s0 + j.astype(np.int64)
+    x0, y0 = nx * _u01(_h3(sp, p, 22)), ny * _u01(_h3(sp, p, 23))
+    vx = 2.0 * _u01(_h3(sp, p, 24)) - 1.0
+    vy = 2.0 * _u01(_h3(sp, p, 25)) - 1.0
+    sk = _u01(_h3(sp, p, 26)) < skew
+    r = _u01(_h3(sp, p, 27))
+    row = _u01(_h3(sp, p, 28)) < 0.5
+    qr = np.minimum((r * n_rows).astype(np.int64), n_rows - 1)
+    qc = np.minimum((r * n_cols).astype(np.int64), n_cols - 1)
+    y_road = np.floor(((qr + 0.5) * ny) / n_rows) + 0.5
+    x_road = np.floor(((qc + 0.5) * nx) / n_cols) + 0.5
+    on_row, on_col = sk & row, sk & ~row
+    y0 = np.where(on_row, y_road, y0)
+    vx = np.where(on_row, vx * 3.0, vx)
+    vy = np.where(on_row, 0.0, vy)
+    x0 = np.where(on_col, x_road, x0)
+    vy = np.where(on_col, vy * 3.0, vy)
+    vx = np.where(on_col, 0.0, vx)
+    x = np.minimum(np.maximum(x0 + vx * j, 0.0), nx - 2.0 ** -16)
+    y = np.minimum(np.maximum(y0 + vy * j, 0.0), ny - 2.0 ** -16)
+    z = np.full_like(x, 0.5 * nz)
+    lab = _blob_at(B, x, y, z, m.astype(float))
+    pv = np.array([o["pv"] for o in B] + [0.0])
+    q = p * np.uint64(steps) + j.astype(np.uint64)
+    v = _noisy(pv[lab], sp, q, noise, False)
+    return p.astype(np.int64), m.astype(float), np.column_stack([x, y, z]), v

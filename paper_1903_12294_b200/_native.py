@@ -99,6 +99,7 @@ _SIGNATURES = {
     "mfseg_synth_points": (C.c_int, [P(Synth), vp, vp, vp, vp, vp]),
     "mfseg_synth_field_window": (C.c_int, [P(Synth), i32, i32, i32, i32, vp, vp]),
     "mfseg_synth_points_window": (C.c_int, [P(Synth), i64, i64, i32, i32, vp, vp, vp, vp, vp]),
+    "mfseg_synth_taxi_points": (C.c_int, [P(Synth), i32, f64, f64, i64, i64, vp, vp, vp, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

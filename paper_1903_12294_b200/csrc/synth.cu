@@ -144,6 +144,57 @@ __global__ void k_synth_points(mfseg_synth s, Blobs B, long long p0, long long w
     }
 }
 
+// Taxi-like 2D+t trajectories (configs[3]): `steps` consecutive samples from a
+// uniform random start step; a fraction `skew` of the trajectories drive along
+// one of the road rows / columns (a fraction `road_frac` of them, evenly
+// spread), the rest move freely.  z is the single layer's centre 0.5 * nz.
+__global__ void k_synth_taxi(mfseg_synth s, Blobs B, int steps, double skew, int n_rows, int n_cols,
+                             long long p0, long long wp, long long *traj_id, double *t, double *xyz,
+                             double *value) {
+    const long long n = wp * steps;
+    const double ex = s.nx, ey = s.ny;
+    const double z = DMUL(0.5, (double)s.nz);
+    const int span = s.nt - steps + 1 > 1 ? s.nt - steps + 1 : 1;
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < n;
+         w += (long long)gridDim.x * blockDim.x) {
+        const long long p = p0 + w / steps;
+        const int j = (int)(w % steps);
+        const unsigned long long sp = s.seed ^ 0x7a3c5e91ull;
+        const int s0 = min((int)(u01(h3(sp, p, 21)) * span), span - 1);
+        const int m = s0 + j;
+        double x0 = DMUL(ex, u01(h3(sp, p, 22))), y0 = DMUL(ey, u01(h3(sp, p, 23)));
+        double vx = DSUB(DMUL(2.0, u01(h3(sp, p, 24))), 1.0);
+        double vy = DSUB(DMUL(2.0, u01(h3(sp, p, 25))), 1.0);
+        if (u01(h3(sp, p, 26)) < skew) {
+            const double r = u01(h3(sp, p, 27));
+            if (u01(h3(sp, p, 28)) < 0.5) {   // along a road row
+                const int q = min((int)(r * n_rows), n_rows - 1);
+                y0 = DADD(floor(DDIV(DMUL((double)q + 0.5, ey), (double)n_rows)), 0.5);
+                vy = 0.0;
+                vx = DMUL(vx, 3.0);
+            } else {                           // along a road column
+                const int q = min((int)(r * n_cols), n_cols - 1);
+                x0 = DADD(floor(DDIV(DMUL((double)q + 0.5, ex), (double)n_cols)), 0.5);
+                vx = 0.0;
+                vy = DMUL(vy, 3.0);
+            }
+        }
+        const double mm = (double)j;
+        double x = DADD(x0, DMUL(vx, mm)), y = DADD(y0, DMUL(vy, mm));
+        x = fmin(fmax(x, 0.0), DSUB(ex, 0x1.0p-16));
+        y = fmin(fmax(y, 0.0), DSUB(ey, 0x1.0p-16));
+        const int b = blob_at(B, x, y, z, (double)m);
+        const double v = noisy(b >= 0 ? B.b[b].pv : 0.0, sp, (unsigned long long)(p * steps + j),
+                               s.noise, 0);
+        traj_id[w] = p;
+        t[w] = (double)m;
+        xyz[3 * w] = x;
+        xyz[3 * w + 1] = y;
+        xyz[3 * w + 2] = z;
+        value[w] = v;
+    }
+}
+
 }  // namespace
 }  // namespace mfseg
 
@@ -187,6 +238,25 @@ int mfseg_synth_points_window(const mfseg_synth *s, int64_t p0, int64_t p1, int3
 int mfseg_synth_points(const mfseg_synth *s, int64_t *traj_id, double *t, double *xyz,
                        double *value, void *stream) {
     return mfseg_synth_points_window(s, 0, s->n_traj, 0, s->nt, traj_id, t, xyz, value, stream);
+}
+
+int mfseg_synth_taxi_points(const mfseg_synth *s, int32_t steps, double skew, double road_frac,
+                            int64_t p0, int64_t p1, int64_t *traj_id, double *t, double *xyz,
+                            double *value, void *stream) {
+    if (p0 < 0 || p1 > s->n_traj || p0 > p1 || steps < 1 || steps > s->nt) {
+        set_error("synth_taxi_points: bad trajectory window or steps");
+        return 2;
+    }
+    if (p1 == p0) return 0;
+    Blobs B = make_blobs(s);
+    const int n_rows = (int)(road_frac * s->ny) > 1 ? (int)(road_frac * s->ny) : 1;
+    const int n_cols = (int)(road_frac * s->nx) > 1 ? (int)(road_frac * s->nx) : 1;
+    ::mfseg::count_launch();
+    k_synth_taxi<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(*s, B, steps, skew, n_rows, n_cols, p0,
+                                                             p1 - p0, (long long *)traj_id, t, xyz,
+                                                             value);
+    MFSEG_LAUNCH("k_synth_taxi");
+    return 0;
 }
 
 }  // extern "C"

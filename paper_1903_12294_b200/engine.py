@@ -24,6 +24,7 @@ both and the whole run is bit-identical.
 from __future__ import annotations
 
 import gc
+import threading
 
 import ctypes as C
 import itertools
@@ -52,17 +53,97 @@ def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+class _Stager:
+    """Pageable host -> device uploads through a ring of pinned staging buffers:
+    host threads fill the slots (torch's copy releases the GIL) while the copy
+    engine drains the filled ones, so a pageable array moves at several times the
+    rate of a direct pageable copy (which the driver stages through one small
+    buffer synchronously).  One per process, serialised by a lock."""
+
+    SLOT = 32 << 20
+    SLOTS = 8
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.ring = None
+        self.pool = None
+
+    def _init(self):
+        if self.ring is None:
+            from concurrent.futures import ThreadPoolExecutor
+            self.ring = [torch.empty(self.SLOT, dtype=torch.uint8, pin_memory=True)
+                         for _ in range(self.SLOTS)]
+            self.pool = ThreadPoolExecutor(self.SLOTS, thread_name_prefix="mfseg-stage")
+
+    def upload(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        """dst (device, contiguous) <- src (host, contiguous, same bytes), ordered
+        on the current stream; returns once the last slot is queued."""
+        with self.lock:
+            self._init()
+            sb = src.reshape(-1).view(torch.uint8)
+            db = dst.reshape(-1).view(torch.uint8)
+            n = sb.numel()
+            nch = -(-n // self.SLOT)
+            stream = torch.cuda.current_stream()
+            events = [None] * self.SLOTS
+            futs = {}
+
+            def fill(i):
+                a = i * self.SLOT
+                b = min(n, a + self.SLOT)
+                self.ring[i % self.SLOTS][:b - a].copy_(sb[a:b])
+                return a, b
+
+            for i in range(min(self.SLOTS, nch)):
+                futs[i] = self.pool.submit(fill, i)
+            for i in range(nch):
+                a, b = futs.pop(i).result()
+                slot = i % self.SLOTS
+                db[a:b].copy_(self.ring[slot][:b - a], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                events[slot] = ev
+                j = i + self.SLOTS
+                if j < nch:
+                    ev.synchronize()          # the slot's DMA is done: refill it
+                    futs[j] = self.pool.submit(fill, j)
+            for ev in events:
+                if ev is not None:
+                    ev.synchronize()          # ring buffers are reused by the next call
+
+
+_stager = _Stager()
+_STAGE_MIN_BYTES = 16 << 20
+
+
+def upload(t: torch.Tensor, dev=None) -> torch.Tensor:
+    """Host tensor -> device tensor of the same dtype on the current stream:
+    pinned memory by direct DMA (asynchronous), large pageable arrays through
+    the pinned staging ring, small ones by a plain copy."""
+    dev = dev or device()
+    t = t.contiguous()
+    if t.device.type == "cuda":
+        return t.to(dev)
+    nbytes = t.numel() * t.element_size()
+    if nbytes < _STAGE_MIN_BYTES or t.is_pinned():
+        return t.to(device=dev, non_blocking=True)
+    out = torch.empty(t.shape, dtype=t.dtype, device=dev)
+    _stager.upload(t, out)
+    return out
+
+
 def to_dev(a, dtype=torch.float64, dev=None):
-    """Host array (numpy / tensor) -> contiguous device tensor.  Arrays backed by
-    pinned memory (e.g. numpy views of pinned torch tensors) are copied by DMA
-    asynchronously on the current stream."""
+    """Host array (numpy / tensor) -> contiguous device tensor of `dtype`.  The
+    bytes cross PCIe in the array's own dtype (e.g. f32 field values) and are
+    converted on the device (f32 -> f64 widening is exact, as the reference's
+    host-side astype, ingest.py:39-78); see `upload` for pinned / pageable."""
     dev = dev or device()
     if isinstance(a, torch.Tensor):
-        return a.to(device=dev, dtype=dtype).contiguous()
-    t = torch.from_numpy(np.ascontiguousarray(a))
-    if t.dtype != dtype:
-        t = t.to(dtype)
-    return t.to(device=dev, non_blocking=True).contiguous()
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    d = upload(t, dev)
+    return d if d.dtype == dtype else d.to(dtype)
 
 
 def to_host_async(t: torch.Tensor):

@@ -263,3 +263,23 @@ def synthetic_points_window(dims, nt, n_traj, seed=0, noise=0.05, n_blobs=6, dya
     else:
         tid, t, xyz, v = (torch.cat([p[i] for p in parts]) for i in range(4))
     return DevicePoints(xyz.contiguous(), t.contiguous(), v.contiguous()), tid
+
+
+def synthetic_taxi_points(dims, nt, n_traj, steps=8, skew=0.7, road_frac=0.02, seed=0, noise=0.05,
+                          n_blobs=6, dev=None, p0=0, p1=None):
+    """configs[3]'s taxi-like trajectories (2D+t, nz = 1): `steps` consecutive
+    samples per trajectory from a uniform random start, a fraction `skew` of
+    them on `road_frac` of the rows / columns.  Returns (DevicePoints, traj_id)."""
+    lib = N.load()
+    dev = dev or device()
+    p1 = n_traj if p1 is None else p1
+    s = synth_spec(dims, nt, n_traj, seed, noise, n_blobs, False)
+    n = (p1 - p0) * steps
+    tid = torch.empty(n, dtype=torch.int64, device=dev)
+    t = torch.empty(n, dtype=torch.float64, device=dev)
+    xyz = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    v = torch.empty(n, dtype=torch.float64, device=dev)
+    N.check(lib.mfseg_synth_taxi_points(C.byref(s), steps, skew, road_frac, p0, p1, N.ptr(tid),
+                                        N.ptr(t), N.ptr(xyz), N.ptr(v), stream_ptr()),
+            "mfseg_synth_taxi_points")
+    return DevicePoints(xyz, t, v), tid

@@ -91,6 +91,45 @@ def merge_clusters(centers: Sequence[ClusterCenter], eps_m: float):
     return merge_map, merged
 
 
+def merge_device(state: dict, eps_m: float):
+    """merge_clusters (postproc.py:59-92) on a device centre state (engine
+    DeviceRun.state): the live rows (n_points + n_fields > 0, ascending id,
+    engine.py:72-86) are compacted on the device and merged there, without the
+    host table round trip.  Returns (ids, rep, merged) device tensors: ids of the
+    live rows, their representative (the merge map), and the merged table
+    (ids, loc [4][g], p_c, f_c, n_points, n_fields; NaN = absent)."""
+    lib = N.load()
+    dev = state["loc"].device
+    live = torch.nonzero((state["n_points"] + state["n_fields"]) > 0).flatten()
+    n = int(live.numel())
+    ids = live.to(torch.int32)
+    loc = state["loc"][:, live].contiguous()
+    nan = torch.tensor(float("nan"), dtype=torch.float64, device=dev)
+    pc = torch.where(state["has_p"][live] != 0, state["pval"][live], nan).contiguous()
+    fc = torch.where(state["has_f"][live] != 0, state["fval"][live], nan).contiguous()
+    npt = state["n_points"][live].contiguous()
+    nfl = state["n_fields"][live].contiguous()
+    rep = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    m_ids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    m_loc = torch.empty(4 * max(n, 1), dtype=torch.float64, device=dev)
+    m_p = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    m_f = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    m_np = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    m_nf = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    G = C.c_int32(0)
+    if n:
+        ws_bytes = lib.mfseg_merge_workspace_size(n)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        N.check(lib.mfseg_merge(n, N.ptr(ids), N.ptr(loc), N.ptr(pc), N.ptr(fc), N.ptr(npt),
+                                N.ptr(nfl), float(eps_m), N.ptr(rep), N.ptr(m_ids), N.ptr(m_loc),
+                                N.ptr(m_p), N.ptr(m_f), N.ptr(m_np), N.ptr(m_nf), C.byref(G),
+                                N.ptr(ws), ws_bytes, stream_ptr()), "mfseg_merge")
+    g = G.value
+    merged = {"ids": m_ids[:g], "loc": m_loc[:4 * g].reshape(4, g), "p_c": m_p[:g], "f_c": m_f[:g],
+              "n_points": m_np[:g], "n_fields": m_nf[:g]}
+    return ids, rep[:n], merged
+
+
 @dataclass(frozen=True)
 class FeatureStats:
     """postproc.py:95-112."""
