@@ -54,6 +54,14 @@ __device__ void fallback_one(const FallbackArgs &a, long long idx) {
         s3 = a.pt[idx];
         v = a.pv[idx];
     }
+    // Level `mult`: the centres with |c - s| <= mult * C on every axis
+    // (engine.py:199-205).  Their bins lie within (mult + 2) bins of the sample's
+    // own unclipped bin coordinate on each axis (the +2 covers the rounding of
+    // the bin arithmetic; bins are clipped like CenterGrid's, so centres outside
+    // the extent sit in the edge bins and stay covered), so while that bin box is
+    // small the level scans its bins' centres; otherwise all K.  Either way the
+    // exact box test selects the same set, and the (D, id) minimum is unique.
+    const double sc[4] = {s0, s1, s2, s3};
     double mult = 2.0;
     int best = INT_MAX;
     for (int guard = 0; guard < 1100 && best == INT_MAX; ++guard, mult = DMUL(mult, 2.0)) {
@@ -61,7 +69,7 @@ __device__ void fallback_one(const FallbackArgs &a, long long idx) {
                b3 = DMUL(mult, a.C[3]);
         double bD = INF;
         int bI = INT_MAX;
-        for (int c = lane; c < a.K; c += 32) {
+        auto consider = [&](int c) {
             double dx = DSUB(a.c.x[c], s0), dy = DSUB(a.c.y[c], s1), dz = DSUB(a.c.z[c], s2),
                    dt = DSUB(a.c.t[c], s3);
             if (fabs(dx) <= b0 && fabs(dy) <= b1 && fabs(dz) <= b2 && fabs(dt) <= b3) {
@@ -74,6 +82,33 @@ __device__ void fallback_one(const FallbackArgs &a, long long idx) {
                     bI = c;
                 }
             }
+        };
+        int lo[4], ext[4];
+        long long nbins = 1;
+        const int reach = mult < 1e6 ? (int)mult + 2 : (1 << 28);
+        for (int d = 0; d < 4; ++d) {
+            const double u = floor(DDIV(DSUB(sc[d], a.mins[d]), a.C[d]));
+            const double l = fmax(fmin(u - reach, (double)(a.k[d] - 1)), 0.0);
+            const double h = fmax(fmin(u + reach, (double)(a.k[d] - 1)), 0.0);
+            lo[d] = (int)l;
+            ext[d] = (int)h - (int)l + 1;
+            nbins *= ext[d];
+        }
+        if (a.bin_start && nbins * 4 < a.K) {
+            for (long long q = 0; q < nbins; ++q) {
+                long long r = q;
+                const int bx = lo[0] + (int)(r % ext[0]);
+                r /= ext[0];
+                const int by = lo[1] + (int)(r % ext[1]);
+                r /= ext[1];
+                const int bz = lo[2] + (int)(r % ext[2]);
+                const int bt = lo[3] + (int)(r / ext[2]);
+                const int b = ((bt * a.k[2] + bz) * a.k[1] + by) * a.k[0] + bx;
+                const int e = a.bin_start[b + 1];
+                for (int p = a.bin_start[b] + lane; p < e; p += 32) consider(a.bin_ids[p]);
+            }
+        } else {
+            for (int c = lane; c < a.K; c += 32) consider(c);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {

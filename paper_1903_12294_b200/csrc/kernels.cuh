@@ -123,6 +123,10 @@ struct FallbackArgs {
     const double *times, *values;
     int x0, y0, z0;                    // global cell index of the field's first cell (slabs)
     const double *px, *py, *pz, *pt, *pv;
+    // CenterGrid bins (k_fallback enumerates the bins a widened box can reach)
+    const int *bin_start, *bin_ids;
+    double mins[4];
+    int k[4];
     long long n_samples;
     int *labels;
     const long long *stranded;

@@ -190,6 +190,98 @@ __global__ void k_key_hist(const unsigned *skeys, long long n, long long *cnt) {
     }
 }
 
+// Counting-sort path (few features): tiles of VT consecutive cells of one
+// timestep, 8 warps x VW cells each, 16 cells per lane kept in registers.
+//   k_voxel_hist:    per tile and slot the cell count -> H[(m*ns + s)*tpm + tile]
+//   (exclusive scan of H: every (m, s, tile) run's output offset, in (m, s)
+//    order and, within (m, s), tile order -> stable, cells ascending)
+//   k_voxel_scatter: warp-ordered ranks inside the tile, cells written once.
+constexpr int VT = 4096, VW = VT / 8, VSLOTS = 256;
+
+__device__ __forceinline__ int voxel_slot(const int *slot_of, int lut_len, int l, int *bad) {
+    const int s = (l >= 0 && l < lut_len) ? __ldg(slot_of + l) : -1;
+    if (s < 0) *bad = 1;
+    return s < 0 ? 0 : s;
+}
+
+__global__ void __launch_bounds__(256) k_voxel_hist(const int *flab, long long ncell, int tpm,
+                                                    const int *slot_of, int lut_len, int ns,
+                                                    int *H, int *bad) {
+    __shared__ int hist[VSLOTS];
+    const int tile = blockIdx.x % tpm, m = blockIdx.x / tpm;
+    for (int i = threadIdx.x; i < ns; i += 256) hist[i] = 0;
+    __syncthreads();
+    const long long c0 = (long long)tile * VT;
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < VT / 256; ++k) {
+        const long long c = c0 + k * 256 + threadIdx.x;
+        int s = -1;
+        if (c < ncell) s = voxel_slot(slot_of, lut_len, __ldg(flab + (long long)m * ncell + c), bad);
+        const unsigned grp = __match_any_sync(0xffffffffu, s);
+        if (s >= 0 && lane == __ffs(grp) - 1) atomicAdd(&hist[s], __popc(grp));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ns; i += 256) H[((long long)m * ns + i) * tpm + tile] = hist[i];
+}
+
+__global__ void __launch_bounds__(256) k_voxel_scatter(const int *flab, long long ncell, int tpm,
+                                                       const int *slot_of, int lut_len, int ns,
+                                                       const long long *O, int *cells, int *bad) {
+    __shared__ int wcnt[8][VSLOTS];     // per warp: its cells per slot, then its base in the tile
+    const int tile = blockIdx.x % tpm, m = blockIdx.x / tpm;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 8 * VSLOTS; i += 256) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const long long c0 = (long long)tile * VT + (long long)w * VW;
+    int sl[VW / 32];
+#pragma unroll
+    for (int k = 0; k < VW / 32; ++k) {
+        const long long c = c0 + k * 32 + lane;
+        sl[k] = c < ncell ? voxel_slot(slot_of, lut_len, __ldg(flab + (long long)m * ncell + c), bad) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, sl[k]);
+        if (sl[k] >= 0 && lane == __ffs(grp) - 1) wcnt[w][sl[k]] += __popc(grp);
+        __syncwarp();
+    }
+    __syncthreads();
+    // exclusive prefix over the warps per slot (warp order = cell order)
+    for (int s = threadIdx.x; s < ns; s += 256) {
+        int run = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int c = wcnt[q][s];
+            wcnt[q][s] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < VW / 32; ++k) {
+        const int s = sl[k];
+        const unsigned grp = __match_any_sync(0xffffffffu, s);
+        if (s >= 0) {
+            const int base = wcnt[w][s];
+            const long long dst = O[((long long)m * ns + s) * tpm + tile] + base + __popc(grp & lt);
+            cells[dst] = (int)(c0 + k * 32 + lane);
+        }
+        __syncwarp();
+        if (s >= 0 && lane == __ffs(grp) - 1) wcnt[w][s] += __popc(grp);
+        __syncwarp();
+    }
+}
+
+__global__ void k_voxel_segs(int nseg, int tpm, const long long *O, long long n, long long *seg) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nseg) seg[i] = O[(long long)i * tpm];
+    if (i == 0) seg[nseg] = n;
+}
+
+__global__ void k_widen_i32(const int *in, long long n, long long *out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
 // ------------------------------------------------------------------ feature stats
 // per slot words: [0..1] sum pv, [2..3] sum fv, [4..5] ssq pv, [6..7] ssq fv,
 // [8] n_p, [9] n_f, [10..13] bbox min (ordered bits), [14..17] bbox max
@@ -279,23 +371,51 @@ struct StatArgs {
     int *ovf;
 };
 
-__global__ void k_stats(StatArgs a, int pass) {
-    long long total = a.nf + a.np;
-    long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long base = blockIdx.x * (long long)blockDim.x; base < total; base += stride) {
-        long long q = base + threadIdx.x;
+// One pass over all samples (fields first, then points); slot = feature or -1.
+// SMEM: the block accumulates into a shared-memory copy of the slot records
+// (few features: the global records would serialise every warp's atomics on a
+// handful of addresses) and flushes it once; otherwise warp-aggregated global
+// atomics.  Integer sums: the result does not depend on the path.
+constexpr int STAT_SMEM_SLOTS = 320;   // 320 x 18 x 8 B = 45 KB
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k_stats(StatArgs a, int pass) {
+    extern __shared__ unsigned long long sS[];
+    unsigned long long *S = SMEM ? sS : a.S;
+    if (SMEM) {
+        for (int i = threadIdx.x; i < a.n_slots * SW; i += blockDim.x) {
+            const int w = i % SW;
+            sS[i] = (w >= 10 && w < 14) ? ~0ull : 0ull;
+        }
+        __syncthreads();
+    }
+    const long long total = a.nf + a.np;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const unsigned ncell = a.ncell > 0 ? (unsigned)a.ncell : 1u, nx = (unsigned)a.nx,
+                   ny = (unsigned)a.ny;
+    // (timestep, cell) of the block's first sample, advanced by the stride each
+    // round: no 64-bit division per sample
+    long long base = blockIdx.x * (long long)blockDim.x;
+    long long mb = base / ncell, rb = base % ncell;
+    const long long smq = stride / ncell, smr = stride % ncell;
+    for (; base < total; base += stride) {
+        const long long q = base + threadIdx.x;
         int slot = -1;
-        bool field = q < a.nf;
+        const bool field = q < a.nf;
         double x = 0, y = 0, z = 0, t = 0, v = 0;
         if (q < total) {
             if (field) {
                 slot = a.fslot[q];
                 if (slot >= 0) {
-                    long long r = q % a.ncell;
-                    long long m = q / a.ncell;
-                    x = cell_coord(a.ox, a.sx, a.x0 + r % a.nx);
-                    y = cell_coord(a.oy, a.sy, a.y0 + (r / a.nx) % a.ny);
-                    z = cell_coord(a.oz, a.sz, a.z0 + r / ((long long)a.nx * a.ny));
+                    unsigned ru = (unsigned)rb + threadIdx.x;
+                    long long m = mb;
+                    if (ru >= ncell) {
+                        m += ru / ncell;
+                        ru %= ncell;
+                    }
+                    const unsigned row = ru / nx;
+                    x = cell_coord(a.ox, a.sx, a.x0 + (long long)(ru - row * nx));
+                    y = cell_coord(a.oy, a.sy, a.y0 + (long long)(row % ny));
+                    z = cell_coord(a.oz, a.sz, a.z0 + (long long)(row / ny));
                     t = a.times[m];
                     v = a.values[q];
                 }
@@ -312,9 +432,42 @@ __global__ void k_stats(StatArgs a, int pass) {
             }
         }
         // field and point lanes are aggregated separately
-        stat_add(a.S, field ? slot : -1, true, x, y, z, t, v, a.mean, pass, a.ovf);
-        stat_add(a.S, field ? -1 : slot, false, x, y, z, t, v, a.mean, pass, a.ovf);
+        stat_add(S, field ? slot : -1, true, x, y, z, t, v, a.mean, pass, a.ovf);
+        stat_add(S, field ? -1 : slot, false, x, y, z, t, v, a.mean, pass, a.ovf);
+        mb += smq;
+        rb += smr;
+        if (rb >= ncell) {
+            rb -= ncell;
+            ++mb;
+        }
     }
+    if (SMEM) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.n_slots * SW; i += blockDim.x) {
+            const int w = i % SW;
+            unsigned long long *g = a.S + i;
+            const unsigned long long v = sS[i];
+            if (w < 8) {
+                if ((w & 1) == 0 && (v | sS[i + 1])) atomic_add_fix(g, v, (long long)sS[i + 1]);
+            } else if (w < 10) {
+                if (v) atomicAdd(g, v);
+            } else if (w < 14) {
+                if (v != ~0ull) atomicMin(g, v);
+            } else if (v) {
+                atomicMax(g, v);
+            }
+        }
+    }
+}
+
+int launch_stats(const StatArgs &a, int pass, cudaStream_t st) {
+    ::mfseg::count_launch();
+    if (a.n_slots <= STAT_SMEM_SLOTS)
+        k_stats<true><<<148 * 8, 256, (size_t)a.n_slots * SW * 8, st>>>(a, pass);
+    else
+        k_stats<false><<<148 * 8, 256, 0, st>>>(a, pass);
+    MFSEG_LAUNCH("k_stats");
+    return 0;
 }
 
 __global__ void k_stats_means(int n_slots, const unsigned long long *S, double *mean) {
@@ -571,8 +724,21 @@ int mfseg_relabel(const int32_t *labels, int64_t n, const int32_t *lut, int32_t 
     return 0;
 }
 
+static bool voxel_counting(int32_t n_slots) { return n_slots <= VSLOTS; }
+
 size_t mfseg_voxel_csr_workspace_size(int64_t n, int32_t nt, int32_t n_slots) {
     Carver cv;
+    const long long ncell = nt > 0 ? n / nt : 0;
+    if (voxel_counting(n_slots)) {
+        const long long tpm = (ncell + VT - 1) / VT;
+        const long long nh = (long long)nt * n_slots * tpm;
+        cv.take<int>(nh);
+        cv.take<long long>(nh + 1);
+        cv.take<long long>(nh + 1);
+        cv.take<int>(4);
+        cv.take<char>(scan_tmp_bytes(nh + 1));
+        return cv.off + 256;
+    }
     cv.take<unsigned>(n);
     cv.take<unsigned>(n);
     cv.take<unsigned>(n);
@@ -581,6 +747,48 @@ size_t mfseg_voxel_csr_workspace_size(int64_t n, int32_t nt, int32_t n_slots) {
     cv.take<char>(radix_tmp_bytes(n > 0 ? n : 1));
     cv.take<char>(scan_tmp_bytes((long long)nt * n_slots + 1));
     return cv.off + 256;
+}
+
+static int voxel_csr_counting(const int32_t *flab, int32_t nt, int64_t ncell, const int32_t *slot_of,
+                              int32_t lut_len, int32_t n_slots, int64_t *seg_start, int32_t *cells,
+                              void *workspace, size_t workspace_bytes, cudaStream_t st) {
+    const long long tpm = (ncell + VT - 1) / VT;
+    const long long nh = (long long)nt * n_slots * tpm;
+    if (tpm * nt >= (1ll << 31)) {
+        set_error("voxel_csr: too many tiles");
+        return 2;
+    }
+    Carver cv(workspace, workspace_bytes);
+    int *H = cv.take<int>(nh);
+    long long *H64 = cv.take<long long>(nh + 1);
+    long long *O = cv.take<long long>(nh + 1);
+    int *bad = cv.take<int>(4);
+    const size_t sb = scan_tmp_bytes(nh + 1);
+    void *stmp = cv.take<char>(sb);
+    MFSEG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    MFSEG_CUDA(cudaMemsetAsync(H64 + nh, 0, sizeof(long long), st));
+    const unsigned nb = (unsigned)(tpm * nt);
+    ::mfseg::count_launch();
+    k_voxel_hist<<<nb, 256, 0, st>>>(flab, ncell, (int)tpm, slot_of, lut_len, n_slots, H, bad);
+    ::mfseg::count_launch();
+    k_widen_i32<<<148 * 4, 256, 0, st>>>(H, nh, H64);
+    MFSEG_TRY(scan_exclusive_i64(H64, O, nh + 1, stmp, sb, st));
+    ::mfseg::count_launch();
+    k_voxel_scatter<<<nb, 256, 0, st>>>(flab, ncell, (int)tpm, slot_of, lut_len, n_slots, O, cells,
+                                        bad);
+    const int nseg = nt * n_slots;
+    ::mfseg::count_launch();
+    k_voxel_segs<<<(nseg + 256) / 256, 256, 0, st>>>(nseg, (int)tpm, O, (long long)nt * ncell,
+                                                     (long long *)seg_start);
+    MFSEG_LAUNCH("voxel_csr");
+    int hb = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (hb) {
+        set_error("voxel_csr: a field label has no feature slot");
+        return 2;
+    }
+    return 0;
 }
 
 int mfseg_voxel_csr(const int32_t *flab, int32_t nt, int64_t ncell, const int32_t *slot_of,
@@ -598,6 +806,9 @@ int mfseg_voxel_csr(const int32_t *flab, int32_t nt, int64_t ncell, const int32_
         set_error("voxel_csr: workspace too small");
         return 3;
     }
+    if (voxel_counting(n_slots))
+        return voxel_csr_counting(flab, nt, ncell, slot_of, lut_len, n_slots, seg_start, cells,
+                                  workspace, workspace_bytes, st);
     Carver cv(workspace, workspace_bytes);
     unsigned *keys = cv.take<unsigned>(n);
     unsigned *vals = cv.take<unsigned>(n);
@@ -684,12 +895,10 @@ int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *fi
     MFSEG_CUDA(cudaMemsetAsync(a.ovf, 0, sizeof(int), st));
     ::mfseg::count_launch();
     k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
-    ::mfseg::count_launch();
-    k_stats<<<148 * 8, 256, 0, st>>>(a, 0);
+    MFSEG_TRY(launch_stats(a, 0, st));
     ::mfseg::count_launch();
     k_stats_means<<<gs, 256, 0, st>>>(n_slots, a.S, mean);
-    ::mfseg::count_launch();
-    k_stats<<<148 * 8, 256, 0, st>>>(a, 1);
+    MFSEG_TRY(launch_stats(a, 1, st));
     ::mfseg::count_launch();
     k_stats_final<<<gs, 256, 0, st>>>(n_slots, a.S, mean, stats);
     MFSEG_LAUNCH("feature_stats");
@@ -757,8 +966,7 @@ int mfseg_feature_stats_pass(int32_t n_slots, const mfseg_field *f, const int32_
         ::mfseg::count_launch();
         k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
     }
-    ::mfseg::count_launch();
-    k_stats<<<148 * 8, 256, 0, st>>>(a, pass);
+    MFSEG_TRY(launch_stats(a, pass, st));
     MFSEG_LAUNCH("feature_stats_pass");
     MFSEG_CUDA(cudaMemcpyAsync(ovf_h, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));

@@ -922,6 +922,12 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.acc = P.acc;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
+        a.bin_start = P.g.bin_start;   // the CenterGrid of this pass (all K centres)
+        a.bin_ids = P.g.bin_ids;
+        for (int d = 0; d < 4; ++d) {
+            a.mins[d] = p.mins[d];
+            a.k[d] = p.k[d];
+        }
         // crowded tiles first (may add stranded samples), then the fallback
         const int4 kk = make_int4(p.k[0], p.k[1], p.k[2], p.k[3]);
         MFSEG_TRY(launch_deferred(a, P.g, P.tbin, kk, p.mins, kind == 1 ? P.deferred_f : P.deferred_p,

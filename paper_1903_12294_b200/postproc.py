@@ -199,17 +199,27 @@ def feature_stats_device(n_slots: int, fld: DeviceField, fslot: Optional[torch.T
 
 
 def voxel_csr_device(fslot: torch.Tensor, nt: int, ncell: int, n_slots: int):
-    """Per (timestep, slot) ascending cell lists: (seg_start int64 [(nt*ns)+1], cells int32)."""
+    """Per (timestep, slot) ascending cell lists: (seg_start int64 [(nt*ns)+1], cells int32).
+    Timesteps are processed in groups of < 2^31 samples (one call each)."""
     lib = N.load()
     dev = fslot.device
     seg = torch.empty(nt * n_slots + 1, dtype=torch.int64, device=dev)
     cells = torch.empty(nt * ncell, dtype=torch.int32, device=dev)
     ident = to_dev(np.arange(n_slots, dtype=np.int64), torch.int32, dev)
-    ws_bytes = lib.mfseg_voxel_csr_workspace_size(nt * ncell, nt, n_slots)
+    per = max(1, min(nt, ((1 << 31) - 1) // max(ncell, 1)))
+    ws_bytes = lib.mfseg_voxel_csr_workspace_size(per * ncell, per, n_slots)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    N.check(lib.mfseg_voxel_csr(N.ptr(fslot), nt, ncell, N.ptr(ident), n_slots, n_slots,
-                                N.ptr(seg), N.ptr(cells), N.ptr(ws), ws_bytes, stream_ptr()),
-            "mfseg_voxel_csr")
+    part = torch.empty(per * n_slots + 1, dtype=torch.int64, device=dev) if per < nt else seg
+    for m0 in range(0, nt, per):
+        m1 = min(nt, m0 + per)
+        dst = seg if per >= nt else part
+        N.check(lib.mfseg_voxel_csr(N.ptr(fslot[m0 * ncell:]), m1 - m0, ncell, N.ptr(ident),
+                                    n_slots, n_slots, N.ptr(dst), N.ptr(cells[m0 * ncell:]),
+                                    N.ptr(ws), ws_bytes, stream_ptr()), "mfseg_voxel_csr")
+        if per < nt:   # offsets of this group are relative to its first sample
+            seg[m0 * n_slots:m1 * n_slots] = part[:(m1 - m0) * n_slots] + m0 * ncell
+    if per < nt:
+        seg[nt * n_slots] = nt * ncell
     return seg, cells
 
 

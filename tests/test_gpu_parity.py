@@ -644,3 +644,65 @@ def test_assign_crowded_vs_oracle():
     want_p, want_f = _oracle_labels(ps, fs, cs, ext, C, params)
     np.testing.assert_array_equal(fl, want_f)
     np.testing.assert_array_equal(pl, want_p)
+
+
+@pytest.mark.parametrize("n_slots,nt,ncell", [(7, 3, 10000), (256, 2, 70001), (300, 4, 5000),
+                                              (1, 1, 4097), (49, 5, 4096 * 3)])
+def test_voxel_csr_paths_vs_numpy(n_slots, nt, ncell):
+    """mfseg_voxel_csr (counting sort for <= 256 features, radix sort above):
+    per (timestep, feature) ascending cell lists equal the reference's
+    flatnonzero(lab_m == fid) (postproc.py:162-168)."""
+    from paper_1903_12294_b200.postproc import voxel_csr_device
+    rng = np.random.default_rng(n_slots + nt)
+    # spatially coherent labels with noise, like real segmentations
+    lab = (np.arange(nt * ncell) // 997 + rng.integers(0, 3, nt * ncell)) % n_slots
+    lab = lab.astype(np.int32)
+    seg, cells = voxel_csr_device(torch.as_tensor(lab).cuda(), nt, ncell, n_slots)
+    seg, cells = seg.cpu().numpy(), cells.cpu().numpy()
+    for m in range(nt):
+        lm = lab[m * ncell:(m + 1) * ncell]
+        for s in range(n_slots):
+            want = np.flatnonzero(lm == s)
+            a, b = seg[m * n_slots + s], seg[m * n_slots + s + 1]
+            np.testing.assert_array_equal(cells[a:b], want)
+    assert seg[-1] == nt * ncell
+
+
+@pytest.mark.parametrize("n_slots", [3, 320, 321, 2000])
+def test_feature_stats_smem_and_global_paths_agree(n_slots):
+    """k_stats accumulates in shared memory for <= 320 features and with global
+    atomics above; both must equal a numpy restatement of feature_stats
+    (postproc.py:194-227) on random slots (exact bbox / counts, mean / std 1e-12)."""
+    from paper_1903_12294_b200.engine import DeviceField, DevicePoints
+    from paper_1903_12294_b200.postproc import feature_stats_device
+    rng = np.random.default_rng(n_slots)
+    dims, nt, npnt = (17, 9, 6), 3, 5000
+    ncell = int(np.prod(dims))
+    fv = rng.random(nt * ncell)
+    fld = DeviceField(dims, np.array([0.5, -1.0, 2.0]), np.array([0.25, 1.5, 1.0]),
+                      torch.tensor([0.0, 1.0, 2.5], dtype=torch.float64, device="cuda"),
+                      torch.as_tensor(fv).cuda())
+    xyz, t, pv = rng.random((npnt, 3)) * 5, rng.random(npnt) * 3, rng.random(npnt)
+    pts = DevicePoints(torch.as_tensor(xyz).cuda(), torch.as_tensor(t).cuda(), torch.as_tensor(pv).cuda())
+    fs = rng.integers(-1, n_slots, nt * ncell).astype(np.int32)
+    ps = rng.integers(-1, n_slots, npnt).astype(np.int32)
+    rows = feature_stats_device(n_slots, fld, torch.as_tensor(fs).cuda(), pts, torch.as_tensor(ps).cuda())
+    ii, jj, kk = np.meshgrid(np.arange(dims[0]), np.arange(dims[1]), np.arange(dims[2]), indexing="ij")
+    cx = 0.5 + (ii.transpose(2, 1, 0).ravel() + 0.5) * 0.25
+    cy = -1.0 + (jj.transpose(2, 1, 0).ravel() + 0.5) * 1.5
+    cz = 2.0 + (kk.transpose(2, 1, 0).ravel() + 0.5) * 1.0
+    floc = np.column_stack([np.tile(cx, nt), np.tile(cy, nt), np.tile(cz, nt),
+                            np.repeat([0.0, 1.0, 2.5], ncell)])
+    ploc = np.column_stack([xyz, t])
+    for s in range(0, n_slots, max(1, n_slots // 17)):
+        f, p = fs == s, ps == s
+        loc = np.vstack([floc[f], ploc[p]])
+        if len(loc) == 0:
+            continue
+        np.testing.assert_array_equal(rows[s][0:4], loc.min(0))
+        np.testing.assert_array_equal(rows[s][4:8], loc.max(0))
+        assert rows[s][12] == p.sum() and rows[s][13] == f.sum()
+        if p.any():
+            assert abs(rows[s][8] - pv[p].mean()) <= 1e-12 and abs(rows[s][9] - pv[p].std()) <= 1e-12
+        if f.any():
+            assert abs(rows[s][10] - fv[f].mean()) <= 1e-12 and abs(rows[s][11] - fv[f].std()) <= 1e-12
