@@ -435,7 +435,8 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         // brick is the sum over axes of the smaller endpoint difference (fp32 table
         // values, margin 2^-20 (S_s + S_s*) >> their rounding); the sqrt gap is at
         // least dS / (sqrt S_s,max + sqrt S_s*,max); the value terms differ by at
-        // most w_v |cv_s - cv_s*| (both have values) or w_v max|v - cv_s*| (only s*).
+        // least w_v min(f(v_lo), f(v_hi)), f(v) = |v - cv_s| - |v - cv_s*| (both have
+        // values; f is monotone in v), or -w_v max|v - cv_s*| (only s* has one).
         ubkey = __reduce_min_sync(0xffffffffu, ubkey);
         if ((a.debug & 8) && lane == 0) {
             const int nc = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
@@ -472,21 +473,51 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 float gd = INF_F;
                 if ((keep[r] >> lane & 1u) && s != sstar) {
                     const float *T = S.tab[s];
-                    const float ex0 = T[xa], ex1 = T[xb], ey0 = T[BX + ya], ey1 = T[BX + yb];
-                    const float ez0 = T[OZ + za], ez1 = T[OZ + zb], et0 = T[OT + ta], et1 = T[OT + tb];
-                    const float emax = fmaxf(fmaxf(fmaxf(ex0, ex1), fmaxf(ey0, ey1)),
-                                             fmaxf(fmaxf(ez0, ez1), fmaxf(et0, et1)));
-                    if (emax < INF_F) {   // valid on the whole brick (windows are intervals)
-                        const float dS = (fminf(ex0 - qx0, ex1 - qx1) + fminf(ey0 - qy0, ey1 - qy1)) +
-                                         (fminf(ez0 - qz0, ez1 - qz1) + fminf(et0 - qt0, et1 - qt1));
-                        const float dSlb = dS - 0x1.0p-20f * (shi[r] + shq);
+                    float dS = -INF_F, shs = shi[r];   // -inf: no proof possible
+                    {
+                        const float ex0 = T[xa], ex1 = T[xb], ey0 = T[BX + ya], ey1 = T[BX + yb];
+                        const float ez0 = T[OZ + za], ez1 = T[OZ + zb], et0 = T[OT + ta], et1 = T[OT + tb];
+                        const float emax = fmaxf(fmaxf(fmaxf(ex0, ex1), fmaxf(ey0, ey1)),
+                                                 fmaxf(fmaxf(ez0, ez1), fmaxf(et0, et1)));
+                        if (emax < INF_F)   // valid on the whole brick (windows are intervals)
+                            dS = (fminf(ex0 - qx0, ex1 - qx1) + fminf(ey0 - qy0, ey1 - qy1)) +
+                                 (fminf(ez0 - qz0, ez1 - qz1) + fminf(et0 - qt0, et1 - qt1));
+                    }
+                    if (dS == -INF_F) {
+                        // valid on part of the brick only: s can win only where it is valid,
+                        // so the dominance is proven over the brick's intersection with its
+                        // validity box (index intervals per axis; squared distances peak at
+                        // the interval ends, their differences are linear)
+                        const unsigned b = S.box[s];
+                        const int ia = max(xa, (int)(b & 15u)), ib = min(xb, (int)((b >> 4) & 15u));
+                        const int ja = max(ya, (int)((b >> 8) & 15u)), jb = min(yb, (int)((b >> 12) & 15u));
+                        const int ka = max(za, (int)((b >> 16) & 15u)), kb = min(zb, (int)((b >> 20) & 15u));
+                        const int ma = max(ta, (int)((b >> 24) & 3u)), mb = min(tb, (int)((b >> 26) & 3u));
+                        if (ia <= ib && ja <= jb && ka <= kb && ma <= mb) {
+                            const float *Q = S.tab[sstar];
+                            const float e0 = T[ia], e1 = T[ib], f0 = T[BX + ja], f1 = T[BX + jb];
+                            const float g0 = T[OZ + ka], g1 = T[OZ + kb], h0 = T[OT + ma], h1 = T[OT + mb];
+                            shs = (fmaxf(e0, e1) + fmaxf(f0, f1)) + (fmaxf(g0, g1) + fmaxf(h0, h1));
+                            if (shs < INF_F)
+                                dS = (fminf(e0 - Q[ia], e1 - Q[ib]) + fminf(f0 - Q[BX + ja], f1 - Q[BX + jb])) +
+                                     (fminf(g0 - Q[OZ + ka], g1 - Q[OZ + kb]) +
+                                      fminf(h0 - Q[OT + ma], h1 - Q[OT + mb]));
+                        }
+                    }
+                    if (dS > -INF_F) {
+                        const float dSlb = dS - 0x1.0p-20f * (shs + shq);
                         if (dSlb > 0.f) {
-                            const float den = (sqrt_approx(shi[r]) + rq) * (1.f + 0x1.0p-20f);
+                            const float den = (sqrt_approx(shs) + rq) * (1.f + 0x1.0p-20f);
                             const float gap = __fdividef(dSlb, den) * (1.f - 0x1.0p-19f);
                             float Vb = 0.f;
                             if (USEVAL && wvq > 0.f) {
+                                // both with values: |v - cv_s| - |v - cv_s*| is monotone in v,
+                                // so its minimum over the brick's value range is at an end
                                 const float cvs = S.cvf[s];
-                                const float V = S.wvf[s] > 0.f ? wvf * fabsf(cvs - cvq) : wvf * vq;
+                                const float V = S.wvf[s] > 0.f
+                                    ? wvf * fmaxf(0.f, -fminf(fabsf(vwl - cvs) - fabsf(vwl - cvq),
+                                                              fabsf(vwh - cvs) - fabsf(vwh - cvq)))
+                                    : wvf * vq;
                                 Vb = V * (1.f + 0x1.0p-18f) +
                                      0x1.0p-18f * wvf * (fabsf(cvs) + fabsf(cvq) + vabs);
                             }
@@ -500,6 +531,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 if (dom) gmin = fminf(gmin, gd);
             }
         }
+        if ((a.debug & 8) && lane == 0 && sstar < 0) atomicAdd(a.stats + 30, 1ull);   // no s*
         if ((a.debug & 8) && lane == 0) {
             atomicAdd(a.stats, 1ull);
             atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
@@ -1008,13 +1040,15 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
             if (live) {
                 lo = fminf(lo, (float)v);
                 hi = fmaxf(hi, (float)v);
-                amax = fmax(amax, fabs(v));
-                bad |= !isfinite(v);
             }
         }
         vs = warp_sum_d(vs);
         lo = warp_min_f(lo);
         hi = warp_max_f(hi);
+        // range check of the fixed-point sums, per brick: NaN / inf propagate into
+        // the fp64 sum; |value| is bounded by the fl32 range (inf if it overflows fl32)
+        bad |= !isfinite(vs);
+        amax = fmax(amax, (double)fmaxf(fabsf(lo), fabsf(hi)));
         if (lane == 0) {
             a.brange_out[(size_t)blockIdx.x * 64 + bi] = make_float2(lo, hi);
             unsigned long long flo;
@@ -1025,10 +1059,7 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
             a.bsum_out[(size_t)blockIdx.x * 64 + bi] = make_ulonglong2(flo, (unsigned long long)fhi);
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    bad = __any_sync(0xffffffffu, bad);
-    if (lane == 0 && a.absmax) {
+    if (lane == 0 && a.absmax) {   // amax and bad are warp-uniform
         atomicMax(a.absmax + 5, (unsigned long long)__double_as_longlong(amax));
         if (bad) atomicOr(a.absmax + 6, 1ull);
     }

@@ -330,8 +330,13 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                         const float gap = __fdividef(dSlb, den) * (1.f - 0x1.0p-19f);
                         float Vb = 0.f;
                         if (USEVAL && wvq > 0.f) {
+                            // monotone value-term difference: its minimum over the tile's
+                            // value range is at an end (see k_field_assign5)
                             const float cvs = S.cvf[s];
-                            const float V = S.wvf[s] > 0.f ? C.wvf * fabsf(cvs - cvq) : C.wvf * vq;
+                            const float V = S.wvf[s] > 0.f
+                                ? C.wvf * fmaxf(0.f, -fminf(fabsf(vl - cvs) - fabsf(vl - cvq),
+                                                            fabsf(vh - cvs) - fabsf(vh - cvq)))
+                                : C.wvf * vq;
                             Vb = V * (1.f + 0x1.0p-18f) + 0x1.0p-18f * C.wvf * (fabsf(cvs) + fabsf(cvq) + vabs);
                         }
                         const float rel = 0x1.0p-30f * (C.fwd * den + Wb) + C.slack;

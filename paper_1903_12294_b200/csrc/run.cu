@@ -406,7 +406,9 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.bsum = cv.take<ulonglong2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     {
         const long long bricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
-        P.multi_cap = P.nf > 0 ? (bricks < (1ll << 21) ? bricks : (1ll << 21)) : 0;
+        // every brick can be queued (96 B per brick of <= 256 samples): a full queue
+        // would send the rest to the per-sample exact path (k_deferred), 10-100x slower
+        P.multi_cap = P.nf > 0 ? bricks : 0;
         P.multi = cv.take<MultiItem>(P.multi_cap);
         P.bslot = cv.take<unsigned char>(P.nf > 0 ? bricks : 0);
         P.bmargin = cv.take<float>(P.nf > 0 ? bricks : 0);
@@ -949,8 +951,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
                     F[0], rat(F[1], F[0]), F[2], rat(F[3], F[0]), F[4], rat(F[5], F[4]), rat(F[6], F[5]),
                     Q[0], rat(Q[1], Q[0]), Q[2], h[0], h[1], h[2], h[3]);
             fprintf(stderr, "[mfseg stats] field bricks: kept after cull %.3f, single after cull %.3f, "
-                    "reused %llu, screen items %llu exact samples %llu\n", rat(F[7], F[0]), rat(F[2], F[0]),
-                    h[32], h[33], h[34]);
+                    "reused %llu, screen items %llu exact samples %llu, bricks without s* %.3f\n",
+                    rat(F[7], F[0]), rat(F[2], F[0]), h[32], h[33], h[34], rat(h[38], F[0]));
             fprintf(stderr, "[mfseg stats] point tiles single %.3f kept hist", rat(Q[3], Q[0]));
             for (int q = 0; q < 8; ++q) fprintf(stderr, " %.3f", rat(Q[4 + q], Q[0]));
             fprintf(stderr, " | chunks by candidate rounds 1/2/3/4: %llu %llu %llu %llu", Q[12], Q[13],
