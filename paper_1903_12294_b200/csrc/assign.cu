@@ -123,6 +123,7 @@ __device__ void fallback_one(const FallbackArgs &a, long long idx) {
     }
     if (lane == 0) {
         a.labels[idx] = best == INT_MAX ? -1 : best;
+        if (a.kind == 0 && a.labels_out) a.labels_out[a.perm[idx]] = best == INT_MAX ? -1 : best;
         if (best == INT_MAX) {
             *a.overflow = 3;
             return;
@@ -227,11 +228,13 @@ __device__ void deferred_one(const FallbackArgs &a, const DeferredGeo &G, long l
     if (lane != 0) return;
     if (bI == INT_MAX) {   // stranded: the fallback kernel runs next
         a.labels[idx] = -1;
+        if (a.kind == 0 && a.labels_out) a.labels_out[a.perm[idx]] = -1;
         const unsigned long long q = atomicAdd((unsigned long long *)a.n_stranded, 1ull);
         if ((long long)q < a.cap) ((long long *)a.stranded)[q] = idx;
         return;
     }
     a.labels[idx] = bI;
+    if (a.kind == 0 && a.labels_out) a.labels_out[a.perm[idx]] = bI;
     if (a.accumulate) {
         unsigned long long *p = a.acc + (size_t)bI * MFSEG_ACC_WORDS;
         atomic_add_double_fix(p + ACC_X + 0, s0, a.overflow);

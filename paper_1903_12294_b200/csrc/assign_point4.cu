@@ -161,6 +161,10 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     if (C.stable) {   // unchanged since the last pass: the tile keeps its labels
         const unsigned char ts = a.tslot[tidx];
         if (ts < 254) {   // one label: the per-run tile sums
+            if (a.labels_out) {   // final pass: record-order labels
+                if (live0) a.labels_out[a.perm[p0]] = S.id[ts];
+                if (live1) a.labels_out[a.perm[p1]] = S.id[ts];
+            }
             if (a.accumulate && lane == 0) {
 #pragma unroll
                 for (int d = 0; d < 5; ++d) S.wsum[w][d][ts] = DADD(S.wsum[w][d][ts], wbp->s[d]);
@@ -171,6 +175,10 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         if (ts == 254) {   // several labels (none stranded): slots from the labels
             if (!a.accumulate) return;
             const int lab0 = live0 ? a.labels[p0] : -1, lab1 = live1 ? a.labels[p1] : -1;
+            if (a.labels_out) {
+                if (live0) a.labels_out[a.perm[p0]] = lab0;
+                if (live1) a.labels_out[a.perm[p1]] = lab1;
+            }
             int todo0 = lab0, todo1 = lab1;
             while (true) {
                 const unsigned m0 = __ballot_sync(0xffffffffu, todo0 >= 0),
@@ -478,11 +486,13 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     if (live0) {
         const int lab = C.deferred ? -2 : (sl0 >= 0 ? S.id[sl0] : -1);
         a.labels[p0] = lab;
+        if (a.labels_out) a.labels_out[a.perm[p0]] = lab;
         if (lab < 0) ++nlist;
     }
     if (live1) {
         const int lab = C.deferred ? -2 : (sl1 >= 0 ? S.id[sl1] : -1);
         a.labels[p1] = lab;
+        if (a.labels_out) a.labels_out[a.perm[p1]] = lab;
         if (lab < 0) ++nlist;
     }
     const bool listed = __any_sync(0xffffffffu, nlist > 0);

@@ -90,6 +90,8 @@ struct PointArgs {
     const uint8_t *chas;
     Grid g;
     int *labels;                       // bin-sorted order
+    int *labels_out;                   // final pass: also labels_out[perm[p]] (record order)
+    const unsigned *perm;              // bin-sorted position -> record index
     unsigned long long *acc;
     long long *stranded;
     unsigned long long *n_stranded;
@@ -129,6 +131,8 @@ struct FallbackArgs {
     int k[4];
     long long n_samples;
     int *labels;
+    int *labels_out;                   // points, final pass: also labels_out[perm[idx]]
+    const unsigned *perm;
     const long long *stranded;
     const unsigned long long *n_stranded;
     long long cap;

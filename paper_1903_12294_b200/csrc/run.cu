@@ -734,7 +734,7 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
 // state of the previous pass when it used the same weights (labels of stable
 // field blocks are reused), else null
 int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, int32_t *flabels,
-              int accumulate, const mfseg_centers *prev) {
+              int accumulate, const mfseg_centers *prev, int32_t *plabels_out) {
     cudaStream_t st = P.st;
     const mfseg_params &p = P.p;
     int K = P.K;
@@ -862,6 +862,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.chas = c.has_p;
         a.g = P.g;
         a.labels = P.plabels;
+        a.labels_out = plabels_out;   // final pass: record-order labels stored directly
+        a.perm = P.perm;
         a.acc = P.acc;
         a.stranded = P.stranded_p;
         a.n_stranded = P.counters + 1;
@@ -918,6 +920,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.pv = P.pv;
         a.n_samples = kind == 1 ? P.nf : P.np;
         a.labels = kind == 1 ? flabels : P.plabels;
+        a.labels_out = kind == 1 ? nullptr : plabels_out;
+        a.perm = P.perm;
         a.stranded = kind == 1 ? P.stranded_f : P.stranded_p;
         a.n_stranded = P.counters + (kind == 1 ? 0 : 1);
         a.cap = kind == 1 ? P.cap_f : P.cap_p;
@@ -1051,13 +1055,18 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
     MFSEG_LAUNCH("k_seed");
     int cur = 0;
     int iterations = 0, converged = 0;
+    bool unpermuted = false;
     alignas(16) char flags_host[64];
     for (int pass = 0; pass <= p->max_iterations; ++pass) {
         bool initial = pass == 0;
         // initial assignment: pure space-time nearest seed (engine.py:346-351)
         double wd = initial ? 1.0 : p->w_d, wp = initial ? 0.0 : p->w_p, wf = initial ? 0.0 : p->w_f;
         // from the second weighted pass on, stable field blocks reuse the last labels
-        MFSEG_TRY(plan_pass(P, P.s[cur], wd, wp, wf, field_labels, 1, pass >= 2 ? &P.s[cur ^ 1] : nullptr));
+        // the last possible pass writes the point labels in record order itself
+        const bool last = pass == p->max_iterations;
+        MFSEG_TRY(plan_pass(P, P.s[cur], wd, wp, wf, field_labels, 1, pass >= 2 ? &P.s[cur ^ 1] : nullptr,
+                            last ? point_labels : nullptr));
+        unpermuted = last;
         if (reduce) {
             long long npairs = (long long)K * MFSEG_ACC_WORDS / 2;
             MFSEG_TRY(launch_to_limbs(npairs, P.acc, P.limbs, st));
@@ -1086,7 +1095,7 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
         if (converged) break;
     }
     MFSEG_TRY(check_overflow(P));
-    if (P.np > 0) {
+    if (P.np > 0 && !unpermuted) {   // converged before the last pass
         ::mfseg::count_launch();
         k_unpermute<<<(unsigned)((P.np + 1023) / 1024), 256, 0, st>>>(P.np, P.perm, P.plabels,
                                                                      point_labels);
@@ -1108,13 +1117,7 @@ int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
     MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
     MFSEG_TRY(plan_prepare(P));
-    MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr));
-    if (P.np > 0) {
-        ::mfseg::count_launch();
-        k_unpermute<<<(unsigned)((P.np + 1023) / 1024), 256, 0, st>>>(P.np, P.perm, P.plabels,
-                                                                     point_labels);
-        MFSEG_LAUNCH("k_unpermute");
-    }
+    MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr, point_labels));
     if (acc)
         MFSEG_CUDA(cudaMemcpyAsync(acc, P.acc, sizeof(int64_t) * P.K * MFSEG_ACC_WORDS,
                                    cudaMemcpyDeviceToDevice, st));
