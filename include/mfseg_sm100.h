@@ -227,11 +227,13 @@ int mfseg_link_index(const mfseg_field *f, const mfseg_points *pts, int64_t *key
  * (NaN = absent), n_points/n_fields [n].  Outputs: rep [n] int32 (the merge
  * map, = smallest id of the eligibility component), merged table rows
  * (ascending representative id): m_ids, m_loc [4][n], m_p/m_f, m_np, m_nf
- * and n_merged_host. */
+ * and n_merged_host.  neumaier: 1 = the merged p_c / f_c sums follow CPython
+ * >= 3.12's compensated sum() of floats, 0 = the plain left-to-right sum of
+ * earlier interpreters (postproc.py:85-88 uses the builtin sum). */
 size_t mfseg_merge_workspace_size(int32_t n);
 int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *p_c,
                 const double *f_c, const int64_t *n_points, const int64_t *n_fields,
-                double eps_m, int32_t *rep, int32_t *m_ids, double *m_loc, double *m_p,
+                double eps_m, int32_t neumaier, int32_t *rep, int32_t *m_ids, double *m_loc, double *m_p,
                 double *m_f, int64_t *m_np, int64_t *m_nf, int32_t *n_merged_host,
                 void *workspace, size_t workspace_bytes, void *stream);
 

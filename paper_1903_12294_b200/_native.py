@@ -82,7 +82,7 @@ _SIGNATURES = {
     "mfseg_link_index_workspace_size": (szt, [i64]),
     "mfseg_link_index": (C.c_int, [P(Field), P(Points), vp, vp, P(i64), vp, szt, vp]),
     "mfseg_merge_workspace_size": (szt, [i32]),
-    "mfseg_merge": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp, vp, vp, vp,
+    "mfseg_merge": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, f64, i32, vp, vp, vp, vp, vp, vp, vp,
                               P(i32), vp, szt, vp]),
     "mfseg_relabel": (C.c_int, [vp, i64, vp, i32, vp, vp]),
     "mfseg_voxel_csr_workspace_size": (szt, [i64, i32, i32]),

@@ -72,15 +72,23 @@ __global__ void k_uf_init(int n, int *parent) {
     if (i < n) parent[i] = i;
 }
 
-// one warp per row i, lanes sweep j > i
+// one warp per row i, lanes sweep j > i.  Most eligible pairs join rows that are
+// already connected (a feature of m clusters has ~m^2/2 eligible pairs but m - 1
+// useful ones): a lane skips the union when j's root is row i's current root,
+// which costs one short find instead of the two finds and the CAS of a union.
 __global__ void k_merge_pairs(int n, const double *pc, const double *fc, double eps, int *parent) {
     long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (w >= n) return;
     int i = (int)w;
     double pi = pc[i], fi = fc[i];
-    for (int j = i + 1 + lane; j < n; j += 32)
-        if (values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps)) uf_union(parent, i, j);
+    int ri = uf_find(parent, i);
+    for (int j0 = i + 1; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const bool m = j < n && values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps);
+        if (m && uf_find(parent, j) != ri) uf_union(parent, i, j);
+        if (__any_sync(0xffffffffu, m)) ri = uf_find(parent, i);   // roots only move down
+    }
 }
 
 __global__ void k_uf_flatten(int n, int *parent, const int *ids, int *rep_row, int *rep_id,
@@ -105,7 +113,8 @@ struct MergeOut {
 __global__ void k_merge_groups(int n, const unsigned *skeys, const unsigned *members,
                                const int *is_root, const int *group_of_root, const int *ids,
                                const double *loc, const double *pc, const double *fc,
-                               const long long *np_, const long long *nf_, MergeOut o, int G) {
+                               const long long *np_, const long long *nf_, MergeOut o, int G,
+                               int neumaier) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;   // position in the sorted order
     if (i >= n) return;
     if (i > 0 && skeys[i - 1] == skeys[i]) return;  // not the first member of its group
@@ -113,7 +122,7 @@ __global__ void k_merge_groups(int n, const unsigned *skeys, const unsigned *mem
     int g = group_of_root[root];
     long long n_p = 0, n_f = 0, n_tot = 0;
     double ls[4] = {0.0, 0.0, 0.0, 0.0};
-    double pf = 0.0, pcmp = 0.0, ff = 0.0, fcmp = 0.0;
+    double pf = 0.0, pcmp = 0.0, ff = 0.0, fcmp = 0.0;   // compensation used when neumaier
     for (int q = i; q < n && skeys[q] == (unsigned)root; ++q) {
         int r = (int)members[q];
         long long a = np_[r], b = nf_[r], t = a + b;
@@ -122,18 +131,20 @@ __global__ void k_merge_groups(int n, const unsigned *skeys, const unsigned *mem
         n_tot += t;
         double dt = (double)t;
         for (int d = 0; d < 4; ++d) ls[d] = DADD(ls[d], DMUL(loc[(size_t)d * n + r], dt));
-        if (!isnan(pc[r])) {   // Neumaier step (CPython >= 3.12 sum of floats)
+        if (!isnan(pc[r])) {   // Neumaier step (CPython >= 3.12 sum of floats), else plain
             double x = DMUL(pc[r], (double)a);
             double t2 = DADD(pf, x);
-            pcmp = fabs(pf) >= fabs(x) ? DADD(pcmp, DADD(DSUB(pf, t2), x))
-                                       : DADD(pcmp, DADD(DSUB(x, t2), pf));
+            if (neumaier)
+                pcmp = fabs(pf) >= fabs(x) ? DADD(pcmp, DADD(DSUB(pf, t2), x))
+                                           : DADD(pcmp, DADD(DSUB(x, t2), pf));
             pf = t2;
         }
         if (!isnan(fc[r])) {
             double x = DMUL(fc[r], (double)b);
             double t2 = DADD(ff, x);
-            fcmp = fabs(ff) >= fabs(x) ? DADD(fcmp, DADD(DSUB(ff, t2), x))
-                                       : DADD(fcmp, DADD(DSUB(x, t2), ff));
+            if (neumaier)
+                fcmp = fabs(ff) >= fabs(x) ? DADD(fcmp, DADD(DSUB(ff, t2), x))
+                                           : DADD(fcmp, DADD(DSUB(x, t2), ff));
             ff = t2;
         }
     }
@@ -665,7 +676,7 @@ size_t mfseg_merge_workspace_size(int32_t n) {
 
 int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *p_c,
                 const double *f_c, const int64_t *n_points, const int64_t *n_fields, double eps_m,
-                int32_t *rep, int32_t *m_ids, double *m_loc, double *m_p, double *m_f,
+                int32_t neumaier, int32_t *rep, int32_t *m_ids, double *m_loc, double *m_p, double *m_f,
                 int64_t *m_np, int64_t *m_nf, int32_t *n_merged_host, void *workspace,
                 size_t workspace_bytes, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -709,7 +720,7 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
     ::mfseg::count_launch();
     k_merge_groups<<<g, 256, 0, st>>>(n, skeys, members, is_root, group_of_root, ids, loc, p_c,
                                       f_c, (const long long *)n_points,
-                                      (const long long *)n_fields, o, G);
+                                      (const long long *)n_fields, o, G, neumaier);
     MFSEG_LAUNCH("k_merge_groups");
     if (n_merged_host) *n_merged_host = G;
     return 0;

@@ -16,6 +16,7 @@ polylines / isolated points the API returns are built on the host.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field as dc_field
 from typing import Optional, Sequence
 
@@ -26,6 +27,12 @@ from . import _native as N
 from .engine import (DeviceField, DevicePoints, device, field_to_device, points_to_device,
                      stream_ptr, to_dev)
 from .model import DELTA, ClusterCenter, FieldSet, PointSet, Segmentation
+
+
+# The reference sums merged p_c / f_c with the builtin sum() (postproc.py:85-88),
+# which CPython 3.12 made compensated (Neumaier); the kernel follows the running
+# interpreter so merged tables stay bit-identical to the reference under it.
+NEUMAIER = 1 if sys.version_info >= (3, 12) else 0
 
 
 def _pct_diff(a: float, b: float) -> float:
@@ -75,7 +82,7 @@ def merge_clusters(centers: Sequence[ClusterCenter], eps_m: float):
     ws_bytes = lib.mfseg_merge_workspace_size(n)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     N.check(lib.mfseg_merge(n, N.ptr(ids), N.ptr(loc), N.ptr(pc), N.ptr(fc), N.ptr(npt),
-                            N.ptr(nfl), float(eps_m), N.ptr(rep), N.ptr(m_ids), N.ptr(m_loc),
+                            N.ptr(nfl), float(eps_m), NEUMAIER, N.ptr(rep), N.ptr(m_ids), N.ptr(m_loc),
                             N.ptr(m_p), N.ptr(m_f), N.ptr(m_np), N.ptr(m_nf), C.byref(G),
                             N.ptr(ws), ws_bytes, stream_ptr()), "mfseg_merge")
     g = G.value
@@ -121,7 +128,7 @@ def merge_device(state: dict, eps_m: float):
         ws_bytes = lib.mfseg_merge_workspace_size(n)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
         N.check(lib.mfseg_merge(n, N.ptr(ids), N.ptr(loc), N.ptr(pc), N.ptr(fc), N.ptr(npt),
-                                N.ptr(nfl), float(eps_m), N.ptr(rep), N.ptr(m_ids), N.ptr(m_loc),
+                                N.ptr(nfl), float(eps_m), NEUMAIER, N.ptr(rep), N.ptr(m_ids), N.ptr(m_loc),
                                 N.ptr(m_p), N.ptr(m_f), N.ptr(m_np), N.ptr(m_nf), C.byref(G),
                                 N.ptr(ws), ws_bytes, stream_ptr()), "mfseg_merge")
     g = G.value

@@ -92,3 +92,27 @@ def test_pipeline_artifacts_match_reference(tmp_path):
     for name in (A.SEGMENTATION_JSON, A.MERGE_JSON, A.FEATURES_JSON):
         with open(os.path.join(GOLD, name)) as f1, open(os.path.join(tmp_path, name)) as f2:
             _close_json(json.load(f1), json.load(f2))
+
+
+@pytest.mark.gpu
+def test_device_run_directory_byte_identical(tmp_path, monkeypatch):
+    """save_segmentation_device (labels streamed from device memory in several
+    double-buffered chunks) writes the same bytes as save_segmentation of the
+    host Segmentation of the same run."""
+    import paper_1903_12294_b200 as P
+    from paper_1903_12294_b200 import artifacts as A
+    from paper_1903_12294_b200.engine import run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device, synthetic_device
+    from paper_1903_12294_b200.pipeline import to_segmentation
+    fld, pts, _ = synthetic_device((40, 36, 30), 6, 3000, seed=8)
+    norm = normalize_device(pts, fld, True)
+    ext = domain_extent_device(pts, fld)
+    params = P.ClusterParams(k=(4, 4, 3, 2), eps_c=1e-12, max_iterations=4)
+    r = run_device(pts, fld, ext, params)
+    monkeypatch.setattr(A, "_CHUNK", 10007)          # many chunks, a ragged last one
+    A.save_segmentation_device(str(tmp_path / "dev"), r, params, ext, norm)
+    A.save_segmentation(str(tmp_path / "host"), to_segmentation(r, params, ext), norm)
+    for name in (A.SEGMENTATION_JSON, A.POINT_LABELS_BIN, A.FIELD_LABELS_BIN):
+        assert (tmp_path / "dev" / name).read_bytes() == (tmp_path / "host" / name).read_bytes(), name
+    seg, norm2 = A.load_segmentation(str(tmp_path / "dev"))
+    assert norm2 == norm and len(seg.field_labels) == fld.values.numel()
