@@ -82,12 +82,12 @@ __global__ void k_merge_pairs(int n, const double *pc, const double *fc, double 
     if (w >= n) return;
     int i = (int)w;
     double pi = pc[i], fi = fc[i];
-    int ri = uf_find(parent, i);
-    for (int j0 = i + 1; j0 < n; j0 += 32) {
-        const int j = j0 + lane;
-        const bool m = j < n && values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps);
-        if (m && uf_find(parent, j) != ri) uf_union(parent, i, j);
-        if (__any_sync(0xffffffffu, m)) ri = uf_find(parent, i);   // roots only move down
+    int ri = -1;   // a root of row i seen by this lane (roots stay roots or get linked below)
+    for (int j = i + 1 + lane; j < n; j += 32) {
+        if (!(values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps))) continue;
+        if (ri >= 0 && uf_find(parent, j) == ri) continue;   // ri is still a root: connected
+        uf_union(parent, i, j);
+        ri = uf_find(parent, i);
     }
 }
 
@@ -349,9 +349,10 @@ __device__ void stat_add(unsigned long long *S, int slot, bool field, double x, 
             if (lane == leader) {
                 atomic_add_fix(s + (field ? 2 : 0), lo, hi);
                 atomicAdd(s + (field ? 9 : 8), (unsigned long long)__popc(m));
-                for (int d = 0; d < 4; ++d) {
-                    atomicMin(s + 10 + d, okey(bl[d]));
-                    atomicMax(s + 14 + d, okey(bh[d]));
+                for (int d = 0; d < 4; ++d) {   // atomics only when the box grows
+                    const unsigned long long kl = okey(bl[d]), kh = okey(bh[d]);
+                    if (kl < ((volatile unsigned long long *)s)[10 + d]) atomicMin(s + 10 + d, kl);
+                    if (kh > ((volatile unsigned long long *)s)[14 + d]) atomicMax(s + 14 + d, kh);
                 }
             }
         } else {
