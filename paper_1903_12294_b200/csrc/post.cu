@@ -72,23 +72,15 @@ __global__ void k_uf_init(int n, int *parent) {
     if (i < n) parent[i] = i;
 }
 
-// one warp per row i, lanes sweep j > i.  Most eligible pairs join rows that are
-// already connected (a feature of m clusters has ~m^2/2 eligible pairs but m - 1
-// useful ones): a lane skips the union when j's root is row i's current root,
-// which costs one short find instead of the two finds and the CAS of a union.
+// one warp per row i, lanes sweep j > i
 __global__ void k_merge_pairs(int n, const double *pc, const double *fc, double eps, int *parent) {
     long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (w >= n) return;
     int i = (int)w;
     double pi = pc[i], fi = fc[i];
-    int ri = -1;   // a root of row i seen by this lane (roots stay roots or get linked below)
-    for (int j = i + 1 + lane; j < n; j += 32) {
-        if (!(values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps))) continue;
-        if (ri >= 0 && uf_find(parent, j) == ri) continue;   // ri is still a root: connected
-        uf_union(parent, i, j);
-        ri = uf_find(parent, i);
-    }
+    for (int j = i + 1 + lane; j < n; j += 32)
+        if (values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps)) uf_union(parent, i, j);
 }
 
 __global__ void k_uf_flatten(int n, int *parent, const int *ids, int *rep_row, int *rep_id,

@@ -406,9 +406,29 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.bsum = cv.take<ulonglong2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
     {
         const long long bricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
-        // every brick can be queued (96 B per brick of <= 256 samples): a full queue
-        // would send the rest to the per-sample exact path (k_deferred), 10-100x slower
-        P.multi_cap = P.nf > 0 ? bricks : 0;
+        // every live brick can be queued (96 B per brick of <= 256 samples): a full
+        // queue would send the rest to the per-sample exact path (k_deferred), 10-100x
+        // slower.  Live bricks per block are a product over the axes (thin grids,
+        // e.g. nz = 1, leave most of a block's 64 brick slots empty).
+        long long live = 0;
+        if (P.nf > 0) {
+            int TX, TY, TZ;
+            field_tile_dims(&TX, &TY, &TZ);
+            auto per_axis = [](const std::vector<AxisTile> &v, int g) {
+                long long c = 0;
+                for (const AxisTile &t : v) c += (t.len + g - 1) / g;
+                return c;
+            };
+            const long long lx = per_axis(axis_tiles(P.f.nx, P.f.origin[0], P.f.spacing[0], P.f.offset[0],
+                                                     P.p.mins[0], P.p.C[0], P.p.k[0], TX), 8);
+            const long long ly = per_axis(axis_tiles(P.f.ny, P.f.origin[1], P.f.spacing[1], P.f.offset[1],
+                                                     P.p.mins[1], P.p.C[1], P.p.k[1], TY), 4);
+            const long long lz = per_axis(axis_tiles(P.f.nz, P.f.origin[2], P.f.spacing[2], P.f.offset[2],
+                                                     P.p.mins[2], P.p.C[2], P.p.k[2], TZ), 4);
+            // time tiles: ceil(len / 2) bricks each, at most len: <= nt in all
+            live = lx * ly * lz * (long long)P.f.nt;
+        }
+        P.multi_cap = P.nf > 0 ? (live < bricks ? live : bricks) : 0;
         P.multi = cv.take<MultiItem>(P.multi_cap);
         P.bslot = cv.take<unsigned char>(P.nf > 0 ? bricks : 0);
         P.bmargin = cv.take<float>(P.nf > 0 ? bricks : 0);
