@@ -310,6 +310,19 @@ __device__ __forceinline__ void warp_sum_fix(unsigned long long &lo, long long &
     }
 }
 
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k) {
+    const unsigned hi = (unsigned)(k >> 32);
+    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? (unsigned)k : 0xFFFFFFFFu);
+    return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
+    const unsigned hi = (unsigned)(k >> 32);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)k : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
 // warp-aggregated add of one sample into its slot's accumulators; the value
 // sums are reduced in 128-bit fixed point (exact, order-free)
 __device__ void stat_add(unsigned long long *S, int slot, bool field, double x, double y,
@@ -327,24 +340,22 @@ __device__ void stat_add(unsigned long long *S, int slot, bool field, double x, 
         if (pass == 0) {
             if (mine) d2fix(v, lo, hi, ovf);
             warp_sum_fix(lo, hi);
-            double bl[4] = {x, y, z, t}, bh[4] = {x, y, z, t};
+            // bbox as order-preserving 64-bit keys, reduced with 32-bit REDUX (high
+            // word, then the low word among the lanes holding the extreme high word)
+            const double bv[4] = {x, y, z, t};
+            unsigned long long kl[4], kh[4];
+#pragma unroll
             for (int d = 0; d < 4; ++d) {
-                double a = mine ? bl[d] : __builtin_huge_val();
-                double b = mine ? bh[d] : -__builtin_huge_val();
-                for (int o = 16; o > 0; o >>= 1) {
-                    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
-                    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
-                }
-                bl[d] = a;
-                bh[d] = b;
+                const unsigned long long k = okey(bv[d]);
+                kl[d] = warp_min_u64(mine ? k : ~0ull);
+                kh[d] = warp_max_u64(mine ? k : 0ull);
             }
             if (lane == leader) {
                 atomic_add_fix(s + (field ? 2 : 0), lo, hi);
                 atomicAdd(s + (field ? 9 : 8), (unsigned long long)__popc(m));
                 for (int d = 0; d < 4; ++d) {   // atomics only when the box grows
-                    const unsigned long long kl = okey(bl[d]), kh = okey(bh[d]);
-                    if (kl < ((volatile unsigned long long *)s)[10 + d]) atomicMin(s + 10 + d, kl);
-                    if (kh > ((volatile unsigned long long *)s)[14 + d]) atomicMax(s + 14 + d, kh);
+                    if (kl[d] < ((volatile unsigned long long *)s)[10 + d]) atomicMin(s + 10 + d, kl[d]);
+                    if (kh[d] > ((volatile unsigned long long *)s)[14 + d]) atomicMax(s + 14 + d, kh[d]);
                 }
             }
         } else {
