@@ -299,16 +299,31 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
 // bit b of a keep mask = list position b); otherwise slot = bit + 32 * round.
 // A whole brick labelled by one slot: the count marginals are constants and the
 // value sum is the brick's (fixed-order warp sum, computed once per run).
+// Partial sums of a brick labelled by one slot: count marginals from its live
+// extents (ex x ey x ez x et samples; a brick cut by the block edge -- or by a
+// thin grid, e.g. nz = 1 -- has fewer) and the brick's per-run value sum.
 __device__ __forceinline__ void single_brick_sums(const FieldArgs &a, Smem5 &S, size_t bidx, int one,
-                                                  int bx, int by, int bz, int bt) {
+                                                  int bx, int by, int bz, int bt, int ex, int ey,
+                                                  int ez, int et) {
     const int lane = threadIdx.x & 31;
     unsigned *h = S.hist[one];
-    if (lane < 4) atomicAdd(&h[4 * bx + lane], 32u | (32u << 16));         // 8 x, 32 each
-    else if (lane < 6) atomicAdd(&h[8 + 2 * by + (lane - 4)], 64u | (64u << 16));   // 4 y
-    else if (lane < 8) atomicAdd(&h[16 + 2 * bz + (lane - 6)], 64u | (64u << 16));  // 4 z
-    else if (lane == 8) atomicAdd(&h[24 + bt], 128u | (128u << 16));      // 2 timesteps
-    else if (lane == 9) atomicAdd(&h[26], 256u);
-    else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
+    auto pair = [](int i0, int e, unsigned c) {   // two 16-bit counts: indices i0, i0 + 1
+        return (i0 < e ? c : 0u) | ((i0 + 1 < e ? c : 0u) << 16);
+    };
+    if (lane < 4) {                                                          // 8 x
+        const unsigned w = pair(2 * lane, ex, (unsigned)(ey * ez * et));
+        if (w) atomicAdd(&h[4 * bx + lane], w);
+    } else if (lane < 6) {                                                   // 4 y
+        const unsigned w = pair(2 * (lane - 4), ey, (unsigned)(ex * ez * et));
+        if (w) atomicAdd(&h[8 + 2 * by + (lane - 4)], w);
+    } else if (lane < 8) {                                                   // 4 z
+        const unsigned w = pair(2 * (lane - 6), ez, (unsigned)(ex * ey * et));
+        if (w) atomicAdd(&h[16 + 2 * bz + (lane - 6)], w);
+    } else if (lane == 8) {                                                  // 2 timesteps
+        atomicAdd(&h[24 + bt], pair(0, et, (unsigned)(ex * ey * ez)));
+    } else if (lane == 9) {
+        atomicAdd(&h[26], (unsigned)(ex * ey * ez * et));
+    } else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
         const ulonglong2 vs = a.bsum[bidx];
         const int q = lane - 10;
         const unsigned long long lo = vs.x, hi = vs.y;
@@ -368,14 +383,9 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
     // labelled by one candidate use the per-run brick value range and value
     // sum (k_brick_pre: the field values do not change between passes).
     const size_t bidx = (size_t)blockIdx.x * 64 + bi;
-    double v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = 0.0;
-    if (!FULL) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            v[k] = (livem >> k & 1) ? __ldg(a.values + fbase + (k & 3) * C.plane + (k >> 2) * C.vol) : 0.0;
-    }
+    // live extents of the brick (all full unless the block edge cuts it)
+    const int ex = FULL ? GX : min(GX, C.X.len - GX * bx), ey = FULL ? GY : min(GY, C.Y.len - GY * by);
+    const int ez = FULL ? GZ : min(GZ, C.Z.len - GZ * bz), et = FULL ? GT : min(GT, C.T.len - GT * bt);
 
     int sl[8];
 #pragma unroll
@@ -545,7 +555,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
             for (int k = 0; k < 8; ++k) sl[k] = (livem >> k & 1) ? sstar : -1;
             one = sstar;
-            if (FULL && a.bmargin) {
+            if (a.bmargin) {
                 // proven lower bound of D_s - D_s* over the brick for every other
                 // candidate: culled (lower bound minus s*'s upper bound, with the
                 // cull's error allowances), region-culled, or dominated (its gap)
@@ -617,22 +627,16 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
-        if (FULL && lane == 0 && a.bslot) a.bslot[bidx] = (unsigned char)one;
-        if (a.accumulate && FULL) {
-            single_brick_sums(a, S, bidx, one, bx, by, bz, bt);
-            return;
-        }
-        if (!a.accumulate) return;
+        if (lane == 0 && a.bslot) a.bslot[bidx] = (unsigned char)one;
+        if (a.accumulate) single_brick_sums(a, S, bidx, one, bx, by, bz, bt, ex, ey, ez, et);
+        return;
     }
     int nout = 0;
-    if (one < 0) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (!FULL && !(livem >> k & 1)) continue;
-            const int lab = C.deferred ? -2 : (sl[k] >= 0 ? S.id[sl[k]] : -1);
-            lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
-            if (lab < 0) ++nout;
-        }
+    for (int k = 0; k < 8; ++k) {   // no candidate for the brick: deferred block or stranded
+        if (!FULL && !(livem >> k & 1)) continue;
+        lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = C.deferred ? -2 : -1;
+        ++nout;
     }
     if (__any_sync(0xffffffffu, nout > 0)) {
         unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
@@ -642,68 +646,13 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             if (!(livem >> k & 1)) continue;
-            if (!C.deferred && sl[k] >= 0) continue;
             if (p < cap) lst[p] = fbase + (k & 3) * C.plane + (k >> 2) * C.vol;
             ++p;
         }
     }
 
-    // ---- partial sums: count marginals (shared atomics) + per-warp value sums
-    if (a.accumulate && !C.deferred && C.cnt > 0) {
-        unsigned todo = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (sl[k] >= 0 && (FULL || (livem >> k & 1))) todo |= 1u << k;
-        while (true) {
-            int mine = -1;
-#pragma unroll
-            for (int k = 7; k >= 0; --k)
-                if (todo >> k & 1) mine = sl[k];
-            const unsigned act = __ballot_sync(0xffffffffu, mine >= 0);
-            if (!act) break;
-            const int L = __shfl_sync(0xffffffffu, mine, __ffs(act) - 1);
-            if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 3, 1ull);
-            // count; z counts (8 bits per z); t counts (16 bits per timestep)
-            unsigned c = 0, zp = 0, tp = 0;
-            double vs = 0.0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if ((todo >> k & 1) && sl[k] == L) {
-                    todo &= ~(1u << k);
-                    ++c;
-                    zp += 1u << (8 * (k & 3));
-                    tp += 1u << (16 * (k >> 2));
-                    vs = DADD(vs, v[k]);
-                }
-            }
-            unsigned sx = c + __shfl_xor_sync(0xffffffffu, c, 8);   // column sums
-            sx += __shfl_xor_sync(0xffffffffu, sx, 16);
-            unsigned sy = c + __shfl_xor_sync(0xffffffffu, c, 1);    // row sums
-            sy += __shfl_xor_sync(0xffffffffu, sy, 2);
-            sy += __shfl_xor_sync(0xffffffffu, sy, 4);
-            const unsigned sz = __reduce_add_sync(0xffffffffu, zp);
-            const unsigned st = __reduce_add_sync(0xffffffffu, tp);
-            vs = warp_sum_d(vs);
-            unsigned *h = S.hist[L];
-            if (lane < 8) {
-                const int i = lx;
-                if (sx) atomicAdd(&h[i >> 1], sx << (16 * (i & 1)));
-            }
-            if ((lane & 7) == 0) {
-                const int i = ly;
-                if (sy) atomicAdd(&h[8 + (i >> 1)], sy << (16 * (i & 1)));
-            }
-            if (lane == 0) {   // z pairs (z0, z0+1), (z0+2, z0+3); t pair (t0, t0+1); n
-                const unsigned c0 = sz & 0xFFu, c1 = (sz >> 8) & 0xFFu, c2 = (sz >> 16) & 0xFFu,
-                               c3 = sz >> 24;
-                if (c0 | c1) atomicAdd(&h[16 + (z0 >> 1)], c0 | (c1 << 16));
-                if (c2 | c3) atomicAdd(&h[17 + (z0 >> 1)], c2 | (c3 << 16));
-                atomicAdd(&h[24 + (t0 >> 1)], st);
-                atomicAdd(&h[26], (st & 0xFFFFu) + (st >> 16));
-                add_value_limbs(S.vlimb[L], vs, ovf_local);
-            }
-        }
-    }
+    // (no partial sums here: a brick labelled by one slot returned above with its
+    // per-run sums; the others are stranded or deferred and summed where resolved)
 }
 
 template <bool USEVAL, int MINB>
@@ -945,7 +894,10 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             if (sstable && S.bslot[bi] != 255) {
                 // label provably unchanged since the last pass: labels stay, sums are
                 // constants; the margin shrinks by the bound of this pass's moves
-                if (a.accumulate) single_brick_sums(a, S, bidx, S.bslot[bi], bx, by, bz, bt);
+                if (a.accumulate)
+                    single_brick_sums(a, S, bidx, S.bslot[bi], bx, by, bz, bt, min(GX, X.len - GX * bx),
+                                      min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),
+                                      min(GT, Tm.len - GT * bt));
                 if (!stable && lane == 0)
                     a.bmargin[bidx] = (a.bmargin[bidx] - S.bdec[bi]) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
                 if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
@@ -1059,9 +1011,25 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
             a.bsum_out[(size_t)blockIdx.x * 64 + bi] = make_ulonglong2(flo, (unsigned long long)fhi);
         }
     }
-    if (lane == 0 && a.absmax) {   // amax and bad are warp-uniform
-        atomicMax(a.absmax + 5, (unsigned long long)__double_as_longlong(amax));
-        if (bad) atomicOr(a.absmax + 6, 1ull);
+    // one atomic per block, and only when it raises the maximum (every block
+    // hitting one address would serialise thousands of atomics at the L2)
+    __shared__ double bmax[NW];
+    __shared__ int bbad[NW];
+    if (lane == 0) {   // amax and bad are warp-uniform
+        bmax[w] = amax;
+        bbad[w] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && a.absmax) {
+        double m = bmax[0];
+        int b = bbad[0];
+        for (int q = 1; q < NW; ++q) {
+            m = fmax(m, bmax[q]);
+            b |= bbad[q];
+        }
+        const unsigned long long mk = (unsigned long long)__double_as_longlong(m);
+        if (mk > *(volatile unsigned long long *)(a.absmax + 5)) atomicMax(a.absmax + 5, mk);
+        if (b) atomicOr(a.absmax + 6, 1ull);
     }
 }
 

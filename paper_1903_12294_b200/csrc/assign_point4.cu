@@ -797,10 +797,11 @@ __global__ void __launch_bounds__(256) k_chunk_boxes(const int4 *tiles, const in
         __syncthreads();
         if (bad) bad_s = 1;
         __syncthreads();
-        if (tid < 5) {
+        if (tid < 5) {   // atomics only when they raise the maximum
             double m = amax_s[0][tid];
             for (int q = 1; q < 8; ++q) m = fmax(m, amax_s[q][tid]);
-            atomicMax(absmax + tid, (unsigned long long)__double_as_longlong(m));
+            const unsigned long long mk = (unsigned long long)__double_as_longlong(m);
+            if (mk > *(volatile unsigned long long *)(absmax + tid)) atomicMax(absmax + tid, mk);
         }
         if (tid == 0 && bad_s) atomicOr(absmax + 6, 1ull);
     }
