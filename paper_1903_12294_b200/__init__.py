@@ -14,10 +14,10 @@ from .engine import (CenterGrid, CenterState, accumulate, assign_iteration, fiel
                      has_converged, initial_assignment, max_center_delta, point_distance, run,
                      seed_centers, update_centers)
 from .ingest import (IngestError, LinkIndex, NormalizationRecord, build_link_index,
-                     domain_extent, normalize_variables)
+                     domain_extent, load_field_device, normalize_variables, write_field)
 from .postproc import (Feature, FeatureStats, build_features, feature_stats, merge_clusters,
                        merge_eligible)
-from .pipeline import segment
+from .pipeline import segment, segment_from_files
 from . import artifacts
 
 __all__ = [
@@ -28,6 +28,7 @@ __all__ = [
     "has_converged", "initial_assignment", "interval_distances", "max_center_delta",
     "merge_clusters", "merge_eligible", "normalize_variables", "point_distance", "run",
     "seed_centers", "segment", "space_time_distance", "update_centers", "artifacts",
+    "load_field_device", "write_field", "segment_from_files",
 ]
 
 __version__ = "0.1.0"

@@ -283,3 +283,106 @@ def synthetic_taxi_points(dims, nt, n_traj, steps=8, skew=0.7, road_frac=0.02, s
                                         N.ptr(t), N.ptr(xyz), N.ptr(v), stream_ptr()),
             "mfseg_synth_taxi_points")
     return DevicePoints(xyz, t, v), tid
+
+
+# ============================================================== field files -> device
+
+FIELD_DTYPES = {"f32": "<f4", "f64": "<f8"}   # ingest.py:25
+
+
+def _field_meta(path: str):
+    """Metadata document of a field (ingest.py:39-64), validated like the
+    reference: same keys, order, dtype and time checks, same errors."""
+    import json
+    import os
+    try:
+        with open(path) as f:
+            meta = json.load(f)
+    except FileNotFoundError:
+        raise
+    except (json.JSONDecodeError, UnicodeDecodeError) as e:
+        raise IngestError(f"{path}: malformed field metadata: {e}")
+    for key in ("dims", "origin", "spacing", "times", "variable", "data_files", "dtype", "order"):
+        if key not in meta:
+            raise IngestError(f"{path}: metadata missing key '{key}'")
+    if meta["order"] != "x_fastest":
+        raise IngestError(f"{path}: unsupported order '{meta['order']}'")
+    if meta["dtype"] not in FIELD_DTYPES:
+        raise IngestError(f"{path}: unsupported dtype '{meta['dtype']}'")
+    dims = tuple(int(d) for d in meta["dims"])
+    times = np.asarray(meta["times"], dtype=float)
+    if len(times) != len(meta["data_files"]):
+        raise IngestError(f"{path}: {len(times)} times but {len(meta['data_files'])} data files")
+    if len(times) > 1 and not np.all(np.diff(times) > 0):
+        raise IngestError(f"{path}: timestep times must strictly increase")
+    base = os.path.dirname(os.path.abspath(path))
+    files = [os.path.join(base, fname) for fname in meta["data_files"]]
+    return meta, dims, times, files, np.dtype(FIELD_DTYPES[meta["dtype"]])
+
+
+def load_field_device(path: str, dev=None) -> DeviceField:
+    """load_field (ingest.py:39-78) straight into device memory.
+
+    Each timestep's raw file is read into one of two pinned buffers while the
+    copy engine moves the other one to the device (file reads overlap the
+    PCIe transfer; no pageable host copy of the whole field exists).  f32 files
+    cross PCIe as f32 and are widened on the device (exact, like the
+    reference's `astype(np.float64)`).  Errors match the reference's."""
+    import os
+    meta, dims, times, files, dtype = _field_meta(path)
+    dev = dev or device()
+    ncell = dims[0] * dims[1] * dims[2]
+    nt = len(times)
+    values = torch.empty(nt * ncell, dtype=torch.float64, device=dev)
+    tdtype = torch.float32 if dtype.itemsize == 4 else torch.float64
+    nbytes = ncell * dtype.itemsize
+    bufs = [torch.empty(ncell, dtype=tdtype, pin_memory=True) for _ in range(min(2, nt))]
+    done = [torch.cuda.Event() for _ in bufs]
+    stage = torch.empty(ncell, dtype=tdtype, device=dev) if tdtype != torch.float64 else None
+    stream = torch.cuda.current_stream(dev)
+    for m, fpath in enumerate(files):
+        b = m % len(bufs)
+        if m >= len(bufs):
+            done[b].synchronize()           # the DMA out of this buffer has finished
+        with open(fpath, "rb") as f:            # missing file: FileNotFoundError, as np.fromfile
+            size = os.fstat(f.fileno()).st_size
+            if size != nbytes:
+                got = size // dtype.itemsize
+                raise IngestError(f"{fpath}: expected {ncell} values ({nbytes} bytes), "
+                                  f"got {got} (byte offset {got * dtype.itemsize})")
+            f.readinto(memoryview(bufs[b].numpy()).cast("B"))
+        dst = values[m * ncell:(m + 1) * ncell]
+        if stage is None:
+            dst.copy_(bufs[b], non_blocking=True)
+        else:
+            stage.copy_(bufs[b], non_blocking=True)
+            dst.copy_(stage)                # f32 -> f64 widening on the device
+        done[b].record(stream)
+    for e in done:
+        e.synchronize()
+    return DeviceField(dims, np.asarray(meta["origin"], dtype=float),
+                       np.asarray(meta["spacing"], dtype=float),
+                       torch.as_tensor(times, dtype=torch.float64, device=dev), values)
+
+
+def write_field(path: str, fs: FieldSet, variable: str = "v", dtype: str = "f64") -> None:
+    """The reference's field format (ingest.py:83-106): metadata sidecar + one
+    raw little-endian array per timestep."""
+    import json
+    import os
+    if dtype not in FIELD_DTYPES:
+        raise IngestError(f"unsupported dtype '{dtype}'")
+    base = os.path.dirname(os.path.abspath(path))
+    os.makedirs(base, exist_ok=True)
+    stem = os.path.splitext(os.path.basename(path))[0]
+    data_files = [f"{stem}_{m:04d}.bin" for m in range(len(fs.times))]
+    meta = {"dims": list(fs.dims), "origin": [float(v) for v in fs.origin],
+            "spacing": [float(v) for v in fs.spacing], "times": [float(t) for t in fs.times],
+            "variable": variable, "data_files": data_files, "dtype": dtype, "order": "x_fastest"}
+    np_dtype = np.dtype(FIELD_DTYPES[dtype])
+    values = np.asarray(fs.values)
+    for m, fname in enumerate(data_files):
+        values[m].astype(np_dtype).tofile(os.path.join(base, fname))
+    with open(path, "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+        f.write("\n")

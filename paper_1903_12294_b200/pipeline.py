@@ -56,3 +56,17 @@ def to_segmentation(r: DeviceRun, params, extent) -> Segmentation:
     return Segmentation(point_labels=host_ready(pl), field_labels=host_ready(fl), centers=table,
                         params=params, extent=extent, iterations_used=r.iterations_used,
                         converged=r.converged)
+
+
+def segment_from_files(field_path: str, points: Optional[PointSet], params: ClusterParams,
+                       progress=None):
+    """pipeline.segment over a field stored in the reference's format
+    (ingest.py:39-78): the per-timestep files stream into device memory
+    (ingest.load_field_device) instead of materialising a host FieldSet.
+    Returns (Segmentation, NormalizationRecord, iteration wall times)."""
+    from .ingest import load_field_device
+    dev = device()
+    fld = load_field_device(field_path, dev)
+    pts = points_to_device(points, dev)
+    r, norm, extent, iter_times = segment_device(pts, fld, params, progress=progress)
+    return to_segmentation(r, params, extent), norm, iter_times
