@@ -93,6 +93,8 @@ struct __align__(16) Smem5 {
     float red2[NW];
     float dmax;                     // largest metric change of the block's candidates
     float bdec[64];                 // per reused brick: the margin it uses up this pass
+    float bmarg[64];                // per reused brick: its margin (loaded in the prologue)
+    ulonglong2 bsums[64];           // per reused brick: its per-run value sum (prologue)
     Ctx ctx;
 };
 
@@ -302,7 +304,7 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
 // Partial sums of a brick labelled by one slot: count marginals from its live
 // extents (ex x ey x ez x et samples; a brick cut by the block edge -- or by a
 // thin grid, e.g. nz = 1 -- has fewer) and the brick's per-run value sum.
-__device__ __forceinline__ void single_brick_sums(const FieldArgs &a, Smem5 &S, size_t bidx, int one,
+__device__ __forceinline__ void single_brick_sums(Smem5 &S, ulonglong2 vs, int one,
                                                   int bx, int by, int bz, int bt, int ex, int ey,
                                                   int ez, int et) {
     const int lane = threadIdx.x & 31;
@@ -324,7 +326,6 @@ __device__ __forceinline__ void single_brick_sums(const FieldArgs &a, Smem5 &S, 
     } else if (lane == 9) {
         atomicAdd(&h[26], (unsigned)(ex * ey * ez * et));
     } else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
-        const ulonglong2 vs = a.bsum[bidx];
         const int q = lane - 10;
         const unsigned long long lo = vs.x, hi = vs.y;
         const unsigned long long bits = q < 2 ? lo >> (24 * q)
@@ -628,7 +629,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         for (int k = 0; k < 8; ++k)
             if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
         if (lane == 0 && a.bslot) a.bslot[bidx] = (unsigned char)one;
-        if (a.accumulate) single_brick_sums(a, S, bidx, one, bx, by, bz, bt, ex, ey, ez, et);
+        if (a.accumulate) single_brick_sums(S, a.bsum[bidx], one, bx, by, bz, bt, ex, ey, ez, et);
         return;
     }
     int nout = 0;
@@ -783,12 +784,19 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
             const size_t bidx = (size_t)blockIdx.x * 64 + tid;
             unsigned char sl = a.bslot[bidx];
-            if (sl != 255 && !stable) {
-                // the margin must exceed the change of s* plus the largest change of
-                // any other candidate of the block
-                const float dec = (a.cdelta[S.id[sl]] + dmax) * (1.f + 0x1.0p-20f);
-                S.bdec[tid] = dec;
-                if (!(a.bmargin[bidx] > dec)) sl = 255;
+            if (sl != 255) {
+                // one round of loads for all 64 bricks: the reuse path below then
+                // reads its per-brick constants from shared memory
+                S.bsums[tid] = a.bsum[bidx];
+                if (!stable) {
+                    // the margin must exceed the change of s* plus the largest change of
+                    // any other candidate of the block
+                    const float dec = (a.cdelta[S.id[sl]] + dmax) * (1.f + 0x1.0p-20f);
+                    const float mg = a.bmargin[bidx];
+                    S.bdec[tid] = dec;
+                    S.bmarg[tid] = mg;
+                    if (!(mg > dec)) sl = 255;
+                }
             }
             S.bslot[tid] = sl;
             need = sl == 255 && !(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len ||
@@ -895,11 +903,11 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 // label provably unchanged since the last pass: labels stay, sums are
                 // constants; the margin shrinks by the bound of this pass's moves
                 if (a.accumulate)
-                    single_brick_sums(a, S, bidx, S.bslot[bi], bx, by, bz, bt, min(GX, X.len - GX * bx),
+                    single_brick_sums(S, S.bsums[bi], S.bslot[bi], bx, by, bz, bt, min(GX, X.len - GX * bx),
                                       min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),
                                       min(GT, Tm.len - GT * bt));
                 if (!stable && lane == 0)
-                    a.bmargin[bidx] = (a.bmargin[bidx] - S.bdec[bi]) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
+                    a.bmargin[bidx] = (S.bmarg[bi] - S.bdec[bi]) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
                 if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
                 bi += NW;
                 continue;
