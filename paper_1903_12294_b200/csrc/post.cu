@@ -101,48 +101,74 @@ struct MergeOut {
     long long *m_np, *m_nf;
 };
 
-// one thread per group, members ascending (stable sort by root row)
+// One warp per group (launched per sorted position; only a group's first
+// position works), members ascending (stable sort by root row).  The sums keep
+// the reference's sequential order; the lanes load 32 members' records at a time
+// (the loads overlap) and every lane replays the sequential sums over them from
+// shuffles, so the one long chain of a big group is no longer load-latency bound.
 __global__ void k_merge_groups(int n, const unsigned *skeys, const unsigned *members,
                                const int *is_root, const int *group_of_root, const int *ids,
                                const double *loc, const double *pc, const double *fc,
                                const long long *np_, const long long *nf_, MergeOut o, int G,
                                int neumaier) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;   // position in the sorted order
-    if (i >= n) return;
-    if (i > 0 && skeys[i - 1] == skeys[i]) return;  // not the first member of its group
-    int root = (int)skeys[i];
-    int g = group_of_root[root];
+    const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= n) return;
+    const int i = (int)wid;                        // position in the sorted order
+    if (i > 0 && skeys[i - 1] == skeys[i]) return;   // not the first member of its group
+    const unsigned root = skeys[i];
+    const int g = group_of_root[root];
     long long n_p = 0, n_f = 0, n_tot = 0;
     double ls[4] = {0.0, 0.0, 0.0, 0.0};
     double pf = 0.0, pcmp = 0.0, ff = 0.0, fcmp = 0.0;   // compensation used when neumaier
-    for (int q = i; q < n && skeys[q] == (unsigned)root; ++q) {
-        int r = (int)members[q];
-        long long a = np_[r], b = nf_[r], t = a + b;
-        n_p += a;
-        n_f += b;
-        n_tot += t;
-        double dt = (double)t;
-        for (int d = 0; d < 4; ++d) ls[d] = DADD(ls[d], DMUL(loc[(size_t)d * n + r], dt));
-        if (!isnan(pc[r])) {   // Neumaier step (CPython >= 3.12 sum of floats), else plain
-            double x = DMUL(pc[r], (double)a);
-            double t2 = DADD(pf, x);
-            if (neumaier)
-                pcmp = fabs(pf) >= fabs(x) ? DADD(pcmp, DADD(DSUB(pf, t2), x))
-                                           : DADD(pcmp, DADD(DSUB(x, t2), pf));
-            pf = t2;
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    for (int q0 = i; q0 < n; q0 += 32) {
+        const int q = q0 + lane;
+        const bool in = q < n && skeys[q] == root;
+        long long ma = 0, mb = 0;
+        double ml[4] = {0.0, 0.0, 0.0, 0.0}, mp = nan, mf = nan;
+        if (in) {
+            const int r = (int)members[q];
+            ma = np_[r];
+            mb = nf_[r];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) ml[d] = loc[(size_t)d * n + r];
+            mp = pc[r];
+            mf = fc[r];
         }
-        if (!isnan(fc[r])) {
-            double x = DMUL(fc[r], (double)b);
-            double t2 = DADD(ff, x);
-            if (neumaier)
-                fcmp = fabs(ff) >= fabs(x) ? DADD(fcmp, DADD(DSUB(ff, t2), x))
-                                           : DADD(fcmp, DADD(DSUB(x, t2), ff));
-            ff = t2;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, in));   // lanes 0 .. cnt-1 (contiguous)
+        for (int t = 0; t < cnt; ++t) {
+            const long long a = __shfl_sync(0xffffffffu, ma, t), b = __shfl_sync(0xffffffffu, mb, t);
+            const long long tt = a + b;
+            n_p += a;
+            n_f += b;
+            n_tot += tt;
+            const double dt = (double)tt;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) ls[d] = DADD(ls[d], DMUL(__shfl_sync(0xffffffffu, ml[d], t), dt));
+            const double pv = __shfl_sync(0xffffffffu, mp, t), fv = __shfl_sync(0xffffffffu, mf, t);
+            if (!isnan(pv)) {   // Neumaier step (CPython >= 3.12 sum of floats), else plain
+                const double x = DMUL(pv, (double)a);
+                const double t2 = DADD(pf, x);
+                if (neumaier)
+                    pcmp = fabs(pf) >= fabs(x) ? DADD(pcmp, DADD(DSUB(pf, t2), x))
+                                               : DADD(pcmp, DADD(DSUB(x, t2), pf));
+                pf = t2;
+            }
+            if (!isnan(fv)) {
+                const double x = DMUL(fv, (double)b);
+                const double t2 = DADD(ff, x);
+                if (neumaier)
+                    fcmp = fabs(ff) >= fabs(x) ? DADD(fcmp, DADD(DSUB(ff, t2), x))
+                                               : DADD(fcmp, DADD(DSUB(x, t2), ff));
+                ff = t2;
+            }
         }
+        if (cnt < 32) break;
     }
+    if (lane != 0) return;
     if (pcmp != 0.0 && isfinite(pcmp)) pf = DADD(pf, pcmp);
     if (fcmp != 0.0 && isfinite(fcmp)) ff = DADD(ff, fcmp);
-    double nan = __longlong_as_double(0x7ff8000000000000ll);
     o.m_ids[g] = ids[root];
     for (int d = 0; d < 4; ++d) o.m_loc[(size_t)d * G + g] = DDIV(ls[d], (double)n_tot);
     o.m_p[g] = n_p > 0 ? DDIV(pf, (double)n_p) : nan;
@@ -220,8 +246,15 @@ __global__ void __launch_bounds__(256) k_voxel_hist(const int *flab, long long n
         const long long c = c0 + k * 256 + threadIdx.x;
         int s = -1;
         if (c < ncell) s = voxel_slot(slot_of, lut_len, __ldg(flab + (long long)m * ncell + c), bad);
-        const unsigned grp = __match_any_sync(0xffffffffu, s);
-        if (s >= 0 && lane == __ffs(grp) - 1) atomicAdd(&hist[s], __popc(grp));
+        // labels are spatially coherent: a ballot loop over the round's distinct
+        // slots (mostly one or two) is cheaper than MATCH.ANY
+        unsigned act = __ballot_sync(0xffffffffu, s >= 0);
+        while (act) {
+            const int L = __shfl_sync(0xffffffffu, s, __ffs(act) - 1);
+            const unsigned grp = __ballot_sync(0xffffffffu, s == L);
+            if (lane == __ffs(act) - 1) atomicAdd(&hist[L], __popc(grp));
+            act &= ~grp;
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < ns; i += 256) H[((long long)m * ns + i) * tpm + tile] = hist[i];
@@ -241,8 +274,13 @@ __global__ void __launch_bounds__(256) k_voxel_scatter(const int *flab, long lon
     for (int k = 0; k < VW / 32; ++k) {
         const long long c = c0 + k * 32 + lane;
         sl[k] = c < ncell ? voxel_slot(slot_of, lut_len, __ldg(flab + (long long)m * ncell + c), bad) : -1;
-        const unsigned grp = __match_any_sync(0xffffffffu, sl[k]);
-        if (sl[k] >= 0 && lane == __ffs(grp) - 1) wcnt[w][sl[k]] += __popc(grp);
+        unsigned act = __ballot_sync(0xffffffffu, sl[k] >= 0);
+        while (act) {
+            const int L = __shfl_sync(0xffffffffu, sl[k], __ffs(act) - 1);
+            const unsigned grp = __ballot_sync(0xffffffffu, sl[k] == L);
+            if (lane == __ffs(act) - 1) wcnt[w][L] += __popc(grp);
+            act &= ~grp;
+        }
         __syncwarp();
     }
     __syncthreads();
@@ -261,7 +299,14 @@ __global__ void __launch_bounds__(256) k_voxel_scatter(const int *flab, long lon
 #pragma unroll
     for (int k = 0; k < VW / 32; ++k) {
         const int s = sl[k];
-        const unsigned grp = __match_any_sync(0xffffffffu, s);
+        unsigned grp = 0;
+        unsigned act = __ballot_sync(0xffffffffu, s >= 0);
+        while (act) {   // this lane's group = the lanes with its slot
+            const int L = __shfl_sync(0xffffffffu, s, __ffs(act) - 1);
+            const unsigned g = __ballot_sync(0xffffffffu, s == L);
+            if (s == L) grp = g;
+            act &= ~g;
+        }
         if (s >= 0) {
             const int base = wcnt[w][s];
             const long long dst = O[((long long)m * ns + s) * tpm + tile] + base + __popc(grp & lt);
@@ -722,7 +767,8 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
     MFSEG_CUDA(cudaStreamSynchronize(st));
     MergeOut o{m_ids, m_loc, m_p, m_f, (long long *)m_np, (long long *)m_nf};
     ::mfseg::count_launch();
-    k_merge_groups<<<g, 256, 0, st>>>(n, skeys, members, is_root, group_of_root, ids, loc, p_c,
+    k_merge_groups<<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, st>>>(
+        n, skeys, members, is_root, group_of_root, ids, loc, p_c,
                                       f_c, (const long long *)n_points,
                                       (const long long *)n_fields, o, G, neumaier);
     MFSEG_LAUNCH("k_merge_groups");
