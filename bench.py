@@ -74,6 +74,8 @@ CONFIGS = {
                      "per B200"),
     "small": dict(kind="time", dims=(64, 64, 32), nt=8, n_traj=20_000, k=(8, 8, 4, 4),
                   label="smoke size"),
+    "smallz": dict(kind="z", dims=(64, 64, 32), nt=8, n_traj=20_000, k=(8, 8, 4, 4),
+                   label="smoke size, z-slabs"),
 }
 METRIC = "voxel-timesteps segmented/sec"
 UNIT = "voxel-timesteps/s"
@@ -378,9 +380,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MFSEG_BENCH_BACKEND=gloo runs the multi-rank path functionally on fewer GPUs
+    # than ranks (host-side exchange; no kernel waits on another rank) -- a test
+    # of the code path, not a timing
+    backend = os.environ.get("MFSEG_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1903_12294_b200 import ClusterParams, _native as N
     from paper_1903_12294_b200.engine import DeviceField, DevicePoints, run_device
     from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device

@@ -242,3 +242,27 @@ def test_zslab_offset_single_process_bit_identical():
     st = CenterState.from_device(state)
     np.testing.assert_array_equal(st.loc, ref_state.loc)
     np.testing.assert_array_equal(st.fval, ref_state.fval)
+
+
+@pytest.mark.parametrize("config", ["small", "smallz"])
+def test_bench_two_ranks_functional(config):
+    """bench.py's multi-rank path (rank slabs generated in place, sharded
+    normalisation + extent, per-pass exchange, e2e through segment_sharded) runs
+    end to end under torchrun with two ranks on one GPU (gloo: host-side
+    exchange) and prints one JSON line for the whole job."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MFSEG_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                          str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--config", config, "--steps", "2", "--warmup", "3"],
+                         capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["voxel_timesteps"] == 64 * 64 * 32 * 16
