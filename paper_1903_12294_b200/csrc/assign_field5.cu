@@ -309,23 +309,28 @@ __device__ __forceinline__ void single_brick_sums(Smem5 &S, ulonglong2 vs, int o
                                                   int ez, int et) {
     const int lane = threadIdx.x & 31;
     unsigned *h = S.hist[one];
-    auto pair = [](int i0, int e, unsigned c) {   // two 16-bit counts: indices i0, i0 + 1
-        return (i0 < e ? c : 0u) | ((i0 + 1 < e ? c : 0u) << 16);
-    };
-    if (lane < 4) {                                                          // 8 x
-        const unsigned w = pair(2 * lane, ex, (unsigned)(ey * ez * et));
-        if (w) atomicAdd(&h[4 * bx + lane], w);
-    } else if (lane < 6) {                                                   // 4 y
-        const unsigned w = pair(2 * (lane - 4), ey, (unsigned)(ex * ez * et));
-        if (w) atomicAdd(&h[8 + 2 * by + (lane - 4)], w);
-    } else if (lane < 8) {                                                   // 4 z
-        const unsigned w = pair(2 * (lane - 6), ez, (unsigned)(ex * ey * et));
-        if (w) atomicAdd(&h[16 + 2 * bz + (lane - 6)], w);
-    } else if (lane == 8) {                                                  // 2 timesteps
-        atomicAdd(&h[24 + bt], pair(0, et, (unsigned)(ex * ey * ez)));
-    } else if (lane == 9) {
-        atomicAdd(&h[26], (unsigned)(ex * ey * ez * et));
-    } else if (lane >= 10 && lane < 16) {   // the six value-sum limbs, one per lane
+    if (lane < 10) {   // count marginals: two 16-bit counts (indices i0, i0 + 1) per word
+        const bool full = ex == GX && ey == GY && ez == GZ && et == GT;   // constant counts
+        auto pair = [](int i0, int e, unsigned c) {
+            return (i0 < e ? c : 0u) | ((i0 + 1 < e ? c : 0u) << 16);
+        };
+        if (lane < 4) {                                                      // 8 x
+            const unsigned w = full ? (32u | (32u << 16)) : pair(2 * lane, ex, (unsigned)(ey * ez * et));
+            if (w) atomicAdd(&h[4 * bx + lane], w);
+        } else if (lane < 6) {                                               // 4 y
+            const unsigned w = full ? (64u | (64u << 16))
+                                    : pair(2 * (lane - 4), ey, (unsigned)(ex * ez * et));
+            if (w) atomicAdd(&h[8 + 2 * by + (lane - 4)], w);
+        } else if (lane < 8) {                                               // 4 z
+            const unsigned w = full ? (64u | (64u << 16))
+                                    : pair(2 * (lane - 6), ez, (unsigned)(ex * ey * et));
+            if (w) atomicAdd(&h[16 + 2 * bz + (lane - 6)], w);
+        } else if (lane == 8) {                                              // 2 timesteps
+            atomicAdd(&h[24 + bt], full ? (128u | (128u << 16)) : pair(0, et, (unsigned)(ex * ey * ez)));
+        } else {
+            atomicAdd(&h[26], full ? 256u : (unsigned)(ex * ey * ez * et));
+        }
+    } else if (lane < 16) {   // the six value-sum limbs, one per lane
         const int q = lane - 10;
         const unsigned long long lo = vs.x, hi = vs.y;
         const unsigned long long bits = q < 2 ? lo >> (24 * q)
