@@ -70,3 +70,50 @@ def segment_from_files(field_path: str, points: Optional[PointSet], params: Clus
     pts = points_to_device(points, dev)
     r, norm, extent, iter_times = segment_device(pts, fld, params, progress=progress)
     return to_segmentation(r, params, extent), norm, iter_times
+
+
+def segment_to_dir(outdir: str, field_path: Optional[str], points: Optional[PointSet],
+                   params: ClusterParams, workers: int = 1, chunk_size: Optional[int] = None,
+                   progress=None):
+    """pipeline.segment_to_dir (pipeline.py:48-70): a run directory from a field
+    file in the reference's format (streamed into device memory) and in-memory
+    points (the reference's CSV / derivation front end is host I/O, out of scope).
+
+    Labels go from device memory straight to the label files
+    (artifacts.save_segmentation_device); report.json carries the reference's
+    keys plus throughput keys (`voxel_timesteps_per_s`, `passes`,
+    `device_seconds`).  Returns (DeviceRun, NormalizationRecord, extent)."""
+    import torch
+    from . import artifacts
+    from .ingest import load_field_device
+    dev = device()
+    t0 = time.perf_counter()
+    fld = load_field_device(field_path, dev) if field_path else field_to_device(None, dev)
+    pts = points_to_device(points, dev)
+    t1 = time.perf_counter()
+    r, norm, extent, iter_times = segment_device(pts, fld, params, progress=progress)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    artifacts.save_segmentation_device(outdir, r, params, extent, norm)
+    n_f = int(r.field_labels.numel())
+    passes = 1 + r.iterations_used
+    artifacts.save_report(outdir, {
+        "inputs": {"field": field_path, "points": None if points is None else "in-memory",
+                   "derive": None},
+        "params": params.to_dict(),
+        "workers": workers,
+        "chunk_size": chunk_size,
+        "n_point_samples": int(r.point_labels.numel()),
+        "n_field_samples": n_f,
+        "iterations_used": r.iterations_used,
+        "converged": r.converged,
+        "iteration_seconds": iter_times,
+        "total_seconds": t2 - t1,
+        # extra keys (the deterministic artifacts are untouched)
+        "device": torch.cuda.get_device_name(dev),
+        "passes": passes,
+        "device_seconds": t2 - t1,
+        "load_seconds": t1 - t0,
+        "voxel_timesteps_per_s": n_f / (t2 - t1) if t2 > t1 else None,
+    })
+    return r, norm, extent

@@ -100,3 +100,31 @@ def test_segment_from_files_equals_segment(tmp_path):
     np.testing.assert_array_equal(seg.field_labels, ref.field_labels)
     np.testing.assert_array_equal(seg.point_labels, ref.point_labels)
     assert norm == rnorm
+
+
+@pytest.mark.gpu
+def test_segment_to_dir_from_files(tmp_path):
+    """Files in -> run directory out (labels streamed from the device): the
+    deterministic files equal save_segmentation of pipeline.segment's result;
+    report.json has the reference's keys plus the throughput keys."""
+    import paper_1903_12294_b200 as P
+    from paper_1903_12294_b200 import artifacts as A
+    from paper_1903_12294_b200.ingest import synthetic_device
+    from paper_1903_12294_b200.pipeline import segment_to_dir
+    fld, pts, tid = synthetic_device((20, 18, 14), 5, 250, seed=9)
+    nt = 5
+    fs = P.FieldSet((20, 18, 14), np.zeros(3), np.ones(3), np.arange(nt, dtype=float),
+                    fld.values.cpu().numpy().reshape(nt, -1))
+    ps = P.PointSet(tid.cpu().numpy(), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(), pts.value.cpu().numpy())
+    params = P.ClusterParams(k=(3, 3, 2, 2), eps_c=1e-12, max_iterations=4)
+    write_field(str(tmp_path / "in" / "f.json"), fs, dtype="f64")
+    segment_to_dir(str(tmp_path / "dev"), str(tmp_path / "in" / "f.json"), ps, params)
+    seg, norm, _ = P.segment(ps, fs, params)
+    A.save_segmentation(str(tmp_path / "host"), seg, norm)
+    for name in (A.SEGMENTATION_JSON, A.POINT_LABELS_BIN, A.FIELD_LABELS_BIN):
+        assert (tmp_path / "dev" / name).read_bytes() == (tmp_path / "host" / name).read_bytes(), name
+    rep = A.load_report(str(tmp_path / "dev"))
+    for key in ("inputs", "params", "n_point_samples", "n_field_samples", "iterations_used",
+                "converged", "iteration_seconds", "total_seconds", "voxel_timesteps_per_s", "passes"):
+        assert key in rep, key
+    assert len(rep["iteration_seconds"]) == rep["iterations_used"]
