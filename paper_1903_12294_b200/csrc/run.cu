@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.cuh"
 
 namespace mfseg {
@@ -27,7 +29,17 @@ static PhaseTimer g_timer;
 static cudaEvent_t g_ev[6];
 static bool g_ev_made = false;
 
+// NVTX ranges per phase of a pass (host-side launch regions; free when no tool
+// is attached): grid, field assign, point assign, fallback, exchange + update
+static void nvtx_phase(int i) {
+    static const char *names[5] = {"mfseg grid", "mfseg field assign", "mfseg point assign",
+                                   "mfseg fallback", "mfseg exchange+update"};
+    if (i > 0) nvtxRangePop();
+    if (i < 5) nvtxRangePushA(names[i]);
+}
+
 static void mark(int i, cudaStream_t st) {
+    nvtx_phase(i);
     if (!g_timer.on) return;
     if (!g_ev_made) {
         for (auto &e : g_ev) cudaEventCreate(&e);
@@ -532,7 +544,16 @@ int check_ranges(Plan &P, double field_coord_max) {
 }
 
 // once per run: field axis tiles, timestep bins, point binning + sort + tiles
-int plan_prepare(Plan &P) {
+int plan_prepare_impl(Plan &P);
+
+int plan_prepare(Plan &P) {   // once per run, under one NVTX range
+    nvtxRangePushA("mfseg prepare");
+    const int rc = plan_prepare_impl(P);
+    nvtxRangePop();
+    return rc;
+}
+
+int plan_prepare_impl(Plan &P) {
     cudaStream_t st = P.st;
     const mfseg_params &p = P.p;
     MFSEG_CUDA(cudaMemsetAsync(P.absmax, 0, sizeof(unsigned long long) * 8, st));
@@ -1137,7 +1158,9 @@ int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
     MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
     MFSEG_TRY(plan_prepare(P));
-    MFSEG_TRY(plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr, point_labels));
+    const int rc = plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr, point_labels);
+    nvtx_phase(5);   // close the pass's last NVTX range
+    MFSEG_TRY(rc);
     if (acc)
         MFSEG_CUDA(cudaMemcpyAsync(acc, P.acc, sizeof(int64_t) * P.K * MFSEG_ACC_WORDS,
                                    cudaMemcpyDeviceToDevice, st));
