@@ -147,6 +147,7 @@ DEBUG_EXACT = 2
 DEBUG_STATS = 8
 DEBUG_NO_REUSE = 16
 DEBUG_NO_MARGIN_REUSE = 32
+DEBUG_NO_SEEDS_FAST = 64
 
 
 @contextlib.contextmanager
@@ -162,12 +163,13 @@ def debug_options(flags: int = 0, multi_cap: int = -1):
 
 
 def debug_options_from_env() -> None:
-    """tools/: map the MFSEG_DEBUG / MFSEG_NO_REUSE / MFSEG_NO_MARGIN_REUSE /
+    """tools/: map the MFSEG_DEBUG / MFSEG_NO_REUSE / MFSEG_NO_MARGIN_REUSE / MFSEG_NO_SEEDS_FAST /
     MFSEG_MULTI_CAP environment variables onto this thread's debug options."""
     env = os.environ
     flags = int(env.get("MFSEG_DEBUG", "0") or 0)
     flags |= DEBUG_NO_REUSE if env.get("MFSEG_NO_REUSE") else 0
     flags |= DEBUG_NO_MARGIN_REUSE if env.get("MFSEG_NO_MARGIN_REUSE") else 0
+    flags |= DEBUG_NO_SEEDS_FAST if env.get("MFSEG_NO_SEEDS_FAST") else 0
     load().mfseg_set_debug_options(flags, int(env.get("MFSEG_MULTI_CAP", "-1")))
 
 

@@ -341,6 +341,20 @@ __device__ __forceinline__ void single_brick_sums(Smem5 &S, ulonglong2 vs, int o
     }
 }
 
+// Every live sample of a brick labelled `lab` (the initial pass's interior blocks).
+__device__ __forceinline__ void label_brick(const FieldArgs &a, const Ctx &C, int bx, int by, int bz,
+                                            int bt, int lab) {
+    const int lane = threadIdx.x & 31;
+    const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
+    const int z0 = GZ * bz, t0 = GT * bt;
+    if (lx >= C.X.len || ly >= C.Y.len) return;
+    int *lab_base = a.labels + (((long long)(C.T.start + t0) * a.nz + C.Z.start + z0) * a.ny +
+                                (C.Y.start + ly)) * (long long)a.nx + (C.X.start + lx);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (z0 + (k & 3) < C.Z.len && t0 + (k >> 2) < C.T.len) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
+}
+
 // Every sample of a brick to the exact per-sample path (k_deferred, label -2).
 __device__ __forceinline__ void defer_brick(const FieldArgs &a, const Ctx &C, int bx, int by, int bz, int bt) {
     const int lane = threadIdx.x & 31;
@@ -705,11 +719,19 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         dst[1] = (unsigned long long)hi;
     }
     const int sbin = ((Tm.bin * a.kz + Z.bin) * a.ky + Y.bin) * a.kx + X.bin;
-    const int L0 = a.g.cand_start[sbin], L1 = a.g.cand_start[sbin + 1];
+    // initial pass, every cell of the block interior to its bin (margin 2^-20 of a
+    // bin from every bin boundary, see run.cu seeds_fast_ok): the block's own seed
+    // (id = sbin) is the unique nearest valid candidate of every sample, so the
+    // block is labelled and summed without candidate lists or tables
+    const bool fast0 = a.seeds_fast && X.pad && Y.pad && Z.pad && Tm.pad;
+    const int L0 = fast0 ? 0 : a.g.cand_start[sbin], L1 = fast0 ? 0 : a.g.cand_start[sbin + 1];
     bool deferred = (L1 - L0) > NT;
     int cnt = 0;
     float cvmax = 0.0f;
-    if (!deferred) {
+    if (fast0) {
+        if (tid == 0) S.id[0] = sbin;
+        cnt = 1;
+    } else if (!deferred) {
         // ---- candidates whose validity box meets the block, compacted to slots
         const int ci = L0 + tid;
         bool have = ci < L1;
@@ -775,8 +797,8 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     // stable: nothing changed (labels reusable as they are); sstable: only bounded
     // moves (a brick's label is reusable while its proven margin exceeds twice the
     // largest metric change of the block's candidates; the margin is carried on)
-    const bool sstable = a.reuse && !deferred && cnt > 0 && a.bin_sstable[sbin];
-    const bool stable = sstable && a.bin_stable[sbin];
+    const bool sstable = fast0 || (a.reuse && !deferred && cnt > 0 && a.bin_sstable[sbin]);
+    const bool stable = fast0 || (sstable && a.bin_stable[sbin]);
     bool need_full = true;
     float dmax = 0.f;
     if (sstable) {
@@ -788,7 +810,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         if (tid < 64) {
             const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
             const size_t bidx = (size_t)blockIdx.x * 64 + tid;
-            unsigned char sl = a.bslot[bidx];
+            unsigned char sl = fast0 ? 0 : a.bslot[bidx];
             if (sl != 255) {
                 // one round of loads for all 64 bricks: the reuse path below then
                 // reads its per-brick constants from shared memory
@@ -907,6 +929,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             if (sstable && S.bslot[bi] != 255) {
                 // label provably unchanged since the last pass: labels stay, sums are
                 // constants; the margin shrinks by the bound of this pass's moves
+                if (fast0) label_brick(a, C, bx, by, bz, bt, sbin);   // initial pass: write them
                 if (a.accumulate)
                     single_brick_sums(S, S.bsums[bi], S.bslot[bi], bx, by, bz, bt, min(GX, X.len - GX * bx),
                                       min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),

@@ -54,6 +54,7 @@ struct PCtx {
     long long start;
     bool deferred;
     bool stable;                    // no candidate changed since the last pass
+    bool fast0;                     // initial pass, interior chunk: every point takes slot 0
 };
 
 struct __align__(16) PSmem4 {
@@ -159,8 +160,12 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
     int sl0 = -1, sl1 = -1;
     bool reused = false;   // several labels kept from the last pass: sums only
     if (C.stable) {   // unchanged since the last pass: the tile keeps its labels
-        const unsigned char ts = a.tslot[tidx];
+        const unsigned char ts = C.fast0 ? 0 : a.tslot[tidx];
         if (ts < 254) {   // one label: the per-run tile sums
+            if (C.fast0) {   // initial pass: the labels are new
+                if (live0) a.labels[p0] = S.id[0];
+                if (live1) a.labels[p1] = S.id[0];
+            }
             if (a.labels_out) {   // final pass: record-order labels
                 if (live0) a.labels_out[a.perm[p0]] = S.id[ts];
                 if (live1) a.labels_out[a.perm[p1]] = S.id[ts];
@@ -569,11 +574,33 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         S.ctx.Cf[d] = (float)DMUL(Cd[d], sc);
     }
     __syncthreads();
-    const int L0 = a.g.cand_start[T.x], L1 = a.g.cand_start[T.x + 1];
+    // initial pass (seeds as centres, w_v = 0): a chunk whose exact box lies inside
+    // its bin with the margin seeds_fast_ok (run.cu) proves takes the bin's own seed
+    // (id = bin) for every point -- the unique nearest valid candidate
+    bool fast0 = false;
+    if (a.seeds_fast) {
+        fast0 = true;
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const double ul = DDIV(DSUB(box[d], a.mn[d]), Cd[d]), uh = DDIV(DSUB(box[4 + d], a.mn[d]), Cd[d]);
+            const double fl = floor(ul), fh = floor(uh);
+            if (!(fl >= 0.0 && fl == fh && fl < (double)a.kk[d] && DSUB(ul, fl) >= 0x1.0p-20 &&
+                  DSUB(uh, fh) <= 1.0 - 0x1.0p-20))
+                fast0 = false;
+        }
+    }
+    const int L0 = fast0 ? 0 : a.g.cand_start[T.x], L1 = fast0 ? 0 : a.g.cand_start[T.x + 1];
     bool deferred = (L1 - L0) > CR * NT;
     int cnt = 0;
     float cvmax = 0.f;
-    if (!deferred) {
+    if (fast0) {
+        cnt = 1;
+        if (tid == 0) S.id[0] = T.x;
+        if (a.accumulate) {
+            if (tid == 0) S.n[0] = 0u;
+            for (int e = tid; e < NW * 5 * CAP; e += NT) (&S.wsum[0][0][0])[e] = 0.0;
+        }
+    } else if (!deferred) {
         // ---- candidates classified against the chunk box (exact fp64), compacted
         bool have[CR], full[CR];
         int id[CR];
@@ -678,7 +705,8 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         C.len = T.z;
         C.start = T.y;
         C.deferred = deferred;
-        C.stable = a.reuse && !deferred && cnt > 0 && a.bin_stable[T.x];
+        C.stable = fast0 || (a.reuse && !deferred && cnt > 0 && a.bin_stable[T.x]);
+        C.fast0 = fast0;
     }
     __syncthreads();
     const PCtx &C = S.ctx;

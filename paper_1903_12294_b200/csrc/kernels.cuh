@@ -20,6 +20,8 @@ struct FieldArgs {
     int nx, ny, nz, nt;
     double ox, oy, oz, sx, sy, sz;
     int x0, y0, z0;       // global cell index of the field's first cell (spatial slabs)
+    int seeds_fast;       // initial pass: blocks whose axis tiles are all interior (AxisTile.pad)
+                          // take their own bin's seed (see run.cu seeds_fast_ok)
     const double *times;
     const double *values;
     const AxisTile *xt, *yt, *zt;
@@ -85,6 +87,9 @@ struct PointArgs {
     const WBox *wbox;                  // [tile][POINT_CHUNK / 64] warp-tile boxes
     double Cx, Cy, Cz, Ct;
     double cf, wd, wv;
+    int seeds_fast;                    // initial pass: interior chunks take their bin's seed
+    double mn[4];                      // extent minima and k (the chunks' interior test)
+    int kk[4];
     CentersView c;
     const double *cval;
     const uint8_t *chas;

@@ -273,6 +273,8 @@ struct Plan {
     mfseg_points pts;
     int K;                          // centres
     int NB;                         // bins = k1*k2*k3*k4
+    int seeds_fast;                 // the initial pass may label interior blocks / chunks by
+                                    // their own seed (seeds_fast_ok)
     long long nf, np;
     cudaStream_t st;
     // centre state ping-pong
@@ -323,6 +325,35 @@ struct Plan {
     void *scan_tmp;
     size_t scan_bytes;
 };
+
+// Initial pass (seeds at the bin midpoints mins + (j + 0.5) C, w_v = 0): a sample
+// whose scaled bin coordinate u = (s - min) / C (fp64, as the reference bins it)
+// has a fractional part in [eta, 1 - eta] on every axis is nearer to its own bin's
+// seed than to any other seed by a squared-distance gap of at least
+// 2 eta (C_d c_d)^2 on some axis (c_d = c_f for time, 1 otherwise), and its own
+// seed passes the box test.  seeds_fast_ok checks that this gap dwarfs the fp64
+// error of the reference's D over the 3^4 candidates (then the own seed is the
+// unique argmin, no tie); interior_cell is the per-coordinate test.
+constexpr double SEED_ETA = 0x1.0p-20;
+
+bool interior_coord(double x, double mn, double C, int k) {
+    volatile double u = (x - mn) / C;   // fl(fl(x - mn) / C): no contraction on the host
+    const double f = u - std::floor(u);
+    return u >= 0.0 && u < (double)k && f >= SEED_ETA && f <= 1.0 - SEED_ETA;
+}
+
+bool seeds_fast_ok(const mfseg_params &p) {
+    double dmax2 = 0.0, gmin = INFINITY;
+    for (int d = 0; d < 4; ++d) {
+        const double cs = p.C[d] * (d == 3 ? std::fabs(p.c_f) : 1.0);
+        dmax2 += 4.0 * cs * cs;                     // |c - s| <= 2 C on every axis of a candidate
+        gmin = std::fmin(gmin, 2.0 * SEED_ETA * cs * cs);
+        // the seeds and the binning quotient carry fp64 errors ~2^-52 (|min| / C + k)
+        // bins: far below eta while that stays under 2^28
+        if (!(std::fabs(p.mins[d]) / p.C[d] + (double)p.k[d] < 0x1.0p28)) return false;
+    }
+    return std::isfinite(dmax2) && dmax2 > 0.0 && gmin > 0x1.0p-40 * dmax2;   // fp64 error ~2^-50
+}
 
 // tiles of <= T cells along one axis that never straddle a bin boundary; `off` =
 // global index of the first local cell (spatial slabs: a slab that starts on a
@@ -564,6 +595,19 @@ int plan_prepare_impl(Plan &P) {
         auto xt = axis_tiles(P.f.nx, P.f.origin[0], P.f.spacing[0], P.f.offset[0], p.mins[0], p.C[0], p.k[0], TX);
         auto yt = axis_tiles(P.f.ny, P.f.origin[1], P.f.spacing[1], P.f.offset[1], p.mins[1], p.C[1], p.k[1], TY);
         auto zt = axis_tiles(P.f.nz, P.f.origin[2], P.f.spacing[2], P.f.offset[2], p.mins[2], p.C[2], p.k[2], TZ);
+        // initial-pass flag per tile: every cell interior to its bin (AxisTile.pad)
+        auto flag = [&](std::vector<AxisTile> &v, int d) {
+            for (AxisTile &t : v) {
+                bool ok = true;
+                for (int i = t.start; ok && i < t.start + t.len; ++i)
+                    ok = interior_coord(cell_coord(P.f.origin[d], P.f.spacing[d], (long long)P.f.offset[d] + i),
+                                        p.mins[d], p.C[d], p.k[d]);
+                t.pad = ok;
+            }
+        };
+        flag(xt, 0);
+        flag(yt, 1);
+        flag(zt, 2);
         MFSEG_CUDA(cudaMemcpyAsync(P.xt, xt.data(), sizeof(AxisTile) * xt.size(),
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaMemcpyAsync(P.yt, yt.data(), sizeof(AxisTile) * yt.size(),
@@ -581,7 +625,9 @@ int plan_prepare_impl(Plan &P) {
             const int b = bin_coord(th[m0], p.mins[3], p.C[3], p.k[3]);
             int m1 = m0;
             while (m1 < P.f.nt && m1 - m0 < 4 && bin_coord(th[m1], p.mins[3], p.C[3], p.k[3]) == b) ++m1;
-            tts.push_back(AxisTile{m0, m1 - m0, b, 0});
+            bool ok = true;
+            for (int m = m0; ok && m < m1; ++m) ok = interior_coord(th[m], p.mins[3], p.C[3], p.k[3]);
+            tts.push_back(AxisTile{m0, m1 - m0, b, ok ? 1 : 0});
             m0 = m1;
         }
         P.ntt = (int)tts.size();
@@ -775,14 +821,17 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
 // state of the previous pass when it used the same weights (labels of stable
 // field blocks are reused), else null
 int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, int32_t *flabels,
-              int accumulate, const mfseg_centers *prev, int32_t *plabels_out) {
+              int accumulate, const mfseg_centers *prev, int32_t *plabels_out, int initial) {
+    // the initial pass of mfseg_run: seeds as centres, pure space-time metric
+    const DebugOptions &dbg = debug_options();
+    const int fast0 = initial && P.seeds_fast && wp == 0.0 && wf == 0.0 && wd == 1.0 &&
+                      !(dbg.flags & MFSEG_DEBUG_NO_SEEDS_FAST);
     cudaStream_t st = P.st;
     const mfseg_params &p = P.p;
     int K = P.K;
     CentersView cv = view_of(c, K);
     mark(0, st);
     // validity boxes of the previous pass (structural-change test of the reuse)
-    const DebugOptions &dbg = debug_options();
     const bool reuse = prev && accumulate && !(dbg.flags & MFSEG_DEBUG_NO_REUSE);
     if (P.vbox_prev && P.nf > 0 && accumulate)
         MFSEG_CUDA(cudaMemcpyAsync(P.vbox_prev, P.g.vbox, sizeof(int4) * 2 * K, cudaMemcpyDeviceToDevice, st));
@@ -863,6 +912,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.multi_cap = P.multi_cap;
         a.bslot = P.bslot;
         a.bmargin = a.bslot ? P.bmargin : nullptr;
+        a.seeds_fast = fast0;
         if (reuse && a.bslot) {
             a.reuse = 1;
             a.bin_stable = P.bstable;
@@ -914,6 +964,11 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.stats = P.counters + 16;
         a.deferred_cap = P.cap_p;
         a.tslot = P.tslot;
+        a.seeds_fast = fast0;
+        for (int d = 0; d < 4; ++d) {
+            a.mn[d] = p.mins[d];
+            a.kk[d] = p.k[d];
+        }
         if (reuse && a.tslot) {
             a.reuse = 1;
             a.bin_stable = P.bstable;
@@ -1085,6 +1140,7 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
         return 2;
     }
     int K = P.K;
+    P.seeds_fast = K == P.NB && seeds_fast_ok(*p);   // centres are the seeds in the initial pass (K == NB)
     MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
     MFSEG_TRY(plan_prepare(P));
     double4 mins = make_double4(p->mins[0], p->mins[1], p->mins[2], p->mins[3]);
@@ -1106,7 +1162,7 @@ int mfseg_run(const mfseg_params *p, const mfseg_field *f, const mfseg_points *p
         // the last possible pass writes the point labels in record order itself
         const bool last = pass == p->max_iterations;
         MFSEG_TRY(plan_pass(P, P.s[cur], wd, wp, wf, field_labels, 1, pass >= 2 ? &P.s[cur ^ 1] : nullptr,
-                            last ? point_labels : nullptr));
+                            last ? point_labels : nullptr, initial));
         unpermuted = last;
         if (reduce) {
             long long npairs = (long long)K * MFSEG_ACC_WORDS / 2;
@@ -1158,7 +1214,7 @@ int mfseg_assign(const mfseg_params *p, const mfseg_field *f, const mfseg_points
     MFSEG_TRY(plan_init(P, p, f, pts, workspace, workspace_bytes, st));
     MFSEG_CUDA(cudaMemsetAsync(P.overflow, 0, sizeof(int) * 4, st));
     MFSEG_TRY(plan_prepare(P));
-    const int rc = plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr, point_labels);
+    const int rc = plan_pass(P, centers, p->w_d, p->w_p, p->w_f, field_labels, 1, nullptr, point_labels, 0);
     nvtx_phase(5);   // close the pass's last NVTX range
     MFSEG_TRY(rc);
     if (acc)

@@ -493,14 +493,15 @@ def test_assign_drifted_centres_vs_oracle(w_d, seed):
 
 
 @pytest.mark.parametrize("opts", [dict(multi_cap=0), dict(multi_cap=37), dict(flags=2),
-                                  dict(flags=1), dict(flags=16), dict(flags=32)])
+                                  dict(flags=1), dict(flags=16), dict(flags=32), dict(flags=64)])
 def test_field_brick_queue_paths_agree(opts):
     """k_field_assign5 queues multi-candidate bricks for k_field_screen; a full
     queue (capacity 0 or 37 items) sends the rest to the exact per-sample path
     (k_deferred), debug flag 2 resolves every queued sample in exact fp64 and
     flag 1 disables culling and dominance (most bricks then exceed the
     16-candidate queue limit); flag 16 recomputes the blocks whose candidates
-    did not change since the last pass, flag 32 keeps only exact reuse.  A 6-pass run: labels and
+    did not change since the last pass, flag 32 keeps only exact reuse, flag 64
+    labels the initial pass without the interior-block / chunk shortcut.  A 6-pass run: labels and
     centre positions bit-identical (integer sums), field means within fp64
     rounding (the value
     sums are rounded per record or per sample depending on the path)."""
@@ -525,6 +526,32 @@ def test_field_brick_queue_paths_agree(opts):
         assert (ca.f_c is None) == (cb.f_c is None)
         if ca.f_c is not None:
             assert ca.f_c == pytest.approx(cb.f_c, rel=1e-12, abs=1e-15)
+
+
+@pytest.mark.parametrize("c_f,k,iters", [(1.0, (8, 6, 4, 6), 1), (0.37, (16, 12, 8, 6), 1),
+                                          (2.5, (5, 7, 3, 4), 2)])
+def test_initial_pass_shortcut_is_exact(c_f, k, iters):
+    """The initial pass labels field blocks and point chunks lying inside their
+    bin (margin 2^-20 bin widths) with the bin's own seed without any candidate
+    work: labels and centres must equal the full windowed assignment (debug flag
+    NO_SEEDS_FAST), including the samples on bin faces (integer grid, bins of
+    whole cells) that the shortcut must leave to the exact path."""
+    P = pkg()
+    from paper_1903_12294_b200.engine import run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device
+    dims, nt, ntraj = (96, 80, 48), 18, 20000
+    fld, pts, _ = _synthetic(dims, nt, ntraj, 17, False, n_blobs=2)
+    ext = domain_extent_device(pts, fld)
+    params = P.ClusterParams(k=k, c_f=c_f, eps_c=1e-12, max_iterations=iters)
+    a = run_device(pts, fld, ext, params)
+    with N.debug_options(N.DEBUG_NO_SEEDS_FAST):
+        b = run_device(pts, fld, ext, params)
+    assert torch.equal(a.field_labels, b.field_labels)
+    assert torch.equal(a.point_labels, b.point_labels)
+    sa, sb = P.CenterState.from_device(a.state), P.CenterState.from_device(b.state)
+    np.testing.assert_array_equal(np.asarray(sa.loc), np.asarray(sb.loc))
+    np.testing.assert_array_equal(np.asarray(sa.fval), np.asarray(sb.fval))
+    np.testing.assert_array_equal(np.asarray(sa.pval), np.asarray(sb.pval))
 
 
 @pytest.mark.parametrize("weights", [dict(), dict(c_f=0.5, w_d=0.3, w_p=1.5, w_f=2.0)])
