@@ -120,23 +120,30 @@ __device__ __forceinline__ void d2fix(double x, unsigned long long &lo, long lon
         return;
     }
     if (e == 0) e = 1; else m |= (1ull << 52);
-    int sh = e - 1011;   // m * 2^(e-1075) * 2^64
-    unsigned __int128 u;
-    if (sh >= 0) {
-        if (sh > 73) {
-            if (overflow) *overflow = 1;
-            u = 0;
-        } else {
-            u = ((unsigned __int128)m) << sh;
-        }
+    const int sh = e - 1011;   // m * 2^(e-1075) * 2^64
+    unsigned long long ul, uh;  // |x| * 2^64 (64-bit shifts: no 128-bit shift sequences)
+    if (sh > 73) {
+        if (overflow) *overflow = 1;
+        ul = uh = 0;
+    } else if (sh >= 64) {
+        ul = 0;
+        uh = m << (sh - 64);
+    } else if (sh > 0) {
+        ul = m << sh;
+        uh = m >> (64 - sh);
     } else if (sh > -64) {
-        u = (unsigned __int128)(m >> (-sh));
+        ul = m >> (-sh);
+        uh = 0;
     } else {
-        u = 0;
+        ul = uh = 0;
     }
-    __int128 s = (bits >> 63) ? -(__int128)u : (__int128)u;
-    lo = (unsigned long long)s;
-    hi = (long long)(s >> 64);
+    if (bits >> 63) {   // two's complement negation of (uh, ul)
+        lo = 0ull - ul;
+        hi = (long long)(~uh + (ul == 0 ? 1ull : 0ull));
+    } else {
+        lo = ul;
+        hi = (long long)uh;
+    }
 }
 
 // correctly rounded (nearest-even) double of the 128-bit fixed value * 2^-64

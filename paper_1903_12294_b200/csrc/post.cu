@@ -344,77 +344,6 @@ __device__ __forceinline__ double unokey(unsigned long long b) {
     return __longlong_as_double((long long)r);
 }
 
-__device__ __forceinline__ void warp_sum_fix(unsigned long long &lo, long long &hi) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long ol = __shfl_xor_sync(0xffffffffu, lo, o);
-        long long oh = __shfl_xor_sync(0xffffffffu, hi, o);
-        unsigned long long nl = lo + ol;
-        hi = hi + oh + (nl < lo ? 1 : 0);
-        lo = nl;
-    }
-}
-
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long k) {
-    const unsigned hi = (unsigned)(k >> 32);
-    const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
-    const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? (unsigned)k : 0xFFFFFFFFu);
-    return ((unsigned long long)mh << 32) | ml;
-}
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
-    const unsigned hi = (unsigned)(k >> 32);
-    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)k : 0u);
-    return ((unsigned long long)mh << 32) | ml;
-}
-
-// warp-aggregated add of one sample into its slot's accumulators; the value
-// sums are reduced in 128-bit fixed point (exact, order-free)
-__device__ void stat_add(unsigned long long *S, int slot, bool field, double x, double y,
-                         double z, double t, double v, const double *mean, int pass, int *ovf) {
-    unsigned act = __ballot_sync(0xffffffffu, slot >= 0);
-    int lane = threadIdx.x & 31;
-    while (act) {
-        int leader = __ffs(act) - 1;
-        int L = __shfl_sync(0xffffffffu, slot, leader);
-        bool mine = slot == L;
-        unsigned m = __ballot_sync(0xffffffffu, mine);
-        unsigned long long *s = S + (size_t)L * SW;
-        unsigned long long lo = 0;
-        long long hi = 0;
-        if (pass == 0) {
-            if (mine) d2fix(v, lo, hi, ovf);
-            warp_sum_fix(lo, hi);
-            // bbox as order-preserving 64-bit keys, reduced with 32-bit REDUX (high
-            // word, then the low word among the lanes holding the extreme high word)
-            const double bv[4] = {x, y, z, t};
-            unsigned long long kl[4], kh[4];
-#pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const unsigned long long k = okey(bv[d]);
-                kl[d] = warp_min_u64(mine ? k : ~0ull);
-                kh[d] = warp_max_u64(mine ? k : 0ull);
-            }
-            if (lane == leader) {
-                atomic_add_fix(s + (field ? 2 : 0), lo, hi);
-                atomicAdd(s + (field ? 9 : 8), (unsigned long long)__popc(m));
-                for (int d = 0; d < 4; ++d) {   // atomics only when the box grows
-                    if (kl[d] < ((volatile unsigned long long *)s)[10 + d]) atomicMin(s + 10 + d, kl[d]);
-                    if (kh[d] > ((volatile unsigned long long *)s)[14 + d]) atomicMax(s + 14 + d, kh[d]);
-                }
-            }
-        } else {
-            if (mine) {
-                double dv = DSUB(v, mean[2 * L + (field ? 1 : 0)]);
-                d2fix(DMUL(dv, dv), lo, hi, ovf);
-            }
-            warp_sum_fix(lo, hi);
-            if (lane == leader) atomic_add_fix(s + (field ? 6 : 4), lo, hi);
-        }
-        act &= ~m;
-    }
-}
-
 struct StatArgs {
     int n_slots;
     long long nf, ncell;
@@ -431,102 +360,369 @@ struct StatArgs {
     int *ovf;
 };
 
-// One pass over all samples (fields first, then points); slot = feature or -1.
-// SMEM: the block accumulates into a shared-memory copy of the slot records
-// (few features: the global records would serialise every warp's atomics on a
-// handful of addresses) and flushes it once; otherwise warp-aggregated global
-// atomics.  Integer sums: the result does not depend on the path.
+// One pass over the samples: every lane accumulates the run of samples of one
+// feature it meets (128-bit fixed-point value sums, counts, bounding box) in
+// registers and adds the run to its slot record when the feature changes and
+// at the end -- a few atomics per run instead of a warp reduction per 32
+// samples.  Each warp takes a contiguous range of the samples, 32 consecutive
+// ones per step (coalesced loads), so a lane's runs are long.  SMEM: the block
+// accumulates into a shared-memory copy of the slot records (few features: the
+// global ones would serialise the final flushes on a handful of addresses) and
+// adds it to the global records once.  Integer sums and min/max keys: the
+// result does not depend on the order, the grid or the partition of the samples.
 constexpr int STAT_SMEM_SLOTS = 320;   // 320 x 18 x 8 B = 45 KB
+constexpr int STAT_BLOCKS = 148 * 8;
+
+__device__ __forceinline__ void add_fix(unsigned long long &lo, long long &hi, unsigned long long l,
+                                        long long h) {
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(l), "l"(h));
+}
+
+// d2fix (common.cuh) for the per-sample statistics: the same value (|x| 2^64
+// truncated toward zero, negated for x < 0) from the integer and fractional
+// parts by hardware conversions instead of shifts on the exponent
+__device__ __forceinline__ void d2fix_stat(double x, unsigned long long &lo, long long &hi, int *ovf) {
+    const double ax = fabs(x);
+    if (!(ax < 0x1.0p62)) {   // also NaN / inf
+        d2fix(x, lo, hi, ovf);
+        return;
+    }
+    const double ih = trunc(ax);
+    const unsigned long long uh = (unsigned long long)ih;
+    const unsigned long long ul = __double2ull_rz(DMUL(DSUB(ax, ih), 0x1.0p64));   // exact difference
+    if (x < 0.0) {
+        lo = 0ull - ul;
+        hi = (long long)(~uh + (ul == 0 ? 1ull : 0ull));
+    } else {
+        lo = ul;
+        hi = (long long)uh;
+    }
+}
+
+// bounding-box keys into a slot record (atomics only when the box grows)
+__device__ __forceinline__ void bbox_flush(unsigned long long *s, const unsigned long long *k0,
+                                           const unsigned long long *k1) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        if (k0[d] < ((volatile unsigned long long *)s)[10 + d]) atomicMin(s + 10 + d, k0[d]);
+        if (k1[d] > ((volatile unsigned long long *)s)[14 + d]) atomicMax(s + 14 + d, k1[d]);
+    }
+}
+
 template <bool SMEM>
-__global__ void __launch_bounds__(256) k_stats(StatArgs a, int pass) {
+__device__ __forceinline__ unsigned long long *stat_records(const StatArgs &a) {
     extern __shared__ unsigned long long sS[];
-    unsigned long long *S = SMEM ? sS : a.S;
     if (SMEM) {
         for (int i = threadIdx.x; i < a.n_slots * SW; i += blockDim.x) {
             const int w = i % SW;
             sS[i] = (w >= 10 && w < 14) ? ~0ull : 0ull;
         }
         __syncthreads();
+        return sS;
     }
-    const long long total = a.nf + a.np;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    const unsigned ncell = a.ncell > 0 ? (unsigned)a.ncell : 1u, nx = (unsigned)a.nx,
-                   ny = (unsigned)a.ny;
-    // (timestep, cell) of the block's first sample, advanced by the stride each
-    // round: no 64-bit division per sample
-    long long base = blockIdx.x * (long long)blockDim.x;
-    long long mb = base / ncell, rb = base % ncell;
-    const long long smq = stride / ncell, smr = stride % ncell;
-    for (; base < total; base += stride) {
-        const long long q = base + threadIdx.x;
-        int slot = -1;
-        const bool field = q < a.nf;
-        double x = 0, y = 0, z = 0, t = 0, v = 0;
-        if (q < total) {
-            if (field) {
-                slot = a.fslot[q];
-                if (slot >= 0) {
-                    unsigned ru = (unsigned)rb + threadIdx.x;
-                    long long m = mb;
-                    if (ru >= ncell) {
-                        m += ru / ncell;
-                        ru %= ncell;
-                    }
-                    const unsigned row = ru / nx;
-                    x = cell_coord(a.ox, a.sx, a.x0 + (long long)(ru - row * nx));
-                    y = cell_coord(a.oy, a.sy, a.y0 + (long long)(row % ny));
-                    z = cell_coord(a.oz, a.sz, a.z0 + (long long)(row / ny));
-                    t = a.times[m];
-                    v = a.values[q];
-                }
-            } else {
-                long long p = q - a.nf;
-                slot = a.pslot[p];
-                if (slot >= 0) {
-                    x = a.xyz[3 * p];
-                    y = a.xyz[3 * p + 1];
-                    z = a.xyz[3 * p + 2];
-                    t = a.pt[p];
-                    v = a.pv[p];
-                }
-            }
-        }
-        // field and point lanes are aggregated separately
-        stat_add(S, field ? slot : -1, true, x, y, z, t, v, a.mean, pass, a.ovf);
-        stat_add(S, field ? -1 : slot, false, x, y, z, t, v, a.mean, pass, a.ovf);
-        mb += smq;
-        rb += smr;
-        if (rb >= ncell) {
-            rb -= ncell;
-            ++mb;
-        }
-    }
-    if (SMEM) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < a.n_slots * SW; i += blockDim.x) {
-            const int w = i % SW;
-            unsigned long long *g = a.S + i;
-            const unsigned long long v = sS[i];
-            if (w < 8) {
-                if ((w & 1) == 0 && (v | sS[i + 1])) atomic_add_fix(g, v, (long long)sS[i + 1]);
-            } else if (w < 10) {
-                if (v) atomicAdd(g, v);
-            } else if (w < 14) {
-                if (v != ~0ull) atomicMin(g, v);
-            } else if (v) {
-                atomicMax(g, v);
-            }
+    return a.S;
+}
+
+template <bool SMEM>
+__device__ __forceinline__ void stat_records_flush(const StatArgs &a) {
+    extern __shared__ unsigned long long sS[];
+    if (!SMEM) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.n_slots * SW; i += blockDim.x) {
+        const int w = i % SW;
+        unsigned long long *g = a.S + i;
+        const unsigned long long v = sS[i];
+        if (w < 8) {
+            if ((w & 1) == 0 && (v | sS[i + 1])) atomic_add_fix(g, v, (long long)sS[i + 1]);
+        } else if (w < 10) {
+            if (v) atomicAdd(g, v);
+        } else if (w < 14) {
+            if (v != ~0ull) atomicMin(g, v);
+        } else if (v) {
+            atomicMax(g, v);
         }
     }
 }
 
+// this warp's contiguous share [q0, q1) of n samples (whole 32-sample steps)
+__device__ __forceinline__ void warp_share(long long n, long long &q0, long long &q1) {
+    const long long W = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const long long steps = (n + 31) >> 5, per = (steps + W - 1) / W;
+    q0 = min(n, gw * per * 32);
+    q1 = min(n, (gw + 1) * per * 32);
+}
+
+// Field samples: each lane takes 8 consecutive samples of every 256-sample
+// segment of its warp's range (vector loads), so along x its runs follow the
+// feature; the next segment is the next 256 cells (the same x strip of the next
+// rows when nx = 256).  The run's bounding box is kept in cell indices
+// (cell_coord is monotone in the index: the coordinate box is the keys of the
+// extreme indices) and time keys; y, z, t are only re-examined at row changes.
+__device__ __forceinline__ void field_run_flush(unsigned long long *S, const StatArgs &a, int pass, int rs,
+                                                unsigned rn, unsigned long long lo, long long hi,
+                                                const unsigned *b0, const unsigned *b1, unsigned long long t0,
+                                                unsigned long long t1) {
+    unsigned long long *s = S + (size_t)rs * SW;
+    if (pass == 1) {
+        atomic_add_fix(s + 6, lo, hi);
+        return;
+    }
+    atomic_add_fix(s + 2, lo, hi);
+    atomicAdd(s + 9, (unsigned long long)rn);
+    const unsigned long long ka = okey(cell_coord(a.ox, a.sx, a.x0 + (long long)b0[0])),
+                             kb = okey(cell_coord(a.ox, a.sx, a.x0 + (long long)b1[0])),
+                             kc = okey(cell_coord(a.oy, a.sy, a.y0 + (long long)b0[1])),
+                             kd = okey(cell_coord(a.oy, a.sy, a.y0 + (long long)b1[1])),
+                             ke = okey(cell_coord(a.oz, a.sz, a.z0 + (long long)b0[2])),
+                             kf = okey(cell_coord(a.oz, a.sz, a.z0 + (long long)b1[2]));
+    const unsigned long long k0[4] = {min(ka, kb), min(kc, kd), min(ke, kf), t0};
+    const unsigned long long k1[4] = {max(ka, kb), max(kc, kd), max(ke, kf), t1};
+    bbox_flush(s, k0, k1);
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k_stats_field(StatArgs a, int pass) {
+    unsigned long long *S = stat_records<SMEM>(a);
+    const int lane = threadIdx.x & 31;
+    long long q0, q1;
+    {   // this warp's contiguous share of whole 256-sample segments
+        const long long W = (long long)gridDim.x * (blockDim.x >> 5);
+        const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        const long long segs = (a.nf + 255) >> 8, per = (segs + W - 1) / W;
+        q0 = min(a.nf, gw * per * 256);
+        q1 = min(a.nf, (gw + 1) * per * 256);
+    }
+    const unsigned nx = (unsigned)a.nx, ny = (unsigned)a.ny, nz = (unsigned)a.nz;
+    const long long plane = (long long)nx * ny;
+    unsigned dx, dy, dz, dm;   // 256 in (timestep, z, y, x) digits
+    {
+        long long r = 256;
+        dm = (unsigned)(r / a.ncell);
+        r %= a.ncell;
+        dz = (unsigned)(r / plane);
+        r %= plane;
+        dy = (unsigned)(r / nx);
+        dx = (unsigned)(r % nx);
+    }
+    unsigned ix = 0, iy = 0, iz = 0, m = 0;   // the lane's first sample of the segment
+    if (q0 < q1) {
+        const long long q = q0 + 8 * lane;
+        m = (unsigned)(q / a.ncell);
+        long long r = q % a.ncell;
+        iz = (unsigned)(r / plane);
+        r %= plane;
+        iy = (unsigned)(r / nx);
+        ix = (unsigned)(r % nx);
+    }
+    const bool vec = ((reinterpret_cast<uintptr_t>(a.fslot) | reinterpret_cast<uintptr_t>(a.values)) & 15) == 0;
+    int ovf = 0;
+    int rs = -1;                       // the run's slot
+    unsigned rn = 0;
+    unsigned long long lo = 0;
+    long long hi = 0;
+    unsigned b0[3] = {0, 0, 0}, b1[3] = {0, 0, 0};   // index box (x, y, z)
+    unsigned long long t0 = 0, t1 = 0, tk = 0;
+    unsigned mk = 0xFFFFFFFFu;
+    double mu = 0.0;
+    for (long long sb = q0; sb < q1; sb += 256) {
+        const long long qb = sb + 8 * lane;
+        int sl[8];
+        double vv[8];
+        if (vec && qb + 8 <= q1) {
+            const int4 s0 = *reinterpret_cast<const int4 *>(a.fslot + qb);
+            const int4 s1 = *reinterpret_cast<const int4 *>(a.fslot + qb + 4);
+            sl[0] = s0.x; sl[1] = s0.y; sl[2] = s0.z; sl[3] = s0.w;
+            sl[4] = s1.x; sl[5] = s1.y; sl[6] = s1.z; sl[7] = s1.w;
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+                const double2 v2 = *reinterpret_cast<const double2 *>(a.values + qb + k);
+                vv[k] = v2.x;
+                vv[k + 1] = v2.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                sl[k] = qb + k < q1 ? a.fslot[qb + k] : -1;
+                vv[k] = sl[k] >= 0 ? a.values[qb + k] : 0.0;
+            }
+        }
+        unsigned jx = ix, jy = iy, jz = iz, jm = m;
+        bool row = true;   // y / z / t not yet examined in this row for the run
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int slot = sl[k];
+            if (slot >= 0) {
+                if (slot != rs) {
+                    if (rs >= 0) field_run_flush(S, a, pass, rs, rn, lo, hi, b0, b1, t0, t1);
+                    rs = slot;
+                    rn = 0;
+                    lo = 0;
+                    hi = 0;
+                    b0[0] = b1[0] = jx;
+                    row = true;
+                    if (pass == 0) {
+                        b0[1] = b1[1] = jy;
+                        b0[2] = b1[2] = jz;
+                        if (jm != mk) {
+                            tk = okey(a.times[jm]);
+                            mk = jm;
+                        }
+                        t0 = t1 = tk;
+                    } else {
+                        mu = a.mean[2 * slot + 1];
+                    }
+                }
+                unsigned long long l;
+                long long h;
+                if (pass == 0) {
+                    d2fix_stat(vv[k], l, h, &ovf);
+                    ++rn;
+                    b0[0] = min(b0[0], jx);
+                    b1[0] = max(b1[0], jx);
+                    if (row) {
+                        row = false;
+                        b0[1] = min(b0[1], jy);
+                        b1[1] = max(b1[1], jy);
+                        b0[2] = min(b0[2], jz);
+                        b1[2] = max(b1[2], jz);
+                        if (jm != mk) {
+                            tk = okey(a.times[jm]);
+                            mk = jm;
+                        }
+                        t0 = min(t0, tk);
+                        t1 = max(t1, tk);
+                    }
+                } else {
+                    const double dv = DSUB(vv[k], mu);
+                    d2fix_stat(DMUL(dv, dv), l, h, &ovf);
+                }
+                add_fix(lo, hi, l, h);
+            }
+            if (++jx == nx) {   // next row
+                jx = 0;
+                row = true;
+                if (++jy == ny) {
+                    jy = 0;
+                    if (++jz == nz) {
+                        jz = 0;
+                        ++jm;
+                    }
+                }
+            }
+        }
+        // the lane's first sample of the next segment: + 256
+        unsigned c;
+        ix += dx;
+        c = ix >= nx;
+        ix -= c ? nx : 0u;
+        iy += dy + c;
+        c = iy >= ny;
+        iy -= c ? ny : 0u;
+        iz += dz + c;
+        c = iz >= nz;
+        iz -= c ? nz : 0u;
+        m += dm + c;
+    }
+    if (rs >= 0) field_run_flush(S, a, pass, rs, rn, lo, hi, b0, b1, t0, t1);
+    if (ovf) *a.ovf = 1;
+    stat_records_flush<SMEM>(a);
+}
+
+// Point samples (record order: a trajectory's samples are consecutive).
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k_stats_points(StatArgs a, int pass) {
+    unsigned long long *S = stat_records<SMEM>(a);
+    const int lane = threadIdx.x & 31;
+    long long q0, q1;
+    warp_share(a.np, q0, q1);
+    int ovf = 0;
+    int rs = -1;
+    unsigned rn = 0;
+    unsigned long long lo = 0;
+    long long hi = 0;
+    unsigned long long k0[4] = {0, 0, 0, 0}, k1[4] = {0, 0, 0, 0};
+    double mu = 0.0;
+    for (long long base = q0; base < q1; base += 32) {
+        const long long q = base + lane;
+        const int slot = q < q1 ? a.pslot[q] : -1;
+        if (slot >= 0) {
+            const double v = a.pv[q];
+            unsigned long long k[4];
+            if (pass == 0) {
+                k[0] = okey(a.xyz[3 * q]);
+                k[1] = okey(a.xyz[3 * q + 1]);
+                k[2] = okey(a.xyz[3 * q + 2]);
+                k[3] = okey(a.pt[q]);
+            }
+            if (slot != rs) {
+                if (rs >= 0) {
+                    unsigned long long *s = S + (size_t)rs * SW;
+                    if (pass == 0) {
+                        atomic_add_fix(s, lo, hi);
+                        atomicAdd(s + 8, (unsigned long long)rn);
+                        bbox_flush(s, k0, k1);
+                    } else {
+                        atomic_add_fix(s + 4, lo, hi);
+                    }
+                }
+                rs = slot;
+                rn = 0;
+                lo = 0;
+                hi = 0;
+                if (pass == 0) {
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) k0[d] = k1[d] = k[d];
+                } else {
+                    mu = a.mean[2 * slot];
+                }
+            }
+            unsigned long long l;
+            long long h;
+            if (pass == 0) {
+                d2fix_stat(v, l, h, &ovf);
+                ++rn;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    k0[d] = min(k0[d], k[d]);
+                    k1[d] = max(k1[d], k[d]);
+                }
+            } else {
+                const double dv = DSUB(v, mu);
+                d2fix_stat(DMUL(dv, dv), l, h, &ovf);
+            }
+            add_fix(lo, hi, l, h);
+        }
+    }
+    if (rs >= 0) {
+        unsigned long long *s = S + (size_t)rs * SW;
+        if (pass == 0) {
+            atomic_add_fix(s, lo, hi);
+            atomicAdd(s + 8, (unsigned long long)rn);
+            bbox_flush(s, k0, k1);
+        } else {
+            atomic_add_fix(s + 4, lo, hi);
+        }
+    }
+    if (ovf) *a.ovf = 1;
+    stat_records_flush<SMEM>(a);
+}
+
 int launch_stats(const StatArgs &a, int pass, cudaStream_t st) {
-    ::mfseg::count_launch();
-    if (a.n_slots <= STAT_SMEM_SLOTS)
-        k_stats<true><<<148 * 8, 256, (size_t)a.n_slots * SW * 8, st>>>(a, pass);
-    else
-        k_stats<false><<<148 * 8, 256, 0, st>>>(a, pass);
-    MFSEG_LAUNCH("k_stats");
+    const bool sm = a.n_slots <= STAT_SMEM_SLOTS;
+    const size_t bytes = sm ? (size_t)a.n_slots * SW * 8 : 0;
+    if (a.nf > 0) {
+        ::mfseg::count_launch();
+        if (sm) k_stats_field<true><<<STAT_BLOCKS, 256, bytes, st>>>(a, pass);
+        else k_stats_field<false><<<STAT_BLOCKS, 256, 0, st>>>(a, pass);
+        MFSEG_LAUNCH("k_stats_field");
+    }
+    if (a.np > 0) {
+        ::mfseg::count_launch();
+        if (sm) k_stats_points<true><<<STAT_BLOCKS, 256, bytes, st>>>(a, pass);
+        else k_stats_points<false><<<STAT_BLOCKS, 256, 0, st>>>(a, pass);
+        MFSEG_LAUNCH("k_stats_points");
+    }
     return 0;
 }
 
@@ -909,70 +1105,6 @@ size_t mfseg_feature_stats_workspace_size(int32_t n_slots) {
     return cv.off + 256;
 }
 
-int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
-                        const mfseg_points *pts, const int32_t *point_slot, double *stats,
-                        void *workspace, size_t workspace_bytes, void *stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (n_slots <= 0) return 0;
-    if (workspace_bytes < mfseg_feature_stats_workspace_size(n_slots)) {
-        set_error("feature_stats: workspace too small");
-        return 3;
-    }
-    Carver cv(workspace, workspace_bytes);
-    StatArgs a;
-    memset(&a, 0, sizeof a);
-    a.n_slots = n_slots;
-    a.S = cv.take<unsigned long long>((long long)n_slots * SW);
-    double *mean = cv.take<double>(2ll * n_slots);
-    a.mean = mean;
-    a.ovf = cv.take<int>(4);
-    if (f && f->nt > 0 && field_slot) {
-        a.ncell = (long long)f->nx * f->ny * f->nz;
-        a.nf = a.ncell * f->nt;
-        a.nx = f->nx;
-        a.ny = f->ny;
-        a.nz = f->nz;
-        a.ox = f->origin[0];
-        a.oy = f->origin[1];
-        a.oz = f->origin[2];
-        a.x0 = f->offset[0];
-        a.y0 = f->offset[1];
-        a.z0 = f->offset[2];
-        a.sx = f->spacing[0];
-        a.sy = f->spacing[1];
-        a.sz = f->spacing[2];
-        a.times = f->times;
-        a.values = f->values;
-        a.fslot = field_slot;
-    }
-    if (pts && pts->n > 0 && point_slot) {
-        a.np = pts->n;
-        a.xyz = pts->xyz;
-        a.pt = pts->t;
-        a.pv = pts->value;
-        a.pslot = point_slot;
-    }
-    unsigned gs = (unsigned)((n_slots + 255) / 256);
-    MFSEG_CUDA(cudaMemsetAsync(a.ovf, 0, sizeof(int), st));
-    ::mfseg::count_launch();
-    k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
-    MFSEG_TRY(launch_stats(a, 0, st));
-    ::mfseg::count_launch();
-    k_stats_means<<<gs, 256, 0, st>>>(n_slots, a.S, mean);
-    MFSEG_TRY(launch_stats(a, 1, st));
-    ::mfseg::count_launch();
-    k_stats_final<<<gs, 256, 0, st>>>(n_slots, a.S, mean, stats);
-    MFSEG_LAUNCH("feature_stats");
-    int h = 0;
-    MFSEG_CUDA(cudaMemcpyAsync(&h, a.ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
-    MFSEG_CUDA(cudaStreamSynchronize(st));
-    if (h) {
-        set_error("feature_stats: fixed-point overflow");
-        return 4;
-    }
-    return 0;
-}
-
 static void stat_args(StatArgs &a, int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
                       const mfseg_points *pts, const int32_t *point_slot) {
     memset(&a, 0, sizeof a);
@@ -1003,6 +1135,43 @@ static void stat_args(StatArgs &a, int32_t n_slots, const mfseg_field *f, const 
         a.pv = pts->value;
         a.pslot = point_slot;
     }
+}
+
+int mfseg_feature_stats(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,
+                        const mfseg_points *pts, const int32_t *point_slot, double *stats,
+                        void *workspace, size_t workspace_bytes, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_slots <= 0) return 0;
+    if (workspace_bytes < mfseg_feature_stats_workspace_size(n_slots)) {
+        set_error("feature_stats: workspace too small");
+        return 3;
+    }
+    Carver cv(workspace, workspace_bytes);
+    StatArgs a;
+    stat_args(a, n_slots, f, field_slot, pts, point_slot);
+    a.S = cv.take<unsigned long long>((long long)n_slots * SW);
+    double *mean = cv.take<double>(2ll * n_slots);
+    a.mean = mean;
+    a.ovf = cv.take<int>(4);
+    unsigned gs = (unsigned)((n_slots + 255) / 256);
+    MFSEG_CUDA(cudaMemsetAsync(a.ovf, 0, sizeof(int), st));
+    ::mfseg::count_launch();
+    k_stats_init<<<gs, 256, 0, st>>>(n_slots, a.S);
+    MFSEG_TRY(launch_stats(a, 0, st));
+    ::mfseg::count_launch();
+    k_stats_means<<<gs, 256, 0, st>>>(n_slots, a.S, mean);
+    MFSEG_TRY(launch_stats(a, 1, st));
+    ::mfseg::count_launch();
+    k_stats_final<<<gs, 256, 0, st>>>(n_slots, a.S, mean, stats);
+    MFSEG_LAUNCH("feature_stats");
+    int h = 0;
+    MFSEG_CUDA(cudaMemcpyAsync(&h, a.ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    if (h) {
+        set_error("feature_stats: fixed-point overflow");
+        return 4;
+    }
+    return 0;
 }
 
 int mfseg_feature_stats_pass(int32_t n_slots, const mfseg_field *f, const int32_t *field_slot,

@@ -18,6 +18,7 @@ for env in sys.argv[2:] or [""]:
         os.environ.pop(e)
     if env:
         os.environ[env] = "1"
+    _N.debug_options_from_env()
     run_device(pts, fld, ext, params); torch.cuda.synchronize()
     lib.mfseg_timing_enable(1)
     r = run_device(pts, fld, ext, params); torch.cuda.synchronize()
