@@ -245,7 +245,11 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
             if (r < C.nrounds && s < C.cnt) {
                 const float4 rc = S.rc[s];
                 const float rcv[4] = {rc.x, rc.y, rc.z, rc.w};
-                float ql = 0.f, qh = 0.f, qu = 0.f;
+                // per axis the distance range over [b1, a1]: nearest max(0, b1, -a1),
+                // farthest max(a1, -b1).  (Clamping to the guard band +-cw changes
+                // neither for a candidate that is not out of range, and the farthest
+                // distance is the upper bound of a fully valid one.)
+                float ql = 0.f, qu = 0.f;
                 bool wfull = true, none = false;
 #pragma unroll
                 for (int d = 0; d < 4; ++d) {
@@ -253,14 +257,12 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                     const float a1 = rcv[d] - wl[d], b1 = rcv[d] - wh[d];   // a1 >= b1
                     if (a1 < -cw || b1 > cw) none = true;
                     if (!(a1 <= cn && b1 >= -cn)) wfull = false;
-                    const float e1 = fminf(a1, cw), e2 = fmaxf(b1, -cw);
-                    const float mx = fmaxf(fabsf(e1), fabsf(e2));
-                    const float mn = (e2 <= 0.f && e1 >= 0.f) ? 0.f : fminf(fabsf(e1), fabsf(e2));
-                    const float mu = fmaxf(fabsf(a1), fabsf(b1));
+                    const float mn = fmaxf(fmaxf(b1, -a1), 0.f);
+                    const float mu = fmaxf(a1, -b1);
                     ql = fmaf(mn, mn, ql);
-                    qh = fmaf(mx, mx, qh);
                     qu = fmaf(mu, mu, qu);
                 }
+                const float qh = qu;
                 float vtl = 0.f, vth = 0.f;
                 if (USEVAL) {
                     const float wvs = S.wvf[s];
