@@ -268,9 +268,9 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                     const float wvs = S.wvf[s];
                     if (wvs > 0.f) {
                         const float cvs = S.cvf[s];
-                        const float pl = vl - cvs, ph = vh - cvs;
-                        vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
-                        vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
+                        const float pl = vl - cvs, ph = vh - cvs;   // pl <= ph
+                        vtl = wvs * fmaxf(fmaxf(pl, -ph), 0.f);
+                        vth = wvs * fmaxf(ph, -pl);
                     }
                 }
                 if (!none) dl[r] = fmaf(C.fwd, sqrt_approx(ql), vtl);
