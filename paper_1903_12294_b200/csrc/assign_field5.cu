@@ -256,9 +256,9 @@ __device__ __forceinline__ int region_list(Smem5 &S, const Ctx &C, int rbx, int 
                 const float wvs = S.wvf[s];
                 if (wvs > 0.0f) {
                     const float cvs = S.cvf[s];
-                    const float pl = vl - cvs, ph = vh - cvs;
-                    vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
-                    vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
+                    const float pl = vl - cvs, ph = vh - cvs;   // pl <= ph
+                    vtl = wvs * fmaxf(fmaxf(pl, -ph), 0.f);
+                    vth = wvs * fmaxf(ph, -pl);
                 }
             }
             dlr = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);
@@ -437,9 +437,9 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                     const float wvs = S.wvf[s];
                     if (wvs > 0.0f) {
                         const float cvs = S.cvf[s];
-                        const float pl = vwl - cvs, ph = vwh - cvs;
-                        vtl = wvs * ((pl <= 0.f && ph >= 0.f) ? 0.f : fminf(fabsf(pl), fabsf(ph)));
-                        vth = wvs * fmaxf(fabsf(pl), fabsf(ph));
+                        const float pl = vwl - cvs, ph = vwh - cvs;   // pl <= ph
+                        vtl = wvs * fmaxf(fmaxf(pl, -ph), 0.f);
+                        vth = wvs * fmaxf(ph, -pl);
                     }
                 }
                 dl[r] = fmaf(fwd, sqrt_approx((qx.x + qy.x) + (qz.x + qt.x)), vtl);

@@ -111,6 +111,37 @@ class _Stager:
                 if ev is not None:
                     ev.synchronize()          # ring buffers are reused by the next call
 
+    def download(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        """dst (host, pageable, contiguous) <- src (device, contiguous, same bytes):
+        the copy engine fills the pinned slots in turn on the current stream and
+        host threads drain each into dst once its DMA has completed."""
+        with self.lock:
+            self._init()
+            sb = src.reshape(-1).view(torch.uint8)
+            db = dst.reshape(-1).view(torch.uint8)
+            n = sb.numel()
+            nch = -(-n // self.SLOT)
+            stream = torch.cuda.current_stream()
+            drains = [None] * self.SLOTS
+
+            def drain(slot, a, b, ev):
+                ev.synchronize()
+                db[a:b].copy_(self.ring[slot][:b - a])
+
+            for i in range(nch):
+                slot = i % self.SLOTS
+                if drains[slot] is not None:
+                    drains[slot].result()      # the slot's previous chunk is out
+                a = i * self.SLOT
+                b = min(n, a + self.SLOT)
+                self.ring[slot][:b - a].copy_(sb[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                drains[slot] = self.pool.submit(drain, slot, a, b, ev)
+            for f in drains:
+                if f is not None:
+                    f.result()
+
 
 _stager = _Stager()
 _STAGE_MIN_BYTES = 16 << 20
@@ -168,6 +199,21 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     if t.numel() == 0:
         return t.cpu().numpy()
     return host_ready(to_host_async(t))
+
+
+def download(t: torch.Tensor, dtype=None) -> np.ndarray:
+    """Device tensor -> new pageable numpy array (converted to `dtype` on the
+    device first, e.g. int32 -> int64 indices): large arrays through the pinned
+    staging ring, without allocating page-locked memory of their size."""
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    t = t.contiguous()
+    nbytes = t.numel() * t.element_size()
+    if t.device.type != "cuda" or nbytes < _STAGE_MIN_BYTES:
+        return t.cpu().numpy()
+    out = torch.empty(t.shape, dtype=t.dtype)
+    _stager.download(t, out)
+    return out.numpy()
 
 
 @dataclass

@@ -24,8 +24,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .engine import (DeviceField, DevicePoints, device, field_to_device, points_to_device,
-                     stream_ptr, to_dev)
+from .engine import (DeviceField, DevicePoints, device, download, field_to_device,
+                     points_to_device, stream_ptr, to_dev)
 from .model import DELTA, ClusterCenter, FieldSet, PointSet, Segmentation
 
 
@@ -254,11 +254,11 @@ def _split_trajectories(fid_of_slot, pslot, traj_id, t, feats):
     """Polylines / isolated points per time-ordered trajectory (postproc.py:152-160,
     176-191): ordering and run detection on the GPU, list building on the host."""
     order, starts, _ = split_trajectories_device(traj_id, t, pslot)
-    order_h = order.cpu().numpy().astype(np.int64)
-    st = starts.cpu().numpy().astype(np.int64)
-    if len(st) < 2:
+    if starts.numel() < 2:
         return
-    run_fid = fid_of_slot[pslot.cpu().numpy()[order_h[st[:-1]]]]
+    order_h = download(order, torch.int64)
+    st = download(starts, torch.int64)
+    run_fid = fid_of_slot[download(pslot[order[starts[:-1].long()].long()])]
     poly = np.diff(st) >= 2
     by_fid = np.argsort(run_fid, kind="stable")  # runs grouped by feature, order kept
     fs = run_fid[by_fid]
@@ -305,8 +305,7 @@ def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSe
     if pts.n:
         pl = to_dev(np.asarray(seg.point_labels), torch.int32, dev)
         pslot = feature_slots_device(pl, lut)
-        ps_h = pslot.cpu().numpy()
-        if np.any(ps_h < 0):
+        if bool((pslot < 0).any()):
             raise KeyError("point label without a merge_map entry")
         _split_trajectories(np.asarray(fids), pslot,
                             to_dev(np.asarray(points.traj_id, np.int64), torch.int64, dev), pts.t,
@@ -316,7 +315,7 @@ def build_features(seg: Segmentation, merge_map: Optional[dict], points: PointSe
         fslot = feature_slots_device(fl, lut)
         ncell = int(np.prod(fld.dims))
         seg_start, cells = voxel_csr_device(fslot, fld.nt, ncell, n_slots)
-        ss, ch = seg_start.cpu().numpy(), cells.cpu().numpy().astype(np.int64)
+        ss, ch = seg_start.cpu().numpy(), download(cells, torch.int64)
         for m in range(fld.nt):
             for s, f in enumerate(fids):
                 a, b = ss[m * n_slots + s], ss[m * n_slots + s + 1]

@@ -128,3 +128,24 @@ def test_segment_to_dir_from_files(tmp_path):
                 "converged", "iteration_seconds", "total_seconds", "voxel_timesteps_per_s", "passes"):
         assert key in rep, key
     assert len(rep["iteration_seconds"]) == rep["iterations_used"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,dtype", [(123_456_789, "int32"), (9_999_991, "float64"), (1000, "int32")])
+def test_staged_transfers_round_trip(n, dtype):
+    """Pageable arrays through the pinned staging ring (engine._Stager): upload
+    (to_dev) and download (engine.download, with on-device int32 -> int64
+    widening) reproduce the bytes, also for sizes that are not a multiple of the
+    32 MB slot and below the staging threshold."""
+    import torch
+    from paper_1903_12294_b200.engine import download, to_dev
+    rng = np.random.default_rng(n)
+    a = (rng.integers(-2**31, 2**31 - 1, n, dtype=np.int64).astype(np.int32) if dtype == "int32"
+         else rng.standard_normal(n))
+    d = to_dev(a, torch.int32 if dtype == "int32" else torch.float64)
+    assert np.array_equal(d.cpu().numpy(), a)
+    np.testing.assert_array_equal(download(d), a)
+    if dtype == "int32":
+        w = download(d, torch.int64)
+        assert w.dtype == np.int64
+        np.testing.assert_array_equal(w, a.astype(np.int64))
