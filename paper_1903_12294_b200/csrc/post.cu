@@ -823,11 +823,64 @@ __device__ __forceinline__ unsigned long long dkey(double x) {   // order-preser
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void k_tkeys(long long n, const double *t, unsigned long long *k, unsigned *v) {
+// time keys restricted to the bits that vary (the bits above and below are the
+// same in every key, so the order is kept and the radix sort takes fewer passes)
+__global__ void k_tkeys(long long n, const double *t, int lo, unsigned long long mask, unsigned long long *k,
+                        unsigned *v) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    k[i] = dkey(t[i]);
+    k[i] = (dkey(t[i]) >> lo) & mask;
     v[i] = (unsigned)i;
+}
+
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, (long long)__shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, (long long)__shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// One pass over the points: the trajectory id range, the bits in which the time
+// keys differ from the first one, and whether the records are already in
+// lexsort((t, traj_id)) order (then the stable sort is the identity).
+__global__ void k_tscan(long long n, const double *t, const long long *tid, unsigned long long *misc) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    unsigned long long span = 0;
+    int unsorted = 0;
+    const unsigned long long k0 = dkey(t[0]);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long id = tid[i];
+        const double ti = t[i];
+        lo = min(lo, id);
+        hi = max(hi, id);
+        span |= dkey(ti) ^ k0;
+        if (i > 0) {
+            const long long ip = tid[i - 1];
+            unsorted |= id < ip || (id == ip && ti < t[i - 1]);
+        }
+    }
+    lo = warp_min_ll(lo);
+    hi = warp_max_ll(hi);
+    span = __reduce_or_sync(0xffffffffu, (unsigned)span) | ((unsigned long long)__reduce_or_sync(
+                                                                 0xffffffffu, (unsigned)(span >> 32)) << 32);
+    unsorted = __reduce_or_sync(0xffffffffu, unsorted);
+    if ((threadIdx.x & 31) == 0) {
+        // signed -> order-preserving unsigned for the atomics
+        atomicMin(&misc[1], (unsigned long long)lo ^ 0x8000000000000000ull);
+        atomicMax(&misc[2], (unsigned long long)hi ^ 0x8000000000000000ull);
+        if (span) atomicOr(&misc[3], span);
+        if (unsorted) atomicOr(&misc[4], 1ull);
+    }
+}
+
+__global__ void k_iota_u32(long long n, unsigned *v) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (unsigned)i;
 }
 
 // over the sorted times: unique flags and the smallest positive gap between uniques
@@ -848,18 +901,6 @@ __global__ void k_trank(long long n, const int *urank_incl, const unsigned *perm
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
     trank[perm[i]] = (unsigned)(urank_incl[i] - 1);
-}
-
-__global__ void k_traj_minmax(long long n, const long long *tid, unsigned long long *mm) {
-    long long lo = LLONG_MAX, hi = LLONG_MIN;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
-        lo = min(lo, tid[i]);
-        hi = max(hi, tid[i]);
-    }
-    // signed -> order-preserving unsigned for the atomics
-    atomicMin(&mm[0], (unsigned long long)lo ^ 0x8000000000000000ull);
-    atomicMax(&mm[1], (unsigned long long)hi ^ 0x8000000000000000ull);
 }
 
 __global__ void k_lex_keys(long long n, const long long *tid, const unsigned *trank, long long tmin,
@@ -1297,7 +1338,7 @@ size_t mfseg_traj_split_workspace_size(int64_t n) {
     cv.take<int>(n);
     cv.take<int>(n);
     cv.take<unsigned>(n);
-    cv.take<unsigned long long>(4);
+    cv.take<unsigned long long>(6);
     const size_t rb = radix_tmp_bytes(n > 0 ? n : 1), sb = scan_tmp_bytes(n > 0 ? n : 1);
     cv.take<char>(rb > sb ? rb : sb);
     return cv.off + 256;
@@ -1327,30 +1368,42 @@ static int traj_split_impl(int64_t n, const int64_t *traj_id, const double *t,
     int *ex = cv.take<int>(n);
     int *incl = cv.take<int>(n);
     unsigned *trank = cv.take<unsigned>(n);
-    unsigned long long *misc = cv.take<unsigned long long>(4);   // min gap, traj min, traj max
+    unsigned long long *misc = cv.take<unsigned long long>(6);   // min gap, traj min / max, span, unsorted
     const size_t rb = radix_tmp_bytes(n), sb = scan_tmp_bytes(n);
     void *tmp = cv.take<char>(rb > sb ? rb : sb);
     const size_t tmpb = rb > sb ? rb : sb;
     const unsigned g = (unsigned)((n + 255) / 256);
-    const unsigned long long init[3] = {0x7FF0000000000000ull, ~0ull, 0ull};   // +inf, min, max
+    const unsigned long long init[5] = {0x7FF0000000000000ull, ~0ull, 0ull, 0ull, 0ull};   // +inf, min, max
     MFSEG_CUDA(cudaMemcpyAsync(misc, init, sizeof init, cudaMemcpyHostToDevice, st));
+    ::mfseg::count_launch();
+    k_tscan<<<148 * 4, 256, 0, st>>>(n, t, (const long long *)traj_id, misc);
+    MFSEG_LAUNCH("k_tscan");
+    unsigned long long h[5];
+    MFSEG_CUDA(cudaMemcpyAsync(h, misc, sizeof h, cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaStreamSynchronize(st));
+    const bool in_order = h[4] == 0;
+    int klo = 0, kbits = 1;
+    if (h[3]) {
+        klo = __builtin_ctzll(h[3]);
+        kbits = 64 - __builtin_clzll(h[3]) - klo;
+    }
+    const unsigned long long kmask = kbits >= 64 ? ~0ull : ((1ull << kbits) - 1);
     // 1. sorted unique times -> stride and per-point t ranks
     ::mfseg::count_launch();
-    k_tkeys<<<g, 256, 0, st>>>(n, t, k0, v0);
-    MFSEG_TRY(radix_sort_pairs64(k0, v0, k1, v1, n, 64, tmp, tmpb, st));
+    k_tkeys<<<g, 256, 0, st>>>(n, t, klo, kmask, k0, v0);
+    MFSEG_TRY(radix_sort_pairs64(k0, v0, k1, v1, n, kbits, tmp, tmpb, st));
     ::mfseg::count_launch();
     k_tunique<<<g, 256, 0, st>>>(n, k1, v1, t, flag, misc);
     MFSEG_TRY(scan_exclusive_i32(flag, ex, n, tmp, tmpb, st));
     ::mfseg::count_launch();
     k_inclusive_from_exclusive<<<g, 256, 0, st>>>(n, flag, ex, incl);
-    ::mfseg::count_launch();
-    k_trank<<<g, 256, 0, st>>>(n, incl, v1, trank);
-    ::mfseg::count_launch();
-    k_traj_minmax<<<148 * 4, 256, 0, st>>>(n, (const long long *)traj_id, misc + 1);
+    if (!in_order) {
+        ::mfseg::count_launch();
+        k_trank<<<g, 256, 0, st>>>(n, incl, v1, trank);
+    }
     MFSEG_LAUNCH("traj_split ranks");
-    unsigned long long h[3];
     int nu = 0;
-    MFSEG_CUDA(cudaMemcpyAsync(h, misc, sizeof h, cudaMemcpyDeviceToHost, st));
+    MFSEG_CUDA(cudaMemcpyAsync(h, misc, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaMemcpyAsync(&nu, incl + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
     MFSEG_CUDA(cudaStreamSynchronize(st));
     double stride;
@@ -1363,8 +1416,13 @@ static int traj_split_impl(int64_t n, const int64_t *traj_id, const double *t,
     while ((1ll << tbits) < nu) ++tbits;
     int rbits = 0;
     while (rbits < 64 && (range >> rbits) != 0) ++rbits;
-    // 2. lexsort((t, traj_id)): one stable sort of (traj - min, t rank)
-    if (rbits + tbits <= 64) {
+    // 2. lexsort((t, traj_id)): one stable sort of (traj - min, t rank); the
+    // identity when the records are in that order already
+    if (in_order) {
+        ::mfseg::count_launch();
+        k_iota_u32<<<g, 256, 0, st>>>(n, v1);
+        MFSEG_LAUNCH("k_iota_u32");
+    } else if (rbits + tbits <= 64) {
         ::mfseg::count_launch();
         k_lex_keys<<<g, 256, 0, st>>>(n, (const long long *)traj_id, trank, tmin, tbits, k0, v0);
         MFSEG_TRY(radix_sort_pairs64(k0, v0, k1, v1, n, rbits + tbits > 0 ? rbits + tbits : 1, tmp,

@@ -581,19 +581,26 @@ def test_reuse_of_unchanged_blocks_is_exact(weights):
     np.testing.assert_array_equal(np.asarray(sa.pval), np.asarray(sb.pval))
 
 
-@pytest.mark.parametrize("seed,n,n_traj,single_time", [(0, 5000, 300, False), (1, 200000, 7000, False),
-                                                       (2, 1000, 50, True)])
-def test_traj_split_matches_numpy(seed, n, n_traj, single_time):
+@pytest.mark.parametrize("seed,n,n_traj,single_time,t0,presorted",
+                         [(0, 5000, 300, False, 0.0, False), (1, 200000, 7000, False, 0.0, False),
+                          (2, 1000, 50, True, 0.0, False), (3, 100000, 3000, False, -7.3, True),
+                          (4, 50000, 400, False, 1.7e9, True), (5, 50000, 400, False, -3.0, False)])
+def test_traj_split_matches_numpy(seed, n, n_traj, single_time, t0, presorted):
     """mfseg_traj_split vs the reference's lexsort + run rules (postproc.py:152-160,
     176-191): negative and sparse trajectory ids, repeated times, time gaps,
-    label changes; a single unique time (stride = inf)."""
+    label changes; a single unique time (stride = inf); times of both signs and
+    epoch-scale times (the time keys are sorted on their varying bits only);
+    records already in (trajectory, time) order (the sort is skipped)."""
     from paper_1903_12294_b200.postproc import split_trajectories_device
     rng = np.random.default_rng(seed)
     tid = rng.choice(np.arange(-50, 10 * n_traj, 10), n_traj, replace=False)[rng.integers(0, n_traj, n)]
     times = np.array([0.0]) if single_time else np.sort(rng.choice(np.arange(0, 60) * 0.25, 40,
                                                                    replace=False))
-    t = times[rng.integers(0, len(times), n)]
+    t = times[rng.integers(0, len(times), n)] + t0
     lab = rng.integers(0, 4, n).astype(np.int32)
+    if presorted:
+        o = np.lexsort((t, tid))
+        tid, t, lab = tid[o], t[o], lab[o]
     order, starts, stride = split_trajectories_device(torch.as_tensor(tid), torch.as_tensor(t).cuda(),
                                                       torch.as_tensor(lab))
     # numpy restatement of the reference
