@@ -72,15 +72,71 @@ __global__ void k_uf_init(int n, int *parent) {
     if (i < n) parent[i] = i;
 }
 
-// one warp per row i, lanes sweep j > i
-__global__ void k_merge_pairs(int n, const double *pc, const double *fc, double eps, int *parent) {
-    long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
+// p_c sort keys (order-preserving bits; every NaN last) and rows
+__global__ void k_merge_pkeys(int n, const double *pc, unsigned long long *k, unsigned *v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double p = pc[i];
+    const unsigned long long b = (unsigned long long)__double_as_longlong(p);
+    k[i] = isnan(p) ? ~0ull : ((b >> 63) ? ~b : (b | 0x8000000000000000ull));
+    v[i] = (unsigned)i;
+}
+
+// The rows sorted by p_c: the rows whose p_c matches row i's form a contiguous
+// run around it (2|a - b| / (|a| + |b| + DELTA) grows as b moves away from a on
+// either side; the NaNs, which only match each other, come last).  One warp per
+// sorted position i sweeps the positions after it until a p_c is beyond the
+// threshold with a 2^-30 relative slack (then so is every later one, and the
+// exact test, decided within 2^-50 of the threshold, fails for them too).  Each
+// matching pair is a union-find edge; the components (and their smallest rows)
+// are those of the all-pairs sweep.
+__global__ void k_merge_pairs_sorted(int n, const unsigned *srow, const double *pc, const double *fc,
+                                     double eps, int *parent) {
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (w >= n) return;
-    int i = (int)w;
-    double pi = pc[i], fi = fc[i];
-    for (int j = i + 1 + lane; j < n; j += 32)
-        if (values_match(pi, pc[j], eps) && values_match(fi, fc[j], eps)) uf_union(parent, i, j);
+    const int i = (int)w;
+    const int ri = (int)srow[i];
+    const double pi = pc[ri], fi = fc[ri];
+    const bool pn = isnan(pi);
+    for (int j0 = i + 1; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        bool beyond = j >= n;
+        if (!beyond) {
+            const int rj = (int)srow[j];
+            const double pj = pc[rj];
+            if (!pn) {
+                const double r = DMUL(2.0, fabs(DSUB(pi, pj))), s = DADD(DADD(fabs(pi), fabs(pj)), DELTA);
+                beyond = isnan(pj) || r > eps * s * (1.0 + 0x1.0p-30);
+            }
+            if (!beyond && values_match(pi, pj, eps) && values_match(fi, fc[rj], eps)) {
+                // cached (possibly stale) parents: a stale parent is still an ancestor,
+                // so equal answers prove one component; otherwise the CAS-based union
+                // resolves the roots exactly
+                int a = ri, b = rj, pa, pb;
+                while ((pa = __ldca(parent + a)) != a) a = pa;
+                while ((pb = __ldca(parent + b)) != b) b = pb;
+                if (a != b) uf_union(parent, a, b);
+            }
+        }
+        if (__any_sync(0xffffffffu, beyond)) break;
+    }
+}
+
+// the members' records in group order (the sequential sums below read them
+// contiguously): counts (as bits), loc[4], p_c, f_c
+__global__ void k_merge_gather(int n, const unsigned *members, const long long *np_, const long long *nf_,
+                               const double *loc, const double *pc, const double *fc, double *rec) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int r = (int)members[q];
+    double *o = rec + (size_t)q * 8;
+    o[0] = __longlong_as_double(np_[r]);
+    o[1] = __longlong_as_double(nf_[r]);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) o[2 + d] = loc[(size_t)d * n + r];
+    o[6] = pc[r];
+    o[7] = fc[r];
 }
 
 __global__ void k_uf_flatten(int n, int *parent, const int *ids, int *rep_row, int *rep_id,
@@ -102,75 +158,73 @@ struct MergeOut {
 };
 
 // One warp per group (launched per sorted position; only a group's first
-// position works), members ascending (stable sort by root row).  The sums keep
-// the reference's sequential order; the lanes load 32 members' records at a time
-// (the loads overlap) and every lane replays the sequential sums over them from
-// shuffles, so the one long chain of a big group is no longer load-latency bound.
-__global__ void k_merge_groups(int n, const unsigned *skeys, const unsigned *members,
-                               const int *is_root, const int *group_of_root, const int *ids,
-                               const double *loc, const double *pc, const double *fc,
-                               const long long *np_, const long long *nf_, MergeOut o, int G,
-                               int neumaier) {
+// position works), members ascending (stable sort by root row), records
+// gathered contiguously (k_merge_gather).  The sums keep the reference's
+// sequential order.  The lanes load a batch of 32 members' records into shared
+// memory (the next batch's loads are in flight meanwhile) and split the chains:
+// lanes 0-3 the count-weighted location sums, lane 4 the point-value sum, lane
+// 5 the field-value sum (Neumaier steps as CPython >= 3.12's sum of floats when
+// `neumaier`, else plain), every lane the counts.
+constexpr int MG_WARPS = 8;
+__global__ void __launch_bounds__(32 * MG_WARPS) k_merge_groups(int n, const unsigned *skeys, const int *group_of_root,
+                                                               const int *ids, const double *rec, MergeOut o, int G,
+                                                               int neumaier) {
+    __shared__ double buf[MG_WARPS][32][9];   // 9: no bank conflicts on the column reads
     const long long wid = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (wid >= n) return;
     const int i = (int)wid;                        // position in the sorted order
     if (i > 0 && skeys[i - 1] == skeys[i]) return;   // not the first member of its group
     const unsigned root = skeys[i];
     const int g = group_of_root[root];
     long long n_p = 0, n_f = 0, n_tot = 0;
-    double ls[4] = {0.0, 0.0, 0.0, 0.0};
-    double pf = 0.0, pcmp = 0.0, ff = 0.0, fcmp = 0.0;   // compensation used when neumaier
+    double acc = 0.0, cmp = 0.0;   // lane 0-3: loc sum d; 4: p sum; 5: f sum
     const double nan = __longlong_as_double(0x7ff8000000000000ll);
-    for (int q0 = i; q0 < n; q0 += 32) {
-        const int q = q0 + lane;
-        const bool in = q < n && skeys[q] == root;
-        long long ma = 0, mb = 0;
-        double ml[4] = {0.0, 0.0, 0.0, 0.0}, mp = nan, mf = nan;
-        if (in) {
-            const int r = (int)members[q];
-            ma = np_[r];
-            mb = nf_[r];
+    const int col = lane < 6 ? 2 + lane : 2;       // record column of this lane's chain
+    double nxt[8];
+    bool nin = i + lane < n && skeys[i + lane] == root;
 #pragma unroll
-            for (int d = 0; d < 4; ++d) ml[d] = loc[(size_t)d * n + r];
-            mp = pc[r];
-            mf = fc[r];
+    for (int c = 0; c < 8; ++c) nxt[c] = nin ? rec[(size_t)(i + lane) * 8 + c] : 0.0;
+    for (int q0 = i; q0 < n; q0 += 32) {
+        const int cnt = __popc(__ballot_sync(0xffffffffu, nin));   // lanes 0 .. cnt-1 (contiguous)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) buf[w][lane][c] = nxt[c];
+        __syncwarp();
+        const bool more = cnt == 32 && q0 + 32 < n;
+        if (more) {   // prefetch the next batch
+            const int q = q0 + 32 + lane;
+            nin = q < n && skeys[q] == root;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) nxt[c] = nin ? rec[(size_t)q * 8 + c] : 0.0;
         }
-        const int cnt = __popc(__ballot_sync(0xffffffffu, in));   // lanes 0 .. cnt-1 (contiguous)
+        // branch-free steps (the chains only depend on acc / cmp: the loads of the
+        // next members are scheduled ahead)
+        const bool comp = neumaier && (lane == 4 || lane == 5);
+#pragma unroll 4
         for (int t = 0; t < cnt; ++t) {
-            const long long a = __shfl_sync(0xffffffffu, ma, t), b = __shfl_sync(0xffffffffu, mb, t);
+            const long long a = __double_as_longlong(buf[w][t][0]), b = __double_as_longlong(buf[w][t][1]);
             const long long tt = a + b;
             n_p += a;
             n_f += b;
             n_tot += tt;
-            const double dt = (double)tt;
-#pragma unroll
-            for (int d = 0; d < 4; ++d) ls[d] = DADD(ls[d], DMUL(__shfl_sync(0xffffffffu, ml[d], t), dt));
-            const double pv = __shfl_sync(0xffffffffu, mp, t), fv = __shfl_sync(0xffffffffu, mf, t);
-            if (!isnan(pv)) {   // Neumaier step (CPython >= 3.12 sum of floats), else plain
-                const double x = DMUL(pv, (double)a);
-                const double t2 = DADD(pf, x);
-                if (neumaier)
-                    pcmp = fabs(pf) >= fabs(x) ? DADD(pcmp, DADD(DSUB(pf, t2), x))
-                                               : DADD(pcmp, DADD(DSUB(x, t2), pf));
-                pf = t2;
-            }
-            if (!isnan(fv)) {
-                const double x = DMUL(fv, (double)b);
-                const double t2 = DADD(ff, x);
-                if (neumaier)
-                    fcmp = fabs(ff) >= fabs(x) ? DADD(fcmp, DADD(DSUB(ff, t2), x))
-                                               : DADD(fcmp, DADD(DSUB(x, t2), ff));
-                ff = t2;
-            }
+            const double v = buf[w][t][col];
+            const double x = DMUL(v, (double)(lane < 4 ? tt : lane == 4 ? a : b));
+            const double t2 = DADD(acc, x);
+            const bool skip = lane >= 4 && isnan(v);   // a member without the value kind
+            if (comp && !skip)
+                cmp = fabs(acc) >= fabs(x) ? DADD(cmp, DADD(DSUB(acc, t2), x))
+                                           : DADD(cmp, DADD(DSUB(x, t2), acc));
+            acc = skip ? acc : t2;
         }
-        if (cnt < 32) break;
+        __syncwarp();
+        if (!more) break;
     }
+    if (lane == 4 || lane == 5)
+        if (cmp != 0.0 && isfinite(cmp)) acc = DADD(acc, cmp);
+    const double pf = __shfl_sync(0xffffffffu, acc, 4), ff = __shfl_sync(0xffffffffu, acc, 5);
+    if (lane < 4) o.m_loc[(size_t)lane * G + g] = DDIV(acc, (double)n_tot);
     if (lane != 0) return;
-    if (pcmp != 0.0 && isfinite(pcmp)) pf = DADD(pf, pcmp);
-    if (fcmp != 0.0 && isfinite(fcmp)) ff = DADD(ff, fcmp);
     o.m_ids[g] = ids[root];
-    for (int d = 0; d < 4; ++d) o.m_loc[(size_t)d * G + g] = DDIV(ls[d], (double)n_tot);
     o.m_p[g] = n_p > 0 ? DDIV(pf, (double)n_p) : nan;
     o.m_f[g] = n_f > 0 ? DDIV(ff, (double)n_f) : nan;
     o.m_np[g] = n_p;
@@ -957,6 +1011,11 @@ size_t mfseg_merge_workspace_size(int32_t n) {
     cv.take<int>(n + 1);      // group_of_root
     cv.take<char>(radix_tmp_bytes(n > 0 ? n : 1));
     cv.take<char>(scan_tmp_bytes(n + 1));
+    cv.take<unsigned long long>(n);   // p keys
+    cv.take<unsigned long long>(n);   // sorted p keys
+    cv.take<unsigned>(n);             // rows
+    cv.take<unsigned>(n);             // rows by p
+    cv.take<double>(8ll * n);         // member records in group order
     return cv.off + 256;
 }
 
@@ -987,12 +1046,18 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
     void *rtmp = cv.take<char>(rb);
     size_t sb = scan_tmp_bytes(n + 1);
     void *stmp = cv.take<char>(sb);
+    unsigned long long *pk = cv.take<unsigned long long>(n), *pks = cv.take<unsigned long long>(n);
+    unsigned *prow = cv.take<unsigned>(n), *srow = cv.take<unsigned>(n);
+    double *rec = cv.take<double>(8ll * n);
     unsigned g = (unsigned)((n + 255) / 256);
     ::mfseg::count_launch();
     k_uf_init<<<g, 256, 0, st>>>(n, parent);
     ::mfseg::count_launch();
-    k_merge_pairs<<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, st>>>(n, p_c, f_c, eps_m,
-                                                                               parent);
+    k_merge_pkeys<<<g, 256, 0, st>>>(n, p_c, pk, prow);
+    MFSEG_TRY(radix_sort_pairs64(pk, prow, pks, srow, n, 64, rtmp, rb, st));
+    ::mfseg::count_launch();
+    k_merge_pairs_sorted<<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, st>>>(n, srow, p_c, f_c,
+                                                                                      eps_m, parent);
     MFSEG_CUDA(cudaMemsetAsync(is_root, 0, sizeof(int) * (n + 1), st));
     ::mfseg::count_launch();
     k_uf_flatten<<<g, 256, 0, st>>>(n, parent, ids, rep_row, rep, keys, vals, is_root);
@@ -1004,10 +1069,11 @@ int mfseg_merge(int32_t n, const int32_t *ids, const double *loc, const double *
     MFSEG_CUDA(cudaStreamSynchronize(st));
     MergeOut o{m_ids, m_loc, m_p, m_f, (long long *)m_np, (long long *)m_nf};
     ::mfseg::count_launch();
-    k_merge_groups<<<(unsigned)(((long long)n * 32 + 255) / 256), 256, 0, st>>>(
-        n, skeys, members, is_root, group_of_root, ids, loc, p_c,
-                                      f_c, (const long long *)n_points,
-                                      (const long long *)n_fields, o, G, neumaier);
+    k_merge_gather<<<g, 256, 0, st>>>(n, members, (const long long *)n_points, (const long long *)n_fields, loc,
+                                      p_c, f_c, rec);
+    ::mfseg::count_launch();
+    k_merge_groups<<<(unsigned)(((long long)n + MG_WARPS - 1) / MG_WARPS), 32 * MG_WARPS, 0, st>>>(
+        n, skeys, group_of_root, ids, rec, o, G, neumaier);
     MFSEG_LAUNCH("k_merge_groups");
     if (n_merged_host) *n_merged_host = G;
     return 0;
