@@ -705,12 +705,14 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             dst = S.yf[i];
         } else if (tid < OT) {
             const int i = tid - OZ;
-            cv = cell_coord(a.oz, a.sz, a.z0 + Z.start + min(i, Z.len - 1));
+            cv = a.swap_zt ? a.times[Z.start + min(i, Z.len - 1)]
+                           : cell_coord(a.oz, a.sz, a.z0 + Z.start + min(i, Z.len - 1));
             S.z[i] = cv;
             dst = S.zf[i];
         } else {
             const int i = tid - OT;
-            cv = a.times[Tm.start + min(i, Tm.len - 1)];
+            cv = a.swap_zt ? cell_coord(a.oz, a.sz, a.z0 + Tm.start + min(i, Tm.len - 1))
+                           : a.times[Tm.start + min(i, Tm.len - 1)];
             S.t[i] = cv;
             dst = S.tf[i];
         }
@@ -739,7 +741,8 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         unsigned box = 0;
         if (have) {
             id = a.g.cand_ids[ci];
-            const int4 b0 = a.g.vbox[2 * id], b1 = a.g.vbox[2 * id + 1];
+            const int4 b0 = a.g.vbox[2 * id], br = a.g.vbox[2 * id + 1];
+            const int4 b1 = a.swap_zt ? make_int4(br.z, br.w, br.x, br.y) : br;   // kernel (z, t) ranges
             const int xa = max(b0.x - X.start, 0), xb = min(b0.y - X.start, X.len - 1);
             const int ya = max(b0.z - Y.start, 0), yb = min(b0.w - Y.start, Y.len - 1);
             const int za = max(b1.x - Z.start, 0), zb = min(b1.y - Z.start, Z.len - 1);
@@ -847,12 +850,12 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             else if (ax == 1)
                 table_row<BY, GY>(S.tab[p] + BX, S.qmm[p] + QY, S.y, cc, 1.0, false, (b >> 8) & 15u,
                                   (b >> 12) & 15u, Y.len);
-            else if (ax == 2)
-                table_row<BZ, GZ>(S.tab[p] + OZ, S.qmm[p] + QZ, S.z, cc, 1.0, false, (b >> 16) & 15u,
-                                  (b >> 20) & 15u, Z.len);
+            else if (ax == 2)   // (the time axis carries the c_f scale)
+                table_row<BZ, GZ>(S.tab[p] + OZ, S.qmm[p] + QZ, S.z, cc, a.cf, a.swap_zt != 0,
+                                  (b >> 16) & 15u, (b >> 20) & 15u, Z.len);
             else
-                table_row<BT, GT>(S.tab[p] + OT, S.qmm[p] + QT, S.t, cc, a.cf, true, (b >> 24) & 3u,
-                                  (b >> 26) & 3u, Tm.len);
+                table_row<BT, GT>(S.tab[p] + OT, S.qmm[p] + QT, S.t, cc, a.cf, a.swap_zt == 0,
+                                  (b >> 24) & 3u, (b >> 26) & 3u, Tm.len);
         }
         if (a.accumulate) {
             for (int e = tid; e < cnt * HW; e += NT) (&S.hist[0][0])[e] = 0u;
@@ -988,7 +991,8 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 atomicAdd(dst + 13, (unsigned long long)n);
                 continue;
             }
-            atomic_add_fix(dst + (wd < 4 ? 2 * wd : 10), (unsigned long long)acc, (long long)(acc >> 64));
+            const int word = wd < 2 ? 2 * wd : wd < 4 ? 2 * (a.swap_zt ? 5 - wd : wd) : 10;   // real axis
+            atomic_add_fix(dst + word, (unsigned long long)acc, (long long)(acc >> 64));
         }
     }
     if (ovf_local) *a.overflow = 1;

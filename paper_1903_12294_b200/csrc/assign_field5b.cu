@@ -105,8 +105,12 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
         // sample coordinates (reference formula); index clamped for dead lanes
         const double px = cell_coord(a.ox, a.sx, a.x0 + it.x0 + min(lxr, ex - 1));
         const double py = cell_coord(a.oy, a.sy, a.y0 + it.y0 + min(lyr, ey - 1));
-        if (lane < 4) Q.pz[lane] = cell_coord(a.oz, a.sz, a.z0 + gz0 + min(lane, ez - 1));
-        else if (lane < 6) Q.pt[lane - 4] = a.times[gt0 + min(lane - 4, et - 1)];
+        if (lane < 4)
+            Q.pz[lane] = a.swap_zt ? a.times[gz0 + min(lane, ez - 1)]
+                                   : cell_coord(a.oz, a.sz, a.z0 + gz0 + min(lane, ez - 1));
+        else if (lane < 6)
+            Q.pt[lane - 4] = a.swap_zt ? cell_coord(a.oz, a.sz, a.z0 + gt0 + min(lane - 4, et - 1))
+                                       : a.times[gt0 + min(lane - 4, et - 1)];
         const double *pz = Q.pz, *pt = Q.pt;
         // stage the kept candidates; largest |cv| among them (certification's W)
         float cvmax = 0.f;
@@ -125,7 +129,8 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             Q.c[2][lane] = a.c.z[id];
             Q.c[3][lane] = a.c.t[id];
             Q.b0[lane] = a.g.vbox[2 * id];
-            Q.b1[lane] = a.g.vbox[2 * id + 1];
+            const int4 br = a.g.vbox[2 * id + 1];
+            Q.b1[lane] = a.swap_zt ? make_int4(br.z, br.w, br.x, br.y) : br;   // kernel (z, t) ranges
             if (USEVAL && has) cvmax = fabsf((float)cv);
         }
         __syncwarp();
@@ -156,7 +161,8 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             for (int q = 0; q < 4; ++q) {
                 tz[q] = INF_F;
                 if (gz0 + q >= bb.x && gz0 + q <= bb.y) {
-                    const double d = DSUB(cz, pz[q]);
+                    double d = DSUB(cz, pz[q]);
+                    if (a.swap_zt) d = DMUL(a.cf, d);   // the kernel's z axis is time
                     tz[q] = to_f(DMUL(d, d));
                 }
             }
@@ -164,7 +170,8 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             for (int r = 0; r < 2; ++r) {
                 tt[r] = INF_F;
                 if (gt0 + r >= bb.z && gt0 + r <= bb.w) {
-                    const double d = DMUL(a.cf, DSUB(ct, pt[r]));
+                    double d = DSUB(ct, pt[r]);
+                    if (!a.swap_zt) d = DMUL(a.cf, d);
                     tt[r] = to_f(DMUL(d, d));
                 }
             }
@@ -225,8 +232,10 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
                           gz <= bb.y && gt >= bb.z && gt <= bb.w))
                         continue;
                     const double cx = Q.c[0][j], cy = Q.c[1][j], cz = Q.c[2][j], ct = Q.c[3][j];
-                    const double dx = DSUB(cx, px), dy = DSUB(cy, py), dz = DSUB(cz, pzk);
-                    const double dt = DMUL(a.cf, DSUB(ct, ptk));
+                    // (real z and t differences: the kernel's z axis is time when swapped)
+                    const double dkz = DSUB(cz, pzk), dkt = DSUB(ct, ptk);
+                    const double dx = DSUB(cx, px), dy = DSUB(cy, py), dz = a.swap_zt ? dkt : dkz;
+                    const double dt = DMUL(a.cf, a.swap_zt ? dkz : dkt);
                     // fp32 screen value of this pair (prune outside the margin)
                     const float sq = ((to_f(DMUL(dx, dx)) + to_f(DMUL(dy, dy))) + to_f(DMUL(dz, dz))) +
                                      to_f(DMUL(dt, dt));
@@ -337,7 +346,8 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
                 }
                 unsigned long long *dst = a.acc + (size_t)Q.id[L] * MFSEG_ACC_WORDS;
                 if (lane == 1) d2fix(vs, lo, hi, &ovf_local);
-                if (gi == 0 || lane == 1) atomic_add_fix(dst + (lane == 1 ? ACC_FV : 2 * grp), lo, hi);
+                const int word = lane == 1 ? ACC_FV : 2 * (a.swap_zt && grp >= 2 ? 5 - grp : grp);   // real axis
+                if (gi == 0 || lane == 1) atomic_add_fix(dst + word, lo, hi);
                 if (lane == 2) atomicAdd(dst + ACC_NF, (unsigned long long)((st & 0xFFFFu) + (st >> 16)));
             }
         }

@@ -22,6 +22,13 @@ struct FieldArgs {
     int x0, y0, z0;       // global cell index of the field's first cell (spatial slabs)
     int seeds_fast;       // initial pass: blocks whose axis tiles are all interior (AxisTile.pad)
                           // take their own bin's seed (see run.cu seeds_fast_ok)
+    // Thin fields (nz = 1, k_z = 1): the kernels' z axis runs over the timesteps and
+    // their t axis over the single z plane, so blocks and bricks fill along time
+    // (the layouts coincide: plane stride = volume stride).  zt then holds time
+    // tiles and tt the z tile, nz / nt / kz / kt and the centres' z / t pointers are
+    // passed swapped; coordinates, the c_f scale, the validity boxes, the exact
+    // metric and the accumulator words follow the real axes (run.cu plan_pass).
+    int swap_zt;
     const double *times;
     const double *values;
     const AxisTile *xt, *yt, *zt;

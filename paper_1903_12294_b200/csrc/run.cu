@@ -1,5 +1,6 @@
 // Host-side runtime of the segmentation core: workspace plan, point binning,
 // field tiling, the pass loop of engine.run (engine.py:323-381) and the C ABI.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -273,6 +274,8 @@ struct Plan {
     mfseg_points pts;
     int K;                          // centres
     int NB;                         // bins = k1*k2*k3*k4
+    int swap_zt;                    // thin field: the field kernels' z axis is time (FieldArgs)
+    long long nbricks;              // brick records allocated (64 per block)
     int seeds_fast;                 // the initial pass may label interior blocks / chunks by
                                     // their own seed (seeds_fast_ok)
     long long nf, np;
@@ -440,15 +443,20 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         P.ntz = (int)axis_tile_count(P.f.nz, P.f.origin[2], P.f.spacing[2], P.f.offset[2], P.p.mins[2], P.p.C[2],
                                      P.p.k[2], TZ);
     }
+    // thin fields (one z plane and one z bin): blocks and bricks run along time
+    P.swap_zt = P.nf > 0 && P.f.nz == 1 && P.f.nt > 1 && P.p.k[2] == 1 &&
+                !(debug_options().flags & MFSEG_DEBUG_NO_ZT_SWAP);
     P.xt = cv.take<AxisTile>(P.ntx);
     P.yt = cv.take<AxisTile>(P.nty);
-    P.zt = cv.take<AxisTile>(P.ntz);
+    P.zt = cv.take<AxisTile>(std::max(P.ntz, P.f.nt > 0 ? P.f.nt : 1));   // z tiles, or time tiles
     P.tbin = cv.take<int>(P.f.nt > 0 ? P.f.nt : 1);
     P.tt = cv.take<AxisTile>(P.f.nt > 0 ? P.f.nt : 1);
-    P.brange = cv.take<float2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
-    P.bsum = cv.take<ulonglong2>(64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1));
+    // blocks <= ntx nty ntz nt either way (swapped: ntz = 1 z tile, <= nt time tiles)
+    P.nbricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
+    P.brange = cv.take<float2>(P.nbricks);
+    P.bsum = cv.take<ulonglong2>(P.nbricks);
     {
-        const long long bricks = 64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1);
+        const long long bricks = P.nbricks;
         // every live brick can be queued (96 B per brick of <= 256 samples): a full
         // queue would send the rest to the per-sample exact path (k_deferred), 10-100x
         // slower.  Live bricks per block are a product over the axes (thin grids,
@@ -612,8 +620,7 @@ int plan_prepare_impl(Plan &P) {
                                    cudaMemcpyHostToDevice, st));
         MFSEG_CUDA(cudaMemcpyAsync(P.yt, yt.data(), sizeof(AxisTile) * yt.size(),
                                    cudaMemcpyHostToDevice, st));
-        MFSEG_CUDA(cudaMemcpyAsync(P.zt, zt.data(), sizeof(AxisTile) * zt.size(),
-                                   cudaMemcpyHostToDevice, st));
+
         // time tiles: runs of <= 4 timesteps with the same t-bin (host copy of the
         // times; bin_coord on the host rounds exactly like the device)
         std::vector<double> th(P.f.nt);
@@ -631,6 +638,26 @@ int plan_prepare_impl(Plan &P) {
             m0 = m1;
         }
         P.ntt = (int)tts.size();
+        if (P.swap_zt) {
+            // the kernels' z axis runs over time: runs of <= TZ timesteps with the same
+            // t-bin; their t axis over the single z tile
+            std::vector<AxisTile> zts;
+            for (int m0 = 0; m0 < P.f.nt;) {
+                const int b = bin_coord(th[m0], p.mins[3], p.C[3], p.k[3]);
+                int m1 = m0;
+                while (m1 < P.f.nt && m1 - m0 < TZ && bin_coord(th[m1], p.mins[3], p.C[3], p.k[3]) == b) ++m1;
+                bool ok = true;
+                for (int m = m0; ok && m < m1; ++m) ok = interior_coord(th[m], p.mins[3], p.C[3], p.k[3]);
+                zts.push_back(AxisTile{m0, m1 - m0, b, ok ? 1 : 0});
+                m0 = m1;
+            }
+            tts = zt;
+            zt = zts;
+            P.ntz = (int)zt.size();
+            P.ntt = (int)tts.size();
+        }
+        MFSEG_CUDA(cudaMemcpyAsync(P.zt, zt.data(), sizeof(AxisTile) * zt.size(),
+                                   cudaMemcpyHostToDevice, st));
         for (int m = 0; m < P.f.nt; ++m) {
             if (!std::isfinite(th[m])) {
                 set_error("non-finite field time");
@@ -659,8 +686,9 @@ int plan_prepare_impl(Plan &P) {
             memset(&va, 0, sizeof va);
             va.nx = P.f.nx;
             va.ny = P.f.ny;
-            va.nz = P.f.nz;
-            va.nt = P.f.nt;
+            va.nz = P.swap_zt ? P.f.nt : P.f.nz;   // (swapped: the planes are the timesteps)
+            va.nt = P.swap_zt ? 1 : P.f.nt;
+            va.swap_zt = P.swap_zt;
             va.values = P.f.values;
             va.xt = P.xt;
             va.yt = P.yt;
@@ -676,9 +704,7 @@ int plan_prepare_impl(Plan &P) {
             va.absmax = P.absmax;
             MFSEG_TRY(launch_brick_pre(va, st));
         }
-        if (P.bslot)
-            MFSEG_CUDA(cudaMemsetAsync(P.bslot, 255,
-                                       64ll * P.ntx * P.nty * P.ntz * (P.f.nt > 0 ? P.f.nt : 1), st));
+        if (P.bslot) MFSEG_CUDA(cudaMemsetAsync(P.bslot, 255, P.nbricks, st));
     }
     long long n = P.np;
     if (n > 0) {
@@ -863,8 +889,9 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         memset(&a, 0, sizeof a);
         a.nx = P.f.nx;
         a.ny = P.f.ny;
-        a.nz = P.f.nz;
-        a.nt = P.f.nt;
+        a.nz = P.swap_zt ? P.f.nt : P.f.nz;   // (swapped: the planes are the timesteps)
+        a.nt = P.swap_zt ? 1 : P.f.nt;
+        a.swap_zt = P.swap_zt;
         a.ox = P.f.origin[0];
         a.oy = P.f.origin[1];
         a.oz = P.f.origin[2];
@@ -889,12 +916,13 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.ntt = P.ntt;
         a.kx = p.k[0];
         a.ky = p.k[1];
-        a.kz = p.k[2];
-        a.kt = p.k[3];
+        a.kz = P.swap_zt ? p.k[3] : p.k[2];
+        a.kt = P.swap_zt ? p.k[2] : p.k[3];
         a.cf = p.c_f;
         a.wd = wd;
         a.wv = wf;
         a.c = cv;
+        if (P.swap_zt) std::swap(a.c.z, a.c.t);   // the kernels' z axis is time
         a.cval = c.fval;
         a.chas = c.has_f;
         a.g = P.g;

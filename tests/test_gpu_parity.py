@@ -554,6 +554,35 @@ def test_initial_pass_shortcut_is_exact(c_f, k, iters):
     np.testing.assert_array_equal(np.asarray(sa.pval), np.asarray(sb.pval))
 
 
+@pytest.mark.parametrize("c_f,nz,kz", [(1.0, 1, 1), (0.45, 1, 1), (2.0, 1, 1), (1.0, 1, 2)])
+def test_thin_field_time_blocks_are_exact(c_f, nz, kz):
+    """Fields of one z plane and one z bin run the field kernels with their z axis
+    over the timesteps (FieldArgs.swap_zt): labels, positions and point values
+    equal the z-axis blocking (debug flag NO_ZT_SWAP) bit for bit, field values
+    within fp64 rounding, for several time scales c_f; a second z bin (k_z = 2)
+    keeps the z blocking."""
+    P = pkg()
+    from paper_1903_12294_b200.engine import run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
+    dims, nt, ntraj = (120, 72, nz), 37, 15000
+    fld, pts, _ = _synthetic(dims, nt, ntraj, 23, False, n_blobs=3)
+    normalize_device(pts, fld, True)
+    ext = domain_extent_device(pts, fld)
+    params = P.ClusterParams(k=(7, 5, kz, 6), c_f=c_f, eps_c=1e-12, max_iterations=6)
+    a = run_device(pts, fld, ext, params)
+    with N.debug_options(N.DEBUG_NO_ZT_SWAP):
+        b = run_device(pts, fld, ext, params)
+    assert a.iterations_used == b.iterations_used
+    assert torch.equal(a.field_labels, b.field_labels)
+    assert torch.equal(a.point_labels, b.point_labels)
+    sa, sb = P.CenterState.from_device(a.state), P.CenterState.from_device(b.state)
+    np.testing.assert_array_equal(np.asarray(sa.loc), np.asarray(sb.loc))   # integer sums
+    np.testing.assert_array_equal(np.asarray(sa.pval), np.asarray(sb.pval))
+    # field value sums are fp64 per brick before the exact fixed-point total: the
+    # brick shape changes their rounding (as the other blocking paths)
+    np.testing.assert_allclose(np.asarray(sa.fval), np.asarray(sb.fval), rtol=1e-12, atol=1e-15)
+
+
 @pytest.mark.parametrize("weights", [dict(), dict(c_f=0.5, w_d=0.3, w_p=1.5, w_f=2.0)])
 def test_reuse_of_unchanged_blocks_is_exact(weights):
     """A 10-iteration run on a mid-size case where, in the later passes, many

@@ -229,3 +229,40 @@ def test_large_absolute_coordinates_vs_oracle():
                     origin=(1e6, -2e6, 3.5e5), times=times, xyz_shift=(1e6, -2e6, 3.5e5),
                     w=dict(c_f=1e-3))
     assert got["field"] > 0 and got["point"] > 0
+
+
+# ------------------------------------------------------------------ thin (2-D + time) fields
+
+@pytest.mark.parametrize("c_f,seed", [(1.0, 7), (0.6, 8)])
+def test_thin_field_full_run_vs_oracle(c_f, seed):
+    """A field of one z plane (the configs[3] shape, k_z = 1): the field kernels
+    run their z axis over the timesteps (FieldArgs.swap_zt).  Full run against
+    the C oracle: labels array_equal, centres within 1e-12."""
+    from oracle import c_oracle
+    from paper_1903_12294_b200 import ClusterParams
+    from paper_1903_12294_b200.engine import run_device
+    from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
+    dims, nt, ntraj = (96, 80, 1), 40, 30_000
+    fld, pts, _ = _gen(dims, nt, ntraj, seed, False)
+    params = ClusterParams(k=(6, 5, 1, 7), eps_c=1e-12, max_iterations=6, c_f=c_f)
+    normalize_device(pts, fld, params.normalize)
+    ext = domain_extent_device(pts, fld)
+    r = run_device(pts, fld, ext, params)
+    ploc = np.column_stack([_host(pts.xyz), _host(pts.t)])
+    ref = c_oracle.run_grid(ploc, _host(pts.value), dims, fld.origin, fld.spacing, _host(fld.times),
+                            _host(fld.values), ext.mins, ext.maxs, params.k, c_f=params.c_f,
+                            w_d=params.w_d, w_p=params.w_p, w_f=params.w_f, eps_c=params.eps_c,
+                            max_iterations=params.max_iterations, threads=THREADS)
+    np.testing.assert_array_equal(_host(r.field_labels), ref["field_labels"])
+    np.testing.assert_array_equal(_host(r.point_labels), ref["point_labels"])
+    assert r.iterations_used == ref["iterations_used"]
+    st = _state_arrays(r.state)
+    _close(st.loc, ref["loc"], 1e-12)
+    _close(st.fval, ref["fval"], 1e-12)
+    _close(st.pval, ref["pval"], 1e-12)
+
+
+def test_configs3_geometry_windows_vs_oracle():
+    """configs[3]-like thin geometry (one z plane, 16-cell x 16-cell x 8-step bins)."""
+    got = _windowed((512, 512, 1), 48, 300_000, (32, 32, 1, 6), 9, passes=(1, 4))
+    assert got["field"] > 1_000_000 and got["point"] > 0
