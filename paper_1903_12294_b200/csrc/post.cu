@@ -435,10 +435,14 @@ __device__ __forceinline__ void add_fix(unsigned long long &lo, long long &hi, u
 // d2fix (common.cuh) for the per-sample statistics: the same value (|x| 2^64
 // truncated toward zero, negated for x < 0) from the integer and fractional
 // parts by hardware conversions instead of shifts on the exponent
+__device__ __noinline__ void d2fix_rare(double x, unsigned long long &lo, long long &hi, int *ovf) {
+    d2fix(x, lo, hi, ovf);
+}
+
 __device__ __forceinline__ void d2fix_stat(double x, unsigned long long &lo, long long &hi, int *ovf) {
     const double ax = fabs(x);
-    if (!(ax < 0x1.0p62)) {   // also NaN / inf
-        d2fix(x, lo, hi, ovf);
+    if (!(ax < 0x1.0p62)) {   // also NaN / inf (out of line: keeps the hot loops small)
+        d2fix_rare(x, lo, hi, ovf);
         return;
     }
     const double ih = trunc(ax);
@@ -498,25 +502,23 @@ __device__ __forceinline__ void stat_records_flush(const StatArgs &a) {
     }
 }
 
-// this warp's contiguous share [q0, q1) of n samples (whole 32-sample steps)
-__device__ __forceinline__ void warp_share(long long n, long long &q0, long long &q1) {
-    const long long W = (long long)gridDim.x * (blockDim.x >> 5);
-    const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const long long steps = (n + 31) >> 5, per = (steps + W - 1) / W;
-    q0 = min(n, gw * per * 32);
-    q1 = min(n, (gw + 1) * per * 32);
-}
-
 // Field samples: each lane takes 8 consecutive samples of every 256-sample
 // segment of its warp's range (vector loads), so along x its runs follow the
 // feature; the next segment is the next 256 cells (the same x strip of the next
 // rows when nx = 256).  The run's bounding box is kept in cell indices
 // (cell_coord is monotone in the index: the coordinate box is the keys of the
 // extreme indices) and time keys; y, z, t are only re-examined at row changes.
-__device__ __forceinline__ void field_run_flush(unsigned long long *S, const StatArgs &a, int pass, int rs,
-                                                unsigned rn, unsigned long long lo, long long hi,
-                                                const unsigned *b0, const unsigned *b1, unsigned long long t0,
-                                                unsigned long long t1) {
+// (out of line: runs end rarely, and eight inlined copies in the unrolled sample
+// loop overflowed the instruction cache)
+struct FieldGeom {
+    double ox, oy, oz, sx, sy, sz;
+    int x0, y0, z0;
+};
+
+__device__ __noinline__ void field_run_flush(unsigned long long *S, FieldGeom gm, int pass, int rs,
+                                             unsigned rn, unsigned long long lo, long long hi, unsigned bx0,
+                                             unsigned bx1, unsigned by0, unsigned by1, unsigned bz0, unsigned bz1,
+                                             unsigned long long t0, unsigned long long t1) {
     unsigned long long *s = S + (size_t)rs * SW;
     if (pass == 1) {
         atomic_add_fix(s + 6, lo, hi);
@@ -524,12 +526,12 @@ __device__ __forceinline__ void field_run_flush(unsigned long long *S, const Sta
     }
     atomic_add_fix(s + 2, lo, hi);
     atomicAdd(s + 9, (unsigned long long)rn);
-    const unsigned long long ka = okey(cell_coord(a.ox, a.sx, a.x0 + (long long)b0[0])),
-                             kb = okey(cell_coord(a.ox, a.sx, a.x0 + (long long)b1[0])),
-                             kc = okey(cell_coord(a.oy, a.sy, a.y0 + (long long)b0[1])),
-                             kd = okey(cell_coord(a.oy, a.sy, a.y0 + (long long)b1[1])),
-                             ke = okey(cell_coord(a.oz, a.sz, a.z0 + (long long)b0[2])),
-                             kf = okey(cell_coord(a.oz, a.sz, a.z0 + (long long)b1[2]));
+    const unsigned long long ka = okey(cell_coord(gm.ox, gm.sx, gm.x0 + (long long)bx0)),
+                             kb = okey(cell_coord(gm.ox, gm.sx, gm.x0 + (long long)bx1)),
+                             kc = okey(cell_coord(gm.oy, gm.sy, gm.y0 + (long long)by0)),
+                             kd = okey(cell_coord(gm.oy, gm.sy, gm.y0 + (long long)by1)),
+                             ke = okey(cell_coord(gm.oz, gm.sz, gm.z0 + (long long)bz0)),
+                             kf = okey(cell_coord(gm.oz, gm.sz, gm.z0 + (long long)bz1));
     const unsigned long long k0[4] = {min(ka, kb), min(kc, kd), min(ke, kf), t0};
     const unsigned long long k1[4] = {max(ka, kb), max(kc, kd), max(ke, kf), t1};
     bbox_flush(s, k0, k1);
@@ -570,6 +572,7 @@ __global__ void __launch_bounds__(256) k_stats_field(StatArgs a, int pass) {
         ix = (unsigned)(r % nx);
     }
     const bool vec = ((reinterpret_cast<uintptr_t>(a.fslot) | reinterpret_cast<uintptr_t>(a.values)) & 15) == 0;
+    const FieldGeom gm{a.ox, a.oy, a.oz, a.sx, a.sy, a.sz, a.x0, a.y0, a.z0};
     int ovf = 0;
     int rs = -1;                       // the run's slot
     unsigned rn = 0;
@@ -608,7 +611,9 @@ __global__ void __launch_bounds__(256) k_stats_field(StatArgs a, int pass) {
             const int slot = sl[k];
             if (slot >= 0) {
                 if (slot != rs) {
-                    if (rs >= 0) field_run_flush(S, a, pass, rs, rn, lo, hi, b0, b1, t0, t1);
+                    if (rs >= 0)
+                        field_run_flush(S, gm, pass, rs, rn, lo, hi, b0[0], b1[0], b0[1], b1[1], b0[2], b1[2],
+                                        t0, t1);
                     rs = slot;
                     rn = 0;
                     lo = 0;
@@ -678,18 +683,43 @@ __global__ void __launch_bounds__(256) k_stats_field(StatArgs a, int pass) {
         iz -= c ? nz : 0u;
         m += dm + c;
     }
-    if (rs >= 0) field_run_flush(S, a, pass, rs, rn, lo, hi, b0, b1, t0, t1);
+    if (rs >= 0)
+        field_run_flush(S, gm, pass, rs, rn, lo, hi, b0[0], b1[0], b0[1], b1[1], b0[2], b1[2], t0, t1);
     if (ovf) *a.ovf = 1;
     stat_records_flush<SMEM>(a);
 }
 
-// Point samples (record order: a trajectory's samples are consecutive).
+// Point samples (record order: a trajectory's samples are consecutive): as the
+// field kernel, each lane takes 8 consecutive records of every 256-record
+// segment of its warp's range, so a lane's run follows one trajectory.
+__device__ __noinline__ void point_run_flush(unsigned long long *S, int pass, int rs, unsigned rn,
+                                             unsigned long long lo, long long hi, unsigned long long a0,
+                                             unsigned long long a1, unsigned long long a2, unsigned long long a3,
+                                             unsigned long long c0, unsigned long long c1, unsigned long long c2,
+                                             unsigned long long c3) {
+    unsigned long long *s = S + (size_t)rs * SW;
+    if (pass == 1) {
+        atomic_add_fix(s + 4, lo, hi);
+        return;
+    }
+    atomic_add_fix(s, lo, hi);
+    atomicAdd(s + 8, (unsigned long long)rn);
+    const unsigned long long k0[4] = {a0, a1, a2, a3}, k1[4] = {c0, c1, c2, c3};
+    bbox_flush(s, k0, k1);
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(256) k_stats_points(StatArgs a, int pass) {
     unsigned long long *S = stat_records<SMEM>(a);
     const int lane = threadIdx.x & 31;
     long long q0, q1;
-    warp_share(a.np, q0, q1);
+    {   // this warp's contiguous share of whole 256-record segments
+        const long long W = (long long)gridDim.x * (blockDim.x >> 5);
+        const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        const long long segs = (a.np + 255) >> 8, per = (segs + W - 1) / W;
+        q0 = min(a.np, gw * per * 256);
+        q1 = min(a.np, (gw + 1) * per * 256);
+    }
     int ovf = 0;
     int rs = -1;
     unsigned rn = 0;
@@ -697,36 +727,32 @@ __global__ void __launch_bounds__(256) k_stats_points(StatArgs a, int pass) {
     long long hi = 0;
     unsigned long long k0[4] = {0, 0, 0, 0}, k1[4] = {0, 0, 0, 0};
     double mu = 0.0;
-    for (long long base = q0; base < q1; base += 32) {
-        const long long q = base + lane;
-        const int slot = q < q1 ? a.pslot[q] : -1;
-        if (slot >= 0) {
+    for (long long sb = q0; sb < q1; sb += 256) {
+        const long long qb = sb + 8 * lane;
+#pragma unroll 2
+        for (int k = 0; k < 8; ++k) {
+            const long long q = qb + k;
+            const int slot = q < q1 ? a.pslot[q] : -1;
+            if (slot < 0) continue;
             const double v = a.pv[q];
-            unsigned long long k[4];
+            unsigned long long kk[4];
             if (pass == 0) {
-                k[0] = okey(a.xyz[3 * q]);
-                k[1] = okey(a.xyz[3 * q + 1]);
-                k[2] = okey(a.xyz[3 * q + 2]);
-                k[3] = okey(a.pt[q]);
+                kk[0] = okey(a.xyz[3 * q]);
+                kk[1] = okey(a.xyz[3 * q + 1]);
+                kk[2] = okey(a.xyz[3 * q + 2]);
+                kk[3] = okey(a.pt[q]);
             }
             if (slot != rs) {
-                if (rs >= 0) {
-                    unsigned long long *s = S + (size_t)rs * SW;
-                    if (pass == 0) {
-                        atomic_add_fix(s, lo, hi);
-                        atomicAdd(s + 8, (unsigned long long)rn);
-                        bbox_flush(s, k0, k1);
-                    } else {
-                        atomic_add_fix(s + 4, lo, hi);
-                    }
-                }
+                if (rs >= 0)
+                    point_run_flush(S, pass, rs, rn, lo, hi, k0[0], k0[1], k0[2], k0[3], k1[0], k1[1], k1[2],
+                                    k1[3]);
                 rs = slot;
                 rn = 0;
                 lo = 0;
                 hi = 0;
                 if (pass == 0) {
 #pragma unroll
-                    for (int d = 0; d < 4; ++d) k0[d] = k1[d] = k[d];
+                    for (int d = 0; d < 4; ++d) k0[d] = k1[d] = kk[d];
                 } else {
                     mu = a.mean[2 * slot];
                 }
@@ -738,8 +764,8 @@ __global__ void __launch_bounds__(256) k_stats_points(StatArgs a, int pass) {
                 ++rn;
 #pragma unroll
                 for (int d = 0; d < 4; ++d) {
-                    k0[d] = min(k0[d], k[d]);
-                    k1[d] = max(k1[d], k[d]);
+                    k0[d] = min(k0[d], kk[d]);
+                    k1[d] = max(k1[d], kk[d]);
                 }
             } else {
                 const double dv = DSUB(v, mu);
@@ -748,16 +774,8 @@ __global__ void __launch_bounds__(256) k_stats_points(StatArgs a, int pass) {
             add_fix(lo, hi, l, h);
         }
     }
-    if (rs >= 0) {
-        unsigned long long *s = S + (size_t)rs * SW;
-        if (pass == 0) {
-            atomic_add_fix(s, lo, hi);
-            atomicAdd(s + 8, (unsigned long long)rn);
-            bbox_flush(s, k0, k1);
-        } else {
-            atomic_add_fix(s + 4, lo, hi);
-        }
-    }
+    if (rs >= 0)
+        point_run_flush(S, pass, rs, rn, lo, hi, k0[0], k0[1], k0[2], k0[3], k1[0], k1[1], k1[2], k1[3]);
     if (ovf) *a.ovf = 1;
     stat_records_flush<SMEM>(a);
 }

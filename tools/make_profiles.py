@@ -44,7 +44,8 @@ CAPS = (("fa5", "field_assign5", "pass 1 of `tools/prof_run.py c2 2`"),
         ("pa4mid", "point_assign4_mid", "pass 5 of `tools/prof_run.py c2 10`"),
         ("fa5mid_c3", "field_assign5_mid_c3", "pass 5 of `tools/prof_run.py c3 10`"),
         ("screenmid_c3", "field_screen_mid_c3", "pass 5 of `tools/prof_run.py c3 10`"),
-        ("stats_c2", "stats_c2", "first k_stats launch of bench.py post stages (c2)"))
+        ("fa5_c4", "field_assign5_c4", "pass 2 of `tools/prof_run.py c4 3` (thin field, time blocks)"),
+        ("stats_c2", "stats_field_c2", "first k_stats_field launch (pass 0) of bench.py post stages (c2)"))
 for rep, name, which in CAPS:
     path = os.path.join(G, rep + ".ncu-rep")
     if not os.path.exists(path):
