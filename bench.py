@@ -570,7 +570,7 @@ def post_stages(r, fld, pts, tid, hbm):
         return out, a.elapsed_time(b)
 
     out = {}
-    for _ in range(2):   # second round timed (allocator warm)
+    for _ in range(3):   # last round timed (allocator and module state warm)
         (ids, rep, merged), t_merge = timed(lambda: merge_device(r.state, 0.05))
         n_live = int(ids.numel())
         fids = torch.unique(rep)
