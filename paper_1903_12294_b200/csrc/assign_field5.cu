@@ -341,6 +341,40 @@ __device__ __forceinline__ void single_brick_sums(Smem5 &S, ulonglong2 vs, int o
     }
 }
 
+// A run of nb full bricks of one warp labelled by one slot (the warp's bricks
+// share bx and by; zc / tc count them per bz / bt): their count marginals and
+// summed per-run value sums in one set of shared atomics (single_brick_sums per
+// brick would issue nb sets).  Integer sums: the totals are the same.
+// (rc packs 4-bit counts: bz = 0..3 in bits 0-15, bt = 0..1 in 16-23, nb in 24-27)
+__device__ __forceinline__ void run_brick_sums(Smem5 &S, int one, int bx, int by, unsigned rc,
+                                               unsigned long long vlo, unsigned long long vhi) {
+    const int lane = threadIdx.x & 31;
+    const unsigned nb = (rc >> 24) & 15u;
+    unsigned *h = S.hist[one];
+    auto two = [](unsigned c) { return c | (c << 16); };
+    if (lane < 4) {                                      // 8 x: 32 samples per brick each
+        atomicAdd(&h[4 * bx + lane], two(32u * nb));
+    } else if (lane < 6) {                               // 4 y: 64 each
+        atomicAdd(&h[8 + 2 * by + (lane - 4)], two(64u * nb));
+    } else if (lane < 14) {                              // 4 z per bz: 64 each
+        const int bz = (lane - 6) >> 1;
+        const unsigned c = (rc >> (4 * bz)) & 15u;
+        if (c) atomicAdd(&h[16 + 2 * bz + ((lane - 6) & 1)], two(64u * c));
+    } else if (lane < 16) {                              // 2 timesteps per bt: 128 each
+        const unsigned c = (rc >> (16 + 4 * (lane - 14))) & 15u;
+        if (c) atomicAdd(&h[24 + (lane - 14)], two(128u * c));
+    } else if (lane == 16) {
+        atomicAdd(&h[26], 256u * nb);
+    } else if (lane < 23) {                              // the six value-sum limbs
+        const int q = lane - 17;
+        const unsigned long long bits = q < 2 ? vlo >> (24 * q)
+                                      : q == 2 ? (vlo >> 48) | (vhi << 16)
+                                               : vhi >> (24 * q - 64);
+        atomicAdd(&S.vlimb[one][q], q < 5 ? (unsigned)(bits & 0xFFFFFFu) : (unsigned)(bits & 0xFFu) |
+                                                ((bits & 0x80u) ? 0xFFFFFF00u : 0u));
+    }
+}
+
 // Every live sample of a brick labelled `lab` (the initial pass's interior blocks).
 __device__ __forceinline__ void label_brick(const FieldArgs &a, const Ctx &C, int bx, int by, int bz,
                                             int bt, int lab) {
@@ -922,6 +956,9 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     __syncthreads();
     // bricks: warp w takes w, w + 8, ... (the partial sums are order-free integers,
     // so which warp takes which brick does not affect the result)
+    int rslot = -1;                       // run of reused full bricks with one slot
+    unsigned rc = 0;                      // its packed counts (run_brick_sums)
+    unsigned long long rvlo = 0, rvhi = 0;
     for (int bi = w; bi < 64;) {
         const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
         if (!(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= Tm.len)) {
@@ -933,10 +970,26 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 // label provably unchanged since the last pass: labels stay, sums are
                 // constants; the margin shrinks by the bound of this pass's moves
                 if (fast0) label_brick(a, C, bx, by, bz, bt, sbin);   // initial pass: write them
-                if (a.accumulate)
-                    single_brick_sums(S, S.bsums[bi], S.bslot[bi], bx, by, bz, bt, min(GX, X.len - GX * bx),
-                                      min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),
-                                      min(GT, Tm.len - GT * bt));
+                if (a.accumulate) {
+                    const int sl = S.bslot[bi];
+                    if (full) {   // into the warp's run (flushed when the slot changes)
+                        if (sl != rslot) {
+                            if (rc) run_brick_sums(S, rslot, bx, by, rc, rvlo, rvhi);
+                            rslot = sl;
+                            rc = 0;
+                            rvlo = rvhi = 0;
+                        }
+                        rc += (1u << (4 * bz)) + (1u << (16 + 4 * bt)) + (1u << 24);
+                        const ulonglong2 v = S.bsums[bi];
+                        const unsigned long long n = rvlo + v.x;
+                        rvhi += v.y + (n < rvlo ? 1ull : 0ull);
+                        rvlo = n;
+                    } else {
+                        single_brick_sums(S, S.bsums[bi], sl, bx, by, bz, bt, min(GX, X.len - GX * bx),
+                                          min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),
+                                          min(GT, Tm.len - GT * bt));
+                    }
+                }
                 if (!stable && lane == 0)
                     a.bmargin[bidx] = (S.bmarg[bi] - S.bdec[bi]) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
                 if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
@@ -968,6 +1021,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         }
         bi += NW;
     }
+    if (rc) run_brick_sums(S, rslot, w & 1, (w >> 1) & 3, rc, rvlo, rvhi);
 
     // ---- once per block: marginals x fixed-point coordinates -> global 128-bit sums
     if (a.accumulate && !deferred && cnt > 0) {
