@@ -416,7 +416,7 @@ __device__ __forceinline__ void defer_brick(const FieldArgs &a, const Ctx &C, in
 }
 
 template <bool USEVAL, bool FULL, int NR, bool LIST>
-__device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bi, int bx,
+__device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bi, int bx,
                                       int by, int bz, int bt, int region, int nlist, int &ovf_local) {
     const int lane = threadIdx.x & 31;
     const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
@@ -653,7 +653,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                 it.meta = nkeep | min(GX, C.X.len - GX * bx) << 8 | min(GY, C.Y.len - GY * by) << 12 |
                           min(GZ, C.Z.len - GZ * bz) << 16 | min(GT, C.T.len - GT * bt) << 20;
             }
-            return;
+            return -1;
             }
             int nd = 0;
             int *lab_base = a.labels + fbase;
@@ -670,7 +670,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
                     if (p < a.deferred_cap) a.deferred[p] = fbase + (k & 3) * C.plane + (k >> 2) * C.vol;
                     ++p;
                 }
-            return;
+            return -1;
         }
     }
 
@@ -682,8 +682,9 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
         for (int k = 0; k < 8; ++k)
             if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
         if (lane == 0 && a.bslot) a.bslot[bidx] = (unsigned char)one;
+        if (FULL) return one;   // the caller adds it to its warp's run of full bricks
         if (a.accumulate) single_brick_sums(S, a.bsum[bidx], one, bx, by, bz, bt, ex, ey, ez, et);
-        return;
+        return -1;
     }
     int nout = 0;
 #pragma unroll
@@ -707,6 +708,7 @@ __device__ __forceinline__ void brick(const FieldArgs &a, Smem5 &S, const Ctx &C
 
     // (no partial sums here: a brick labelled by one slot returned above with its
     // per-run sums; the others are stranded or deferred and summed where resolved)
+    return -1;
 }
 
 template <bool USEVAL, int MINB>
@@ -1011,9 +1013,23 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                                      : region_list<USEVAL, 4>(S, C, bx, by, bz, bz, bt, bt, vl, vh, a.debug);
             }
             if (nlb >= 0) {
-                if (full)
-                    brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb, ovf_local);
-                else
+                if (full) {
+                    const int one = brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb,
+                                                                 ovf_local);
+                    if (one >= 0 && a.accumulate) {   // single-slot full brick: into the warp's run
+                        if (one != rslot) {
+                            if (rc) run_brick_sums(S, rslot, bx, by, rc, rvlo, rvhi);
+                            rslot = one;
+                            rc = 0;
+                            rvlo = rvhi = 0;
+                        }
+                        rc += (1u << (4 * bz)) + (1u << (16 + 4 * bt)) + (1u << 24);
+                        const ulonglong2 v = a.bsum[bidx];
+                        const unsigned long long n = rvlo + v.x;
+                        rvhi += v.y + (n < rvlo ? 1ull : 0ull);
+                        rvlo = n;
+                    }
+                } else
                     brick<USEVAL, false, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb, ovf_local);
             } else {
                 defer_brick(a, C, bx, by, bz, bt);   // > 32 survivors in one brick: exact path
