@@ -63,6 +63,7 @@ struct ScreenCand {            // one warp's kept candidates, staged in shared m
     int id[MULTI_MAX], has[MULTI_MAX];
     double v[8][32];          // the brick's samples (k, lane)
     double pz[4], pt[2];      // its z-plane and timestep coordinates
+    float tab[MULTI_MAX][18]; // per candidate: the brick's fp32 table entries x[8] y[4] z[4] t[2]
 };
 
 template <bool USEVAL>
@@ -136,6 +137,42 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
         __syncwarp();
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cvmax = fmaxf(cvmax, __shfl_xor_sync(0xffffffffu, cvmax, o));
+        // the candidates' table entries over the brick (as the block tables: an fp64
+        // difference and square rounded once, +inf outside the validity box; c_f on
+        // the time axis), computed once per item by the warp instead of per lane
+        for (int e = lane; e < nk * 18; e += 32) {
+            const int j = e / 18, q = e - 18 * j;
+            const int4 b0 = Q.b0[j], bb = Q.b1[j];
+            float val = INF_F;
+            if (q < 8) {
+                if (it.x0 + q >= b0.x && it.x0 + q <= b0.y) {
+                    const double d = DSUB(Q.c[0][j], cell_coord(a.ox, a.sx, a.x0 + it.x0 + min(q, ex - 1)));
+                    val = to_f(DMUL(d, d));
+                }
+            } else if (q < 12) {
+                const int r = q - 8;
+                if (it.y0 + r >= b0.z && it.y0 + r <= b0.w) {
+                    const double d = DSUB(Q.c[1][j], cell_coord(a.oy, a.sy, a.y0 + it.y0 + min(r, ey - 1)));
+                    val = to_f(DMUL(d, d));
+                }
+            } else if (q < 16) {
+                const int r = q - 12;
+                if (gz0 + r >= bb.x && gz0 + r <= bb.y) {
+                    double d = DSUB(Q.c[2][j], Q.pz[r]);
+                    if (a.swap_zt) d = DMUL(a.cf, d);   // the kernel's z axis is time
+                    val = to_f(DMUL(d, d));
+                }
+            } else {
+                const int r = q - 16;
+                if (gt0 + r >= bb.z && gt0 + r <= bb.w) {
+                    double d = DSUB(Q.c[3][j], Q.pt[r]);
+                    if (!a.swap_zt) d = DMUL(a.cf, d);
+                    val = to_f(DMUL(d, d));
+                }
+            }
+            Q.tab[j][q] = val;
+        }
+        __syncwarp();
 
         // ---- screen over the kept candidates
         unsigned b1[8], b2[8];
@@ -146,35 +183,9 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
         }
 #pragma unroll 1
         for (int j = 0; j < nk; ++j) {
-            const int4 b0 = Q.b0[j], bb = Q.b1[j];
-            const double cx = Q.c[0][j], cy = Q.c[1][j], cz = Q.c[2][j], ct = Q.c[3][j];
-            float tx = INF_F, ty = INF_F, tz[4], tt[2];
-            if (gx >= b0.x && gx <= b0.y) {
-                const double d = DSUB(cx, px);
-                tx = to_f(DMUL(d, d));
-            }
-            if (gy >= b0.z && gy <= b0.w) {
-                const double d = DSUB(cy, py);
-                ty = to_f(DMUL(d, d));
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                tz[q] = INF_F;
-                if (gz0 + q >= bb.x && gz0 + q <= bb.y) {
-                    double d = DSUB(cz, pz[q]);
-                    if (a.swap_zt) d = DMUL(a.cf, d);   // the kernel's z axis is time
-                    tz[q] = to_f(DMUL(d, d));
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                tt[r] = INF_F;
-                if (gt0 + r >= bb.z && gt0 + r <= bb.w) {
-                    double d = DSUB(ct, pt[r]);
-                    if (!a.swap_zt) d = DMUL(a.cf, d);
-                    tt[r] = to_f(DMUL(d, d));
-                }
-            }
+            const float *tb = Q.tab[j];
+            const float tx = tb[lxr], ty = tb[8 + lyr];
+            const float tz[4] = {tb[12], tb[13], tb[14], tb[15]}, tt[2] = {tb[16], tb[17]};
             const float cvs = USEVAL ? Q.cvf[j] : 0.f, wvs = USEVAL ? Q.wvf[j] : 0.f;
             const float axy = tx + ty;
 #pragma unroll
