@@ -92,8 +92,6 @@ struct __align__(16) Smem5 {
     float rcg[NW];                  // per region: min over its culled candidates of dl (1-2^-16) - 2^-15 Wb
     float red2[NW];
     float dmax;                     // largest metric change of the block's candidates
-    float bdec[64];                 // per reused brick: the margin it uses up this pass
-    float bmarg[64];                // per reused brick: its margin (loaded in the prologue)
     ulonglong2 bsums[64];           // per reused brick: its per-run value sum (prologue)
     Ctx ctx;
 };
@@ -859,9 +857,10 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                     // any other candidate of the block
                     const float dec = (a.cdelta[S.id[sl]] + dmax) * (1.f + 0x1.0p-20f);
                     const float mg = a.bmargin[bidx];
-                    S.bdec[tid] = dec;
-                    S.bmarg[tid] = mg;
                     if (!(mg > dec)) sl = 255;
+                    else   // reused: the margin shrinks by the bound of this pass's moves
+                        a.bmargin[bidx] = (mg - dec) * (1.f - 0x1.0p-20f) -
+                                          1e-6f * ((float)a.wd + (USEVAL ? (float)a.wv : 0.0f));
                 }
             }
             S.bslot[tid] = sl;
@@ -970,7 +969,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             const size_t bidx = (size_t)blockIdx.x * 64 + bi;
             if (sstable && S.bslot[bi] != 255) {
                 // label provably unchanged since the last pass: labels stay, sums are
-                // constants; the margin shrinks by the bound of this pass's moves
+                // constants (its margin was updated with the reuse decision above)
                 if (fast0) label_brick(a, C, bx, by, bz, bt, sbin);   // initial pass: write them
                 if (a.accumulate) {
                     const int sl = S.bslot[bi];
@@ -992,8 +991,6 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                                           min(GT, Tm.len - GT * bt));
                     }
                 }
-                if (!stable && lane == 0)
-                    a.bmargin[bidx] = (S.bmarg[bi] - S.bdec[bi]) * (1.f - 0x1.0p-20f) - 1e-6f * (C.fwd + C.wvf);
                 if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
                 bi += NW;
                 continue;
