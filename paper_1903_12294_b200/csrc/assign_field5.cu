@@ -957,44 +957,76 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     __syncthreads();
     // bricks: warp w takes w, w + 8, ... (the partial sums are order-free integers,
     // so which warp takes which brick does not affect the result)
-    int rslot = -1;                       // run of reused full bricks with one slot
+    // the warp's reused bricks, lane-parallel (lane j <-> brick w + 8 j): labels stay,
+    // the sums are constants -- one run per slot (run_brick_sums) for the full ones
+    unsigned needm = 0xFFu;   // bricks j left for the loop below
+    if (sstable) {
+        const int bx = w & 1, by = (w >> 1) & 3;
+        const int bj = w + 8 * (lane & 7), jbz = (bj >> 3) & 3, jbt = bj >> 5;
+        const bool inr = !(GX * bx >= X.len || GY * by >= Y.len || GZ * jbz >= Z.len || GT * jbt >= Tm.len);
+        const int sl = S.bslot[bj];
+        const bool ru = lane < 8 && inr && sl != 255;
+        const unsigned rmask = __ballot_sync(0xffffffffu, ru);
+        needm = ~rmask & 0xFFu;
+        if (rmask) {
+            const bool jfull = GX * bx + GX <= X.len && GY * by + GY <= Y.len && GZ * jbz + GZ <= Z.len &&
+                               GT * jbt + GT <= Tm.len;
+            if (fast0) {   // initial pass: the labels are written once
+                for (unsigned m = rmask; m; m &= m - 1) {
+                    const int b = w + 8 * (__ffs(m) - 1);
+                    label_brick(a, C, bx, by, (b >> 3) & 3, b >> 5, sbin);
+                }
+            }
+            if (a.accumulate) {
+                for (unsigned m = __ballot_sync(0xffffffffu, ru && !jfull); m; m &= m - 1) {   // cut bricks
+                    const int b = w + 8 * (__ffs(m) - 1), bz = (b >> 3) & 3, bt = b >> 5;
+                    single_brick_sums(S, S.bsums[b], S.bslot[b], bx, by, bz, bt, min(GX, X.len - GX * bx),
+                                      min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),
+                                      min(GT, Tm.len - GT * bt));
+                }
+                unsigned fm = __ballot_sync(0xffffffffu, ru && jfull);
+                while (fm) {
+                    const int L = __shfl_sync(0xffffffffu, sl, __ffs(fm) - 1);
+                    const bool in = (fm >> lane & 1u) && sl == L;
+                    fm &= ~__ballot_sync(0xffffffffu, in);
+                    const unsigned rcg = __reduce_add_sync(
+                        0xffffffffu, in ? (1u << (4 * jbz)) + (1u << (16 + 4 * jbt)) + (1u << 24) : 0u);
+                    unsigned long long lo = 0, hi = 0;
+                    if (in) {
+                        const ulonglong2 v = S.bsums[bj];
+                        lo = v.x;
+                        hi = v.y;
+                    }
+#pragma unroll
+                    for (int o = 1; o < 8; o <<= 1) {   // 128-bit sum over lanes 0-7
+                        const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+                        const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+                        const unsigned long long n = lo + l2;
+                        hi = hi + h2 + (n < lo ? 1ull : 0ull);
+                        lo = n;
+                    }
+                    lo = __shfl_sync(0xffffffffu, lo, 0);
+                    hi = __shfl_sync(0xffffffffu, hi, 0);
+                    run_brick_sums(S, L, bx, by, rcg, lo, hi);
+                }
+            }
+            if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, (unsigned long long)__popc(rmask));
+        }
+    }
+    int rslot = -1;                       // run of freshly labelled single-slot full bricks
     unsigned rc = 0;                      // its packed counts (run_brick_sums)
     unsigned long long rvlo = 0, rvhi = 0;
     for (int bi = w; bi < 64;) {
         const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+        if (!(needm >> (bi >> 3) & 1u)) {   // reused above
+            bi += NW;
+            continue;
+        }
         if (!(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= Tm.len)) {
             const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len &&
                               GZ * bz + GZ <= Z.len && GT * bt + GT <= Tm.len;
             const int region = bi & 7, nl = S.nlist[region];
             const size_t bidx = (size_t)blockIdx.x * 64 + bi;
-            if (sstable && S.bslot[bi] != 255) {
-                // label provably unchanged since the last pass: labels stay, sums are
-                // constants (its margin was updated with the reuse decision above)
-                if (fast0) label_brick(a, C, bx, by, bz, bt, sbin);   // initial pass: write them
-                if (a.accumulate) {
-                    const int sl = S.bslot[bi];
-                    if (full) {   // into the warp's run (flushed when the slot changes)
-                        if (sl != rslot) {
-                            if (rc) run_brick_sums(S, rslot, bx, by, rc, rvlo, rvhi);
-                            rslot = sl;
-                            rc = 0;
-                            rvlo = rvhi = 0;
-                        }
-                        rc += (1u << (4 * bz)) + (1u << (16 + 4 * bt)) + (1u << 24);
-                        const ulonglong2 v = S.bsums[bi];
-                        const unsigned long long n = rvlo + v.x;
-                        rvhi += v.y + (n < rvlo ? 1ull : 0ull);
-                        rvlo = n;
-                    } else {
-                        single_brick_sums(S, S.bsums[bi], sl, bx, by, bz, bt, min(GX, X.len - GX * bx),
-                                          min(GY, Y.len - GY * by), min(GZ, Z.len - GZ * bz),
-                                          min(GT, Tm.len - GT * bt));
-                    }
-                }
-                if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, 1ull);   // counters[32]
-                bi += NW;
-                continue;
-            }
             if (lane == 0 && a.bslot) a.bslot[bidx] = 255;
             int nlb = nl;
             if (nl < 0) {
