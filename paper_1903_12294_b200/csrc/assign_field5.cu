@@ -714,14 +714,18 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem5 &S = *reinterpret_cast<Smem5 *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    unsigned tile = blockIdx.x;
-    const int txi = (int)(tile % (unsigned)a.ntx);
-    tile /= (unsigned)a.ntx;
-    const int tyi = (int)(tile % (unsigned)a.nty);
-    tile /= (unsigned)a.nty;
-    const int tzi = (int)(tile % (unsigned)a.ntz);
-    const int tti = (int)(tile / (unsigned)a.ntz);
-    const AxisTile X = a.xt[txi], Y = a.yt[tyi], Z = a.zt[tzi], Tm = a.tt[tti];
+    __shared__ int tix[4];   // the block's axis tiles: one thread decodes the block index
+    if (tid == 0) {
+        unsigned tile = blockIdx.x;
+        tix[0] = (int)(tile % (unsigned)a.ntx);
+        tile /= (unsigned)a.ntx;
+        tix[1] = (int)(tile % (unsigned)a.nty);
+        tile /= (unsigned)a.nty;
+        tix[2] = (int)(tile % (unsigned)a.ntz);
+        tix[3] = (int)(tile / (unsigned)a.ntz);
+    }
+    __syncthreads();
+    const AxisTile X = a.xt[tix[0]], Y = a.yt[tix[1]], Z = a.zt[tix[2]], Tm = a.tt[tix[3]];
     int ovf_local = 0;
 
     // ---- block coordinates (reference formula) + 128-bit fixed-point copies
@@ -1016,12 +1020,9 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     int rslot = -1;                       // run of freshly labelled single-slot full bricks
     unsigned rc = 0;                      // its packed counts (run_brick_sums)
     unsigned long long rvlo = 0, rvhi = 0;
-    for (int bi = w; bi < 64;) {
+    for (unsigned bm = needm; bm; bm &= bm - 1) {   // the bricks not reused above
+        const int bi = w + NW * (__ffs(bm) - 1);
         const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
-        if (!(needm >> (bi >> 3) & 1u)) {   // reused above
-            bi += NW;
-            continue;
-        }
         if (!(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= Tm.len)) {
             const bool full = GX * bx + GX <= X.len && GY * by + GY <= Y.len &&
                               GZ * bz + GZ <= Z.len && GT * bt + GT <= Tm.len;
@@ -1064,7 +1065,6 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 defer_brick(a, C, bx, by, bz, bt);   // > 32 survivors in one brick: exact path
             }
         }
-        bi += NW;
     }
     if (rc) run_brick_sums(S, rslot, w & 1, (w >> 1) & 3, rc, rvlo, rvhi);
 
