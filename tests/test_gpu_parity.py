@@ -769,3 +769,40 @@ def test_feature_stats_smem_and_global_paths_agree(n_slots):
             assert abs(rows[s][8] - pv[p].mean()) <= 1e-12 and abs(rows[s][9] - pv[p].std()) <= 1e-12
         if f.any():
             assert abs(rows[s][10] - fv[f].mean()) <= 1e-12 and abs(rows[s][11] - fv[f].std()) <= 1e-12
+
+
+@pytest.mark.parametrize("seed,n,eps", [(0, 3000, 0.05), (1, 2500, 0.3), (2, 400, 1e-3)])
+def test_merge_random_tables_vs_oracle(seed, n, eps):
+    """mfseg_merge (p_c-sorted window sweep, cached-parent union-find, lane-split
+    ordered sums) against the oracle's all-pairs restatement of postproc.py:59-92
+    on random tables: absent values (None), both signs, values near DELTA,
+    duplicates and clusters of near-equal values; merge map and merged rows
+    bit-identical."""
+    P = pkg()
+    from oracle import mfseg_oracle as O
+    rng = np.random.default_rng(seed)
+    base = rng.choice([0.1, 0.5, 2.0, -0.7, 3e-13], n)
+    pc = base * (1 + rng.normal(0, eps / 3, n))
+    fc = rng.choice([1.0, -4.0, 0.25], n) * (1 + rng.normal(0, eps / 3, n))
+    pc[rng.random(n) < 0.1] = np.nan
+    fc[rng.random(n) < 0.1] = np.nan
+    pc[: n // 50] = pc[n // 50: 2 * (n // 50)]           # exact duplicates
+    ids = np.sort(rng.choice(10 * n, n, replace=False))
+    n_p = np.where(np.isnan(pc), 0, rng.integers(1, 50, n))
+    n_f = np.where(np.isnan(fc), 0, rng.integers(1, 500, n))
+    n_f[(n_p == 0) & (n_f == 0)] = 1
+    fc[(n_f > 0) & np.isnan(fc)] = 0.5
+    loc = rng.random((n, 4)) * 100 - 20
+    rows = [P.ClusterCenter(int(i), *map(float, l), None if np.isnan(p) else float(p),
+                            None if np.isnan(f) else float(f), int(a), int(b))
+            for i, l, p, f, a, b in zip(ids, loc, pc, fc, n_p, n_f)]
+    orows = [O.Summary(int(i), l.copy(), None if np.isnan(p) else float(p), None if np.isnan(f) else float(f),
+                       int(a), int(b)) for i, l, p, f, a, b in zip(ids, loc, pc, fc, n_p, n_f)]
+    mm, merged = P.merge_clusters(rows, eps)
+    omm, omerged = O.merge(orows, eps)
+    assert mm == omm
+    assert len(merged) == len(omerged) and len(merged) < n
+    for g, o in zip(merged, omerged):
+        assert g.id == o.id and g.n_points == o.n_points and g.n_fields == o.n_fields
+        assert (g.x_c, g.y_c, g.z_c, g.t_c) == tuple(float(v) for v in o.loc)
+        assert g.p_c == o.p_c and g.f_c == o.f_c
