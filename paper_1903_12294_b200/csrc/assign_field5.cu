@@ -727,6 +727,17 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     __syncthreads();
     const AxisTile X = a.xt[tix[0]], Y = a.yt[tix[1]], Z = a.zt[tix[2]], Tm = a.tt[tix[3]];
     int ovf_local = 0;
+    // the bricks' reuse state of the last pass, loaded now (no dependence on the
+    // candidates): the latency overlaps the block setup below
+    unsigned char pf_sl = 255;
+    ulonglong2 pf_bs = make_ulonglong2(0ull, 0ull);
+    float pf_mg = 0.f;
+    if (tid < 64 && (a.reuse || a.seeds_fast)) {
+        const size_t bidx = (size_t)blockIdx.x * 64 + tid;
+        if (a.bslot) pf_sl = a.bslot[bidx];
+        if (a.accumulate) pf_bs = a.bsum[bidx];
+        if (a.bmargin) pf_mg = a.bmargin[bidx];
+    }
 
     // ---- block coordinates (reference formula) + 128-bit fixed-point copies
     if (tid < TE) {
@@ -851,16 +862,15 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         if (tid < 64) {
             const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
             const size_t bidx = (size_t)blockIdx.x * 64 + tid;
-            unsigned char sl = fast0 ? 0 : a.bslot[bidx];
+            unsigned char sl = fast0 ? 0 : pf_sl;
             if (sl != 255) {
-                // one round of loads for all 64 bricks: the reuse path below then
-                // reads its per-brick constants from shared memory
-                S.bsums[tid] = a.bsum[bidx];
+                // the per-brick constants of the reuse path below, in shared memory
+                S.bsums[tid] = pf_bs;
                 if (!stable) {
                     // the margin must exceed the change of s* plus the largest change of
                     // any other candidate of the block
                     const float dec = (a.cdelta[S.id[sl]] + dmax) * (1.f + 0x1.0p-20f);
-                    const float mg = a.bmargin[bidx];
+                    const float mg = pf_mg;
                     if (!(mg > dec)) sl = 255;
                     else   // reused: the margin shrinks by the bound of this pass's moves
                         a.bmargin[bidx] = (mg - dec) * (1.f - 0x1.0p-20f) -
