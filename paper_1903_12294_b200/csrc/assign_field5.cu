@@ -801,6 +801,19 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                   ((unsigned)za << 16) | ((unsigned)zb << 20) | ((unsigned)ta << 24) |
                   ((unsigned)tb << 26);
         }
+        // the kept candidates' state, loaded before the compaction's barrier
+        double cx = 0.0, cy = 0.0, cz = 0.0, ct = 0.0, cv = 0.0;
+        bool chas = false;
+        float cdl = 0.f;
+        if (have) {
+            cx = a.c.x[id];
+            cy = a.c.y[id];
+            cz = a.c.z[id];
+            ct = a.c.t[id];
+            chas = a.chas[id] != 0;
+            if (chas) cv = a.cval[id];
+            if (a.reuse) cdl = a.cdelta[id];
+        }
         const unsigned bal = __ballot_sync(0xffffffffu, have);
         float mycv = 0.0f;
         if (lane == 0) S.wc[w] = __popc(bal);
@@ -814,13 +827,11 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         deferred = cnt > CAP;
         if (!deferred && have) {
             const int p = off + __popc(bal & ((1u << lane) - 1u));
-            const bool chas = a.chas[id] != 0;
-            const double cv = chas ? a.cval[id] : 0.0;
             S.id[p] = id;
-            S.c[p][0] = a.c.x[id];
-            S.c[p][1] = a.c.y[id];
-            S.c[p][2] = a.c.z[id];
-            S.c[p][3] = a.c.t[id];
+            S.c[p][0] = cx;
+            S.c[p][1] = cy;
+            S.c[p][2] = cz;
+            S.c[p][3] = ct;
             S.c[p][4] = cv;
             S.box[p] = box;
             S.has[p] = chas;
@@ -833,7 +844,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             if (lane == 0) S.red[w] = mycv;
         }
         if (a.reuse) {   // largest metric change among the block's candidates
-            const float md = warp_max_nn((!deferred && have) ? a.cdelta[id] : 0.f);
+            const float md = warp_max_nn((!deferred && have) ? cdl : 0.f);
             if (lane == 0) S.red2[w] = md;
         }
         __syncthreads();
