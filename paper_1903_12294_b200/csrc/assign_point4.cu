@@ -634,6 +634,14 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
             bal[r] = __ballot_sync(0xffffffffu, have[r]);
             if (lane == 0) S.wc[r * NW + w] = __popc(bal[r]);
         }
+        // the kept candidates' values, loaded before the compaction's barrier
+        bool chs[CR];
+        double cvv[CR];
+#pragma unroll
+        for (int r = 0; r < CR; ++r) {
+            chs[r] = have[r] && a.chas[id[r]] != 0;
+            cvv[r] = chs[r] ? a.cval[id[r]] : 0.0;
+        }
         __syncthreads();
         int off[CR];
 #pragma unroll
@@ -650,8 +658,8 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         for (int r = 0; r < CR; ++r) {
             if (!deferred && have[r]) {
                 const int p = off[r] + __popc(bal[r] & ((1u << lane) - 1u));
-                const bool chas = a.chas[id[r]] != 0;
-                const double cv = chas ? a.cval[id[r]] : 0.0;
+                const bool chas = chs[r];
+                const double cv = cvv[r];
                 S.id[p] = id[r];
                 S.c[p][0] = c4[r][0];
                 S.c[p][1] = c4[r][1];
