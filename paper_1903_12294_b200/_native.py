@@ -149,6 +149,7 @@ DEBUG_NO_REUSE = 16
 DEBUG_NO_MARGIN_REUSE = 32
 DEBUG_NO_SEEDS_FAST = 64
 DEBUG_NO_ZT_SWAP = 128
+DEBUG_NO_BLOCK_CACHE = 256
 
 
 @contextlib.contextmanager
@@ -172,6 +173,7 @@ def debug_options_from_env() -> None:
     flags |= DEBUG_NO_MARGIN_REUSE if env.get("MFSEG_NO_MARGIN_REUSE") else 0
     flags |= DEBUG_NO_SEEDS_FAST if env.get("MFSEG_NO_SEEDS_FAST") else 0
     flags |= DEBUG_NO_ZT_SWAP if env.get("MFSEG_NO_ZT_SWAP") else 0
+    flags |= DEBUG_NO_BLOCK_CACHE if env.get("MFSEG_NO_BLOCK_CACHE") else 0
     load().mfseg_set_debug_options(flags, int(env.get("MFSEG_MULTI_CAP", "-1")))
 
 

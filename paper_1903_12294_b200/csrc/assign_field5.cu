@@ -86,6 +86,8 @@ struct __align__(16) Smem5 {
     unsigned char has[CAP];
     int wc[NW];
     float red[NW];
+    int cidx[CAP];                  // block cache: entry of each slot (-1: absent)
+    int cnz;
     int lst[NW][32];                // per region: candidate slots that survive its cull
     int nlist[NW];                  // list lengths (-1: more than 32 survivors)
     unsigned char bslot[64];        // reused bricks: slot of their label (255: recompute)
@@ -413,6 +415,9 @@ __device__ __forceinline__ void defer_brick(const FieldArgs &a, const Ctx &C, in
         }
 }
 
+// Returns the brick's slot when it is FULL and labelled by one slot (the caller
+// sums it in its run), -1 when it is labelled by one slot and summed here, -2
+// when it is not (queued for k_field_screen, deferred or stranded).
 template <bool USEVAL, bool FULL, int NR, bool LIST>
 __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C, int bi, int bx,
                                       int by, int bz, int bt, int region, int nlist, int &ovf_local) {
@@ -651,7 +656,7 @@ __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C,
                 it.meta = nkeep | min(GX, C.X.len - GX * bx) << 8 | min(GY, C.Y.len - GY * by) << 12 |
                           min(GZ, C.Z.len - GZ * bz) << 16 | min(GT, C.T.len - GT * bt) << 20;
             }
-            return -1;
+            return -2;
             }
             int nd = 0;
             int *lab_base = a.labels + fbase;
@@ -668,7 +673,7 @@ __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C,
                     if (p < a.deferred_cap) a.deferred[p] = fbase + (k & 3) * C.plane + (k >> 2) * C.vol;
                     ++p;
                 }
-            return -1;
+            return -2;
         }
     }
 
@@ -679,7 +684,10 @@ __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C,
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (FULL || (livem >> k & 1)) lab_base[(k & 3) * C.plane + (k >> 2) * C.vol] = lab;
-        if (lane == 0 && a.bslot) a.bslot[bidx] = (unsigned char)one;
+        if (lane == 0 && a.bslot) {
+            a.bslot[bidx] = (unsigned char)one;
+            if (a.bcid) a.bcid[bidx] = lab;
+        }
         if (FULL) return one;   // the caller adds it to its warp's run of full bricks
         if (a.accumulate) single_brick_sums(S, a.bsum[bidx], one, bx, by, bz, bt, ex, ey, ez, et);
         return -1;
@@ -706,7 +714,7 @@ __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C,
 
     // (no partial sums here: a brick labelled by one slot returned above with its
     // per-run sums; the others are stranded or deferred and summed where resolved)
-    return -1;
+    return -2;
 }
 
 template <bool USEVAL, int MINB>
@@ -732,11 +740,58 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
     unsigned char pf_sl = 255;
     ulonglong2 pf_bs = make_ulonglong2(0ull, 0ull);
     float pf_mg = 0.f;
+    int pf_cid = 0;
     if (tid < 64 && (a.reuse || a.seeds_fast)) {
         const size_t bidx = (size_t)blockIdx.x * 64 + tid;
         if (a.bslot) pf_sl = a.bslot[bidx];
         if (a.accumulate) pf_bs = a.bsum[bidx];
         if (a.bmargin) pf_mg = a.bmargin[bidx];
+        if (a.bcid && a.bcache) pf_cid = a.bcid[bidx];
+    }
+
+    // ---- a block whose every brick keeps its label: its sums are those of the pass
+    // that labelled it (block cache), added without the block setup.  The margin
+    // test is the one below with the largest move over all the bin's candidates
+    // (a superset of the block's: never looser)
+    if (a.bcache && a.reuse && !a.seeds_fast && a.accumulate) {
+        const int sbin0 = ((Tm.bin * a.kz + Z.bin) * a.ky + Y.bin) * a.kx + X.bin;
+        const int bn = a.bin_sstable[sbin0] ? a.bcache[blockIdx.x].n : -1;
+        const int L0 = a.g.cand_start[sbin0], L1 = a.g.cand_start[sbin0 + 1];
+        if (bn >= 0 && L1 - L0 <= NT) {
+            const bool stable = a.bin_stable[sbin0];
+            float dmax = 0.f;
+            if (!stable) {
+                float d = L0 + tid < L1 ? a.cdelta[a.g.cand_ids[L0 + tid]] : 0.f;
+                d = warp_max_nn(d);
+                if (lane == 0) S.red2[w] = d;
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < NW; ++q) dmax = fmaxf(dmax, S.red2[q]);
+            }
+            const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
+            const bool live = tid < 64 && !(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len ||
+                                            GT * bt >= Tm.len);
+            float dec = 0.f;
+            bool ok = !live || pf_sl != 255;
+            if (live && ok && !stable) {
+                dec = (a.cdelta[pf_cid] + dmax) * (1.f + 0x1.0p-20f);
+                ok = pf_mg > dec;
+            }
+            if (__syncthreads_and(ok)) {
+                if (live && !stable)
+                    a.bmargin[(size_t)blockIdx.x * 64 + tid] =
+                        (pf_mg - dec) * (1.f - 0x1.0p-20f) - 1e-6f * ((float)a.wd + (USEVAL ? (float)a.wv : 0.0f));
+                const BlockCache &bc = a.bcache[blockIdx.x];
+                for (int e = tid; e < bn * 6; e += NT) {
+                    const int ce = e / 6, q = e - 6 * ce;
+                    unsigned long long *dst = a.acc + (size_t)bc.id[ce] * MFSEG_ACC_WORDS;
+                    if (q == 5) atomicAdd(dst + 13, bc.cnt[ce]);
+                    else atomic_add_fix(dst + (q < 4 ? 2 * q : 10), bc.w[ce][2 * q], (long long)bc.w[ce][2 * q + 1]);
+                }
+                if ((a.debug & 8) && tid < 64 && live) atomicAdd(a.stats + 24, 1ull);
+                return;
+            }
+        }
     }
 
     // ---- block coordinates (reference formula) + 128-bit fixed-point copies
@@ -1038,6 +1093,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, (unsigned long long)__popc(rmask));
         }
     }
+    bool nocache = false;                 // a brick not labelled by one slot (block cache)
     int rslot = -1;                       // run of freshly labelled single-slot full bricks
     unsigned rc = 0;                      // its packed counts (run_brick_sums)
     unsigned long long rvlo = 0, rvhi = 0;
@@ -1067,6 +1123,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 if (full) {
                     const int one = brick<USEVAL, true, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb,
                                                                  ovf_local);
+                    nocache |= one == -2;
                     if (one >= 0 && a.accumulate) {   // single-slot full brick: into the warp's run
                         if (one != rslot) {
                             if (rc) run_brick_sums(S, rslot, bx, by, rc, rvlo, rvhi);
@@ -1080,24 +1137,48 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                         rvhi += v.y + (n < rvlo ? 1ull : 0ull);
                         rvlo = n;
                     }
-                } else
-                    brick<USEVAL, false, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb, ovf_local);
+                } else {
+                    nocache |= brick<USEVAL, false, 1, true>(a, S, C, bi, bx, by, bz, bt, region, nlb,
+                                                             ovf_local) == -2;
+                }
             } else {
                 defer_brick(a, C, bx, by, bz, bt);   // > 32 survivors in one brick: exact path
+                nocache = true;
             }
         }
     }
     if (rc) run_brick_sums(S, rslot, w & 1, (w >> 1) & 3, rc, rvlo, rvhi);
 
     // ---- once per block: marginals x fixed-point coordinates -> global 128-bit sums
+    // (and into the block cache when every brick has one label: up to BC_MAX clusters)
     if (a.accumulate && !deferred && cnt > 0) {
-        __syncthreads();
+        bool cache = __syncthreads_or(nocache) == 0 && a.bcache != nullptr;
+        if (cache) {   // entry of each cluster present (warp 0), in slot order
+            if (w == 0) {
+                int base = 0;
+                for (int r = 0; 32 * r < cnt; ++r) {
+                    const int sl = 32 * r + lane;
+                    const bool nz = sl < cnt && S.hist[sl][26] != 0;
+                    const unsigned b = __ballot_sync(0xffffffffu, nz);
+                    if (sl < cnt) S.cidx[sl] = nz ? base + __popc(b & ((1u << lane) - 1u)) : -1;
+                    base += __popc(b);
+                }
+                if (lane == 0) S.cnz = base;
+            }
+            __syncthreads();
+            cache = S.cnz <= BC_MAX;
+            if (tid == 0) a.bcache[blockIdx.x].n = cache ? S.cnz : -1;
+        } else if (tid == 0 && a.bcache) {
+            a.bcache[blockIdx.x].n = -1;
+        }
         for (int e = tid; e < cnt * 6; e += NT) {
             const int s = e / 6, wd = e - s * 6;
             const unsigned *h = S.hist[s];
             const int n = (int)h[26];
             if (n == 0) continue;
             unsigned long long *dst = a.acc + (size_t)S.id[s] * MFSEG_ACC_WORDS;
+            BlockCache *bcp = cache ? a.bcache + blockIdx.x : nullptr;
+            const int ce = cache ? S.cidx[s] : -1;
             __int128 acc = 0;
             if (wd < 4) {   // one rolled loop for the four axes (small code)
                 static_assert(BX == BY && BY == BZ, "x, y, z marginals share one loop");
@@ -1109,11 +1190,22 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                 acc = value_limbs_total(S.vlimb[s]);
             } else {
                 atomicAdd(dst + 13, (unsigned long long)n);
+                if (bcp) {
+                    bcp->id[ce] = S.id[s];
+                    bcp->cnt[ce] = (unsigned long long)n;
+                }
                 continue;
             }
             const int word = wd < 2 ? 2 * wd : wd < 4 ? 2 * (a.swap_zt ? 5 - wd : wd) : 10;   // real axis
             atomic_add_fix(dst + word, (unsigned long long)acc, (long long)(acc >> 64));
+            if (bcp) {
+                const int q = word < 10 ? word / 2 : 4;
+                bcp->w[ce][2 * q] = (unsigned long long)acc;
+                bcp->w[ce][2 * q + 1] = (unsigned long long)(acc >> 64);
+            }
         }
+    } else if (tid == 0 && a.bcache) {
+        a.bcache[blockIdx.x].n = -1;
     }
     if (ovf_local) *a.overflow = 1;
 }

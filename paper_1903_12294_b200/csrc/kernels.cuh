@@ -75,6 +75,20 @@ struct FieldArgs {
     const unsigned char *bin_sstable;
     const float *cdelta;
     float *bmargin;
+    // a block whose every brick keeps its label contributes the same sums as in
+    // the pass that labelled it: per brick the centre id of its label (bcid) and
+    // per block its per-cluster sums (bcache, n = -1: none) let such a block add
+    // them without its setup (k_field_assign5)
+    int *bcid;
+    struct BlockCache *bcache;
+};
+
+constexpr int BC_MAX = 6;
+struct BlockCache {                   // one field block's per-cluster sums, as added to acc
+    int n;                            // entries (-1: none)
+    int id[BC_MAX];
+    unsigned long long w[BC_MAX][10]; // x, y, z, t, value: 128-bit (lo, hi), real axes
+    unsigned long long cnt[BC_MAX];
 };
 
 struct WBox {                 // one 64-point warp tile of a point chunk (k_point_assign4)

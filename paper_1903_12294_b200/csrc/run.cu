@@ -299,6 +299,8 @@ struct Plan {
     MultiItem *multi;               // multi-candidate bricks for k_field_screen
     long long multi_cap;
     unsigned char *bslot;           // per brick: slot of its single label last pass (255: none)
+    int *bcid;                      // per brick: centre id of that label
+    BlockCache *bcache;             // per field block: its per-cluster sums (k_field_assign5)
     unsigned char *bmark, *bstable; // per sample bin: changed centres / stable neighbourhood
     unsigned char *smark, *sstable; // per sample bin: structural changes (bin, validity box, has)
     float *cdelta;                  // per centre: bound of its metric change in the last update
@@ -483,6 +485,8 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         P.multi = cv.take<MultiItem>(P.multi_cap);
         P.bslot = cv.take<unsigned char>(P.nf > 0 ? bricks : 0);
         P.bmargin = cv.take<float>(P.nf > 0 ? bricks : 0);
+        P.bcid = cv.take<int>(P.nf > 0 ? bricks : 0);
+        P.bcache = cv.take<BlockCache>(P.nf > 0 ? bricks / 64 : 0);
     }
     P.bmark = cv.take<unsigned char>(NB);
     P.bstable = cv.take<unsigned char>(NB);
@@ -705,6 +709,8 @@ int plan_prepare_impl(Plan &P) {
             MFSEG_TRY(launch_brick_pre(va, st));
         }
         if (P.bslot) MFSEG_CUDA(cudaMemsetAsync(P.bslot, 255, P.nbricks, st));
+        if (P.bcache)   // n = -1: no block has cached sums yet
+            MFSEG_CUDA(cudaMemsetAsync(P.bcache, 255, sizeof(BlockCache) * (P.nbricks / 64), st));
     }
     long long n = P.np;
     if (n > 0) {
@@ -940,6 +946,8 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.multi_cap = P.multi_cap;
         a.bslot = P.bslot;
         a.bmargin = a.bslot ? P.bmargin : nullptr;
+        a.bcid = a.bslot ? P.bcid : nullptr;
+        a.bcache = a.bslot && !(dbg.flags & MFSEG_DEBUG_NO_BLOCK_CACHE) ? P.bcache : nullptr;
         a.seeds_fast = fast0;
         if (reuse && a.bslot) {
             a.reuse = 1;

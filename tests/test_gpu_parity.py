@@ -493,7 +493,8 @@ def test_assign_drifted_centres_vs_oracle(w_d, seed):
 
 
 @pytest.mark.parametrize("opts", [dict(multi_cap=0), dict(multi_cap=37), dict(flags=2),
-                                  dict(flags=1), dict(flags=16), dict(flags=32), dict(flags=64)])
+                                  dict(flags=1), dict(flags=16), dict(flags=32), dict(flags=64),
+                                  dict(flags=256)])
 def test_field_brick_queue_paths_agree(opts):
     """k_field_assign5 queues multi-candidate bricks for k_field_screen; a full
     queue (capacity 0 or 37 items) sends the rest to the exact per-sample path
@@ -601,6 +602,10 @@ def test_reuse_of_unchanged_blocks_is_exact(weights):
     a = run_device(pts, fld, ext, params)
     with N.debug_options(N.DEBUG_NO_REUSE):
         b = run_device(pts, fld, ext, params)
+    with N.debug_options(N.DEBUG_NO_BLOCK_CACHE):
+        c = run_device(pts, fld, ext, params)
+    assert torch.equal(a.field_labels, c.field_labels) and torch.equal(a.point_labels, c.point_labels)
+    assert torch.equal(a.state["loc"], c.state["loc"]) and torch.equal(a.state["fval"], c.state["fval"])
     assert a.iterations_used == b.iterations_used
     assert torch.equal(a.field_labels, b.field_labels)
     assert torch.equal(a.point_labels, b.point_labels)
