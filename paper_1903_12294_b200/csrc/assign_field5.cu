@@ -759,15 +759,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         const int L0 = a.g.cand_start[sbin0], L1 = a.g.cand_start[sbin0 + 1];
         if (bn >= 0 && L1 - L0 <= NT) {
             const bool stable = a.bin_stable[sbin0];
-            float dmax = 0.f;
-            if (!stable) {
-                float d = L0 + tid < L1 ? a.cdelta[a.g.cand_ids[L0 + tid]] : 0.f;
-                d = warp_max_nn(d);
-                if (lane == 0) S.red2[w] = d;
-                __syncthreads();
-#pragma unroll
-                for (int q = 0; q < NW; ++q) dmax = fmaxf(dmax, S.red2[q]);
-            }
+            const float dmax = stable ? 0.f : a.bin_dmax[sbin0];
             const int bx = tid & 1, by = (tid >> 1) & 3, bz = (tid >> 3) & 3, bt = tid >> 5;
             const bool live = tid < 64 && !(GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len ||
                                             GT * bt >= Tm.len);

@@ -81,6 +81,7 @@ struct FieldArgs {
     // them without its setup (k_field_assign5)
     int *bcid;
     struct BlockCache *bcache;
+    const float *bin_dmax;       // per sample bin: the largest cdelta among its candidates
 };
 
 constexpr int BC_MAX = 6;

@@ -304,6 +304,8 @@ struct Plan {
     unsigned char *bmark, *bstable; // per sample bin: changed centres / stable neighbourhood
     unsigned char *smark, *sstable; // per sample bin: structural changes (bin, validity box, has)
     float *cdelta;                  // per centre: bound of its metric change in the last update
+    unsigned *cbmax;                // per bin: largest cdelta of its centres (float bits)
+    float *bdmax;                   // per sample bin: largest cdelta among its candidates
     float *bmargin;                 // per brick: proven margin of its single label
     int4 *vbox_prev;                // validity boxes of the previous pass
     unsigned char *tslot;           // per point warp tile: slot of its single label last pass
@@ -493,6 +495,8 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.smark = cv.take<unsigned char>(NB);
     P.sstable = cv.take<unsigned char>(NB);
     P.cdelta = cv.take<float>(K);
+    P.cbmax = cv.take<unsigned>(NB);
+    P.bdmax = cv.take<float>(NB);
     P.vbox_prev = cv.take<int4>(P.nf > 0 ? 2ll * K : 0);
     P.cap_f = P.nf < (1ll << 22) ? P.nf : (1ll << 22);
     P.stranded_f = cv.take<long long>(P.cap_f);
@@ -771,7 +775,7 @@ CentersView view_of(const mfseg_centers &s, int K) {
 __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, double4 mins, double4 C,
                                int4 k, double cf, double wd, double wf, const int4 *vbox,
                                const int4 *vbox_prev, unsigned char *mark, unsigned char *smark,
-                               float *cdelta) {
+                               float *cdelta, unsigned *cbmax) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= K) return;
     bool ch = cur.has_f[c] != old.has_f[c] || cur.has_p[c] != old.has_p[c] ||
@@ -804,6 +808,8 @@ __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, doub
         bo[q] = bin_coord(old.loc[(size_t)q * K + c], mn[q], CC[q], kk[q]);
     }
     const int fn = ((bn[3] * k.z + bn[2]) * k.y + bn[1]) * k.x + bn[0];
+    // per bin the largest move of its centres (non-negative floats order as their bits)
+    if (cbmax && delta > 0.f) atomicMax(&cbmax[fn], __float_as_uint(delta));
     const int fo = ((bo[3] * k.z + bo[2]) * k.y + bo[1]) * k.x + bo[0];
     mark[fn] = 1;
     mark[fo] = 1;
@@ -822,7 +828,8 @@ __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, doub
 // A sample bin is stable when none of its 3^4 neighbour bins is marked: its
 // candidate list and every candidate's state equal the last pass's.
 __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned char *stable,
-                             const unsigned char *smark, unsigned char *sstable) {
+                             const unsigned char *smark, unsigned char *sstable, const unsigned *cbmax,
+                             float *bdmax) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= NB) return;
     int r = b;
@@ -833,6 +840,7 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
     const int bz = r % k.z;
     const int bt = r / k.z;
     bool ok = true, sok = true;
+    unsigned dm = 0;
     for (int dt = -1; dt <= 1; ++dt)
         for (int dz = -1; dz <= 1; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
@@ -844,9 +852,11 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
                     const int q = ((qt * k.z + qz) * k.y + qy) * k.x + qx;
                     ok = ok && !mark[q];
                     sok = sok && !smark[q];
+                    if (cbmax) dm = max(dm, cbmax[q]);
                 }
     stable[b] = ok;
     sstable[b] = sok;
+    if (bdmax) bdmax[b] = __uint_as_float(dm);   // largest move among the bin's candidates
 }
 
 // one assignment pass for centre state `c` (grid rebuilt here); `prev`: the
@@ -877,15 +887,17 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         const int NB = P.NB;
         MFSEG_CUDA(cudaMemsetAsync(P.bmark, 0, NB, st));
         MFSEG_CUDA(cudaMemsetAsync(P.smark, 0, NB, st));
+        MFSEG_CUDA(cudaMemsetAsync(P.cbmax, 0, sizeof(unsigned) * NB, st));
         ::mfseg::count_launch();
         k_mark_changed<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(
             K, c, *prev, make_double4(p.mins[0], p.mins[1], p.mins[2], p.mins[3]),
             make_double4(p.C[0], p.C[1], p.C[2], p.C[3]), make_int4(p.k[0], p.k[1], p.k[2], p.k[3]),
             p.c_f, wd, wf, P.nf > 0 ? P.g.vbox : nullptr, P.nf > 0 ? P.vbox_prev : nullptr, P.bmark,
-            P.smark, P.cdelta);
+            P.smark, P.cdelta, P.cbmax);
         ::mfseg::count_launch();
         k_bin_stable<<<(unsigned)((NB + 255) / 256), 256, 0, st>>>(
-            NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable, P.smark, P.sstable);
+            NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable, P.smark, P.sstable, P.cbmax,
+            P.bdmax);
         MFSEG_LAUNCH("stable bins");
     }
     if (accumulate)
@@ -948,6 +960,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
         a.bmargin = a.bslot ? P.bmargin : nullptr;
         a.bcid = a.bslot ? P.bcid : nullptr;
         a.bcache = a.bslot && !(dbg.flags & MFSEG_DEBUG_NO_BLOCK_CACHE) ? P.bcache : nullptr;
+        a.bin_dmax = P.bdmax;
         a.seeds_fast = fast0;
         if (reuse && a.bslot) {
             a.reuse = 1;
