@@ -8,10 +8,11 @@ from paper_1903_12294_b200 import _native as _N; _N.debug_options_from_env()  # 
 from paper_1903_12294_b200.engine import run_device
 from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device, synthetic_device
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-fld, pts, _ = synthetic_device(cfg["dims"], cfg["nt"], cfg["n_traj"], seed=0)
+from bench import rank_data, workload
+fld, pts, _, _, _ = rank_data(cfg, 1, 0, 0, torch.device("cuda", 0))   # the bench's data
 normalize_device(pts, fld, True)
 ext = domain_extent_device(pts, fld)
-params = ClusterParams(k=cfg["k"], eps_c=1e-12, max_iterations=10)
+params = ClusterParams(k=workload(cfg, 1)[3], eps_c=1e-12, max_iterations=10)
 lib = N.load()
 for env in sys.argv[2:] or [""]:
     for e in [x for x in os.environ if x.startswith("MFSEG_")]:
