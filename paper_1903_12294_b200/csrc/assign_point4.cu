@@ -67,6 +67,9 @@ struct __align__(16) PSmem4 {
     unsigned char has[CAP], full[CAP];
     int wc[CR * NW];
     float red[NW];
+    int plisted;                    // some point went to the stranded / deferred lists
+    int pcidx[CAP];                 // chunk cache: entry of each slot (-1: absent)
+    int pcnz;
     PCtx ctx;
 };
 
@@ -503,6 +506,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         if (lab < 0) ++nlist;
     }
     const bool listed = __any_sync(0xffffffffu, nlist > 0);
+    if (listed && lane == 0) S.plisted = 1;   // (no chunk cache)
     if (listed) {
         unsigned long long *ctr = C.deferred ? a.n_deferred : a.n_stranded;
         long long *lst = C.deferred ? a.deferred : a.stranded;
@@ -565,9 +569,26 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
     PSmem4 &S = *reinterpret_cast<PSmem4 *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int4 T = a.tiles[blockIdx.x];
+    // a chunk whose bin is stable (no candidate changed) keeps every label: it adds
+    // the per-cluster sums it cached when it last ran (not in the final pass, which
+    // writes the record-order labels)
+    if (a.pcache && a.reuse && !a.labels_out && a.accumulate && a.bin_stable[T.x]) {
+        const PointCache &pc = a.pcache[blockIdx.x];
+        const int pn = pc.n;
+        if (pn >= 0) {
+            for (int e = threadIdx.x; e < pn * 6; e += NT) {
+                const int ce = e / 6, q = e - 6 * ce;
+                unsigned long long *dst = a.acc + (size_t)pc.id[ce] * MFSEG_ACC_WORDS;
+                if (q == 5) atomicAdd(dst + 12, pc.cnt[ce]);
+                else atomic_add_fix(dst + (q < 4 ? 2 * q : 8), pc.w[ce][2 * q], (long long)pc.w[ce][2 * q + 1]);
+            }
+            return;
+        }
+    }
     const double *box = a.tile_box + 8 * (size_t)blockIdx.x;   // lo[4], hi[4]
     const double Cd[4] = {a.Cx, a.Cy, a.Cz, a.Ct};
     int ovf_local = 0;
+    if (tid == 0) S.plisted = 0;
     if (tid < 4) {   // chunk frame: origin, guard bands, fp32 box half-widths
         const int d = tid;
         const double sc = d == 3 ? a.cf : 1.0;
@@ -726,16 +747,42 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         for (int wt = w; 64 * wt < C.len; wt += NW) point_warp<USEVAL, 4>(a, S, C, wt, ovf_local);
     }
 
-    // ---- once per CTA: exact per-slot totals -> global 128-bit sums
+    // ---- once per CTA: exact per-slot totals -> global 128-bit sums (and into the
+    // chunk cache when no point went to the stranded / deferred lists: up to PC_MAX)
     if (a.accumulate && !deferred && cnt > 0) {
         __syncthreads();
+        bool cache = a.pcache != nullptr && S.plisted == 0;
+        if (cache) {
+            if (w == 0) {
+                int base = 0;
+                for (int r = 0; 32 * r < cnt; ++r) {
+                    const int sl = 32 * r + lane;
+                    const bool nz = sl < cnt && S.n[sl] != 0;
+                    const unsigned b = __ballot_sync(0xffffffffu, nz);
+                    if (sl < cnt) S.pcidx[sl] = nz ? base + __popc(b & ((1u << lane) - 1u)) : -1;
+                    base += __popc(b);
+                }
+                if (lane == 0) S.pcnz = base;
+            }
+            __syncthreads();
+            cache = S.pcnz <= PC_MAX;
+            if (tid == 0) a.pcache[blockIdx.x].n = cache ? S.pcnz : -1;
+        } else if (tid == 0 && a.pcache) {
+            a.pcache[blockIdx.x].n = -1;
+        }
         for (int e = tid; e < cnt * 6; e += NT) {
             const int s = e / 6, wd = e - s * 6;
             const unsigned n = S.n[s];
             if (n == 0) continue;
             unsigned long long *dst = a.acc + (size_t)S.id[s] * MFSEG_ACC_WORDS;
+            PointCache *pcp = cache ? a.pcache + blockIdx.x : nullptr;
+            const int ce = cache ? S.pcidx[s] : -1;
             if (wd == 5) {
                 atomicAdd(dst + 12, (unsigned long long)n);   // n_points
+                if (pcp) {
+                    pcp->id[ce] = S.id[s];
+                    pcp->cnt[ce] = (unsigned long long)n;
+                }
                 continue;
             }
             __int128 acc = 0;
@@ -747,7 +794,13 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
                 acc += (__int128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
             }
             atomic_add_fix(dst + (wd < 4 ? 2 * wd : 8), (unsigned long long)acc, (long long)(acc >> 64));
+            if (pcp) {
+                pcp->w[ce][2 * wd] = (unsigned long long)acc;
+                pcp->w[ce][2 * wd + 1] = (unsigned long long)(acc >> 64);
+            }
         }
+    } else if (tid == 0 && a.pcache) {
+        a.pcache[blockIdx.x].n = -1;
     }
     if (ovf_local) *a.overflow = 1;
 }

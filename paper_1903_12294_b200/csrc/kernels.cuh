@@ -134,6 +134,17 @@ struct PointArgs {
     const unsigned char *bin_stable;
     unsigned char *tslot;
     int reuse;
+    // a chunk whose bin is stable keeps every label: its per-cluster sums are those
+    // cached when it last ran (pcache, n = -1: none)
+    struct PointCache *pcache;
+};
+
+constexpr int PC_MAX = 12;
+struct PointCache {                   // one point chunk's per-cluster sums, as added to acc
+    int n;                            // entries (-1: none)
+    int id[PC_MAX];
+    unsigned long long w[PC_MAX][10]; // x, y, z, t, value: 128-bit (lo, hi)
+    unsigned long long cnt[PC_MAX];
 };
 
 // Stranded-sample fallback (engine.py:195-205): field samples (kind 1) are

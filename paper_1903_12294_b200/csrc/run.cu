@@ -309,6 +309,7 @@ struct Plan {
     float *bmargin;                 // per brick: proven margin of its single label
     int4 *vbox_prev;                // validity boxes of the previous pass
     unsigned char *tslot;           // per point warp tile: slot of its single label last pass
+    PointCache *pcache;             // per point chunk: its per-cluster sums (k_point_assign4)
     long long *stranded_f, *deferred_f;
     long long cap_f;
     unsigned long long *absmax;     // [0..3] max |point x, y, z, t|, [4] |point v|, [5] |field v|
@@ -534,6 +535,7 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
     P.tbox = cv.take<double>(8 * P.max_tiles);
     P.wbox = cv.take<WBox>(P.max_tiles * (POINT_CHUNK / 64));
     P.tslot = cv.take<unsigned char>(P.max_tiles * (POINT_CHUNK / 64));
+    P.pcache = cv.take<PointCache>(P.max_tiles);
     P.cap_p = n < (1ll << 22) ? n : (1ll << 22);
     P.stranded_p = cv.take<long long>(P.cap_p);
     P.deferred_p = cv.take<long long>(P.cap_p);
@@ -750,6 +752,7 @@ int plan_prepare_impl(Plan &P) {
                                       P.pv, p.c_f, P.tbox, P.wbox, P.perm, P.pts.xyz, P.pts.t,
                                       P.pts.value, st));
         MFSEG_CUDA(cudaMemsetAsync(P.tslot, 255, P.max_tiles * (POINT_CHUNK / 64), st));
+        MFSEG_CUDA(cudaMemsetAsync(P.pcache, 255, sizeof(PointCache) * P.max_tiles, st));   // n = -1
     }
     return check_ranges(P, field_coord_max);
 }
@@ -1022,6 +1025,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
             a.reuse = 1;
             a.bin_stable = P.bstable;
         }
+        if (a.tslot && !(dbg.flags & MFSEG_DEBUG_NO_BLOCK_CACHE)) a.pcache = P.pcache;
         a.overflow = P.overflow;
         a.accumulate = accumulate;
         a.debug = dbg.flags & MFSEG_DEBUG_KERNEL_BITS;
