@@ -17,7 +17,10 @@ checker.  Three kinds of evidence:
   sample-bin blocks (the field kernel's 16^3 x 4 blocks, the point kernel's
   bin-sorted chunks) chosen among the most crowded bins, plus a uniform random
   sample of the whole box;
-* a case with large absolute coordinates (origin 1e6, times in Unix seconds).
+* a case with large absolute coordinates (origin 1e6, times in Unix seconds);
+* the configs[4] slab geometry (1024 x 1024 x 128 planes x 16 steps) and the
+  thin configs[3] geometry (one z plane: the field kernels block along time),
+  plus full thin-field runs.
 
 Bars: labels bit-exact; centres 1e-12 relative (north_star: 1e-5).
 """
@@ -265,4 +268,13 @@ def test_thin_field_full_run_vs_oracle(c_f, seed):
 def test_configs3_geometry_windows_vs_oracle():
     """configs[3]-like thin geometry (one z plane, 16-cell x 16-cell x 8-step bins)."""
     got = _windowed((512, 512, 1), 48, 300_000, (32, 32, 1, 6), 9, passes=(1, 4))
+    assert got["field"] > 1_000_000 and got["point"] > 0
+
+
+def test_configs4_slab_geometry_windows_vs_oracle():
+    """configs[4] per-GPU slab geometry: 1024 x 1024 x 128 planes x 16 steps,
+    k=(32, 32, 4, 4) (bins of 32^3 cells x 4 timesteps), 16M trajectories' worth
+    of points in the slab scaled down to 4M."""
+    got = _windowed((1024, 1024, 128), 16, 4_000_000, (32, 32, 4, 4), 11, passes=(1, 4),
+                    n_bins=6, n_random=1_000_000)
     assert got["field"] > 1_000_000 and got["point"] > 0
