@@ -997,7 +997,13 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
         // (skipped when every brick of this warp keeps its labels)
         bool wneed = need_full;
         if (sstable && need_full) wneed = __any_sync(0xffffffffu, lane < 8 && S.bslot[w + NW * lane] == 255);
-        if (!deferred && cnt > 0 && wneed && GX * rbx < X.len && GY * rby < Y.len) {
+        if (!deferred && cnt > 0 && cnt <= 32 && wneed) {
+            // one round of candidates: the bricks cull them directly (a region cull
+            // would cost a round of its own and remove nothing from the bricks' round)
+            if (lane < cnt) S.lst[w][lane] = lane;
+            if (lane == 0) S.rcg[w] = INF_F;
+            nl = cnt;
+        } else if (!deferred && cnt > 0 && wneed && GX * rbx < X.len && GY * rby < Y.len) {
             float vl = 0.f, vh = 0.f;
             if (USEVAL) {   // value range of the region = union of its bricks' ranges
                 float lo = INF_F, hi = -INF_F;
