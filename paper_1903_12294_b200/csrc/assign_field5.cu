@@ -1224,41 +1224,59 @@ __global__ void __launch_bounds__(NT) k_brick_pre(FieldArgs a) {
     const long long plane = (long long)a.ny * a.nx, vol = plane * a.nz;
     double amax = 0.0;   // max |value| and non-finite flag (range check of the fixed-point sums)
     bool bad = false;
-#pragma unroll 4
-    for (int bi = w; bi < 64; bi += NW) {   // unrolled: several bricks' loads in flight
-        const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
-        if (GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= T.len) continue;
-        const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
-        const int z0 = GZ * bz, t0 = GT * bt;
-        const long long fbase = (((long long)(T.start + t0) * a.nz + Z.start + z0) * a.ny +
-                                 (Y.start + ly)) * (long long)a.nx + (X.start + lx);
-        float lo = INF_F, hi = -INF_F;
-        double vs = 0.0;
+    // two rounds of four bricks per warp; each round issues its 32 loads per lane
+    // before any is used (HBM latency is covered by the loads in flight)
+#pragma unroll 1
+    for (int b0 = w; b0 < 64; b0 += 4 * NW) {
+        double v[4][8];
+        unsigned lv[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const bool live = lx < X.len && ly < Y.len && z0 + (k & 3) < Z.len && t0 + (k >> 2) < T.len;
-            const double v = live ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
-            vs = DADD(vs, v);
-            if (live) {
-                lo = fminf(lo, (float)v);
-                hi = fmaxf(hi, (float)v);
-            }
+        for (int u = 0; u < 4; ++u) {
+            const int bi = b0 + u * NW;
+            const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+            const int lx = GX * bx + (lane & 7), ly = GY * by + (lane >> 3);
+            const int z0 = GZ * bz, t0 = GT * bt;
+            const long long fbase = (((long long)(T.start + t0) * a.nz + Z.start + z0) * a.ny +
+                                     (Y.start + ly)) * (long long)a.nx + (X.start + lx);
+            lv[u] = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (lx < X.len && ly < Y.len && z0 + (k & 3) < Z.len && t0 + (k >> 2) < T.len) lv[u] |= 1u << k;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                v[u][k] = (lv[u] >> k & 1) ? __ldg(a.values + fbase + (k & 3) * plane + (k >> 2) * vol) : 0.0;
         }
-        vs = warp_sum_d(vs);
-        lo = warp_min_f(lo);
-        hi = warp_max_f(hi);
-        // range check of the fixed-point sums, per brick: NaN / inf propagate into
-        // the fp64 sum; |value| is bounded by the fl32 range (inf if it overflows fl32)
-        bad |= !isfinite(vs);
-        amax = fmax(amax, (double)fmaxf(fabsf(lo), fabsf(hi)));
-        if (lane == 0) {
-            a.brange_out[(size_t)blockIdx.x * 64 + bi] = make_float2(lo, hi);
-            unsigned long long flo;
-            long long fhi;
-            int ovf = 0;
-            d2fix(vs, flo, fhi, &ovf);
-            if (ovf) *a.overflow = 1;
-            a.bsum_out[(size_t)blockIdx.x * 64 + bi] = make_ulonglong2(flo, (unsigned long long)fhi);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int bi = b0 + u * NW;
+            const int bx = bi & 1, by = (bi >> 1) & 3, bz = (bi >> 3) & 3, bt = bi >> 5;
+            if (GX * bx >= X.len || GY * by >= Y.len || GZ * bz >= Z.len || GT * bt >= T.len) continue;
+            float lo = INF_F, hi = -INF_F;
+            double vs = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                vs = DADD(vs, v[u][k]);
+                if (lv[u] >> k & 1) {
+                    lo = fminf(lo, (float)v[u][k]);
+                    hi = fmaxf(hi, (float)v[u][k]);
+                }
+            }
+            vs = warp_sum_d(vs);
+            lo = warp_min_f(lo);
+            hi = warp_max_f(hi);
+            // range check of the fixed-point sums, per brick: NaN / inf propagate into
+            // the fp64 sum; |value| is bounded by the fl32 range (inf if it overflows fl32)
+            bad |= !isfinite(vs);
+            amax = fmax(amax, (double)fmaxf(fabsf(lo), fabsf(hi)));
+            if (lane == 0) {
+                a.brange_out[(size_t)blockIdx.x * 64 + bi] = make_float2(lo, hi);
+                unsigned long long flo;
+                long long fhi;
+                int ovf = 0;
+                d2fix(vs, flo, fhi, &ovf);
+                if (ovf) *a.overflow = 1;
+                a.bsum_out[(size_t)blockIdx.x * 64 + bi] = make_ulonglong2(flo, (unsigned long long)fhi);
+            }
         }
     }
     // one atomic per block, and only when it raises the maximum (every block

@@ -29,7 +29,10 @@ constexpr unsigned INF_BITS = 0x7F800000u;
 constexpr unsigned KEY_MASK = 127u;   // same key truncation as k_field_assign5
 constexpr float KSCR = 0x1.0p-18f;
 constexpr int ACC_FV = 10, ACC_NF = 13;   // accumulator words (assign.cu)
-constexpr int SCREEN_MINB = 3;
+#ifndef MFSEG_SCREEN_MINB
+#define MFSEG_SCREEN_MINB 4
+#endif
+constexpr int SCREEN_MINB = MFSEG_SCREEN_MINB;
 
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;

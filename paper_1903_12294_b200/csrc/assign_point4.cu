@@ -37,7 +37,10 @@ constexpr unsigned INF_BITS = 0x7F800000u;
 
 constexpr int NT = 128, NW = 4;   // 4 warps: a short per-CTA tail, 6 CTAs per SM
 constexpr int CR = 2;             // raw candidate rounds of NT (up to 256 per bin)
-constexpr int MINB = 6;
+#ifndef MFSEG_POINT_MINB
+#define MFSEG_POINT_MINB 6
+#endif
+constexpr int MINB = MFSEG_POINT_MINB;
 constexpr int CAP = 128;
 constexpr unsigned SLOT_MASK = 127u;
 constexpr float KSCR = 0x1.0p-18f;

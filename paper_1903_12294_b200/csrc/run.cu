@@ -128,7 +128,7 @@ __global__ void k_tbins(int nt, const double *times, double mn, double C, int k,
 // bin (t, z, y, x bits from high to low), so consecutive points - a warp's
 // 64 - form compact 4D blocks.  Tiles are cut per (bin, interval) group.
 __global__ void k_point_keys(long long n, const double *xyz, const double *t, double4 mins,
-                             double4 C, int4 k, const double *times, int nt, int sub_bits,
+                             double4 C, double4 inv, int4 k, const double *times, int nt, int sub_bits,
                              unsigned *keys, unsigned *vals) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -137,9 +137,18 @@ __global__ void k_point_keys(long long n, const double *xyz, const double *t, do
     const int kk[4] = {k.x, k.y, k.z, k.w};
     int b[4];
     unsigned sd[4];
+    const double iC[4] = {inv.x, inv.y, inv.z, inv.w};
     for (int d = 0; d < 4; ++d) {
-        const double u = DDIV(DSUB(c[d], mn[d]), CC[d]);
-        b[d] = bin_coord(c[d], mn[d], CC[d], kk[d]);
+        // u = fl((c - mn) / C) as bin_coord computes it; the quotient only enters
+        // through floor(u) and floor(8 u), so a reciprocal product (within a few
+        // ulps of it) serves unless 8 u lies near an integer: then divide exactly
+        const double dd = DSUB(c[d], mn[d]);
+        double u = DMUL(dd, iC[d]);
+        const double e = DMUL(u, 8.0), fe = floor(e);
+        const double tol = 1e-13 * fabs(e) + 1e-13;
+        if (!(fabs(e) < 1e15) || e - fe < tol || fe + 1.0 - e < tol) u = DDIV(dd, CC[d]);
+        const double q = floor(u);   // bin_coord's clamps
+        b[d] = !(q >= 0.0) ? 0 : (q >= (double)(kk[d] - 1) ? kk[d] - 1 : (int)q);
         const double f = floor(DMUL(u, 8.0)) - 8.0 * b[d];
         sd[d] = f < 0.0 ? 0u : (f > 7.0 ? 7u : (unsigned)f);
     }
@@ -725,7 +734,8 @@ int plan_prepare_impl(Plan &P) {
         int4 k = make_int4(p.k[0], p.k[1], p.k[2], p.k[3]);
         unsigned gb = (unsigned)((n + 255) / 256);
         ::mfseg::count_launch();
-        k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, k, P.f.times, P.nint,
+        const double4 inv = make_double4(1.0 / p.C[0], 1.0 / p.C[1], 1.0 / p.C[2], 1.0 / p.C[3]);
+        k_point_keys<<<gb, 256, 0, st>>>(n, P.pts.xyz, P.pts.t, mins, C, inv, k, P.f.times, P.nint,
                                          P.sub_bits, P.keys, P.vals);
         MFSEG_LAUNCH("k_point_keys");
         if (P.key_bits > 32) {

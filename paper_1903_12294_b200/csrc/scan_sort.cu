@@ -131,10 +131,15 @@ __global__ void k_digit_hist(const K *keys, long long n, int shift, unsigned *co
     for (int i = threadIdx.x; i < 256; i += RS_BLOCK) h[i] = 0;
     __syncthreads();
     long long base = (long long)blockIdx.x * RS_TILE;
-    for (int j = threadIdx.x; j < RS_TILE; j += RS_BLOCK) {
-        long long i = base + j;
-        if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & 255u], 1u);
+    K kk[RS_TILE / RS_BLOCK];   // every load in flight before the first atomic
+#pragma unroll
+    for (int j = 0; j < RS_TILE / RS_BLOCK; ++j) {
+        const long long i = base + j * RS_BLOCK + threadIdx.x;
+        kk[j] = i < n ? keys[i] : K(0);
     }
+#pragma unroll
+    for (int j = 0; j < RS_TILE / RS_BLOCK; ++j)
+        if (base + j * RS_BLOCK + threadIdx.x < n) atomicAdd(&h[(unsigned)(kk[j] >> shift) & 255u], 1u);
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += RS_BLOCK) counts[(long long)d * tiles + blockIdx.x] = h[d];
 }
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
     __shared__ __align__(16) unsigned char raw[RAW];
     __shared__ unsigned wpre[RS_WARPS][256];   // tile-local start of (warp, digit)
     __shared__ unsigned loc[257];              // tile-local start of each digit
+    __shared__ unsigned goff[256];             // global start of each digit's run minus loc
     unsigned (*run)[256] = reinterpret_cast<unsigned (*)[256]>(raw);
     K *sk = reinterpret_cast<K *>(raw);
     unsigned *sv = nullptr;
@@ -165,11 +171,15 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
     unsigned vv[RS_ROUNDS], rk[RS_ROUNDS];
     unsigned lt = (1u << lane) - 1u;
 #pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {   // every load in flight before the ranking
+        const long long i = base + r * 32 + lane;
+        kk[r] = i < n ? keys[i] : K(0);
+        vv[r] = i < n ? vals[i] : 0u;
+    }
+#pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
         long long i = base + r * 32 + lane;
         bool in = i < n;
-        kk[r] = in ? keys[i] : K(0);
-        vv[r] = in ? vals[i] : 0u;
         unsigned d = in ? ((unsigned)(kk[r] >> shift) & 255u) : 256u;
         unsigned peers = __match_any_sync(0xffffffffu, d);
         unsigned before = in ? run[w][d] : 0u;
@@ -213,6 +223,8 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
         if (threadIdx.x == 31) loc[256] = run_s;
     }
     __syncthreads();
+    if (STAGE && threadIdx.x < 256) goff[threadIdx.x] = offs[(long long)threadIdx.x * tiles + blockIdx.x] - loc[threadIdx.x];
+    __syncthreads();
     if constexpr (!STAGE) {   // 64-bit keys: direct scatter (link index, trajectory split)
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 5) k_digit_scatter(const K *keys, co
         for (int i = threadIdx.x; i < items; i += RS_BLOCK) {
             const K k = sk[i];
             const unsigned d = (unsigned)(k >> shift) & 255u;
-            const unsigned pos = offs[(long long)d * tiles + blockIdx.x] + (unsigned)i - loc[d];
+            const unsigned pos = goff[d] + (unsigned)i;
             ko[pos] = k;
             vo[pos] = sv[i];
         }
