@@ -492,6 +492,42 @@ def test_assign_drifted_centres_vs_oracle(w_d, seed):
     np.testing.assert_array_equal(pl, want_p)
 
 
+@pytest.mark.parametrize("seed", [31, 32])
+def test_points_on_bin_and_subcell_edges_vs_oracle(seed):
+    """Point sort keys take the bin from a reciprocal product and divide exactly
+    only near a sub-cell edge (k_point_keys): points placed exactly on bin and
+    eighth-of-bin edges of a non-dyadic extent, and one ulp either side, are
+    binned and labelled like the C oracle's fl((x - min) / C)."""
+    P = pkg()
+    rng = np.random.default_rng(seed)
+    ext = P.DomainExtent(0.1, 1.37, -0.3, 0.71, 0.05, 0.93, 3.0, 17.7)
+    params = P.ClusterParams(k=(7, 5, 3, 6), w_d=1.0, w_p=1.0, w_f=1.0)
+    C = P.interval_distances(ext, params.k)
+    mins, maxs = ext.mins, ext.maxs
+    n = 60000
+    loc = np.empty((n, 4))
+    for d in range(4):
+        j = rng.integers(0, 8 * params.k[d] + 1, n)
+        x = mins[d] + j * (C[d] / 8.0)
+        step = rng.integers(-1, 2, n)
+        x = np.where(step < 0, np.nextafter(x, -np.inf), np.where(step > 0, np.nextafter(x, np.inf), x))
+        loc[:, d] = np.clip(x, mins[d], maxs[d])
+    ps = P.PointSet(np.arange(n, dtype=np.int64) // 8, loc[:, 3].copy(), loc[:, :3].copy(), rng.random(n))
+    dims, nt = (5, 4, 3), 2
+    fs = P.FieldSet(dims, np.array([0.2, -0.2, 0.1]), np.array([0.25, 0.2, 0.25]), np.array([4.0, 9.0]),
+                    rng.random((nt, int(np.prod(dims)))))
+    K = params.k_total
+    cs = P.CenterState.from_seeds(P.seed_centers(ext, params.k) + rng.uniform(-0.45, 0.45, (K, 4)) * C)
+    cs.pval = np.where(rng.random(K) < 0.8, rng.random(K), np.nan)
+    cs.fval = np.where(rng.random(K) < 0.8, rng.random(K), np.nan)
+    cs.has_p, cs.has_f = ~np.isnan(cs.pval), ~np.isnan(cs.fval)
+    grid = P.CenterGrid(cs.loc, ext, C, params.k)
+    pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
+    want_p, want_f = _oracle_labels(ps, fs, cs, ext, C, params)
+    np.testing.assert_array_equal(pl, want_p)
+    np.testing.assert_array_equal(fl, want_f)
+
+
 @pytest.mark.parametrize("opts", [dict(multi_cap=0), dict(multi_cap=37), dict(flags=2),
                                   dict(flags=1), dict(flags=16), dict(flags=32), dict(flags=64),
                                   dict(flags=256)])
