@@ -116,7 +116,8 @@ int32_t mfseg_timing_read(double *ms_out, int32_t n);
 /* Diagnostics / test knobs for the calling thread (defaults 0 / -1 are the
  * product behaviour; no environment variable is read by the library):
  * flags: bit 0 no tile culling, bit 1 exact fp64 for every surviving
- * candidate, bit 3 per-pass statistics on stderr, bit 4 no reuse of unchanged
+ * candidate, bit 3 per-pass statistics on stderr (the kernels' path counters
+ * only in a library built with -DMFSEG_DEVICE_STATS=1), bit 4 no reuse of unchanged
  * blocks / chunks across passes, bit 5 exact reuse only (no margin reuse);
  * multi_cap >= 0 caps the multi-candidate brick queue (the overflow takes the
  * exact per-sample path).  Results are identical for every setting. */

@@ -505,7 +505,7 @@ __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C,
         // least w_v min(f(v_lo), f(v_hi)), f(v) = |v - cv_s| - |v - cv_s*| (both have
         // values; f is monotone in v), or -w_v max|v - cv_s*| (only s* has one).
         ubkey = __reduce_min_sync(0xffffffffu, ubkey);
-        if ((a.debug & 8) && lane == 0) {
+        if (DEVICE_STATS(a) && lane == 0) {
             const int nc = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
             atomicAdd(a.stats + 7, (unsigned long long)nc);
             if (nc == 1) atomicAdd(a.stats + 2, 1ull);
@@ -598,8 +598,8 @@ __device__ __forceinline__ int brick(const FieldArgs &a, Smem5 &S, const Ctx &C,
                 if (dom) gmin = fminf(gmin, gd);
             }
         }
-        if ((a.debug & 8) && lane == 0 && sstar < 0) atomicAdd(a.stats + 30, 1ull);   // no s*
-        if ((a.debug & 8) && lane == 0) {
+        if (DEVICE_STATS(a) && lane == 0 && sstar < 0) atomicAdd(a.stats + 30, 1ull);   // no s*
+        if (DEVICE_STATS(a) && lane == 0) {
             atomicAdd(a.stats, 1ull);
             atomicAdd(a.stats + 1, (unsigned long long)(__popc(keep[0]) + __popc(keep[1]) +
                                                          __popc(keep[2]) + __popc(keep[3])));
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                     if (q == 5) atomicAdd(dst + 13, bc.cnt[ce]);
                     else atomic_add_fix(dst + (q < 4 ? 2 * q : 10), bc.w[ce][2 * q], (long long)bc.w[ce][2 * q + 1]);
                 }
-                if ((a.debug & 8) && tid < 64 && live) atomicAdd(a.stats + 24, 1ull);
+                if (DEVICE_STATS(a) && tid < 64 && live) atomicAdd(a.stats + 24, 1ull);
                 return;
             }
         }
@@ -1022,7 +1022,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
             const int zg1 = (Z.len - 1) / GZ, tg1 = (Tm.len - 1) / GT;
             nl = C.nrounds <= 3 ? region_list<USEVAL, 3>(S, C, rbx, rby, 0, zg1, 0, tg1, vl, vh, a.debug)
                                 : region_list<USEVAL, 4>(S, C, rbx, rby, 0, zg1, 0, tg1, vl, vh, a.debug);
-            if ((a.debug & 8) && lane == 0) {
+            if (DEVICE_STATS(a) && lane == 0) {
                 atomicAdd(a.stats + 4, 1ull);
                 if (nl >= 0) {
                     atomicAdd(a.stats + 5, 1ull);
@@ -1088,7 +1088,7 @@ __global__ void __launch_bounds__(NT, MINB) k_field_assign5(FieldArgs a) {
                     run_brick_sums(S, L, bx, by, rcg, lo, hi);
                 }
             }
-            if ((a.debug & 8) && lane == 0) atomicAdd(a.stats + 24, (unsigned long long)__popc(rmask));
+            if (DEVICE_STATS(a) && lane == 0) atomicAdd(a.stats + 24, (unsigned long long)__popc(rmask));
         }
     }
     bool nocache = false;                 // a brick not labelled by one slot (block cache)

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
             sl[k] = ok ? (int)(b1[k] & KEY_MASK) : -1;
             if (!ok && (livem >> k & 1)) need |= 1u << k;
         }
-        if ((a.debug & 8) && a.stats) {   // counters[33]: items, [34]: exact samples
+        if (DEVICE_STATS(a) && a.stats) {   // counters[33]: items, [34]: exact samples
             if (lane == 0) atomicAdd(a.stats + 25, 1ull);
             if (need) atomicAdd(a.stats + 26, (unsigned long long)__popc(need));
         }

@@ -371,7 +371,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
                 else keep[3] &= ~db;
             }
         }
-        if ((a.debug & 8) && lane == 0) {
+        if (DEVICE_STATS(a) && lane == 0) {
             const int nk = __popc(keep[0]) + __popc(keep[1]) + __popc(keep[2]) + __popc(keep[3]);
             if (nk == 1 && sdom >= 0) atomicAdd(a.stats + 3, 1ull);
             atomicAdd(a.stats + 4 + min(nk, 7), 1ull);
@@ -447,7 +447,7 @@ __device__ __forceinline__ void point_warp(const PointArgs &a, PSmem4 &S, const 
         sl0 = ok0 ? (int)(a1k & SLOT_MASK) : -1;
         sl1 = ok1 ? (int)(b1k & SLOT_MASK) : -1;
         const bool need0 = live0 && !ok0, need1 = live1 && !ok1;
-        if ((a.debug & 8) && (need0 || need1)) atomicAdd(a.stats + 2, (unsigned long long)(need0 + need1));
+        if (DEVICE_STATS(a) && (need0 || need1)) atomicAdd(a.stats + 2, (unsigned long long)(need0 + need1));
         if (__any_sync(0xffffffffu, need0 || need1) && (need0 || need1)) {
             // exact fp64 over every kept candidate inside the margin (all of them
             // when a box test was inside the guard band or the screen overflowed)
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(NT, MINB) k_point_assign4(PointArgs a) {
         C.wvf = USEVAL ? (float)a.wv : 0.f;
         C.cnt = cnt;
         C.nrounds = (cnt + 31) >> 5;
-        if (a.debug & 8) atomicAdd(a.stats + 11 + min(max(C.nrounds, 1), 4), 1ull);
+        if (DEVICE_STATS(a)) atomicAdd(a.stats + 11 + min(max(C.nrounds, 1), 4), 1ull);
         C.len = T.z;
         C.start = T.y;
         C.deferred = deferred;

@@ -4,6 +4,14 @@
 
 #include "common.cuh"
 
+// Device-side path counters of the assignment kernels (MFSEG_DEBUG_STATS): compiled
+// only into a diagnostics build (-DMFSEG_DEVICE_STATS=1, tools/variant_time.sh); the
+// product build drops the checks from the hot loops.
+#ifndef MFSEG_DEVICE_STATS
+#define MFSEG_DEVICE_STATS 0
+#endif
+#define DEVICE_STATS(args) (MFSEG_DEVICE_STATS && ((args).debug & 8))
+
 namespace mfseg {
 
 // A field brick left with several candidates after culling and dominance:

@@ -1101,7 +1101,10 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
     }
     mark(4, st);
     {
-        if (dbg.flags & MFSEG_DEBUG_STATS) {
+        if (dbg.flags & MFSEG_DEBUG_STATS) {   // (kernel path counters: MFSEG_DEVICE_STATS builds only)
+            if (!MFSEG_DEVICE_STATS)
+                fprintf(stderr, "[mfseg stats] this library was built without -DMFSEG_DEVICE_STATS=1: "
+                                "the kernel path counters below stay 0\n");
             unsigned long long h[40];
             MFSEG_CUDA(cudaMemcpyAsync(h, P.counters, sizeof h, cudaMemcpyDeviceToHost, st));
             MFSEG_CUDA(cudaStreamSynchronize(st));
