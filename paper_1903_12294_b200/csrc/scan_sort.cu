@@ -96,9 +96,40 @@ __global__ void k_tile_scan(const T *in, T *out, long long n, const T *offs) {
     }
 }
 
+// small arrays (the per-pass grid scans over bins, up to 8192 entries): one
+// CTA, one launch; each thread scans a contiguous segment of <= 8 items, all
+// loaded before use (in == out works: reads precede writes)
+constexpr int SCAN_ONE_PER = 8;
+constexpr long long SCAN_ONE_MAX = (long long)SCAN_ONE_PER * SCAN_BLOCK;
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_one(const T *in, T *out, long long n) {
+    __shared__ T sm[32];
+    const long long b = (long long)threadIdx.x * SCAN_ONE_PER;
+    T v[SCAN_ONE_PER];
+    T s = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ONE_PER; ++j) {
+        v[j] = b + j < n ? in[b + j] : T(0);
+        s += v[j];
+    }
+    T ex = block_exclusive_scan<T>(s, sm, nullptr);
+#pragma unroll
+    for (int j = 0; j < SCAN_ONE_PER; ++j) {
+        if (b + j < n) out[b + j] = ex;
+        ex += v[j];
+    }
+}
+
 template <class T>
 int scan_impl(const T *in, T *out, long long n, void *tmp, size_t tmp_bytes, cudaStream_t st) {
     if (n <= 0) return 0;
+    if (n <= SCAN_ONE_MAX) {
+        ::mfseg::count_launch();
+        k_scan_one<T><<<1, SCAN_BLOCK, 0, st>>>(in, out, n);
+        MFSEG_LAUNCH("scan");
+        return 0;
+    }
     long long tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (tmp_bytes < sizeof(T) * (size_t)tiles) {
         set_error("scan: workspace too small");
