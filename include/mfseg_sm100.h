@@ -130,6 +130,7 @@ int32_t mfseg_timing_read(double *ms_out, int32_t n);
 #define MFSEG_DEBUG_NO_SEEDS_FAST 64   /* initial pass: no interior-block shortcut */
 #define MFSEG_DEBUG_NO_ZT_SWAP 128     /* thin fields: blocks along z, not time */
 #define MFSEG_DEBUG_NO_BLOCK_CACHE 256 /* field blocks: no cached sums of fully reused blocks */
+#define MFSEG_DEBUG_DEFERRED_BATCH 512 /* crowded tiles: one sample per lane at any list length */
 int mfseg_set_debug_options(int32_t flags, int64_t multi_cap);
 
 /* ---------------------------------------------------------------- full run

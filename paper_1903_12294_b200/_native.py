@@ -150,6 +150,7 @@ DEBUG_NO_MARGIN_REUSE = 32
 DEBUG_NO_SEEDS_FAST = 64
 DEBUG_NO_ZT_SWAP = 128
 DEBUG_NO_BLOCK_CACHE = 256
+DEBUG_DEFERRED_BATCH = 512
 
 
 @contextlib.contextmanager

@@ -167,11 +167,12 @@ struct DeferredGeo {
     const long long *list;
     const unsigned long long *count;
     long long cap;
+    long long batch_min;   // list length from which samples go one per lane
 };
 
-__device__ void deferred_one(const FallbackArgs &a, const DeferredGeo &G, long long idx) {
-    const int lane = threadIdx.x & 31;
-    double s0, s1, s2, s3, v;
+// the deferred sample's coordinates, value and sample bin
+__device__ __forceinline__ int deferred_sample(const FallbackArgs &a, const DeferredGeo &G, long long idx,
+                                               double &s0, double &s1, double &s2, double &s3, double &v) {
     int bt;
     if (a.kind == 1) {
         long long r = idx;
@@ -198,34 +199,29 @@ __device__ void deferred_one(const FallbackArgs &a, const DeferredGeo &G, long l
     const int bx = bin_coord(s0, G.mins[0], a.C[0], G.k.x);
     const int by = bin_coord(s1, G.mins[1], a.C[1], G.k.y);
     const int bz = bin_coord(s2, G.mins[2], a.C[2], G.k.z);
-    const int sbin = ((bt * G.k.z + bz) * G.k.y + by) * G.k.x + bx;
-    double bD = INF;
-    int bI = INT_MAX;
-    for (int p = G.g.cand_start[sbin] + lane; p < G.g.cand_start[sbin + 1]; p += 32) {
-        const int c = G.g.cand_ids[p];
-        const double dx = DSUB(a.c.x[c], s0), dy = DSUB(a.c.y[c], s1), dz = DSUB(a.c.z[c], s2),
-                     dt = DSUB(a.c.t[c], s3);
-        if (!(fabs(dx) <= a.C[0] && fabs(dy) <= a.C[1] && fabs(dz) <= a.C[2] && fabs(dt) <= a.C[3]))
-            continue;
-        const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
-        const double ct = DMUL(a.cf, dt);
-        const bool h = a.chas[c] != 0;
-        const double D = metric_tail(qq, DMUL(ct, ct), v, h ? a.cval[c] : 0.0, h, a.wv, a.wd);
-        if (better(D, c, bD, bI)) {
-            bD = D;
-            bI = c;
-        }
+    return ((bt * G.k.z + bz) * G.k.y + by) * G.k.x + bx;
+}
+
+// the windowed predicate for one (sample, candidate) pair: (D, id) minimum update
+__device__ __forceinline__ void deferred_pair(const FallbackArgs &a, int c, double s0, double s1, double s2,
+                                              double s3, double v, double &bD, int &bI) {
+    const double dx = DSUB(a.c.x[c], s0), dy = DSUB(a.c.y[c], s1), dz = DSUB(a.c.z[c], s2),
+                 dt = DSUB(a.c.t[c], s3);
+    if (!(fabs(dx) <= a.C[0] && fabs(dy) <= a.C[1] && fabs(dz) <= a.C[2] && fabs(dt) <= a.C[3]))
+        return;
+    const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
+    const double ct = DMUL(a.cf, dt);
+    const bool h = a.chas[c] != 0;
+    const double D = metric_tail(qq, DMUL(ct, ct), v, h ? a.cval[c] : 0.0, h, a.wv, a.wd);
+    if (better(D, c, bD, bI)) {
+        bD = D;
+        bI = c;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double oD = __shfl_xor_sync(0xffffffffu, bD, o);
-        const int oI = __shfl_xor_sync(0xffffffffu, bI, o);
-        if (better(oD, oI, bD, bI)) {
-            bD = oD;
-            bI = oI;
-        }
-    }
-    if (lane != 0) return;
+}
+
+// label, stranded list or per-sample fixed-point sums of one resolved sample
+__device__ __forceinline__ void deferred_finish(const FallbackArgs &a, long long idx, int bI, double s0,
+                                                double s1, double s2, double s3, double v) {
     if (bI == INT_MAX) {   // stranded: the fallback kernel runs next
         a.labels[idx] = -1;
         if (a.kind == 0 && a.labels_out) a.labels_out[a.perm[idx]] = -1;
@@ -246,11 +242,88 @@ __device__ void deferred_one(const FallbackArgs &a, const DeferredGeo &G, long l
     }
 }
 
+// one sample, the warp's lanes over its candidates
+__device__ void deferred_one(const FallbackArgs &a, const DeferredGeo &G, long long idx) {
+    const int lane = threadIdx.x & 31;
+    double s0, s1, s2, s3, v;
+    const int sbin = deferred_sample(a, G, idx, s0, s1, s2, s3, v);
+    double bD = INF;
+    int bI = INT_MAX;
+    for (int p = G.g.cand_start[sbin] + lane; p < G.g.cand_start[sbin + 1]; p += 32)
+        deferred_pair(a, G.g.cand_ids[p], s0, s1, s2, s3, v, bD, bI);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oD = __shfl_xor_sync(0xffffffffu, bD, o);
+        const int oI = __shfl_xor_sync(0xffffffffu, bI, o);
+        if (better(oD, oI, bD, bI)) {
+            bD = oD;
+            bI = oI;
+        }
+    }
+    if (lane == 0) deferred_finish(a, idx, bI, s0, s1, s2, s3, v);
+}
+
+// 32 consecutive list entries, one per lane: when they share a sample bin (the
+// lists are written brick by brick) every lane scans the bin's candidates for
+// its own sample (the candidate loads are warp broadcasts); otherwise one
+// sample at a time
+__device__ void deferred_batch(const FallbackArgs &a, const DeferredGeo &G, long long q0, long long n) {
+    const int lane = threadIdx.x & 31;
+    const long long q = q0 + lane;
+    const bool valid = q < n;
+    const long long idx = valid ? G.list[q] : G.list[q0];
+    double s0, s1, s2, s3, v;
+    const int sbin = deferred_sample(a, G, idx, s0, s1, s2, s3, v);
+    const int sb0 = __shfl_sync(0xffffffffu, sbin, 0);
+    if (!__all_sync(0xffffffffu, sbin == sb0)) {
+        const int m = (int)min(32ll, n - q0);
+        for (int j = 0; j < m; ++j) deferred_one(a, G, __shfl_sync(0xffffffffu, idx, j));
+        return;
+    }
+    double bD = INF;
+    int bI = INT_MAX;
+    const int p1 = G.g.cand_start[sb0 + 1];
+    int p = G.g.cand_start[sb0];
+    for (; p + 4 <= p1; p += 4) {   // four candidates' state in flight
+        int c[4];
+        double cx[4], cy[4], cz[4], ct[4], cv[4];
+        bool ch[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[u] = G.g.cand_ids[p + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            cx[u] = a.c.x[c[u]];
+            cy[u] = a.c.y[c[u]];
+            cz[u] = a.c.z[c[u]];
+            ct[u] = a.c.t[c[u]];
+            ch[u] = a.chas[c[u]] != 0;
+            cv[u] = a.cval[c[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double dx = DSUB(cx[u], s0), dy = DSUB(cy[u], s1), dz = DSUB(cz[u], s2), dt = DSUB(ct[u], s3);
+            if (!(fabs(dx) <= a.C[0] && fabs(dy) <= a.C[1] && fabs(dz) <= a.C[2] && fabs(dt) <= a.C[3]))
+                continue;
+            const double qq = DADD(DADD(DMUL(dx, dx), DMUL(dy, dy)), DMUL(dz, dz));
+            const double tt = DMUL(a.cf, dt);
+            const double D = metric_tail(qq, DMUL(tt, tt), v, ch[u] ? cv[u] : 0.0, ch[u], a.wv, a.wd);
+            if (better(D, c[u], bD, bI)) {
+                bD = D;
+                bI = c[u];
+            }
+        }
+    }
+    for (; p < p1; ++p) deferred_pair(a, G.g.cand_ids[p], s0, s1, s2, s3, v, bD, bI);
+    if (valid) deferred_finish(a, idx, bI, s0, s1, s2, s3, v);
+}
+
 __global__ void k_deferred(FallbackArgs a, DeferredGeo G) {
     const long long n = (long long)*G.count;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (n <= G.cap) {
+    if (n <= G.cap && n >= G.batch_min) {   // many samples: one per lane
+        for (long long q = 32 * wid; q < n; q += 32 * warps) deferred_batch(a, G, q, n);
+    } else if (n <= G.cap) {               // few: the warp's lanes over each sample's candidates
         for (long long q = wid; q < n; q += warps) deferred_one(a, G, G.list[q]);
     } else {
         for (long long q = wid; q < a.n_samples; q += warps)
@@ -330,8 +403,10 @@ int launch_deferred(const FallbackArgs &a, const Grid &g, const int *tbin, const
     G.list = list;
     G.count = count;
     G.cap = cap;
+    constexpr int blocks = 148 * 4, threads = 256;
+    G.batch_min = (debug_options().flags & MFSEG_DEBUG_DEFERRED_BATCH) ? 0 : 16ll * blocks * (threads / 32);
     ::mfseg::count_launch();
-    k_deferred<<<148 * 4, 256, 0, st>>>(a, G);
+    k_deferred<<<blocks, threads, 0, st>>>(a, G);
     MFSEG_LAUNCH("k_deferred");
     return 0;
 }

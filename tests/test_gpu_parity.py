@@ -718,11 +718,14 @@ def test_segment_sharded_single_rank_matches_segment(normalize):
     np.testing.assert_array_equal([c.x_c for c in seg.centers], [c.x_c for c in ref.centers])
 
 
-def test_assign_crowded_vs_oracle():
+@pytest.mark.parametrize("flags", [0, 512])
+def test_assign_crowded_vs_oracle(flags):
     """~1.4 centres per bin: candidate lists of ~100-130 exercise the 4-round
-    variants of both assignment kernels and the deferral of lists > 128;
-    labels bit-exact against the C oracle."""
+    variants of both assignment kernels and the deferral of lists > 128
+    (flags 512: the deferred samples one per lane, k_deferred's path for long
+    lists); labels bit-exact against the C oracle."""
     P = pkg()
+    from paper_1903_12294_b200 import _native as N
     from paper_1903_12294_b200.ingest import domain_extent_device, normalize_device
     dims, nt, ntraj = (64, 48, 32), 12, 6000
     fld, pts, _ = _synthetic(dims, nt, ntraj, 31, False)
@@ -744,7 +747,8 @@ def test_assign_crowded_vs_oracle():
                     fld.values.cpu().numpy().reshape(nt, -1))
     ps = P.PointSet(np.zeros(pts.n, np.int64), pts.t.cpu().numpy(), pts.xyz.cpu().numpy(),
                     pts.value.cpu().numpy())
-    pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
+    with N.debug_options(flags):
+        pl, fl = P.assign_iteration(ps, fs, None, cs, grid, params, C)
     want_p, want_f = _oracle_labels(ps, fs, cs, ext, C, params)
     np.testing.assert_array_equal(fl, want_f)
     np.testing.assert_array_equal(pl, want_p)
