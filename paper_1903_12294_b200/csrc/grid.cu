@@ -122,53 +122,47 @@ __device__ __forceinline__ void unflat(int b, int4 k, int &bx, int &by, int &bz,
     bt = b / k.z;
 }
 
-__global__ void k_cand_count(int nbins, int4 k, const int *bin_start, int *cand_count) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nbins) return;
+// One warp per bin: lane r < 27 takes neighbour row r = (dt, dz, dy) in the
+// reference's loop order (dt outer, dy inner); a row is the x-run of bins
+// [bx - 1, bx + 1], contiguous in bin_ids.  Returns the row's (start, length).
+__device__ __forceinline__ int2 cand_row(long long b, int4 k, const int *bin_start, int lane) {
     int bx, by, bz, bt;
-    unflat(b, k, bx, by, bz, bt);
-    int n = 0;
-    for (int dt = -1; dt <= 1; ++dt) {
-        int qt = bt + dt;
-        if (qt < 0 || qt >= k.w) continue;
-        for (int dz = -1; dz <= 1; ++dz) {
-            int qz = bz + dz;
-            if (qz < 0 || qz >= k.z) continue;
-            for (int dy = -1; dy <= 1; ++dy) {
-                int qy = by + dy;
-                if (qy < 0 || qy >= k.y) continue;
-                int row = ((qt * k.z + qz) * k.y + qy) * k.x;
-                int lo = max(bx - 1, 0), hi = min(bx + 1, k.x - 1);
-                n += bin_start[row + hi + 1] - bin_start[row + lo];
-            }
+    unflat((int)b, k, bx, by, bz, bt);
+    int2 r = make_int2(0, 0);
+    if (lane < 27) {
+        const int qt = bt + lane / 9 - 1, qz = bz + (lane / 3) % 3 - 1, qy = by + lane % 3 - 1;
+        if (qt >= 0 && qt < k.w && qz >= 0 && qz < k.z && qy >= 0 && qy < k.y) {
+            const int row = ((qt * k.z + qz) * k.y + qy) * k.x;
+            const int lo = max(bx - 1, 0), hi = min(bx + 1, k.x - 1);
+            r.x = bin_start[row + lo];
+            r.y = bin_start[row + hi + 1] - r.x;
         }
     }
-    cand_count[b] = n;
+    return r;
+}
+
+__global__ void k_cand_count(int nbins, int4 k, const int *bin_start, int *cand_count) {
+    const int lane = threadIdx.x & 31;
+    const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    if (b >= nbins) return;   // warp-uniform
+    const int n = __reduce_add_sync(0xffffffffu, (unsigned)cand_row(b, k, bin_start, lane).y);
+    if (lane == 0) cand_count[b] = n;
 }
 
 __global__ void k_cand_fill(int nbins, int4 k, const int *bin_start, const int *bin_ids,
                             const int *cand_start, int *cand_ids) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nbins) return;
-    int bx, by, bz, bt;
-    unflat(b, k, bx, by, bz, bt);
-    int o = cand_start[b];
-    for (int dt = -1; dt <= 1; ++dt) {
-        int qt = bt + dt;
-        if (qt < 0 || qt >= k.w) continue;
-        for (int dz = -1; dz <= 1; ++dz) {
-            int qz = bz + dz;
-            if (qz < 0 || qz >= k.z) continue;
-            for (int dy = -1; dy <= 1; ++dy) {
-                int qy = by + dy;
-                if (qy < 0 || qy >= k.y) continue;
-                int row = ((qt * k.z + qz) * k.y + qy) * k.x;
-                int lo = max(bx - 1, 0), hi = min(bx + 1, k.x - 1);
-                for (int p = bin_start[row + lo]; p < bin_start[row + hi + 1]; ++p)
-                    cand_ids[o++] = bin_ids[p];
-            }
-        }
+    const int lane = threadIdx.x & 31;
+    const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    if (b >= nbins) return;   // warp-uniform
+    const int2 r = cand_row(b, k, bin_start, lane);
+    int incl = r.y;   // rows' output offsets: exclusive prefix over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
+    const int o = cand_start[b] + incl - r.y;
+    for (int i = 0; i < r.y; ++i) cand_ids[o + i] = bin_ids[r.x + i];
 }
 
 }  // namespace
@@ -222,11 +216,12 @@ int grid_build(Grid &g, const double *x, const double *y, const double *z, const
     }
     ::mfseg::count_launch();
     k_bin_sort<<<gb, B, 0, st>>>(NB, g.bin_start, g.bin_ids);
+    const unsigned gw = (unsigned)((32ll * NB + B - 1) / B);   // one warp per bin
     ::mfseg::count_launch();
-    k_cand_count<<<gb, B, 0, st>>>(NB, k, g.bin_start, count_tmp);
+    k_cand_count<<<gw, B, 0, st>>>(NB, k, g.bin_start, count_tmp);
     MFSEG_TRY(scan_exclusive_i32(count_tmp, g.cand_start, NB + 1, scan_tmp, sb, st));
     ::mfseg::count_launch();
-    k_cand_fill<<<gb, B, 0, st>>>(NB, k, g.bin_start, g.bin_ids, g.cand_start, g.cand_ids);
+    k_cand_fill<<<gw, B, 0, st>>>(NB, k, g.bin_start, g.bin_ids, g.cand_start, g.cand_ids);
     if (f && f->nt > 0 && K > 0) {
         FieldGeom fg{f->nx, f->ny, f->nz, f->nt, f->origin[0], f->origin[1], f->origin[2],
                      f->spacing[0], f->spacing[1], f->spacing[2], f->offset[0], f->offset[1],
