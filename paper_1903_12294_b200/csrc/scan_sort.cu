@@ -75,9 +75,18 @@ __global__ void k_scan_small(T *a, long long m) {
     }
 }
 
+// offs: the tiles' exclusive offsets (k_scan_small); null: this tile's offset is
+// summed here from the raw tile sums (at most SCAN_BLOCK tiles: one per thread)
 template <class T>
-__global__ void k_tile_scan(const T *in, T *out, long long n, const T *offs) {
+__global__ void k_tile_scan(const T *in, T *out, long long n, const T *offs, const T *sums) {
     __shared__ T sm[32];
+    T off;
+    if (offs) {
+        off = offs[blockIdx.x];
+    } else {
+        const T mine = (int)threadIdx.x < (int)blockIdx.x ? sums[threadIdx.x] : T(0);
+        block_exclusive_scan<T>(mine, sm, &off);
+    }
     long long base = (long long)blockIdx.x * SCAN_TILE + (long long)threadIdx.x * SCAN_ITEMS;
     T v[SCAN_ITEMS];
     T s = 0;
@@ -87,7 +96,7 @@ __global__ void k_tile_scan(const T *in, T *out, long long n, const T *offs) {
         v[j] = i < n ? in[i] : T(0);
         s += v[j];
     }
-    T ex = block_exclusive_scan<T>(s, sm, nullptr) + offs[blockIdx.x];
+    T ex = block_exclusive_scan<T>(s, sm, nullptr) + off;
 #pragma unroll
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         long long i = base + j;
@@ -140,10 +149,15 @@ int scan_impl(const T *in, T *out, long long n, void *tmp, size_t tmp_bytes, cud
     // cover the same tile so the per-tile totals agree.
     ::mfseg::count_launch();
     k_tile_sums<T><<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, n, sums);
-    ::mfseg::count_launch();
-    k_scan_small<T><<<1, SCAN_BLOCK, 0, st>>>(sums, tiles);
-    ::mfseg::count_launch();
-    k_tile_scan<T><<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, out, n, sums);
+    if (tiles <= SCAN_BLOCK) {   // each tile sums its predecessors' totals itself
+        ::mfseg::count_launch();
+        k_tile_scan<T><<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, out, n, nullptr, sums);
+    } else {
+        ::mfseg::count_launch();
+        k_scan_small<T><<<1, SCAN_BLOCK, 0, st>>>(sums, tiles);
+        ::mfseg::count_launch();
+        k_tile_scan<T><<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, out, n, sums, nullptr);
+    }
     MFSEG_LAUNCH("scan");
     return 0;
 }
