@@ -839,13 +839,15 @@ __global__ void k_mark_changed(int K, mfseg_centers cur, mfseg_centers old, doub
 }
 
 // A sample bin is stable when none of its 3^4 neighbour bins is marked: its
-// candidate list and every candidate's state equal the last pass's.
+// candidate list and every candidate's state equal the last pass's.  One warp
+// per bin, the 81 neighbours over the lanes.
 __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned char *stable,
                              const unsigned char *smark, unsigned char *sstable, const unsigned *cbmax,
                              float *bdmax) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= NB) return;
-    int r = b;
+    const int lane = threadIdx.x & 31;
+    const long long b = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    if (b >= NB) return;   // warp-uniform
+    int r = (int)b;
     const int bx = r % k.x;
     r /= k.x;
     const int by = r % k.y;
@@ -854,22 +856,24 @@ __global__ void k_bin_stable(int NB, int4 k, const unsigned char *mark, unsigned
     const int bt = r / k.z;
     bool ok = true, sok = true;
     unsigned dm = 0;
-    for (int dt = -1; dt <= 1; ++dt)
-        for (int dz = -1; dz <= 1; ++dz)
-            for (int dy = -1; dy <= 1; ++dy)
-                for (int dx = -1; dx <= 1; ++dx) {
-                    const int qx = bx + dx, qy = by + dy, qz = bz + dz, qt = bt + dt;
-                    if (qx < 0 || qy < 0 || qz < 0 || qt < 0 || qx >= k.x || qy >= k.y || qz >= k.z ||
-                        qt >= k.w)
-                        continue;
-                    const int q = ((qt * k.z + qz) * k.y + qy) * k.x + qx;
-                    ok = ok && !mark[q];
-                    sok = sok && !smark[q];
-                    if (cbmax) dm = max(dm, cbmax[q]);
-                }
-    stable[b] = ok;
-    sstable[b] = sok;
-    if (bdmax) bdmax[b] = __uint_as_float(dm);   // largest move among the bin's candidates
+    for (int j = lane; j < 81; j += 32) {   // j = (dt, dz, dy, dx) + 1, base 3
+        const int qx = bx + j % 3 - 1, qy = by + (j / 3) % 3 - 1, qz = bz + (j / 9) % 3 - 1,
+                  qt = bt + j / 27 - 1;
+        if (qx < 0 || qy < 0 || qz < 0 || qt < 0 || qx >= k.x || qy >= k.y || qz >= k.z || qt >= k.w)
+            continue;
+        const int q = ((qt * k.z + qz) * k.y + qy) * k.x + qx;
+        ok = ok && !mark[q];
+        sok = sok && !smark[q];
+        if (cbmax) dm = max(dm, cbmax[q]);
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    sok = __all_sync(0xffffffffu, sok);
+    dm = __reduce_max_sync(0xffffffffu, dm);
+    if (lane == 0) {
+        stable[b] = ok;
+        sstable[b] = sok;
+        if (bdmax) bdmax[b] = __uint_as_float(dm);   // largest move among the bin's candidates
+    }
 }
 
 // one assignment pass for centre state `c` (grid rebuilt here); `prev`: the
@@ -908,7 +912,7 @@ int plan_pass(Plan &P, const mfseg_centers &c, double wd, double wp, double wf, 
             p.c_f, wd, wf, P.nf > 0 ? P.g.vbox : nullptr, P.nf > 0 ? P.vbox_prev : nullptr, P.bmark,
             P.smark, P.cdelta, P.cbmax);
         ::mfseg::count_launch();
-        k_bin_stable<<<(unsigned)((NB + 255) / 256), 256, 0, st>>>(
+        k_bin_stable<<<(unsigned)((32ll * NB + 255) / 256), 256, 0, st>>>(
             NB, make_int4(p.k[0], p.k[1], p.k[2], p.k[3]), P.bmark, P.bstable, P.smark, P.sstable, P.cbmax,
             P.bdmax);
         MFSEG_LAUNCH("stable bins");
