@@ -404,7 +404,11 @@ int launch_deferred(const FallbackArgs &a, const Grid &g, const int *tbin, const
     G.count = count;
     G.cap = cap;
     constexpr int blocks = 148 * 4, threads = 256;
-    G.batch_min = (debug_options().flags & MFSEG_DEBUG_DEFERRED_BATCH) ? 0 : 16ll * blocks * (threads / 32);
+#ifndef MFSEG_DEFERRED_BATCH_MUL
+#define MFSEG_DEFERRED_BATCH_MUL 1   // x 32 lanes: from one batch per warp
+#endif
+    G.batch_min = (debug_options().flags & MFSEG_DEBUG_DEFERRED_BATCH)
+                      ? 0 : (long long)MFSEG_DEFERRED_BATCH_MUL * blocks * (threads / 32);
     ::mfseg::count_launch();
     k_deferred<<<blocks, threads, 0, st>>>(a, G);
     MFSEG_LAUNCH("k_deferred");
