@@ -372,10 +372,13 @@ __global__ void __launch_bounds__(256, SCREEN_MINB) k_field_screen(FieldArgs a) 
 int launch_field_screen(const FieldArgs &a, cudaStream_t st) {
     if (!a.multi) return 0;
     ::mfseg::count_launch();
+#ifndef MFSEG_SCREEN_CTAS
+#define MFSEG_SCREEN_CTAS (148 * 32)   // 8 waves of the 4 resident CTAs per SM: even tails
+#endif
     if (a.wv > 0.0)
-        k_field_screen<true><<<148 * 8, 256, 0, st>>>(a);
+        k_field_screen<true><<<MFSEG_SCREEN_CTAS, 256, 0, st>>>(a);
     else
-        k_field_screen<false><<<148 * 8, 256, 0, st>>>(a);
+        k_field_screen<false><<<MFSEG_SCREEN_CTAS, 256, 0, st>>>(a);
     MFSEG_LAUNCH("k_field_screen");
     return 0;
 }
