@@ -92,7 +92,10 @@ struct FieldArgs {
     const float *bin_dmax;       // per sample bin: the largest cdelta among its candidates
 };
 
-constexpr int BC_MAX = 6;
+#ifndef MFSEG_BC_MAX
+#define MFSEG_BC_MAX 6
+#endif
+constexpr int BC_MAX = MFSEG_BC_MAX;   // clusters cached per field block
 struct BlockCache {                   // one field block's per-cluster sums, as added to acc
     int n;                            // entries (-1: none)
     int id[BC_MAX];
@@ -147,7 +150,10 @@ struct PointArgs {
     struct PointCache *pcache;
 };
 
-constexpr int PC_MAX = 12;
+#ifndef MFSEG_PC_MAX
+#define MFSEG_PC_MAX 12
+#endif
+constexpr int PC_MAX = MFSEG_PC_MAX;  // clusters cached per point chunk
 struct PointCache {                   // one point chunk's per-cluster sums, as added to acc
     int n;                            // entries (-1: none)
     int id[PC_MAX];
