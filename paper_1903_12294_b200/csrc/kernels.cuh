@@ -16,7 +16,10 @@ namespace mfseg {
 
 // A field brick left with several candidates after culling and dominance:
 // resolved per sample by k_field_screen (one warp per item).
-constexpr int MULTI_MAX = 16;
+#ifndef MFSEG_MULTI_MAX
+#define MFSEG_MULTI_MAX 16
+#endif
+constexpr int MULTI_MAX = MFSEG_MULTI_MAX;
 struct MultiItem {
     int x0, y0, z0, t0;       // brick origin (global sample indices)
     int meta;                 // nk | live extent x << 8 | y << 12 | z << 16 | t << 20
