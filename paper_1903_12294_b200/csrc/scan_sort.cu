@@ -165,7 +165,10 @@ int scan_impl(const T *in, T *out, long long n, void *tmp, size_t tmp_bytes, cud
 // ------------------------------------------------------------------ radix sort
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
-constexpr int RS_PER_WARP = 256;
+#ifndef MFSEG_RS_PER_WARP
+#define MFSEG_RS_PER_WARP 256
+#endif
+constexpr int RS_PER_WARP = MFSEG_RS_PER_WARP;
 constexpr int RS_TILE = RS_WARPS * RS_PER_WARP;   // 4096
 constexpr int RS_ROUNDS = RS_PER_WARP / 32;       // 16
 
