@@ -124,9 +124,12 @@ __global__ void k_tbins(int nt, const double *times, double mn, double C, int k,
 }
 
 // Sort key of a point: (sample bin, field-timestep interval, sub-cell), the
-// sub-cell being the Morton interleave of 8 subdivisions per axis inside the
-// bin (t, z, y, x bits from high to low), so consecutive points - a warp's
-// 64 - form compact 4D blocks.  Tiles are cut per (bin, interval) group.
+// sub-cell being the top sub_bits of the Morton interleave of 8 subdivisions
+// per axis inside the bin (t, z, y, x bits from high to low), so consecutive
+// points form compact 4D blocks; inside a sub-cell the stable sort keeps the
+// caller's (trajectory) order, which keeps the chunk gather local.  One bit
+// per axis (16 sub-cells) balances the two: finer sub-cells give tighter warp
+// tiles but a scattered gather.  Tiles are cut per (bin, interval) group.
 __global__ void k_point_keys(long long n, const double *xyz, const double *t, double4 mins,
                              double4 C, double4 inv, int4 k, const double *times, int nt, int sub_bits,
                              unsigned *keys, unsigned *vals) {
@@ -531,7 +534,11 @@ size_t plan_carve(Plan &P, void *ws, size_t bytes) {
         long long G = (long long)NB * P.nint;
         int gb = bits_for(G - 1);
         P.ngroups = (int)G;
-        P.sub_bits = gb + 8 <= 32 ? 8 : (32 - gb > 0 ? 32 - gb : 0);   // 4^4 Morton sub-cells
+#ifndef MFSEG_SUB_BITS
+#define MFSEG_SUB_BITS 4   // one Morton bit per axis (tools/variant_time.sh: 2-8 and 12 measured)
+#endif
+        constexpr int SB = MFSEG_SUB_BITS;   // 2^SB Morton sub-cells per bin
+        P.sub_bits = gb + SB <= 32 ? SB : (32 - gb > 0 ? 32 - gb : 0);
         P.key_bits = gb + P.sub_bits;
     }
     const int NG = P.ngroups;
