@@ -197,7 +197,10 @@ struct FallbackArgs {
 };
 
 // points per chunk of k_point_assign4 (8 warps x 4 warp tiles of 64 points)
-constexpr int POINT_CHUNK = 2048;
+#ifndef MFSEG_POINT_CHUNK
+#define MFSEG_POINT_CHUNK 2048
+#endif
+constexpr int POINT_CHUNK = MFSEG_POINT_CHUNK;
 
 // grid.cu
 size_t grid_workspace_bytes(int K, int NB);
